@@ -1,0 +1,465 @@
+"""Pins of the fp64 oracle against things other than itself (CPU only).
+
+Every pin names the passage or mathematical fact it follows. A plausible
+mistake in the oracle (a dropped term, a wrong sign or index, a transposed
+operand, a mis-ordered shard map or a wrong collective) fails at least one:
+
+  * SPEC worked value and identity             -> dense product
+  * brute-force pure-Python loops on tiny shapes            -> dense product
+  * central finite differences of 1/2 ||Y||^2      -> dX, dW, db formulas
+  * every mode's rank-by-rank program == dense     -> programs + shard maps
+  * degenerate p=1 and 2.5D d=1 == 2D      -> programs
+  * ledger == Table tp-comm-vol where exact     -> fabric + programs
+  * Table plug-ins of S:L518-520                            -> closed forms
+  * paper's measured memory reductions              -> memory closed forms
+  * exact-integer inputs give integer results               -> used by GPU bit-exact tests
+"""
+from fractions import Fraction
+import itertools
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+from oracle import closed_forms as cf
+from oracle import dense, programs
+from oracle.fabric import Fabric
+from oracle.grid import ConstraintViolation, build_grid
+from oracle.shards import IndivisibleDim, LayerSpec, extent, gather_full, shard
+
+import synth
+
+# (mode, world, depth, spec-kwargs) grids exercised by the oracle (p > #GPUs is fine here)
+GRIDS = [
+    ("1d", 1, 1, {"split_1d": "col"}), ("1d", 2, 1, {"split_1d": "col"}),
+    ("1d", 4, 1, {"split_1d": "col"}), ("1d", 3, 1, {"split_1d": "row"}),
+    ("1d", 4, 1, {"split_1d": "row"}), ("1d", 8, 1, {"split_1d": "row"}),
+    ("2d", 1, 1, {}), ("2d", 4, 1, {}), ("2d", 9, 1, {}),
+    ("2.5d", 4, 1, {}), ("2.5d", 8, 2, {}), ("2.5d", 8, 2, {"w_depth_sharded": True}),
+    ("2.5d", 2, 2, {}), ("2.5d", 12, 3, {}),
+    ("3d", 1, 1, {"parity": 0}), ("3d", 8, 1, {"parity": 0}), ("3d", 8, 1, {"parity": 1}),
+]
+
+
+def _bruteforce_matmul(A, B):
+    M, K = len(A), len(A[0])
+    N = len(B[0])
+    out = [[0.0] * N for _ in range(M)]
+    for i in range(M):
+        for j in range(N):
+            s = 0.0
+            for k in range(K):
+                s += float(A[i][k]) * float(B[k][j])
+            out[i][j] = s
+    return np.array(out)
+
+
+def _rel(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    den = max(np.linalg.norm(b), 1e-300)
+    return np.linalg.norm(a - b) / den
+
+
+# ----------------------------------------------------------------------------- dense
+
+def test_spec_worked_value():
+    g = load_golden("spec_matmul_2x2.json")
+    assert np.array_equal(dense.matmul(g["A"], g["B"]), np.array(g["AB"], np.float64))
+    assert np.array_equal(dense.matmul(g["A"], np.eye(2)), np.array(g["A"], np.float64))
+    with pytest.raises(ValueError):
+        dense.matmul(np.zeros((2, 3)), np.zeros((4, 5)))
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_dense_matches_bruteforce(seed):
+    rng = np.random.default_rng(seed)
+    M, K, N = rng.integers(1, 6, size=3)
+    X, W = rng.standard_normal((M, K)), rng.standard_normal((K, N))
+    b = rng.standard_normal(N)
+    alpha = 0.75
+    Y = dense.linear_fwd(X, W, b, alpha)
+    ref = alpha * _bruteforce_matmul(X.tolist(), W.tolist()) + b[None, :]
+    assert np.allclose(Y, ref, rtol=1e-13, atol=1e-13)
+    dY = rng.standard_normal((M, N))
+    dX, dW, db = dense.linear_bwd(dY, X, W, alpha)
+    assert np.allclose(dX, alpha * _bruteforce_matmul(dY.tolist(), W.T.tolist()), atol=1e-13)
+    assert np.allclose(dW, alpha * _bruteforce_matmul(X.T.tolist(), dY.tolist()), atol=1e-13)
+    assert np.allclose(db, [sum(dY[i][j] for i in range(M)) for j in range(N)], atol=1e-13)
+
+
+def _fd_check(f, params, grads, h=1e-5):
+    """Central differences of scalar f w.r.t. every entry of every param."""
+    for P, G in zip(params, grads):
+        fd = np.zeros_like(P)
+        for idx in np.ndindex(P.shape):
+            old = P[idx]
+            P[idx] = old + h
+            fp = f()
+            P[idx] = old - h
+            fm = f()
+            P[idx] = old
+            fd[idx] = (fp - fm) / (2 * h)
+        assert _rel(G, fd) <= 1e-6, (G, fd)
+
+
+@pytest.mark.parametrize("seed", [7, 11])
+def test_gradients_match_finite_differences(seed):
+    """parallel/serial grads vs central FD of 1/2||Y||^2, rel <= 1e-6 at h=1e-5."""
+    rng = np.random.default_rng(seed)
+    M, K, N = 4, 5, 3
+    X, W, b = rng.standard_normal((M, K)), rng.standard_normal((K, N)), rng.standard_normal(N)
+    alpha = 1.3
+    loss = lambda: 0.5 * np.sum(dense.linear_fwd(X, W, b, alpha) ** 2)
+    dY = dense.linear_fwd(X, W, b, alpha)             # dL/dY = Y
+    dX, dW, db = dense.linear_bwd(dY, X, W, alpha)
+    _fd_check(loss, [X, W, b], [dX, dW, db])
+
+
+def test_mlp2_gradients_match_finite_differences():
+    rng = np.random.default_rng(3)
+    M, H, F = 3, 4, 6
+    X, W1, W2 = rng.standard_normal((M, H)), rng.standard_normal((H, F)), rng.standard_normal((F, H))
+    loss = lambda: 0.5 * np.sum(dense.mlp2_fwd(X, W1, W2)[1] ** 2)
+    Y1, Y2 = dense.mlp2_fwd(X, W1, W2)
+    dX, dW1, dW2, _ = dense.mlp2_bwd(Y2, X, Y1, W1, W2)
+    _fd_check(loss, [X, W1, W2], [dX, dW1, dW2])
+
+
+# ----------------------------------------------------------------------------- grids
+
+def test_mesh_examples():
+    g = load_golden("mesh_examples.json")
+    for m in g["meshes"]:
+        if "error" in m:
+            with pytest.raises(ConstraintViolation):
+                build_grid(m["mode"], m["world"], m["depth"])
+        else:
+            assert list(build_grid(m["mode"], m["world"], m["depth"]).dims) == m["dims"]
+    for e in g["groups"]:
+        gr = build_grid(e["mode"], e["world"]).groups_along(e["axis"])
+        if "groups" in e:
+            assert gr == e["groups"]
+        else:
+            assert len(gr) == e["n_groups"] and all(len(x) == e["group_size"] for x in gr)
+
+
+@pytest.mark.parametrize("mode,world,depth", [("1d", 5, 1), ("2d", 9, 1), ("2.5d", 18, 2),
+                                              ("3d", 27, 1), ("2.5d", 8, 2), ("3d", 8, 1)])
+def test_grid_invariants(mode, world, depth):
+    g = build_grid(mode, world, depth)
+    for r in range(world):
+        assert g.rank_of(g.coords(r)) == r
+    for axis in range(len(g.dims)):
+        groups = g.groups_along(axis)
+        flat = sorted(itertools.chain.from_iterable(groups))
+        assert flat == list(range(world))                     # partition
+        for grp in groups:
+            cs = [g.coords(r) for r in grp]
+            assert [c[axis] for c in cs] == list(range(g.dims[axis]))   # ascending coord
+
+
+@pytest.mark.parametrize("mode,world,depth", [("2d", 8, 1), ("2d", 2, 1), ("3d", 4, 1),
+                                              ("3d", 6, 1), ("2.5d", 8, 3), ("2.5d", 6, 2)])
+def test_grid_constraint_violations(mode, world, depth):
+    with pytest.raises(ConstraintViolation):
+        build_grid(mode, world, depth)
+
+
+# ----------------------------------------------------------------------------- shard maps
+
+def _dims_for(mode, world, depth):
+    g = build_grid(mode, world, depth)
+    q, d = g.q, g.d
+    unit = {"1d": world, "2d": q, "2.5d": q * d, "3d": q * q}[mode]
+    return g, 2 * unit, 3 * unit, 2 * unit    # M, K, N
+
+
+@pytest.mark.parametrize("mode,world,depth,kw", GRIDS)
+def test_shard_maps_cover_with_replication(mode, world, depth, kw):
+    g, M, K, N = _dims_for(mode, world, depth)
+    spec = LayerSpec(M, K, N, **kw)
+    full = {"X": (M, K), "W": (K, N), "Y": (M, N), "B": (1, N)}
+    for t, shp in full.items():
+        cover = np.zeros(shp, dtype=np.int64)
+        for r in range(world):
+            e = extent(g, spec, r, t)
+            cover[e.row0:e.row0 + e.rows, e.col0:e.col0 + e.cols] += 1
+        # every element is held by the same number of ranks (the replication factor)
+        assert cover.min() == cover.max() >= 1
+        rep = cover.max()
+        expect = {("1d", "col"): {"X": world, "W": 1, "Y": 1, "B": 1},
+                  ("1d", "row"): {"X": 1, "W": 1, "Y": world, "B": world}}
+        if mode == "1d":
+            assert rep == expect[(mode, kw["split_1d"])][t]
+        elif t == "B":
+            assert rep == world // g.q
+        elif mode == "2.5d" and t == "W" and not kw.get("w_depth_sharded"):
+            assert rep == g.d                                 # replicated per plane (A6)
+        else:
+            assert rep == 1                                   # 1/p of the tensor
+
+
+@pytest.mark.parametrize("mode,world,depth,kw", GRIDS)
+def test_shard_gather_roundtrip_iota(mode, world, depth, kw):
+    g, M, K, N = _dims_for(mode, world, depth)
+    spec = LayerSpec(M, K, N, **kw)
+    for t, shp in {"X": (M, K), "W": (K, N), "Y": (M, N)}.items():
+        G = np.arange(np.prod(shp), dtype=np.float64).reshape(shp)
+        assert np.array_equal(gather_full(g, spec, shard(g, spec, G, t), t), G)
+
+
+def test_3d_parity_composition():
+    """Y(parity 0) of layer 1 is exactly X(parity 1) of layer 2 (reading A9)."""
+    g = build_grid("3d", 8)
+    s0, s1 = LayerSpec(16, 8, 12, parity=0), LayerSpec(16, 12, 8, parity=1)
+    for r in range(8):
+        assert extent(g, s0, r, "Y") == extent(g, s1, r, "X")
+        assert extent(g, s1, r, "Y") == extent(g, s0, r, "X")
+
+
+def test_indivisible_is_hard_error():
+    g = build_grid("2d", 4)
+    with pytest.raises(IndivisibleDim):
+        extent(g, LayerSpec(5, 4, 4), 0, "X")
+    with pytest.raises(IndivisibleDim):
+        extent(build_grid("3d", 8), LayerSpec(8, 6, 4), 0, "X")   # K not divisible by l^2
+
+
+# ----------------------------------------------------------------------------- programs
+
+def _inputs(M, K, N, seed):
+    X, W, dY, b = synth.layer_inputs(seed, M, K, N, with_bias=True, dtype="fp32")
+    return [np.asarray(a, np.float64) for a in (X, W, dY, b)]
+
+
+def run_layer(mode, world, depth, spec, X, W, dY, b, alpha=1.0):
+    g = build_grid(mode, world, depth)
+    fab = Fabric()
+    Xs, Ws = shard(g, spec, X, "X"), shard(g, spec, W, "W")
+    bs = shard(g, spec, b, "B") if b is not None else None
+    Ys, saved = programs.layer_fwd(g, spec, Xs, Ws, bs, alpha, fab)
+    dYs = shard(g, spec, dY, "Y")
+    dXs, dWs, dbs = programs.layer_bwd(g, spec, dYs, Xs, Ws, alpha, fab, saved)
+    out = (gather_full(g, spec, Ys, "Y"), gather_full(g, spec, dXs, "X"),
+           gather_full(g, spec, dWs, "W"), gather_full(g, spec, dbs, "B"))
+    return out, fab.ledger
+
+
+@pytest.mark.parametrize("mode,world,depth,kw", GRIDS)
+@pytest.mark.parametrize("seed", [42, 5])
+def test_every_scheme_reassembles_dense(mode, world, depth, kw, seed):
+    """S:L331 oracle equivalence: gathered Y, dX, dW, db == dense, fp64."""
+    g, M, K, N = _dims_for(mode, world, depth)
+    spec = LayerSpec(M, K, N, **kw)
+    X, W, dY, b = _inputs(M, K, N, seed)
+    (Y, dX, dW, db), ledger = run_layer(mode, world, depth, spec, X, W, dY, b, alpha=0.5)
+    Yr = dense.linear_fwd(X, W, b, 0.5)
+    dXr, dWr, dbr = dense.linear_bwd(dY, X, W, 0.5)
+    for got, ref in ((Y, Yr), (dX, dXr), (dW, dWr), (db, dbr)):
+        assert _rel(got, ref) <= 1e-12
+    assert ledger.total() == ledger.total_received()          # conservation
+
+
+@pytest.mark.parametrize("mode,world,depth", [("1d", 4, 1), ("2d", 4, 1), ("2.5d", 8, 2),
+                                              ("3d", 8, 1), ("1d", 1, 1)])
+def test_two_layer_chain(mode, world, depth):
+    g = build_grid(mode, world, depth)
+    unit = {"1d": world, "2d": g.q, "2.5d": g.q * g.d, "3d": g.q * g.q}[mode]
+    M, H = 2 * unit, 3 * unit
+    s1, s2 = programs.mlp2_specs(g, M, H)
+    X, W1, dY2, _ = _inputs(M, H, H, 1)
+    W2 = np.asarray(synth.tensor(1, 99, H, H, scale=0.3, dtype="fp32"), np.float64)
+    fab = Fabric()
+    Xs, W1s, W2s = shard(g, s1, X, "X"), shard(g, s1, W1, "W"), shard(g, s2, W2, "W")
+    Y1s, sv1 = programs.layer_fwd(g, s1, Xs, W1s, fab=fab)
+    Y2s, sv2 = programs.layer_fwd(g, s2, Y1s, W2s, fab=fab)     # Y1 layout IS layer-2 X layout
+    dY2s = shard(g, s2, dY2, "Y")
+    dY1s, dW2s, _ = programs.layer_bwd(g, s2, dY2s, Y1s, W2s, fab=fab, saved=sv2)
+    dXs, dW1s, _ = programs.layer_bwd(g, s1, dY1s, Xs, W1s, fab=fab, saved=sv1)
+    Y1, Y2 = dense.mlp2_fwd(X, W1, W2)
+    dX, dW1, dW2, _ = dense.mlp2_bwd(dY2, X, Y1, W1, W2)
+    assert _rel(gather_full(g, s2, Y2s, "Y"), Y2) <= 1e-12
+    assert _rel(gather_full(g, s1, dXs, "X"), dX) <= 1e-12
+    assert _rel(gather_full(g, s1, dW1s, "W"), dW1) <= 1e-12
+    assert _rel(gather_full(g, s2, dW2s, "W"), dW2) <= 1e-12
+
+
+@pytest.mark.parametrize("mode", ["1d", "2d", "2.5d", "3d"])
+def test_p1_is_serial_with_zero_volume(mode):
+    spec = LayerSpec(6, 5, 4)
+    X, W, dY, b = _inputs(6, 5, 4, 9)
+    (Y, dX, dW, db), ledger = run_layer(mode, 1, 1, spec, X, W, dY, b)
+    assert np.array_equal(Y, X @ W + b[None, :])
+    assert ledger.total() == 0
+
+
+def test_25d_depth1_is_2d():
+    """P:L526 "When depth=1, it is close to 2D": identical results and volumes."""
+    spec = LayerSpec(8, 6, 4)
+    X, W, dY, b = _inputs(8, 6, 4, 3)
+    o2, l2 = run_layer("2d", 4, 1, spec, X, W, dY, None)
+    o25, l25 = run_layer("2.5d", 4, 1, spec, X, W, dY, None)
+    for a, c in zip(o2[:3], o25[:3]):
+        assert np.array_equal(a, c)
+    assert l2.total() == l25.total()
+
+
+def test_exact_integer_inputs_give_exact_results():
+    """Ternary entries, K <= 256: every product and sum is an exact small integer
+    (the GPU bit-exact pin relies on this)."""
+    M, K, N = 16, 256, 24
+    X = synth.tensor(4, 0, M, K, kind="ternary")
+    W = synth.tensor(4, 1, K, N, kind="ternary")
+    assert set(np.unique(X)) <= {-1.0, 0.0, 1.0}
+    Y = dense.matmul(X, W)
+    assert np.array_equal(Y, np.round(Y)) and np.abs(Y).max() <= K
+    assert np.array_equal(Y, _bruteforce_matmul(X.tolist(), W.tolist()))
+    (Yg, _, _, _), _ = run_layer("2d", 4, 1, LayerSpec(M, K, N), X, W, np.zeros((M, N)), None)
+    assert np.array_equal(Yg, Y)
+
+
+# ----------------------------------------------------------------------------- ledgers
+
+def test_spec_collective_examples():
+    g = load_golden("collective_volumes.json")
+    fab = Fabric()
+    fab.broadcast([0, 1, 2, 3], 0, np.zeros(g["broadcast"]["m"]))
+    assert fab.ledger.total() == g["broadcast"]["volume"]
+    fab = Fabric()
+    out = fab.all_reduce([0, 1, 2, 3], {r: np.array([float(v)]) for r, v in enumerate(g["all_reduce"]["scalars"])})
+    assert all(out[r][0] == g["all_reduce"]["sum"] for r in range(4))
+    fab = Fabric()
+    fab.all_reduce([0, 1, 2, 3], {r: np.zeros(g["all_reduce"]["m"]) for r in range(4)})
+    assert fab.ledger.total() == g["all_reduce"]["volume"]
+    fab = Fabric()
+    out = fab.all_gather([0, 1], {0: np.array([1.0]), 1: np.array([2.0])})
+    assert list(out[0]) == [1.0, 2.0] and fab.ledger.total() == g["all_gather"]["volume"]
+    fab = Fabric()
+    ins = g["reduce_scatter"]["inputs"]
+    out = fab.reduce_scatter([0, 1], {0: np.array(ins[0], float), 1: np.array(ins[1], float)})
+    assert [list(out[0]), list(out[1])] == g["reduce_scatter"]["outputs"]
+
+
+def test_summa_2d_spec_volumes():
+    """j=2, S_x=S_w=16 -> fwd 32, fwd+bwd 96, bwd 64 even with dY = 0."""
+    gv = load_golden("collective_volumes.json")["summa2d"]
+    g = build_grid("2d", 4)
+    spec = LayerSpec(4, 4, 4)                              # S_x = S_w = 16
+    X, W, dY, _ = _inputs(4, 4, 4, 42)
+    fab = Fabric()
+    Xs, Ws = shard(g, spec, X, "X"), shard(g, spec, W, "W")
+    Ys, sv = programs.layer_fwd(g, spec, Xs, Ws, fab=fab)
+    assert fab.ledger.total() == gv["fwd"]
+    zero = shard(g, spec, np.zeros((4, 4)), "Y")
+    dX, dW, _ = programs.layer_bwd(g, spec, zero, Xs, Ws, fab=fab, saved=sv)
+    assert all(not np.any(dX[r]) and not np.any(dW[r]) for r in range(4))
+    assert fab.ledger.total() - fab.ledger.total("all_reduce") == gv["fwd+bwd"]
+    assert gv["fwd+bwd"] - gv["fwd"] == gv["bwd"]
+
+
+@pytest.mark.parametrize("j", [2, 3])
+def test_2d_volume_equals_table_exactly(j):
+    """3(j-1)(S_x+S_w), ratio exactly 1 (reading A4)."""
+    M, K, N = 2 * j, 3 * j, 3 * j                           # square W (S_y = S_x)
+    spec = LayerSpec(M, K, N)
+    X, W, dY, _ = _inputs(M, K, N, 0)
+    _, led = run_layer("2d", j * j, 1, spec, X, W, dY, None)
+    moved = led.total() - led.total("all_reduce")          # db all-reduce is extra (bias)
+    assert moved == cf.paper_comm_volume("2d", M * K, K * N, j=j)
+    assert moved == cf.counted_volume("2d", M, K, N, q=j)
+
+
+@pytest.mark.parametrize("p", [2, 3, 4])
+def test_1d_volume_equals_table_per_layer(p):
+    """one ring all-reduce of S_x per layer fwd+bwd: 2(p-1) S_x (reading A3).
+    Column split: AR of dX (S_x); row split: AR of Y (S_y = S_x for square W)."""
+    M, K = 4, 2 * p
+    X, W, dY, _ = _inputs(M, K, K, 1)
+    for split in ("col", "row"):
+        _, led = run_layer("1d", p, 1, LayerSpec(M, K, K, split_1d=split), X, W, dY, None)
+        assert led.total() == cf.paper_comm_volume("1d", M * K, K * K, p=p)
+        assert led.total() == cf.counted_volume("1d", M, K, K, p=p, split_1d=split)
+
+
+@pytest.mark.parametrize("d,k", [(2, 2), (1, 2), (2, 3)])
+def test_25d_volume_per_plane_equals_table(d, k):
+    """P:L375 per plane: 3(k-1)(S_x/d + S_w); the depth all-reduce of dW is extra (A11)."""
+    M, K, N = 2 * d * k, 2 * k, 2 * k
+    X, W, dY, _ = _inputs(M, K, N, 2)
+    _, led = run_layer("2.5d", d * k * k, d, LayerSpec(M, K, N), X, W, dY, None)
+    ar = led.total("all_reduce")
+    depth_ar = cf.counted_volume("2.5d", M, K, N, q=k, d=d, part="depth")
+    plane = Fraction(led.total() - ar, d)
+    assert plane == cf.paper_comm_volume("2.5d", M * K, K * N, k=k, d=d)
+    assert depth_ar == 2 * (d - 1) * K * N
+
+
+def test_3d_volume_ratio_is_l():
+    """P:L377 2(l-1)/l (S_x+S_w+S_y) vs the schedule's 2(l-1)(...): ratio l (reading A10)."""
+    M, K, N = 8, 8, 8
+    X, W, dY, _ = _inputs(M, K, N, 4)
+    _, led = run_layer("3d", 8, 1, LayerSpec(M, K, N), X, W, dY, None)
+    moved = led.total() - led.total("all_reduce")
+    paper = cf.paper_comm_volume("3d", M * K, K * N, M * N, l=2)
+    assert Fraction(moved) / paper == 2
+    assert moved == cf.counted_volume("3d", M, K, N, q=2)
+
+
+def test_volumes_independent_of_data():
+    spec = LayerSpec(8, 8, 8)
+    a, la = run_layer("3d", 8, 1, spec, *_inputs(8, 8, 8, 1))
+    z = np.zeros((8, 8))
+    b, lb = run_layer("3d", 8, 1, spec, z, z, z, np.zeros(8))
+    assert dict(la.sent) == dict(lb.sent)
+
+
+def test_table_plugins():
+    g = load_golden("table_plugins.json")
+    Sx = g["b"] * g["s"] * g["h"]
+    Sw = g["h"] * g["h"]
+    for c in g["cases"]:
+        kw = {k: v for k, v in c.items() if k not in ("mode", "value")}
+        assert cf.paper_comm_volume(c["mode"], Sx, Sw, **kw) == c["value"]
+
+
+def test_scaling_ordering_at_p64():
+    """P:L415 advanced modes 'significantly lower' than 1D at large p (h=1024,s=512,b=32)."""
+    Sx, Sw = 32 * 512 * 1024, 1024 * 1024
+    v1 = cf.paper_comm_volume("1d", Sx, Sw, p=64)
+    assert cf.paper_comm_volume("2d", Sx, Sw, j=8) < v1
+    assert cf.paper_comm_volume("3d", Sx, Sw, l=4) < v1
+    assert cf.paper_comm_volume("1d", Sx, Sw, p=1) == 0
+
+
+# ----------------------------------------------------------------------------- memory
+
+def test_memory_closed_form_matches_shard_extents():
+    for mode, world, depth, kw in GRIDS:
+        g, M, K, N = _dims_for(mode, world, depth)
+        spec = LayerSpec(M, K, N, **kw)
+        cfm = cf.memory_per_rank(mode, M, K, N, world, g.q, g.d, kw.get("split_1d", "col"),
+                                 kw.get("w_depth_sharded", False))
+        for r in range(world):
+            for t in ("X", "W", "Y"):
+                e = extent(g, spec, r, t)
+                assert e.rows * e.cols == cfm[t], (mode, world, t)
+
+
+def test_memory_reductions_match_paper_range_test():
+    """P:L81. At M = h = 16384, p = 8 the closed form gives 63.2% (2.5D) and 73.7% (3D)
+    vs the paper's measured 62% and 74.2%. For the batch-512 pair the hidden size is not
+    stated: solving a/w from the 3D figure predicts the 2.5D figure."""
+    g = load_golden("paper_memory.json")
+    bh = g["by_hidden"]
+    r25 = cf.memory_reduction_vs_1d("2.5d", bh["h"], bh["h"], bh["p"], q=bh["q"], d=bh["d"])
+    r3 = cf.memory_reduction_vs_1d("3d", bh["h"], bh["h"], bh["p"], q=bh["l"])
+    assert abs(r25 - bh["reduction_25d"]) < 0.015 and abs(r3 - bh["reduction_3d"]) < 0.015
+    # depth-sharded W would make 2.5D == 3D, which the paper's numbers exclude (reading A6)
+    assert abs(r25 - r3) > 0.05
+    for case in (bh, g["by_batch"]):
+        p = case["p"]
+        # 3D: 1 - (3x/p + 2/p) / ((2+1/p)x + 2/p) = R  ->  solve for x = a/w
+        R = case["reduction_3d"]
+        x = (2 / p - (1 - R) * 2 / p) / ((1 - R) * (2 + 1 / p) - 3 / p)
+        pred25 = 1 - (3 * x / p + 2 * 2 / p) / ((2 + 1 / p) * x + 2 / p)
+        assert abs(pred25 - case["reduction_25d"]) < 0.03
