@@ -1,0 +1,200 @@
+/*
+ * tp_b200.h — C ABI of the B200-native multi-dimensional tensor-parallel linear layer.
+ *
+ * The operation (PAPER.md = P:Lnnn, SPEC.md = S:Lnnn; DESIGN.md lists every reading):
+ *   Y = alpha * X . W + b,  dX = alpha * dY . W^T,  dW = alpha * X^T . dY,  db = 1^T dY
+ * with X [M,K], W [K,N], Y [M,N] row-major (reading A1), partitioned over
+ * p GPUs in one of four modes:
+ *   TP_1D    Megatron column / row split
+ *   TP_2D    SUMMA on a q x q grid, p = q^2
+ *   TP_2P5D  q x q x d grid, depth d given by the user, p = d q^2
+ *   TP_3D    l x l x l cube, p = l^3
+ * Grid constraints P:L530; no silent fallback to 1D.
+ *
+ * Conventions for every entry point:
+ *   - Pointers named x, w, y, dy, dx, dw, bias, dbias, saved, ws, A, B, C, D, dst,
+ *     global, shard are DEVICE pointers on the grid's CUDA device, owned by the
+ *     caller; the library never frees them. Host pointers appear only where noted.
+ *   - Shards are dense row-major blocks: a tensor's local block of extent
+ *     (rows, cols) (see tp_shard_extent) is stored with row stride = cols elements.
+ *   - dtype TP_BF16: operands and outputs bf16, fp32 accumulate (tcgen05/TMEM);
+ *     TP_FP32: everything fp32 (SIMT FFMA path). Bias has the operand dtype.
+ *   - `stream` is a cudaStream_t passed as void*. Work is stream-ordered: it
+ *     starts after prior work on `stream` and later work on `stream` sees the
+ *     results. No host synchronisation, EXCEPT with TP_TRANSPORT_LOCAL, whose
+ *     collectives rendezvous on the host (each rank must be on its own thread).
+ *   - Every argument check runs on the host BEFORE anything is enqueued. On error
+ *     nothing is enqueued, the status says which class, tp_last_error() (thread-
+ *     local) says why.
+ *   - Collective contract (like NCCL): every rank of a grid calls tp_linear_fwd /
+ *     tp_linear_bwd with an identical descriptor, in the same order.
+ */
+#ifndef TP_B200_H
+#define TP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  TP_OK = 0,
+  TP_ERR_CONSTRAINT = 1,  /* world does not factor as the mode requires */
+  TP_ERR_INDIVISIBLE = 2, /* a dim is not divisible by the mode's split */
+  TP_ERR_SHAPE = 3,       /* bad shape / alignment (TMA needs 16-byte row strides and bases) */
+  TP_ERR_ARG = 4,         /* null / out-of-range argument */
+  TP_ERR_CUDA = 5,        /* a CUDA runtime call failed */
+  TP_ERR_NCCL = 6,        /* an NCCL call failed */
+  TP_ERR_WORKSPACE = 7,   /* ws_bytes smaller than tp_workspace_size() */
+  TP_ERR_UNSUPPORTED = 8  /* valid request this build does not implement */
+} tp_status;
+
+typedef enum { TP_1D = 1, TP_2D = 2, TP_2P5D = 3, TP_3D = 4 } tp_mode;
+typedef enum { TP_BF16 = 0, TP_FP32 = 1 } tp_dtype;
+
+/* How ranks talk.
+ *   NCCL  one process (or thread) per GPU; id128 = ncclUniqueId from rank 0's
+ *         tp_get_unique_id, broadcast by the caller (e.g. torch.distributed).
+ *         Per-axis communicators come from ncclCommSplit.
+ *   LOCAL all ranks in ONE process, one host thread per rank, any devices
+ *         (several ranks may share a device). Collectives are stream-ordered
+ *         device copies / reduction kernels between the ranks' buffers, after a
+ *         host rendezvous. Used to run multi-rank grids on a single GPU.
+ *   NONE  no communication: grid planning (extents, workspace) for any world,
+ *         compute only when world == 1. */
+typedef enum { TP_TRANSPORT_NCCL = 0, TP_TRANSPORT_LOCAL = 1, TP_TRANSPORT_NONE = 2 } tp_transport;
+
+typedef enum { TP_TENSOR_X = 0, TP_TENSOR_W = 1, TP_TENSOR_Y = 2, TP_TENSOR_BIAS = 3 } tp_tensor;
+
+/* tp_linear_desc.flags */
+#define TP_FLAG_W25_DEPTH_SHARDED 0x1u /* 2.5D: W also split over depth (1/p at rest); AG in fwd, RS of dW */
+#define TP_FLAG_SERIAL 0x2u            /* debug: run collectives on the compute stream (no overlap) */
+
+typedef struct tp_grid tp_grid; /* opaque; library-owned (communicators, streams, events) */
+
+typedef struct {
+  int64_t M, K, N;   /* GLOBAL shape: X [M,K], W [K,N], Y [M,N] */
+  tp_dtype dtype;
+  int split_1d;      /* TP_1D only: 0 = column-parallel (W split by columns), 1 = row-parallel */
+  int parity_3d;     /* TP_3D only: 0 or 1; parity 1 swaps axes b and c so Y(0) == X(1) layout */
+  uint32_t flags;    /* TP_FLAG_* */
+  float alpha;       /* Y = alpha * X.W + b */
+} tp_linear_desc;
+
+/* ---- errors ------------------------------------------------------------------------- */
+const char* tp_status_string(tp_status s);
+/* Detail of the last error on the calling thread ("" if none). Valid until the next call. */
+const char* tp_last_error(void);
+/* Library version string, and the CUDA arch it was built for ("sm_100a"). */
+const char* tp_version(void);
+
+/* ---- grid (P:L287 parallel context) ---------------------- */
+/* Writes a 128-byte rendezvous id into id128 (host memory, 128 bytes).
+ * NCCL: ncclGetUniqueId (call on ONE rank, share the bytes). LOCAL: a fresh
+ * process-unique tag naming an in-process world. NONE: zeros. */
+tp_status tp_get_unique_id(tp_transport transport, void* id128);
+
+/* Creates this rank's view of the grid and its per-axis communicators.
+ *   mode   TP_1D .. TP_3D;  world = p;  rank in [0, p)
+ *   q      side: 2D j, 2.5D k, 3D l; pass 0 to derive it from world (and d)
+ *   d      2.5D depth (>= 1); ignored (treated as 1) by other modes
+ *   cuda_device  the GPU of this rank
+ *   id128  host pointer to the id from tp_get_unique_id (unused for NONE)
+ * Coordinates are row-major: 1D (r); 2D rank = i q + j; 2.5D rank = dep q^2 + i q + j
+ * (depth outermost); 3D rank = a l^2 + b l + c. Groups along an axis list
+ * their members by ascending coordinate.
+ * Errors: TP_ERR_CONSTRAINT if world does not factor; TP_ERR_ARG; TP_ERR_NCCL/CUDA.
+ * NCCL/LOCAL init is collective: all ranks of the world must call it. */
+tp_status tp_grid_init(tp_grid** grid, tp_mode mode, int world, int rank, int q, int d,
+                       int cuda_device, tp_transport transport, const void* id128);
+
+/* coords[0..2]: 1D (r,0,0); 2D (i,j,0); 2.5D (dep,i,j); 3D (a,b,c). */
+tp_status tp_grid_coords(const tp_grid* grid, int coords[3]);
+/* dims[0..2] of the grid (unused = 1) and the number of axes. */
+tp_status tp_grid_dims(const tp_grid* grid, int dims[3], int* ndims);
+/* Members (global ranks, ascending coordinate) of this rank's line along `axis`;
+ * members must hold dims[axis] ints. */
+tp_status tp_grid_group(const tp_grid* grid, int axis, int* members);
+tp_status tp_grid_destroy(tp_grid* grid);
+
+/* ---- layout (P:L524 2D, P:L526 2.5D, P:L528 3D, P:L486-488 1D) ----------------------- */
+/* Global block of `tensor` held by this rank: rows [row0, row0+rows), cols [col0, col0+cols).
+ * BIAS is a [1, N] row. Gradients share their tensor's extent (dX~X, dW~W, dY~Y, db~BIAS).
+ * Errors: TP_ERR_INDIVISIBLE (no padding), TP_ERR_ARG. Host only. */
+tp_status tp_shard_extent(const tp_grid* grid, const tp_linear_desc* desc, tp_tensor tensor,
+                          int64_t* row0, int64_t* rows, int64_t* col0, int64_t* cols);
+
+/* Device bytes the caller must provide: ws (scratch, reusable after the call's work
+ * completes on `stream`) and saved (written by fwd, read by the matching bwd: the 3D
+ * gathered X and W, the 2.5D depth-gathered W). Either may be 0. The same ws size
+ * serves fwd and bwd. Host only. */
+tp_status tp_workspace_size(const tp_grid* grid, const tp_linear_desc* desc, size_t* ws_bytes,
+                            size_t* saved_bytes);
+
+/* ---- the hot path --------------------------------------------------------------------- */
+/* Forward. x, w: this rank's shards; bias: this rank's bias shard or NULL; y: output
+ * shard (written); saved: saved_bytes of device memory (NULL iff saved_bytes == 0);
+ * ws: ws_bytes >= tp_workspace_size. Computes Y = alpha X.W + b in the mode's layout. */
+tp_status tp_linear_fwd(tp_grid* grid, const tp_linear_desc* desc, const void* x, const void* w,
+                        const void* bias, void* y, void* saved, void* ws, size_t ws_bytes,
+                        void* stream);
+
+/* Backward of the forward that wrote `saved`. dy: this rank's dY shard (Y's layout).
+ * Writes dx (X's layout; may be NULL to skip), dw (W's layout), dbias (bias layout;
+ * NULL to skip). x, w: the same shards given to fwd. */
+tp_status tp_linear_bwd(tp_grid* grid, const tp_linear_desc* desc, const void* dy, const void* x,
+                        const void* w, const void* saved, void* dx, void* dw, void* dbias,
+                        void* ws, size_t ws_bytes, void* stream);
+
+/* Model-boundary split/gather: copy this rank's block of the dense
+ * row-major global tensor (device) into `shard`, or back. Bit-exact copies. */
+tp_status tp_pack(const tp_grid* grid, const tp_linear_desc* desc, tp_tensor tensor,
+                  const void* global, void* shard, void* stream);
+tp_status tp_unpack(const tp_grid* grid, const tp_linear_desc* desc, tp_tensor tensor,
+                    const void* shard, void* global, void* stream);
+
+/* ---- kernels exposed for parity tests and benchmarks ----------------------------------- */
+/* Local GEMM, the per-step shard product of every mode:
+ *   D[M,N] = alpha * (op(A) . op(B) + C) + bias[col]
+ * op(A) = A [M,K] row-major (lda >= K) if trans_a == 0, else A is stored [K,M] (lda >= M);
+ * op(B) = B [K,N] row-major (ldb >= N) if trans_b == 0, else B is stored [N,K] (ldb >= K).
+ * C: fp32 [M,N] (ldc) or NULL; bias: in_dtype [N] or NULL; D: out_dtype, ldd.
+ * TP_BF16 inputs run the tcgen05/TMEM/TMA kernel (bf16 x bf16 -> fp32), TP_FP32 inputs
+ * the SIMT fp32 kernel. bf16 operands need lda, ldb multiples of 8 and 16-byte aligned
+ * bases (TMA), else TP_ERR_SHAPE. D may alias C (in-place accumulate). */
+tp_status tp_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, tp_dtype in_dtype,
+                  const void* A, int64_t lda, const void* B, int64_t ldb, const float* C,
+                  int64_t ldc, void* D, int64_t ldd, tp_dtype out_dtype, float alpha,
+                  const void* bias, void* stream);
+
+/* db = 1^T dY: column sums of a [rows, cols] row-major matrix (ld), fp32 accumulate. */
+tp_status tp_colsum(const void* src, int64_t rows, int64_t cols, int64_t ld, tp_dtype dtype,
+                    void* dst, void* stream);
+
+/* Seeded synthetic input generator (the same counter-based SplitMix64 as synth/):
+ * fills dst[r*ld + c] (r < rows, c < cols) with element (g_row0 + r, g_col0 + c) of the
+ * global [*, g_cols] tensor of stream (seed, tensor_id). kind 0 = uniform in
+ * [-1,1) * scale on a 24-bit grid, kind 1 = ternary {-1,0,1}; quantised RNE to dtype. */
+tp_status tp_fill(void* dst, tp_dtype dtype, int64_t rows, int64_t cols, int64_t ld,
+                  uint64_t seed, int tensor_id, int kind, float scale, int64_t g_row0,
+                  int64_t g_col0, int64_t g_cols, void* stream);
+
+/* Writes `bytes` to a scratch buffer (device) to evict L2 between timed steps. */
+tp_status tp_l2_flush(void* scratch, size_t bytes, void* stream);
+
+/* ---- instrumentation -------------------------------------------------------------------- */
+/* When enabled, every GEMM launch is bracketed by CUDA events on its launching stream. */
+tp_status tp_prof_enable(int on);
+tp_status tp_prof_reset(void);
+/* kernel_class: 0 = tcgen05 GEMM, 1 = SIMT GEMM. Synchronises the recorded events and
+ * returns the summed device time (ms), the launch count and the algorithmic flops. */
+tp_status tp_prof_read(int kernel_class, double* total_ms, int64_t* launches, double* flops);
+/* Number of kernels this library has launched since load (all classes). */
+int64_t tp_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TP_B200_H */

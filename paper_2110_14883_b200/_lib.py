@@ -1,0 +1,80 @@
+"""ctypes binding of libtp_b200.so (include/tp_b200.h). Argument marshalling only.
+
+The library is built in-tree (python -m paper_2110_14883_b200.build). There is no
+fallback: if the .so is missing or fails to load, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtp_b200.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python -m paper_2110_14883_b200.build` "
+        "(there is no CPU or PyTorch fallback for the tensor-parallel path)")
+
+lib = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
+
+# enums (tp_b200.h)
+TP_OK, TP_ERR_CONSTRAINT, TP_ERR_INDIVISIBLE, TP_ERR_SHAPE, TP_ERR_ARG = 0, 1, 2, 3, 4
+TP_ERR_CUDA, TP_ERR_NCCL, TP_ERR_WORKSPACE, TP_ERR_UNSUPPORTED = 5, 6, 7, 8
+TP_1D, TP_2D, TP_2P5D, TP_3D = 1, 2, 3, 4
+TP_BF16, TP_FP32 = 0, 1
+TP_TRANSPORT_NCCL, TP_TRANSPORT_LOCAL, TP_TRANSPORT_NONE = 0, 1, 2
+TP_TENSOR_X, TP_TENSOR_W, TP_TENSOR_Y, TP_TENSOR_BIAS = 0, 1, 2, 3
+TP_FLAG_W25_DEPTH_SHARDED = 0x1
+TP_FLAG_SERIAL = 0x2
+
+EXPORTED = [
+    "tp_status_string", "tp_last_error", "tp_version", "tp_get_unique_id", "tp_grid_init",
+    "tp_grid_coords", "tp_grid_dims", "tp_grid_group", "tp_grid_destroy", "tp_shard_extent",
+    "tp_workspace_size", "tp_linear_fwd", "tp_linear_bwd", "tp_pack", "tp_unpack", "tp_gemm",
+    "tp_colsum", "tp_fill", "tp_l2_flush", "tp_prof_enable", "tp_prof_reset", "tp_prof_read",
+    "tp_launch_count",
+]
+
+
+class tp_linear_desc(C.Structure):
+    _fields_ = [("M", C.c_int64), ("K", C.c_int64), ("N", C.c_int64), ("dtype", C.c_int),
+                ("split_1d", C.c_int), ("parity_3d", C.c_int), ("flags", C.c_uint32),
+                ("alpha", C.c_float)]
+
+
+_vp, _i, _i64, _sz, _f = C.c_void_p, C.c_int, C.c_int64, C.c_size_t, C.c_float
+_P64 = C.POINTER(C.c_int64)
+
+_sigs = {
+    "tp_status_string": (C.c_char_p, [_i]),
+    "tp_last_error": (C.c_char_p, []),
+    "tp_version": (C.c_char_p, []),
+    "tp_get_unique_id": (_i, [_i, _vp]),
+    "tp_grid_init": (_i, [C.POINTER(_vp), _i, _i, _i, _i, _i, _i, _i, _vp]),
+    "tp_grid_coords": (_i, [_vp, C.POINTER(_i)]),
+    "tp_grid_dims": (_i, [_vp, C.POINTER(_i), C.POINTER(_i)]),
+    "tp_grid_group": (_i, [_vp, _i, C.POINTER(_i)]),
+    "tp_grid_destroy": (_i, [_vp]),
+    "tp_shard_extent": (_i, [_vp, C.POINTER(tp_linear_desc), _i, _P64, _P64, _P64, _P64]),
+    "tp_workspace_size": (_i, [_vp, C.POINTER(tp_linear_desc), C.POINTER(_sz), C.POINTER(_sz)]),
+    "tp_linear_fwd": (_i, [_vp, C.POINTER(tp_linear_desc), _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "tp_linear_bwd": (_i, [_vp, C.POINTER(tp_linear_desc), _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                           _vp, _sz, _vp]),
+    "tp_pack": (_i, [_vp, C.POINTER(tp_linear_desc), _i, _vp, _vp, _vp]),
+    "tp_unpack": (_i, [_vp, C.POINTER(tp_linear_desc), _i, _vp, _vp, _vp]),
+    "tp_gemm": (_i, [_i, _i, _i64, _i64, _i64, _i, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64,
+                     _i, _f, _vp, _vp]),
+    "tp_colsum": (_i, [_vp, _i64, _i64, _i64, _i, _vp, _vp]),
+    "tp_fill": (_i, [_vp, _i, _i64, _i64, _i64, C.c_uint64, _i, _i, _f, _i64, _i64, _i64, _vp]),
+    "tp_l2_flush": (_i, [_vp, _sz, _vp]),
+    "tp_prof_enable": (_i, [_i]),
+    "tp_prof_reset": (_i, []),
+    "tp_prof_read": (_i, [_i, C.POINTER(C.c_double), _P64, C.POINTER(C.c_double)]),
+    "tp_launch_count": (_i64, []),
+}
+
+for _name, (_res, _args) in _sigs.items():
+    _fn = getattr(lib, _name)
+    _fn.restype = _res
+    _fn.argtypes = _args

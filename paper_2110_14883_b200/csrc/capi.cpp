@@ -1,0 +1,511 @@
+// The C ABI (include/tp_b200.h): argument validation, the grid / parallel context
+// ("parallel context manager"), and dispatch into the per-mode schedules.
+#include <cstring>
+#include <mutex>
+
+#include "sched.h"
+
+namespace tp {
+
+namespace {
+thread_local std::string t_err;
+}
+
+void set_error(const std::string& msg) { t_err = msg; }
+
+tp_status fail(tp_status s, const std::string& msg) {
+  t_err = msg;
+  return s;
+}
+
+std::atomic<int64_t> g_launches{0};
+
+// ---- instrumentation: events around GEMM launches --------------------------------------
+namespace {
+struct ProfRec {
+  int cls;
+  double flops;
+  cudaEvent_t a, b;
+};
+std::mutex g_prof_mu;
+std::vector<ProfRec> g_prof;
+std::atomic<bool> g_prof_on{false};
+}  // namespace
+
+bool prof_on() { return g_prof_on.load(std::memory_order_relaxed); }
+
+int prof_begin(int cls, cudaStream_t s, double flops) {
+  if (!prof_on()) return -1;
+  ProfRec r{cls, flops, nullptr, nullptr};
+  cudaEventCreate(&r.a);
+  cudaEventCreate(&r.b);
+  cudaEventRecord(r.a, s);
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof.push_back(r);
+  return static_cast<int>(g_prof.size()) - 1;
+}
+
+void prof_end(int token, cudaStream_t s) {
+  if (token < 0) return;
+  cudaEvent_t b;
+  {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    if (token >= static_cast<int>(g_prof.size())) return;
+    b = g_prof[token].b;
+  }
+  cudaEventRecord(b, s);
+}
+
+}  // namespace tp
+
+using namespace tp;
+
+std::vector<int> tp_grid::group_members(int ax) const {
+  std::vector<int> out;
+  int c[3] = {coords[0], coords[1], coords[2]};
+  for (int v = 0; v < dims[ax]; ++v) {
+    c[ax] = v;
+    int r = 0;
+    for (int k = 0; k < ndims; ++k) r = r * dims[k] + c[k];
+    out.push_back(r);
+  }
+  return out;
+}
+
+namespace {
+
+int iroot(int p, int e) {
+  for (int c = 1; c <= p; ++c) {
+    int64_t v = 1;
+    for (int k = 0; k < e; ++k) v *= c;
+    if (v == p) return c;
+    if (v > p) break;
+  }
+  return -1;
+}
+
+tp_status plan_grid(tp_grid* g, tp_mode mode, int world, int rank, int q, int d) {
+  if (world < 1) return fail(TP_ERR_ARG, "world must be >= 1");
+  if (rank < 0 || rank >= world) return fail(TP_ERR_ARG, "rank out of range");
+  g->mode = mode;
+  g->world = world;
+  g->rank = rank;
+  switch (mode) {
+    case TP_1D:
+      g->ndims = 1;
+      g->dims[0] = world;
+      g->q = world;
+      g->d = 1;
+      break;
+    case TP_2D: {
+      const int j = iroot(world, 2);
+      if (j < 0) return fail(TP_ERR_CONSTRAINT, "2D needs p = j^2, got " + std::to_string(world));
+      if (q > 0 && q != j) return fail(TP_ERR_CONSTRAINT, "2D: q*q != world");
+      g->ndims = 2;
+      g->dims[0] = g->dims[1] = j;
+      g->q = j;
+      g->d = 1;
+      break;
+    }
+    case TP_2P5D: {
+      if (d < 1 || world % d)
+        return fail(TP_ERR_CONSTRAINT, "2.5D needs p = d*k^2 (p=" + std::to_string(world) +
+                                           ", d=" + std::to_string(d) + ")");
+      const int k = iroot(world / d, 2);
+      if (k < 0)
+        return fail(TP_ERR_CONSTRAINT, "2.5D needs p = d*k^2 (p=" + std::to_string(world) +
+                                           ", d=" + std::to_string(d) + ")");
+      if (q > 0 && q != k) return fail(TP_ERR_CONSTRAINT, "2.5D: d*q*q != world");
+      g->ndims = 3;
+      g->dims[0] = d;
+      g->dims[1] = g->dims[2] = k;
+      g->q = k;
+      g->d = d;
+      break;
+    }
+    case TP_3D: {
+      const int l = iroot(world, 3);
+      if (l < 0) return fail(TP_ERR_CONSTRAINT, "3D needs p = l^3, got " + std::to_string(world));
+      if (q > 0 && q != l) return fail(TP_ERR_CONSTRAINT, "3D: q^3 != world");
+      g->ndims = 3;
+      g->dims[0] = g->dims[1] = g->dims[2] = l;
+      g->q = l;
+      g->d = 1;
+      break;
+    }
+    default:
+      return fail(TP_ERR_ARG, "unknown mode");
+  }
+  int r = rank;
+  for (int k = g->ndims - 1; k >= 0; --k) {
+    g->coords[k] = r % g->dims[k];
+    r /= g->dims[k];
+  }
+  return TP_OK;
+}
+
+// Color of this rank's line along `ax`: the rank with that coordinate zeroed (unique per line).
+int line_color(const tp_grid* g, int ax) {
+  int c[3] = {g->coords[0], g->coords[1], g->coords[2]};
+  c[ax] = 0;
+  int r = 0;
+  for (int k = 0; k < g->ndims; ++k) r = r * g->dims[k] + c[k];
+  return r;
+}
+
+tp_status check_desc(const tp_grid* g, const tp_linear_desc* d) {
+  if (!g) return fail(TP_ERR_ARG, "grid is null");
+  if (!d) return fail(TP_ERR_ARG, "desc is null");
+  if (d->dtype != TP_BF16 && d->dtype != TP_FP32) return fail(TP_ERR_ARG, "unknown dtype");
+  return check_divisible(g, d);
+}
+
+tp_status plan_sizes(tp_grid* g, const tp_linear_desc* d, size_t* ws, size_t* saved) {
+  Run R;
+  R.g = g;
+  R.d = d;
+  R.plan = true;
+  TP_TRY(sched_fwd(R, nullptr, nullptr, nullptr, nullptr));
+  size_t wf = R.ws.off, sf = R.saved.off;
+  Run B;
+  B.g = g;
+  B.d = d;
+  B.plan = true;
+  // plan with every optional output present (the largest footprint)
+  char dummy;
+  TP_TRY(sched_bwd(B, nullptr, nullptr, nullptr, &dummy, &dummy, &dummy));
+  *ws = std::max(wf, B.ws.off);
+  *saved = sf;
+  return TP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tp_status_string(tp_status s) {
+  switch (s) {
+    case TP_OK: return "TP_OK";
+    case TP_ERR_CONSTRAINT: return "TP_ERR_CONSTRAINT";
+    case TP_ERR_INDIVISIBLE: return "TP_ERR_INDIVISIBLE";
+    case TP_ERR_SHAPE: return "TP_ERR_SHAPE";
+    case TP_ERR_ARG: return "TP_ERR_ARG";
+    case TP_ERR_CUDA: return "TP_ERR_CUDA";
+    case TP_ERR_NCCL: return "TP_ERR_NCCL";
+    case TP_ERR_WORKSPACE: return "TP_ERR_WORKSPACE";
+    case TP_ERR_UNSUPPORTED: return "TP_ERR_UNSUPPORTED";
+  }
+  return "TP_ERR_UNKNOWN";
+}
+
+const char* tp_last_error(void) { return t_err.c_str(); }
+
+const char* tp_version(void) { return "tp_b200 0.1 sm_100a"; }
+
+tp_status tp_get_unique_id(tp_transport transport, void* id128) {
+  if (!id128) return fail(TP_ERR_ARG, "id128 is null");
+  switch (transport) {
+    case TP_TRANSPORT_NCCL: return nccl_unique_id(id128);
+    case TP_TRANSPORT_LOCAL: return local_unique_id(id128);
+    case TP_TRANSPORT_NONE: std::memset(id128, 0, 128); return TP_OK;
+  }
+  return fail(TP_ERR_ARG, "unknown transport");
+}
+
+tp_status tp_grid_init(tp_grid** out, tp_mode mode, int world, int rank, int q, int d,
+                       int cuda_device, tp_transport transport, const void* id128) {
+  if (!out) return fail(TP_ERR_ARG, "grid out-pointer is null");
+  *out = nullptr;
+  if (mode != TP_2P5D) d = 1;
+  auto g = std::make_unique<tp_grid>();
+  TP_TRY(plan_grid(g.get(), mode, world, rank, q, d));
+  g->device = cuda_device;
+  g->transport = transport;
+  if (transport == TP_TRANSPORT_NONE) {
+    *out = g.release();
+    return TP_OK;
+  }
+  if (transport != TP_TRANSPORT_NCCL && transport != TP_TRANSPORT_LOCAL)
+    return fail(TP_ERR_ARG, "unknown transport");
+  if (!id128) return fail(TP_ERR_ARG, "id128 is null");
+  TP_CUDA(cudaSetDevice(cuda_device));
+  TP_CUDA(cudaStreamCreateWithFlags(&g->comm_stream, cudaStreamNonBlocking));
+  for (auto& e : g->events) TP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  tp_status st = TP_OK;
+  if (transport == TP_TRANSPORT_NCCL) {
+    g->nccl = nccl_world_create(world, rank, id128, &st);
+    if (st != TP_OK) return st;
+  }
+  for (int ax = 0; ax < g->ndims; ++ax) {
+    if (g->dims[ax] == 1) continue;
+    const int pos = g->coords[ax];
+    if (transport == TP_TRANSPORT_NCCL)
+      g->axis[ax] = make_nccl_comm(g->nccl, line_color(g.get(), ax), pos, g->dims[ax], pos, &st);
+    else
+      g->axis[ax] = make_local_comm(id128, world, g->group_members(ax), pos, cuda_device, &st);
+    if (st != TP_OK) {
+      tp_grid_destroy(g.release());
+      return st;
+    }
+  }
+  *out = g.release();
+  return TP_OK;
+}
+
+tp_status tp_grid_coords(const tp_grid* g, int coords[3]) {
+  if (!g || !coords) return fail(TP_ERR_ARG, "null argument");
+  for (int k = 0; k < 3; ++k) coords[k] = k < g->ndims ? g->coords[k] : 0;
+  return TP_OK;
+}
+
+tp_status tp_grid_dims(const tp_grid* g, int dims[3], int* ndims) {
+  if (!g || !dims || !ndims) return fail(TP_ERR_ARG, "null argument");
+  for (int k = 0; k < 3; ++k) dims[k] = k < g->ndims ? g->dims[k] : 1;
+  *ndims = g->ndims;
+  return TP_OK;
+}
+
+tp_status tp_grid_group(const tp_grid* g, int axis, int* members) {
+  if (!g || !members) return fail(TP_ERR_ARG, "null argument");
+  if (axis < 0 || axis >= g->ndims) return fail(TP_ERR_ARG, "axis out of range");
+  auto m = g->group_members(axis);
+  std::memcpy(members, m.data(), m.size() * sizeof(int));
+  return TP_OK;
+}
+
+tp_status tp_grid_destroy(tp_grid* g) {
+  if (!g) return TP_OK;
+  if (g->comm_stream) cudaStreamSynchronize(g->comm_stream);
+  for (auto& a : g->axis) a.reset();
+  if (g->nccl) nccl_world_destroy(g->nccl);
+  for (auto& e : g->events)
+    if (e) cudaEventDestroy(e);
+  if (g->comm_stream) cudaStreamDestroy(g->comm_stream);
+  delete g;
+  return TP_OK;
+}
+
+tp_status tp_shard_extent(const tp_grid* g, const tp_linear_desc* d, tp_tensor tensor,
+                          int64_t* row0, int64_t* rows, int64_t* col0, int64_t* cols) {
+  TP_TRY(check_desc(g, d));
+  if (!row0 || !rows || !col0 || !cols) return fail(TP_ERR_ARG, "null output");
+  Ext e;
+  TP_TRY(extent(g, d, tensor, &e));
+  *row0 = e.r0;
+  *rows = e.rows;
+  *col0 = e.c0;
+  *cols = e.cols;
+  return TP_OK;
+}
+
+tp_status tp_workspace_size(const tp_grid* g, const tp_linear_desc* d, size_t* ws_bytes,
+                            size_t* saved_bytes) {
+  TP_TRY(check_desc(g, d));
+  if (!ws_bytes || !saved_bytes) return fail(TP_ERR_ARG, "null output");
+  return plan_sizes(const_cast<tp_grid*>(g), d, ws_bytes, saved_bytes);
+}
+
+static tp_status ready_to_run(tp_grid* g, const tp_linear_desc* d, size_t ws_bytes, void* ws,
+                              const void* saved, size_t* need_saved) {
+  TP_TRY(check_desc(g, d));
+  if (g->world > 1 && g->transport == TP_TRANSPORT_NONE)
+    return fail(TP_ERR_ARG, "transport NONE can only compute when world == 1");
+  size_t need_ws = 0;
+  TP_TRY(plan_sizes(g, d, &need_ws, need_saved));
+  if (ws_bytes < need_ws || (need_ws && !ws))
+    return fail(TP_ERR_WORKSPACE, "ws_bytes " + std::to_string(ws_bytes) + " < required " +
+                                      std::to_string(need_ws));
+  if (*need_saved && !saved) return fail(TP_ERR_WORKSPACE, "saved buffer required");
+  return TP_OK;
+}
+
+static void begin_run(Run& R, tp_grid* g, const tp_linear_desc* d, void* ws, void* saved,
+                      cudaStream_t s) {
+  R.g = g;
+  R.d = d;
+  R.s = s;
+  const bool serial = (d->flags & TP_FLAG_SERIAL) || !g->comm_stream;
+  R.cs = serial ? s : g->comm_stream;
+  R.ws.base = static_cast<char*>(ws);
+  R.saved.base = static_cast<char*>(saved);
+}
+
+tp_status tp_linear_fwd(tp_grid* g, const tp_linear_desc* d, const void* x, const void* w,
+                        const void* bias, void* y, void* saved, void* ws, size_t ws_bytes,
+                        void* stream) {
+  size_t need_saved = 0;
+  TP_TRY(ready_to_run(g, d, ws_bytes, ws, saved, &need_saved));
+  if ((d->M && d->K && !x) || (d->K && d->N && !w) || (d->M && d->N && !y))
+    return fail(TP_ERR_ARG, "null shard pointer");
+  TP_CUDA(cudaSetDevice(g->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Run R;
+  begin_run(R, g, d, ws, saved, s);
+  if (R.cs != s) {
+    cudaEvent_t e = g->ev();
+    TP_CUDA(cudaEventRecord(e, s));
+    TP_CUDA(cudaStreamWaitEvent(R.cs, e, 0));
+  }
+  tp_status st = sched_fwd(R, x, w, bias, y);
+  if (R.cs != s) {
+    cudaEvent_t e = g->ev();
+    cudaEventRecord(e, R.cs);
+    cudaStreamWaitEvent(s, e, 0);
+  }
+  return st;
+}
+
+tp_status tp_linear_bwd(tp_grid* g, const tp_linear_desc* d, const void* dy, const void* x,
+                        const void* w, const void* saved, void* dx, void* dw, void* dbias, void* ws,
+                        size_t ws_bytes, void* stream) {
+  size_t need_saved = 0;
+  TP_TRY(ready_to_run(g, d, ws_bytes, ws, saved, &need_saved));
+  if ((d->M && d->N && !dy) || (d->K && d->N && !dw) || (d->M && d->K && !x) ||
+      (d->K && d->N && !w))
+    return fail(TP_ERR_ARG, "null shard pointer");
+  TP_CUDA(cudaSetDevice(g->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Run R;
+  begin_run(R, g, d, ws, const_cast<void*>(saved), s);
+  if (R.cs != s) {
+    cudaEvent_t e = g->ev();
+    TP_CUDA(cudaEventRecord(e, s));
+    TP_CUDA(cudaStreamWaitEvent(R.cs, e, 0));
+  }
+  tp_status st = sched_bwd(R, dy, x, w, dx, dw, dbias);
+  if (R.cs != s) {
+    cudaEvent_t e = g->ev();
+    cudaEventRecord(e, R.cs);
+    cudaStreamWaitEvent(s, e, 0);
+  }
+  return st;
+}
+
+static tp_status pack_common(const tp_grid* g, const tp_linear_desc* d, tp_tensor t, bool pack,
+                             const void* src, void* dst, void* stream) {
+  TP_TRY(check_desc(g, d));
+  Ext e;
+  TP_TRY(extent(g, d, t, &e));
+  if (e.rows * e.cols == 0) return TP_OK;
+  if (!src || !dst) return fail(TP_ERR_ARG, "null pointer");
+  const int64_t gcols = (t == TP_TENSOR_X) ? d->K : d->N;
+  const size_t esz = dtype_size(d->dtype);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (g->transport != TP_TRANSPORT_NONE) TP_CUDA(cudaSetDevice(g->device));
+  if (pack) {
+    const char* base = static_cast<const char*>(src) + (e.r0 * gcols + e.c0) * esz;
+    return launch_copy2d(base, gcols, dst, e.cols, e.rows, e.cols, esz, s);
+  }
+  char* base = static_cast<char*>(dst) + (e.r0 * gcols + e.c0) * esz;
+  return launch_copy2d(src, e.cols, base, gcols, e.rows, e.cols, esz, s);
+}
+
+tp_status tp_pack(const tp_grid* g, const tp_linear_desc* d, tp_tensor t, const void* global,
+                  void* shard, void* stream) {
+  return pack_common(g, d, t, true, global, shard, stream);
+}
+
+tp_status tp_unpack(const tp_grid* g, const tp_linear_desc* d, tp_tensor t, const void* shard,
+                    void* global, void* stream) {
+  return pack_common(g, d, t, false, shard, global, stream);
+}
+
+tp_status tp_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, tp_dtype in_dtype,
+                  const void* A, int64_t lda, const void* B, int64_t ldb, const float* C,
+                  int64_t ldc, void* D, int64_t ldd, tp_dtype out_dtype, float alpha,
+                  const void* bias, void* stream) {
+  if (in_dtype != TP_BF16 && in_dtype != TP_FP32) return fail(TP_ERR_ARG, "in_dtype");
+  if (out_dtype != TP_BF16 && out_dtype != TP_FP32) return fail(TP_ERR_ARG, "out_dtype");
+  GemmArgs a;
+  a.M = M;
+  a.N = N;
+  a.K = K;
+  a.A = A;
+  a.lda = lda;
+  a.trans_a = trans_a != 0;
+  a.B = B;
+  a.ldb = ldb;
+  a.trans_b = trans_b != 0;
+  a.C = C;
+  a.ldc = ldc;
+  a.D = D;
+  a.ldd = ldd;
+  a.in_dtype = in_dtype;
+  a.out_dtype = out_dtype;
+  a.alpha = alpha;
+  a.bias = bias;
+  return gemm(a, static_cast<cudaStream_t>(stream));
+}
+
+tp_status tp_colsum(const void* src, int64_t rows, int64_t cols, int64_t ld, tp_dtype dtype,
+                    void* dst, void* stream) {
+  if (rows < 0 || cols < 0 || ld < cols) return fail(TP_ERR_SHAPE, "colsum shape");
+  if (!dst || (rows && cols && !src)) return fail(TP_ERR_ARG, "null pointer");
+  // fp32 scratch: a small, cached per-thread device buffer
+  thread_local float* scratch = nullptr;
+  thread_local int64_t cap = 0;
+  if (cap < cols) {
+    if (scratch) cudaFree(scratch);
+    TP_CUDA(cudaMalloc(&scratch, std::max<int64_t>(cols, 1024) * sizeof(float)));
+    cap = std::max<int64_t>(cols, 1024);
+  }
+  return launch_colsum(src, rows, cols, ld, dtype, dst, scratch, static_cast<cudaStream_t>(stream));
+}
+
+tp_status tp_fill(void* dst, tp_dtype dtype, int64_t rows, int64_t cols, int64_t ld, uint64_t seed,
+                  int tensor_id, int kind, float scale, int64_t g_row0, int64_t g_col0,
+                  int64_t g_cols, void* stream) {
+  if (rows < 0 || cols < 0 || ld < cols) return fail(TP_ERR_SHAPE, "fill shape");
+  if (!dst && rows && cols) return fail(TP_ERR_ARG, "null pointer");
+  if (kind != 0 && kind != 1) return fail(TP_ERR_ARG, "kind must be 0 (uniform) or 1 (ternary)");
+  if (g_col0 + cols > g_cols) return fail(TP_ERR_SHAPE, "block exceeds global columns");
+  return launch_fill(dst, dtype, rows, cols, ld, seed, tensor_id, kind, scale, g_row0, g_col0,
+                     g_cols, static_cast<cudaStream_t>(stream));
+}
+
+tp_status tp_l2_flush(void* scratch, size_t bytes, void* stream) {
+  if (!scratch) return fail(TP_ERR_ARG, "null pointer");
+  TP_CUDA(cudaMemsetAsync(scratch, static_cast<int>(g_launches.load() & 0xFF), bytes,
+                          static_cast<cudaStream_t>(stream)));
+  return TP_OK;
+}
+
+tp_status tp_prof_enable(int on) {
+  g_prof_on.store(on != 0);
+  return TP_OK;
+}
+
+tp_status tp_prof_reset(void) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  for (auto& r : g_prof) {
+    cudaEventSynchronize(r.b);
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  g_prof.clear();
+  return TP_OK;
+}
+
+tp_status tp_prof_read(int cls, double* total_ms, int64_t* launches, double* flops) {
+  if (!total_ms || !launches || !flops) return fail(TP_ERR_ARG, "null output");
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  double ms = 0, fl = 0;
+  int64_t n = 0;
+  for (auto& r : g_prof) {
+    if (r.cls != cls) continue;
+    TP_CUDA(cudaEventSynchronize(r.b));
+    float e = 0;
+    TP_CUDA(cudaEventElapsedTime(&e, r.a, r.b));
+    ms += e;
+    fl += r.flops;
+    ++n;
+  }
+  *total_ms = ms;
+  *launches = n;
+  *flops = fl;
+  return TP_OK;
+}
+
+int64_t tp_launch_count(void) { return g_launches.load(); }
+
+}  // extern "C"

@@ -1,0 +1,155 @@
+// fp32-mode local GEMM ("3xTF32 ... or SIMT FFMA"): the correctness mode of
+// config C1 (BASELINE.json configs[0], batch 16 x hidden 64, fp32). Plain smem-tiled FFMA,
+// fp32 accumulate; relative error ~1e-7, inside the north star's 1e-5 bar that plain TF32
+// misses (reading A12). Also the GEMM dispatcher and the K == 0 epilogue.
+#include <cuda_bf16.h>
+
+#include "tp_internal.h"
+
+namespace tp {
+namespace {
+
+constexpr int TM = 64, TN = 64, TK = 16;
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(256) gemm_simt_kernel(int M, int N, int K, const float* __restrict__ A,
+                                                        int64_t lda, const float* __restrict__ B,
+                                                        int64_t ldb, const float* C, int64_t ldc,
+                                                        void* D, int64_t ldd, int out_bf16,
+                                                        float alpha, const float* __restrict__ bias) {
+  __shared__ float As[TK][TM + 4];
+  __shared__ float Bs[TK][TN + 4];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const int m0 = blockIdx.y * TM, n0 = blockIdx.x * TN;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += TK) {
+    for (int idx = threadIdx.x; idx < TM * TK; idx += 256) {
+      int mm, kk;
+      if (TA) { mm = idx % TM; kk = idx / TM; } else { kk = idx % TK; mm = idx / TK; }
+      const int gm = m0 + mm, gk = k0 + kk;
+      float v = 0.f;
+      if (gm < M && gk < K) v = TA ? A[int64_t(gk) * lda + gm] : A[int64_t(gm) * lda + gk];
+      As[kk][mm] = v;
+    }
+    for (int idx = threadIdx.x; idx < TN * TK; idx += 256) {
+      int nn, kk;
+      if (TB) { kk = idx % TK; nn = idx / TK; } else { nn = idx % TN; kk = idx / TN; }
+      const int gn = n0 + nn, gk = k0 + kk;
+      float v = 0.f;
+      if (gn < N && gk < K) v = TB ? B[int64_t(gn) * ldb + gk] : B[int64_t(gk) * ldb + gn];
+      Bs[kk][nn] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < TK; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int gm = m0 + ty * 4 + i;
+    if (gm >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int gn = n0 + tx * 4 + j;
+      if (gn >= N) continue;
+      float x = acc[i][j];
+      if (C) x += C[int64_t(gm) * ldc + gn];
+      x *= alpha;
+      if (bias) x += bias[gn];
+      if (out_bf16)
+        reinterpret_cast<__nv_bfloat16*>(D)[int64_t(gm) * ldd + gn] = __float2bfloat16_rn(x);
+      else
+        reinterpret_cast<float*>(D)[int64_t(gm) * ldd + gn] = x;
+    }
+  }
+}
+
+__global__ void gemm_k0_kernel(int64_t M, int64_t N, const float* C, int64_t ldc, void* D,
+                               int64_t ldd, int out_bf16, float alpha, const void* bias,
+                               int bias_bf16) {
+  const int64_t total = M * N;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = i / N, c = i % N;
+    float x = C ? C[r * ldc + c] : 0.f;
+    x *= alpha;
+    if (bias)
+      x += bias_bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(bias)[c])
+                     : reinterpret_cast<const float*>(bias)[c];
+    if (out_bf16)
+      reinterpret_cast<__nv_bfloat16*>(D)[r * ldd + c] = __float2bfloat16_rn(x);
+    else
+      reinterpret_cast<float*>(D)[r * ldd + c] = x;
+  }
+}
+
+}  // namespace
+
+tp_status gemm_simt_f32(const GemmArgs& g, cudaStream_t s) {
+  dim3 grid(static_cast<unsigned>((g.N + TN - 1) / TN), static_cast<unsigned>((g.M + TM - 1) / TM));
+  if (grid.y > 65535) return fail(TP_ERR_UNSUPPORTED, "fp32 GEMM: M too large for SIMT grid");
+  const float* A = static_cast<const float*>(g.A);
+  const float* B = static_cast<const float*>(g.B);
+  const float* bias = static_cast<const float*>(g.bias);
+  const int ob = g.out_dtype == TP_BF16;
+  const int M = int(g.M), N = int(g.N), K = int(g.K);
+  const int tok = prof_begin(1, s, 2.0 * double(g.M) * double(g.N) * double(g.K));
+  if (!g.trans_a && !g.trans_b)
+    gemm_simt_kernel<false, false><<<grid, 256, 0, s>>>(M, N, K, A, g.lda, B, g.ldb, g.C, g.ldc, g.D, g.ldd, ob, g.alpha, bias);
+  else if (!g.trans_a && g.trans_b)
+    gemm_simt_kernel<false, true><<<grid, 256, 0, s>>>(M, N, K, A, g.lda, B, g.ldb, g.C, g.ldc, g.D, g.ldd, ob, g.alpha, bias);
+  else if (g.trans_a && !g.trans_b)
+    gemm_simt_kernel<true, false><<<grid, 256, 0, s>>>(M, N, K, A, g.lda, B, g.ldb, g.C, g.ldc, g.D, g.ldd, ob, g.alpha, bias);
+  else
+    gemm_simt_kernel<true, true><<<grid, 256, 0, s>>>(M, N, K, A, g.lda, B, g.ldb, g.C, g.ldc, g.D, g.ldd, ob, g.alpha, bias);
+  count_launch();
+  prof_end(tok, s);
+  TP_CUDA(cudaGetLastError());
+  return TP_OK;
+}
+
+tp_status gemm_k0(const GemmArgs& g, cudaStream_t s) {
+  const int64_t total = g.M * g.N;
+  if (total == 0) return TP_OK;
+  const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 4096));
+  gemm_k0_kernel<<<blocks, 256, 0, s>>>(g.M, g.N, g.C, g.ldc, g.D, g.ldd, g.out_dtype == TP_BF16,
+                                        g.alpha, g.bias, g.in_dtype == TP_BF16);
+  count_launch();
+  TP_CUDA(cudaGetLastError());
+  return TP_OK;
+}
+
+tp_status gemm(const GemmArgs& g, cudaStream_t s) {
+  if (g.M < 0 || g.N < 0 || g.K < 0) return fail(TP_ERR_SHAPE, "gemm: negative dim");
+  if (g.M == 0 || g.N == 0) return TP_OK;
+  if (!g.D) return fail(TP_ERR_ARG, "gemm: D is null");
+  const int64_t need_ldd = g.N;
+  if (g.ldd < need_ldd) return fail(TP_ERR_SHAPE, "gemm: ldd < N");
+  if (g.C && g.ldc < g.N) return fail(TP_ERR_SHAPE, "gemm: ldc < N");
+  if (g.K == 0) return gemm_k0(g, s);
+  if (!g.A || !g.B) return fail(TP_ERR_ARG, "gemm: A or B is null");
+  if (g.lda < (g.trans_a ? g.M : g.K)) return fail(TP_ERR_SHAPE, "gemm: lda too small");
+  if (g.ldb < (g.trans_b ? g.K : g.N)) return fail(TP_ERR_SHAPE, "gemm: ldb too small");
+  if (g.M > INT32_MAX || g.N > INT32_MAX || g.K > INT32_MAX)
+    return fail(TP_ERR_UNSUPPORTED, "gemm: dims must fit int32");
+  if (g.in_dtype == TP_FP32) return gemm_simt_f32(g, s);
+  // TMA: 16-byte aligned bases and row strides (bf16: multiples of 8 elements)
+  if ((reinterpret_cast<uintptr_t>(g.A) % 16) || (reinterpret_cast<uintptr_t>(g.B) % 16) ||
+      (g.lda % 8) || (g.ldb % 8))
+    return fail(TP_ERR_SHAPE,
+                "gemm(bf16): TMA needs 16-byte aligned A/B and row strides that are multiples "
+                "of 8 elements (lda=" + std::to_string(g.lda) + ", ldb=" + std::to_string(g.ldb) + ")");
+  return gemm_tc_bf16(g, s);
+}
+
+}  // namespace tp

@@ -1,0 +1,233 @@
+// HBM-bound helper kernels: shard pack/unpack, bias-gradient column sums
+// (a-12), the seeded input generator, and the n-way sum used by the in-process transport.
+// Plain coalesced CUDA with 16-byte vector accesses where alignment allows; grids are sized
+// in multiples of the SM count (grid-stride loops).
+#include <cuda_bf16.h>
+
+#include "tp_internal.h"
+
+namespace tp {
+namespace {
+
+int blocks_for(int64_t work, int per_block) {
+  int64_t b = (work + per_block - 1) / per_block;
+  const int64_t cap = 148 * 8;
+  if (b > cap) b = cap;
+  return b < 1 ? 1 : static_cast<int>(b);
+}
+
+// ---- 2-D strided copy ----------------------------------------------------------------------
+__global__ void copy2d_vec16(const uint4* __restrict__ src, int64_t sld, uint4* __restrict__ dst,
+                             int64_t dld, int64_t rows, int64_t cols16) {
+  const int64_t total = rows * cols16;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = i / cols16, c = i % cols16;
+    dst[r * dld + c] = src[r * sld + c];
+  }
+}
+
+template <typename T>
+__global__ void copy2d_scalar(const T* __restrict__ src, int64_t sld, T* __restrict__ dst,
+                              int64_t dld, int64_t rows, int64_t cols) {
+  const int64_t total = rows * cols;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = i / cols, c = i % cols;
+    dst[r * dld + c] = src[r * sld + c];
+  }
+}
+
+// ---- column sums: db = 1^T dY --------------------------------------------------------------
+// Block (x: 64 column pairs, y: row slab). Each thread sums a column pair over its slab in
+// fp32, then one atomicAdd per column into the fp32 scratch.
+template <typename T>
+__global__ void colsum_partial(const T* __restrict__ src, int64_t rows, int64_t cols, int64_t ld,
+                               int64_t rows_per_slab, float* __restrict__ acc) {
+  const int64_t c = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x);
+  if (c >= cols) return;
+  const int64_t r0 = blockIdx.y * rows_per_slab;
+  const int64_t r1 = min(rows, r0 + rows_per_slab);
+  float s = 0.f;
+  for (int64_t r = r0; r < r1; ++r) {
+    if constexpr (sizeof(T) == 2)
+      s += __bfloat162float(src[r * ld + c]);
+    else
+      s += src[r * ld + c];
+  }
+  atomicAdd(&acc[c], s);
+}
+
+template <typename T>
+__global__ void store_f32(const float* __restrict__ acc, T* __restrict__ dst, int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    if constexpr (sizeof(T) == 2)
+      dst[i] = __float2bfloat16_rn(acc[i]);
+    else
+      dst[i] = acc[i];
+  }
+}
+
+// ---- seeded generator (same counter-based SplitMix64 as synth/__init__.py) -----------------
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void fill_kernel(void* dst, int bf16, int64_t rows, int64_t cols, int64_t ld,
+                            uint64_t sseed, int kind, float scale, int64_t r0, int64_t c0,
+                            int64_t gcols) {
+  const int64_t total = rows * cols;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = i / cols, c = i % cols;
+    const uint64_t ctr = static_cast<uint64_t>(r0 + r) * static_cast<uint64_t>(gcols) +
+                         static_cast<uint64_t>(c0 + c);
+    const uint64_t z = mix64(sseed + (ctr + 1ull) * 0x9E3779B97F4A7C15ull);
+    float v;
+    if (kind == 0) {
+      const int64_t n = static_cast<int64_t>(z >> 40) - (1ll << 23);
+      v = __fmul_rn(static_cast<float>(n), 1.1920928955078125e-07f);  // 2^-23, exact
+      v = __fmul_rn(v, scale);
+    } else {
+      v = static_cast<float>(static_cast<int>((z >> 32) % 3ull)) - 1.0f;
+    }
+    if (bf16)
+      reinterpret_cast<__nv_bfloat16*>(dst)[r * ld + c] = __float2bfloat16_rn(v);
+    else
+      reinterpret_cast<float*>(dst)[r * ld + c] = v;
+  }
+}
+
+// ---- n-way sum (in-process transport reductions) -------------------------------------------
+struct Ptrs {
+  const void* p[16];
+};
+
+__global__ void sum_n_bf16(Ptrs in, int n, __nv_bfloat16* __restrict__ out, size_t count) {
+  const size_t pairs = count / 2;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < pairs;
+       i += size_t(gridDim.x) * blockDim.x) {
+    float2 s = make_float2(0.f, 0.f);
+    for (int j = 0; j < n; ++j) {
+      float2 f = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(in.p[j])[i]);
+      s.x += f.x;
+      s.y += f.y;
+    }
+    reinterpret_cast<__nv_bfloat162*>(out)[i] = __floats2bfloat162_rn(s.x, s.y);
+  }
+  if ((count & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    float s = 0.f;
+    for (int j = 0; j < n; ++j)
+      s += __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(in.p[j])[count - 1]);
+    out[count - 1] = __float2bfloat16_rn(s);
+  }
+}
+
+__global__ void sum_n_f32(Ptrs in, int n, float* __restrict__ out, size_t count) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < count;
+       i += size_t(gridDim.x) * blockDim.x) {
+    float s = 0.f;
+    for (int j = 0; j < n; ++j) s += reinterpret_cast<const float*>(in.p[j])[i];
+    out[i] = s;
+  }
+}
+
+}  // namespace
+
+tp_status launch_copy2d(const void* src, int64_t src_ld, void* dst, int64_t dst_ld, int64_t rows,
+                        int64_t cols, size_t esz, cudaStream_t s) {
+  if (rows <= 0 || cols <= 0) return TP_OK;
+  const size_t rb = cols * esz;
+  const bool vec = (reinterpret_cast<uintptr_t>(src) % 16 == 0) &&
+                   (reinterpret_cast<uintptr_t>(dst) % 16 == 0) && (rb % 16 == 0) &&
+                   ((src_ld * esz) % 16 == 0) && ((dst_ld * esz) % 16 == 0);
+  if (vec) {
+    const int64_t c16 = rb / 16;
+    copy2d_vec16<<<blocks_for(rows * c16, 256), 256, 0, s>>>(
+        static_cast<const uint4*>(src), src_ld * esz / 16, static_cast<uint4*>(dst),
+        dst_ld * esz / 16, rows, c16);
+  } else if (esz == 2) {
+    copy2d_scalar<uint16_t><<<blocks_for(rows * cols, 256), 256, 0, s>>>(
+        static_cast<const uint16_t*>(src), src_ld, static_cast<uint16_t*>(dst), dst_ld, rows, cols);
+  } else {
+    copy2d_scalar<uint32_t><<<blocks_for(rows * cols, 256), 256, 0, s>>>(
+        static_cast<const uint32_t*>(src), src_ld, static_cast<uint32_t*>(dst), dst_ld, rows, cols);
+  }
+  count_launch();
+  TP_CUDA(cudaGetLastError());
+  return TP_OK;
+}
+
+tp_status launch_colsum(const void* src, int64_t rows, int64_t cols, int64_t ld, tp_dtype dt,
+                        void* dst, float* scratch, cudaStream_t s) {
+  if (cols <= 0) return TP_OK;
+  TP_CUDA(cudaMemsetAsync(scratch, 0, cols * sizeof(float), s));
+  if (rows > 0) {
+    const int64_t colblocks = (cols + 127) / 128;
+    int64_t slabs = (148 * 4 + colblocks - 1) / colblocks;
+    if (slabs > rows) slabs = rows;
+    if (slabs < 1) slabs = 1;
+    if (slabs > 65535) slabs = 65535;
+    const int64_t per = (rows + slabs - 1) / slabs;
+    slabs = (rows + per - 1) / per;
+    dim3 grid(static_cast<unsigned>(colblocks), static_cast<unsigned>(slabs));
+    if (dt == TP_BF16)
+      colsum_partial<__nv_bfloat16><<<grid, 128, 0, s>>>(static_cast<const __nv_bfloat16*>(src),
+                                                         rows, cols, ld, per, scratch);
+    else
+      colsum_partial<float><<<grid, 128, 0, s>>>(static_cast<const float*>(src), rows, cols, ld,
+                                                 per, scratch);
+    count_launch();
+  }
+  if (dt == TP_BF16)
+    store_f32<__nv_bfloat16><<<blocks_for(cols, 256), 256, 0, s>>>(
+        scratch, static_cast<__nv_bfloat16*>(dst), cols);
+  else
+    store_f32<float><<<blocks_for(cols, 256), 256, 0, s>>>(scratch, static_cast<float*>(dst), cols);
+  count_launch();
+  TP_CUDA(cudaGetLastError());
+  return TP_OK;
+}
+
+tp_status launch_fill(void* dst, tp_dtype dt, int64_t rows, int64_t cols, int64_t ld, uint64_t seed,
+                      int tensor_id, int kind, float scale, int64_t r0, int64_t c0, int64_t gcols,
+                      cudaStream_t s) {
+  if (rows <= 0 || cols <= 0) return TP_OK;
+  // stream seed s_t = mix(seed + (tensor_id + 1) * GOLDEN)   (synth.stream_seed)
+  uint64_t z = seed + static_cast<uint64_t>(tensor_id + 1) * 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  const uint64_t sseed = z ^ (z >> 31);
+  fill_kernel<<<blocks_for(rows * cols, 256), 256, 0, s>>>(dst, dt == TP_BF16, rows, cols, ld, sseed,
+                                                           kind, scale, r0, c0, gcols);
+  count_launch();
+  TP_CUDA(cudaGetLastError());
+  return TP_OK;
+}
+
+tp_status launch_sum_n(const void* const* in, int n, void* out, size_t count, tp_dtype dt,
+                       cudaStream_t s) {
+  if (count == 0) return TP_OK;
+  if (n < 1 || n > 16) return fail(TP_ERR_UNSUPPORTED, "sum_n: 1..16 inputs");
+  Ptrs p{};
+  for (int i = 0; i < n; ++i) p.p[i] = in[i];
+  if (dt == TP_BF16)
+    sum_n_bf16<<<blocks_for(static_cast<int64_t>(count / 2 + 1), 256), 256, 0, s>>>(
+        p, n, static_cast<__nv_bfloat16*>(out), count);
+  else
+    sum_n_f32<<<blocks_for(static_cast<int64_t>(count), 256), 256, 0, s>>>(p, n, static_cast<float*>(out),
+                                                                           count);
+  count_launch();
+  TP_CUDA(cudaGetLastError());
+  return TP_OK;
+}
+
+tp_status launch_memset(void* dst, size_t bytes, cudaStream_t s) {
+  if (bytes) TP_CUDA(cudaMemsetAsync(dst, 0, bytes, s));
+  return TP_OK;
+}
+
+}  // namespace tp

@@ -1,0 +1,517 @@
+// Per-mode schedules of the tensor-parallel linear layer: which collective moves which shard,
+// which local GEMM runs where, on which stream, in which order (SURVEY 8(a) a-3 .. a-13).
+//
+// Streams and overlap (a-13): all compute runs on the caller's stream `s`; collectives run on
+// the grid's communication stream `cs`, ordered with events only (no host sync). SUMMA panels
+// are double-buffered: the broadcast for step t+2 is issued into the buffer step t has
+// finished with, so step t+1's transfer overlaps step t's GEMM; the reduce of step k's
+// partial overlaps step k+1's GEMM. In 3D the reduce-scatter of dX overlaps the dW GEMM.
+// Every collective's root uses its own shard in place (no staging copy).
+#include "sched.h"
+
+namespace tp {
+namespace {
+
+// ---- extents -----------------------------------------------------------------------------
+bool divides(int64_t a, int64_t b) { return b > 0 && a % b == 0; }
+
+struct Ctx {
+  Run& R;
+  tp_grid* g;
+  const tp_linear_desc* d;
+  tp_dtype dt;
+  size_t esz;
+  explicit Ctx(Run& r) : R(r), g(r.g), d(r.d), dt(r.d->dtype), esz(dtype_size(r.d->dtype)) {}
+
+  void* ws(size_t elems, size_t es = 0) { return R.ws.take(elems * (es ? es : esz)); }
+  void* sv(size_t elems) { return R.saved.take(elems * esz); }
+
+  cudaEvent_t record(cudaStream_t st) {
+    cudaEvent_t e = g->ev();
+    cudaEventRecord(e, st);
+    return e;
+  }
+  tp_status order(cudaStream_t from, cudaStream_t to) {  // `to` waits for work so far on `from`
+    if (from == to) return TP_OK;
+    TP_CUDA(cudaStreamWaitEvent(to, record(from), 0));
+    return TP_OK;
+  }
+  // D[M,N] = alpha * (op(A).op(B) + C) + bias
+  tp_status mm(int64_t M, int64_t N, int64_t K, const void* A, bool ta, const void* B, bool tb,
+               void* D, tp_dtype out, float alpha, const float* C, const void* bias) {
+    GemmArgs a;
+    a.M = M;
+    a.N = N;
+    a.K = K;
+    a.A = A;
+    a.trans_a = ta;
+    a.lda = ta ? M : K;
+    a.B = B;
+    a.trans_b = tb;
+    a.ldb = tb ? K : N;
+    a.C = C;
+    a.ldc = N;
+    a.D = D;
+    a.ldd = N;
+    a.in_dtype = dt;
+    a.out_dtype = out;
+    a.alpha = alpha;
+    a.bias = bias;
+    return gemm(a, R.s);
+  }
+  // column sums of a [rows, cols] shard into out (dtype dt); fp32 scratch from ws
+  tp_status colsum(const void* src, int64_t rows, int64_t cols, void* out, float* scratch) {
+    return launch_colsum(src, rows, cols, cols, dt, out, scratch, R.s);
+  }
+};
+
+}  // namespace
+
+tp_status check_divisible(const tp_grid* g, const tp_linear_desc* d) {
+  const int64_t M = d->M, K = d->K, N = d->N;
+  const int p = g->world, q = g->q, dd = g->d;
+  auto bad = [&](const char* what, int64_t a, int64_t b) {
+    return fail(TP_ERR_INDIVISIBLE, std::string(what) + "=" + std::to_string(a) +
+                                         " not divisible by " + std::to_string(b));
+  };
+  if (M < 0 || K < 0 || N < 0) return fail(TP_ERR_SHAPE, "negative dimension");
+  switch (g->mode) {
+    case TP_1D:
+      if (d->split_1d == 0 && !divides(N, p)) return bad("1D col: N", N, p);
+      if (d->split_1d == 1 && !divides(K, p)) return bad("1D row: K", K, p);
+      if (d->split_1d != 0 && d->split_1d != 1) return fail(TP_ERR_ARG, "split_1d must be 0 or 1");
+      break;
+    case TP_2D:
+      if (!divides(M, q)) return bad("M", M, q);
+      if (!divides(K, q)) return bad("K", K, q);
+      if (!divides(N, q)) return bad("N", N, q);
+      break;
+    case TP_2P5D: {
+      const bool sh = d->flags & TP_FLAG_W25_DEPTH_SHARDED;
+      if (!divides(M, int64_t(dd) * q)) return bad("M", M, int64_t(dd) * q);
+      if (!divides(N, q)) return bad("N", N, q);
+      if (!divides(K, sh ? int64_t(q) * dd : q)) return bad("K", K, sh ? int64_t(q) * dd : q);
+      break;
+    }
+    case TP_3D:
+      if (!divides(M, int64_t(q) * q)) return bad("M", M, int64_t(q) * q);
+      if (!divides(K, int64_t(q) * q)) return bad("K", K, int64_t(q) * q);
+      if (!divides(N, q)) return bad("N", N, q);
+      if (d->parity_3d != 0 && d->parity_3d != 1) return fail(TP_ERR_ARG, "parity_3d must be 0 or 1");
+      break;
+  }
+  return TP_OK;
+}
+
+tp_status extent(const tp_grid* g, const tp_linear_desc* d, int tensor, Ext* e) {
+  TP_TRY(check_divisible(g, d));
+  if (tensor < TP_TENSOR_X || tensor > TP_TENSOR_BIAS) return fail(TP_ERR_ARG, "unknown tensor");
+  const int64_t M = d->M, K = d->K, N = d->N;
+  const int64_t fr[4] = {M, K, M, 1}, fc[4] = {K, N, N, N};
+  auto set = [&](int64_t r0, int64_t rows, int64_t c0, int64_t cols) {
+    e->r0 = r0;
+    e->rows = rows;
+    e->c0 = c0;
+    e->cols = cols;
+    return TP_OK;
+  };
+  const int* c = g->coords;
+  switch (g->mode) {
+    case TP_1D: {
+      const int64_t r = c[0], p = g->world;
+      if (d->split_1d == 0) {
+        if (tensor == TP_TENSOR_X) return set(0, M, 0, K);
+        if (tensor == TP_TENSOR_W) return set(0, K, r * N / p, N / p);
+        if (tensor == TP_TENSOR_Y) return set(0, M, r * N / p, N / p);
+        return set(0, 1, r * N / p, N / p);
+      }
+      if (tensor == TP_TENSOR_X) return set(0, M, r * K / p, K / p);
+      if (tensor == TP_TENSOR_W) return set(r * K / p, K / p, 0, N);
+      return set(0, fr[tensor], 0, fc[tensor]);
+    }
+    case TP_2D: {
+      const int64_t i = c[0], j = c[1], q = g->q;
+      if (tensor == TP_TENSOR_X) return set(i * M / q, M / q, j * K / q, K / q);
+      if (tensor == TP_TENSOR_W) return set(i * K / q, K / q, j * N / q, N / q);
+      if (tensor == TP_TENSOR_Y) return set(i * M / q, M / q, j * N / q, N / q);
+      return set(0, 1, j * N / q, N / q);
+    }
+    case TP_2P5D: {
+      const int64_t dep = c[0], i = c[1], j = c[2], q = g->q, dd = g->d;
+      const int64_t mb = M / (dd * q);
+      if (tensor == TP_TENSOR_X) return set((dep * q + i) * mb, mb, j * K / q, K / q);
+      if (tensor == TP_TENSOR_W) {
+        if (d->flags & TP_FLAG_W25_DEPTH_SHARDED) {
+          const int64_t h = K / (q * dd);
+          return set(i * K / q + dep * h, h, j * N / q, N / q);
+        }
+        return set(i * K / q, K / q, j * N / q, N / q);
+      }
+      if (tensor == TP_TENSOR_Y) return set((dep * q + i) * mb, mb, j * N / q, N / q);
+      return set(0, 1, j * N / q, N / q);
+    }
+    case TP_3D: {
+      const int64_t l = g->q, a = c[0];
+      int64_t b = c[1], cc = c[2];
+      if (d->parity_3d == 1) std::swap(b, cc);  // parity 1: roles of axes b and c swap
+      const int64_t mb = M / (l * l), kb = K / (l * l);
+      if (tensor == TP_TENSOR_X) return set((a * l + cc) * mb, mb, b * K / l, K / l);
+      if (tensor == TP_TENSOR_W) return set((b * l + a) * kb, kb, cc * N / l, N / l);
+      if (tensor == TP_TENSOR_Y) return set((a * l + b) * mb, mb, cc * N / l, N / l);
+      return set(0, 1, cc * N / l, N / l);
+    }
+  }
+  return fail(TP_ERR_ARG, "bad mode");
+}
+
+namespace {
+
+// =========================================================================== 1D (a-3, a-4)
+tp_status fwd_1d(Ctx& C, const void* x, const void* w, const void* bias, void* y) {
+  const tp_linear_desc* d = C.d;
+  const int p = C.g->world, r = C.g->coords[0];
+  const int64_t M = d->M, K = d->K, N = d->N;
+  if (d->split_1d == 0) {  // column-parallel: Y_r = X.W_r, no communication
+    if (C.R.plan) return TP_OK;
+    return C.mm(M, N / p, K, x, false, w, false, y, C.dt, d->alpha, nullptr, bias);
+  }
+  // row-parallel: Y = AR_p(X_r.W_r); bias enters once, on rank 0's partial
+  const int64_t Kl = K / p;
+  void* P = p > 1 ? C.ws(M * N) : y;
+  if (C.R.plan) return TP_OK;
+  TP_TRY(C.mm(M, N, Kl, x, false, w, false, P, C.dt, d->alpha, nullptr, r == 0 ? bias : nullptr));
+  if (p > 1) {
+    TP_TRY(C.order(C.R.s, C.R.cs));
+    TP_TRY(C.g->axis[0]->allreduce(P, y, M * N, C.dt, C.R.cs));
+  }
+  return TP_OK;
+}
+
+tp_status bwd_1d(Ctx& C, const void* dy, const void* x, const void* w, void* dx, void* dw,
+                 void* dbias) {
+  const tp_linear_desc* d = C.d;
+  const int p = C.g->world;
+  const int64_t M = d->M, K = d->K, N = d->N;
+  if (d->split_1d == 0) {
+    const int64_t Nl = N / p;
+    void* P = (dx && p > 1) ? C.ws(M * K) : dx;
+    float* scratch = dbias ? static_cast<float*>(C.ws(Nl, 4)) : nullptr;
+    if (C.R.plan) return TP_OK;
+    if (dx) {  // dX = AR_p(dY_r . W_r^T): the column split's only collective
+      TP_TRY(C.mm(M, K, Nl, dy, false, w, true, P, C.dt, d->alpha, nullptr, nullptr));
+      if (p > 1) {
+        TP_TRY(C.order(C.R.s, C.R.cs));
+        TP_TRY(C.g->axis[0]->allreduce(P, dx, M * K, C.dt, C.R.cs));
+      }
+    }
+    // dW_r = X^T . dY_r overlaps the all-reduce
+    TP_TRY(C.mm(K, Nl, M, x, true, dy, false, dw, C.dt, d->alpha, nullptr, nullptr));
+    if (dbias) TP_TRY(C.colsum(dy, M, Nl, dbias, scratch));
+    return TP_OK;
+  }
+  const int64_t Kl = K / p;
+  float* scratch = dbias ? static_cast<float*>(C.ws(N, 4)) : nullptr;
+  if (C.R.plan) return TP_OK;
+  if (dx) TP_TRY(C.mm(M, Kl, N, dy, false, w, true, dx, C.dt, d->alpha, nullptr, nullptr));
+  TP_TRY(C.mm(Kl, N, M, x, true, dy, false, dw, C.dt, d->alpha, nullptr, nullptr));
+  if (dbias) TP_TRY(C.colsum(dy, M, N, dbias, scratch));
+  return TP_OK;
+}
+
+// =========================================================================== 2D / 2.5D
+struct Plane {
+  Comm* row;    // line along j (fixed i): X panels move here, dX partials reduce here
+  Comm* col;    // line along i (fixed j): W panels move here, dW partials reduce here
+  Comm* depth;  // 2.5D depth line (nullptr for 2D or d == 1)
+  int i, j, q, d;
+  int64_t mb, kq, nq;
+};
+
+Plane plane_of(Ctx& C) {
+  Plane P{};
+  const tp_grid* g = C.g;
+  P.q = g->q;
+  if (g->mode == TP_2D) {
+    P.i = g->coords[0];
+    P.j = g->coords[1];
+    P.col = g->axis[0].get();
+    P.row = g->axis[1].get();
+    P.depth = nullptr;
+    P.d = 1;
+  } else {
+    P.i = g->coords[1];
+    P.j = g->coords[2];
+    P.depth = g->axis[0].get();
+    P.col = g->axis[1].get();
+    P.row = g->axis[2].get();
+    P.d = g->d;
+  }
+  P.mb = C.d->M / (int64_t(P.d) * P.q);
+  P.kq = C.d->K / P.q;
+  P.nq = C.d->N / P.q;
+  return P;
+}
+
+// SUMMA "AB" (a-5): for t: bcast X[i,t] along row i, W[t,j] along column j; Y += X_t W_t.
+tp_status summa_ab(Ctx& C, const Plane& P, const void* x, const void* W, const void* bias, void* y) {
+  const float alpha = C.d->alpha;
+  if (P.q == 1) {
+    if (C.R.plan) return TP_OK;
+    return C.mm(P.mb, P.nq, P.kq, x, false, W, false, y, C.dt, alpha, nullptr, bias);
+  }
+  void* bx[2] = {C.ws(P.mb * P.kq), C.ws(P.mb * P.kq)};
+  void* bw[2] = {C.ws(P.kq * P.nq), C.ws(P.kq * P.nq)};
+  float* acc = static_cast<float*>(C.ws(P.mb * P.nq, 4));
+  if (C.R.plan) return TP_OK;
+  cudaEvent_t ready[2] = {};
+  auto xpan = [&](int t) { return P.j == t ? const_cast<void*>(x) : bx[t & 1]; };
+  auto wpan = [&](int t) { return P.i == t ? const_cast<void*>(W) : bw[t & 1]; };
+  auto issue = [&](int t) -> tp_status {
+    TP_TRY(P.row->group_start());
+    TP_TRY(P.row->bcast(xpan(t), P.mb * P.kq, C.dt, t, C.R.cs));
+    TP_TRY(P.col->bcast(wpan(t), P.kq * P.nq, C.dt, t, C.R.cs));
+    TP_TRY(P.row->group_end());
+    ready[t & 1] = C.record(C.R.cs);
+    return TP_OK;
+  };
+  TP_TRY(issue(0));
+  TP_TRY(issue(1));
+  for (int t = 0; t < P.q; ++t) {
+    TP_CUDA(cudaStreamWaitEvent(C.R.s, ready[t & 1], 0));
+    const bool last = t == P.q - 1;
+    TP_TRY(C.mm(P.mb, P.nq, P.kq, xpan(t), false, wpan(t), false, last ? y : acc,
+                last ? C.dt : TP_FP32, last ? alpha : 1.f, t > 0 ? acc : nullptr,
+                last ? bias : nullptr));
+    if (t + 2 < P.q) {
+      TP_TRY(C.order(C.R.s, C.R.cs));  // panel buffers of step t are free again
+      TP_TRY(issue(t + 2));
+    }
+  }
+  return TP_OK;
+}
+
+// SUMMA "ABT" (a-6): dX[i,k] = reduce_row( dY[i,j] . W[k,j]^T ), W panels down the columns.
+tp_status summa_abt(Ctx& C, const Plane& P, const void* dy, const void* W, void* dx) {
+  const float alpha = C.d->alpha;
+  if (P.q == 1) {
+    if (C.R.plan) return TP_OK;
+    return C.mm(P.mb, P.kq, P.nq, dy, false, W, true, dx, C.dt, alpha, nullptr, nullptr);
+  }
+  void* bw[2] = {C.ws(P.kq * P.nq), C.ws(P.kq * P.nq)};
+  void* bp[2] = {C.ws(P.mb * P.kq), C.ws(P.mb * P.kq)};
+  if (C.R.plan) return TP_OK;
+  cudaEvent_t ready[2] = {};
+  auto wpan = [&](int k) { return P.i == k ? const_cast<void*>(W) : bw[k & 1]; };
+  auto issue = [&](int k) -> tp_status {
+    TP_TRY(P.col->bcast(wpan(k), P.kq * P.nq, C.dt, k, C.R.cs));
+    ready[k & 1] = C.record(C.R.cs);
+    return TP_OK;
+  };
+  TP_TRY(issue(0));
+  TP_TRY(issue(1));
+  for (int k = 0; k < P.q; ++k) {
+    TP_CUDA(cudaStreamWaitEvent(C.R.s, ready[k & 1], 0));
+    void* part = P.j == k ? dx : bp[k & 1];  // the root reduces in place into dX
+    TP_TRY(C.mm(P.mb, P.kq, P.nq, dy, false, wpan(k), true, part, C.dt, alpha, nullptr, nullptr));
+    TP_TRY(C.order(C.R.s, C.R.cs));
+    TP_TRY(P.row->reduce(part, dx, P.mb * P.kq, C.dt, k, C.R.cs));
+    if (k + 2 < P.q) TP_TRY(issue(k + 2));
+  }
+  return TP_OK;
+}
+
+// SUMMA "ATB" (a-7): dW[k,j] = reduce_col( X[i,k]^T . dY[i,j] ), X panels along the rows.
+tp_status summa_atb(Ctx& C, const Plane& P, const void* x, const void* dy, void* dwt) {
+  const float alpha = C.d->alpha;
+  if (P.q == 1) {
+    if (C.R.plan) return TP_OK;
+    return C.mm(P.kq, P.nq, P.mb, x, true, dy, false, dwt, C.dt, alpha, nullptr, nullptr);
+  }
+  void* bx[2] = {C.ws(P.mb * P.kq), C.ws(P.mb * P.kq)};
+  void* bp[2] = {C.ws(P.kq * P.nq), C.ws(P.kq * P.nq)};
+  if (C.R.plan) return TP_OK;
+  cudaEvent_t ready[2] = {};
+  auto xpan = [&](int k) { return P.j == k ? const_cast<void*>(x) : bx[k & 1]; };
+  auto issue = [&](int k) -> tp_status {
+    TP_TRY(P.row->bcast(xpan(k), P.mb * P.kq, C.dt, k, C.R.cs));
+    ready[k & 1] = C.record(C.R.cs);
+    return TP_OK;
+  };
+  TP_TRY(issue(0));
+  TP_TRY(issue(1));
+  for (int k = 0; k < P.q; ++k) {
+    TP_CUDA(cudaStreamWaitEvent(C.R.s, ready[k & 1], 0));
+    void* part = P.i == k ? dwt : bp[k & 1];
+    TP_TRY(C.mm(P.kq, P.nq, P.mb, xpan(k), true, dy, false, part, C.dt, alpha, nullptr, nullptr));
+    TP_TRY(C.order(C.R.s, C.R.cs));
+    TP_TRY(P.col->reduce(part, dwt, P.kq * P.nq, C.dt, k, C.R.cs));
+    if (k + 2 < P.q) TP_TRY(issue(k + 2));
+  }
+  return TP_OK;
+}
+
+tp_status fwd_2d(Ctx& C, const void* x, const void* w, const void* bias, void* y) {
+  Plane P = plane_of(C);
+  const void* W = w;
+  if (C.g->mode == TP_2P5D && (C.d->flags & TP_FLAG_W25_DEPTH_SHARDED) && P.d > 1) {
+    // depth-sharded W: all-gather the depth pieces of W[i,j] (row-contiguous) into `saved`
+    void* Wfull = C.sv(P.kq * P.nq);
+    if (!C.R.plan) {
+      TP_TRY(P.depth->allgather(w, Wfull, (P.kq / P.d) * P.nq, C.dt, C.R.cs));
+      TP_TRY(C.order(C.R.cs, C.R.s));
+    }
+    W = Wfull;
+  }
+  return summa_ab(C, P, x, W, bias, y);
+}
+
+tp_status bwd_2d(Ctx& C, const void* dy, const void* x, const void* w, const void* saved, void* dx,
+                 void* dw, void* dbias) {
+  Plane P = plane_of(C);
+  const bool sharded = C.g->mode == TP_2P5D && (C.d->flags & TP_FLAG_W25_DEPTH_SHARDED) && P.d > 1;
+  const void* W = sharded ? saved : w;
+  const bool depth = P.d > 1;
+  void* dwt = depth ? C.ws(P.kq * P.nq) : dw;
+  float* scratch = dbias ? static_cast<float*>(C.ws(P.nq, 4)) : nullptr;
+  void* db_t[2] = {dbias ? C.ws(P.nq) : nullptr, dbias ? C.ws(P.nq) : nullptr};
+  // the two SUMMA chains carve separate buffers so both pipelines can stay in flight
+  if (dx) TP_TRY(summa_abt(C, P, dy, W, dx));
+  TP_TRY(summa_atb(C, P, x, dy, dwt));
+  if (C.R.plan) return TP_OK;
+  if (depth) {  // 2.5D: sum the planes' dW partials over depth (a-8)
+    TP_TRY(C.order(C.R.s, C.R.cs));
+    if (sharded)
+      TP_TRY(P.depth->reducescatter(dwt, dw, (P.kq / P.d) * P.nq, C.dt, C.R.cs));
+    else
+      TP_TRY(P.depth->allreduce(dwt, dw, P.kq * P.nq, C.dt, C.R.cs));
+  }
+  if (dbias) {  // db[j] = sum over the ranks holding column block j (a-12)
+    const bool need_col = P.q > 1, need_dep = depth;
+    void* first = (need_col || need_dep) ? db_t[0] : dbias;
+    TP_TRY(C.colsum(dy, P.mb, P.nq, first, scratch));
+    if (need_col || need_dep) {
+      TP_TRY(C.order(C.R.s, C.R.cs));
+      const void* cur = first;
+      if (need_col) {
+        void* dst = need_dep ? db_t[1] : dbias;
+        TP_TRY(P.col->allreduce(cur, dst, P.nq, C.dt, C.R.cs));
+        cur = dst;
+      }
+      if (need_dep) TP_TRY(P.depth->allreduce(cur, dbias, P.nq, C.dt, C.R.cs));
+    }
+  }
+  return TP_OK;
+}
+
+// =========================================================================== 3D (a-9, a-10)
+struct Cube {
+  Comm *cx, *cw, *cy;  // X-gather / W-gather / Y-scatter lines
+  int ys_coord;         // this rank's coordinate along the Y-scatter axis
+  int64_t l, mb, ml, kb, kl, nl;
+};
+
+Cube cube_of(Ctx& C) {
+  const tp_grid* g = C.g;
+  Cube Q{};
+  const int ax_x = C.d->parity_3d == 0 ? 2 : 1;  // parity 0: X over c, Y over b
+  const int ax_y = C.d->parity_3d == 0 ? 1 : 2;
+  Q.cx = g->axis[ax_x].get();
+  Q.cw = g->axis[0].get();
+  Q.cy = g->axis[ax_y].get();
+  Q.ys_coord = g->coords[ax_y];
+  Q.l = g->q;
+  Q.mb = C.d->M / (Q.l * Q.l);
+  Q.ml = C.d->M / Q.l;
+  Q.kb = C.d->K / (Q.l * Q.l);
+  Q.kl = C.d->K / Q.l;
+  Q.nl = C.d->N / Q.l;
+  return Q;
+}
+
+tp_status fwd_3d(Ctx& C, const void* x, const void* w, const void* bias, void* y) {
+  Cube Q = cube_of(C);
+  const float alpha = C.d->alpha;
+  if (Q.l == 1) {
+    if (C.R.plan) return TP_OK;
+    return C.mm(C.d->M, C.d->N, C.d->K, x, false, w, false, y, C.dt, alpha, nullptr, bias);
+  }
+  void* Xg = C.sv(Q.ml * Q.kl);  // X[a,b] [M/l, K/l], kept for backward
+  void* Wg = C.sv(Q.kl * Q.nl);  // W[b,c] [K/l, N/l]
+  void* P = C.ws(Q.ml * Q.nl);
+  if (C.R.plan) return TP_OK;
+  TP_TRY(Q.cx->group_start());
+  TP_TRY(Q.cx->allgather(x, Xg, Q.mb * Q.kl, C.dt, C.R.cs));
+  TP_TRY(Q.cw->allgather(w, Wg, Q.kb * Q.nl, C.dt, C.R.cs));
+  TP_TRY(Q.cx->group_end());
+  TP_TRY(C.order(C.R.cs, C.R.s));
+  TP_TRY(C.mm(Q.ml, Q.nl, Q.kl, Xg, false, Wg, false, P, C.dt, alpha, nullptr,
+              Q.ys_coord == 0 ? bias : nullptr));
+  TP_TRY(C.order(C.R.s, C.R.cs));
+  TP_TRY(Q.cy->reducescatter(P, y, Q.mb * Q.nl, C.dt, C.R.cs));
+  return TP_OK;
+}
+
+tp_status bwd_3d(Ctx& C, const void* dy, const void* x, const void* w, const void* saved, void* dx,
+                 void* dw, void* dbias) {
+  Cube Q = cube_of(C);
+  const float alpha = C.d->alpha;
+  if (Q.l == 1) {
+    float* scratch = dbias ? static_cast<float*>(C.ws(C.d->N, 4)) : nullptr;
+    if (C.R.plan) return TP_OK;
+    const int64_t M = C.d->M, K = C.d->K, N = C.d->N;
+    if (dx) TP_TRY(C.mm(M, K, N, dy, false, w, true, dx, C.dt, alpha, nullptr, nullptr));
+    TP_TRY(C.mm(K, N, M, x, true, dy, false, dw, C.dt, alpha, nullptr, nullptr));
+    if (dbias) TP_TRY(C.colsum(dy, M, N, dbias, scratch));
+    return TP_OK;
+  }
+  const char* sv = static_cast<const char*>(saved);
+  const void* Xg = sv;
+  const void* Wg = sv ? sv + (((Q.ml * Q.kl * C.esz) + 255) & ~size_t(255)) : nullptr;
+  void* dYg = C.ws(Q.ml * Q.nl);
+  void* Px = dx ? C.ws(Q.ml * Q.kl) : nullptr;
+  void* Pw = C.ws(Q.kl * Q.nl);
+  float* scratch = dbias ? static_cast<float*>(C.ws(Q.nl, 4)) : nullptr;
+  void* dbt = dbias ? C.ws(Q.nl) : nullptr;
+  if (C.R.plan) return TP_OK;
+  TP_TRY(Q.cy->allgather(dy, dYg, Q.mb * Q.nl, C.dt, C.R.cs));  // dY[a,c]
+  TP_TRY(C.order(C.R.cs, C.R.s));
+  if (dx) {
+    TP_TRY(C.mm(Q.ml, Q.kl, Q.nl, dYg, false, Wg, true, Px, C.dt, alpha, nullptr, nullptr));
+    TP_TRY(C.order(C.R.s, C.R.cs));
+    TP_TRY(Q.cx->reducescatter(Px, dx, Q.mb * Q.kl, C.dt, C.R.cs));  // overlaps the dW GEMM
+  }
+  TP_TRY(C.mm(Q.kl, Q.nl, Q.ml, Xg, true, dYg, false, Pw, C.dt, alpha, nullptr, nullptr));
+  if (dbias) TP_TRY(C.colsum(dYg, Q.ml, Q.nl, dbt, scratch));
+  TP_TRY(C.order(C.R.s, C.R.cs));
+  TP_TRY(Q.cw->reducescatter(Pw, dw, Q.kb * Q.nl, C.dt, C.R.cs));
+  if (dbias) TP_TRY(Q.cw->allreduce(dbt, dbias, Q.nl, C.dt, C.R.cs));
+  return TP_OK;
+}
+
+}  // namespace
+
+tp_status sched_fwd(Run& R, const void* x, const void* w, const void* bias, void* y) {
+  Ctx C(R);
+  switch (R.g->mode) {
+    case TP_1D: return fwd_1d(C, x, w, bias, y);
+    case TP_2D:
+    case TP_2P5D: return fwd_2d(C, x, w, bias, y);
+    case TP_3D: return fwd_3d(C, x, w, bias, y);
+  }
+  return fail(TP_ERR_ARG, "bad mode");
+}
+
+tp_status sched_bwd(Run& R, const void* dy, const void* x, const void* w, void* dx, void* dw,
+                    void* dbias) {
+  Ctx C(R);
+  const void* saved = R.saved.base;
+  switch (R.g->mode) {
+    case TP_1D: return bwd_1d(C, dy, x, w, dx, dw, dbias);
+    case TP_2D:
+    case TP_2P5D: return bwd_2d(C, dy, x, w, saved, dx, dw, dbias);
+    case TP_3D: return bwd_3d(C, dy, x, w, saved, dx, dw, dbias);
+  }
+  return fail(TP_ERR_ARG, "bad mode");
+}
+
+}  // namespace tp

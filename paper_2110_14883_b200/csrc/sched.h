@@ -1,0 +1,41 @@
+// Per-mode forward/backward schedules (SURVEY 8(a) rows a-3 .. a-10, a-13).
+#pragma once
+
+#include "tp_internal.h"
+
+namespace tp {
+
+struct Ext {
+  int64_t r0 = 0, rows = 0, c0 = 0, cols = 0;
+};
+
+// Divisibility (hard error, no padding) and the per-rank extents of SURVEY 8(a).
+tp_status check_divisible(const tp_grid* g, const tp_linear_desc* d);
+tp_status extent(const tp_grid* g, const tp_linear_desc* d, int tensor, Ext* e);
+
+// Bump allocator over the caller's workspace; with base == nullptr it only measures.
+struct Carver {
+  char* base = nullptr;
+  size_t off = 0;
+  void* take(size_t bytes) {
+    off = (off + 255) & ~size_t(255);
+    void* p = base ? base + off : nullptr;
+    off += bytes;
+    return p;
+  }
+};
+
+struct Run {
+  tp_grid* g = nullptr;
+  const tp_linear_desc* d = nullptr;
+  cudaStream_t s = nullptr;   // caller's stream: compute
+  cudaStream_t cs = nullptr;  // communication stream (== s when serial)
+  bool plan = false;          // carve only: nothing is enqueued
+  Carver ws, saved;
+};
+
+tp_status sched_fwd(Run& R, const void* x, const void* w, const void* bias, void* y);
+tp_status sched_bwd(Run& R, const void* dy, const void* x, const void* w, void* dx, void* dw,
+                    void* dbias);
+
+}  // namespace tp

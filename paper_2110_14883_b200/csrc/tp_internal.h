@@ -1,0 +1,137 @@
+// Internal declarations shared by the library's translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/tp_b200.h"
+
+namespace tp {
+
+// ---- errors ---------------------------------------------------------------------------
+void set_error(const std::string& msg);
+tp_status fail(tp_status s, const std::string& msg);
+
+#define TP_CUDA(call)                                                                   \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return ::tp::fail(TP_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define TP_TRY(call)               \
+  do {                             \
+    tp_status s_ = (call);         \
+    if (s_ != TP_OK) return s_;    \
+  } while (0)
+
+inline size_t dtype_size(tp_dtype t) { return t == TP_BF16 ? 2 : 4; }
+
+// ---- instrumentation ------------------------------------------------------------------
+extern std::atomic<int64_t> g_launches;
+inline void count_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+bool prof_on();
+// Opens a timed region for kernel class `cls` on `s`; returns a token for prof_end.
+int prof_begin(int cls, cudaStream_t s, double flops);
+void prof_end(int token, cudaStream_t s);
+
+// ---- kernels (layout.cu) ------------------------------------------------------------------
+tp_status launch_copy2d(const void* src, int64_t src_ld, void* dst, int64_t dst_ld, int64_t rows,
+                        int64_t cols, size_t esz, cudaStream_t s);
+tp_status launch_colsum(const void* src, int64_t rows, int64_t cols, int64_t ld, tp_dtype dt,
+                        void* dst, float* scratch, cudaStream_t s);
+tp_status launch_fill(void* dst, tp_dtype dt, int64_t rows, int64_t cols, int64_t ld,
+                      uint64_t seed, int tensor_id, int kind, float scale, int64_t r0, int64_t c0,
+                      int64_t gcols, cudaStream_t s);
+// out[i] = sum_{j<n} in[j][i] (ascending j), fp32 accumulate; n <= 16.
+tp_status launch_sum_n(const void* const* in, int n, void* out, size_t count, tp_dtype dt,
+                       cudaStream_t s);
+tp_status launch_memset(void* dst, size_t bytes, cudaStream_t s);
+
+// ---- GEMM (gemm_sm100.cu, gemm_simt.cu) --------------------------------------------------
+struct GemmArgs {
+  int64_t M = 0, N = 0, K = 0;
+  const void* A = nullptr;
+  int64_t lda = 0;
+  bool trans_a = false;  // A stored [K,M]
+  const void* B = nullptr;
+  int64_t ldb = 0;
+  bool trans_b = false;  // B stored [N,K]
+  const float* C = nullptr;
+  int64_t ldc = 0;
+  void* D = nullptr;
+  int64_t ldd = 0;
+  tp_dtype in_dtype = TP_BF16;
+  tp_dtype out_dtype = TP_BF16;
+  float alpha = 1.f;
+  const void* bias = nullptr;
+};
+tp_status gemm(const GemmArgs& a, cudaStream_t s);         // dispatch + validation
+tp_status gemm_tc_bf16(const GemmArgs& a, cudaStream_t s);  // tcgen05
+tp_status gemm_simt_f32(const GemmArgs& a, cudaStream_t s); // FFMA
+tp_status gemm_k0(const GemmArgs& a, cudaStream_t s);       // K == 0 epilogue only
+
+// ---- communication ------------------------------------------------------------------------
+// One communicator per grid line (group); `pos` is this rank's position in it.
+class Comm {
+ public:
+  virtual ~Comm() = default;
+  virtual int size() const = 0;
+  virtual int pos() const = 0;
+  // In place: at root `buf` is the source, elsewhere the destination.
+  virtual tp_status bcast(void* buf, size_t count, tp_dtype dt, int root, cudaStream_t s) = 0;
+  // recv (significant at root only) = sum over members of send.
+  virtual tp_status reduce(const void* send, void* recv, size_t count, tp_dtype dt, int root,
+                           cudaStream_t s) = 0;
+  virtual tp_status allreduce(const void* send, void* recv, size_t count, tp_dtype dt,
+                              cudaStream_t s) = 0;
+  // recv = concat over members (ascending) of send [count each].
+  virtual tp_status allgather(const void* send, void* recv, size_t count, tp_dtype dt,
+                              cudaStream_t s) = 0;
+  // recv [count] = slice `pos` of sum over members of send [size*count].
+  virtual tp_status reducescatter(const void* send, void* recv, size_t count, tp_dtype dt,
+                                  cudaStream_t s) = 0;
+  virtual tp_status group_start() { return TP_OK; }
+  virtual tp_status group_end() { return TP_OK; }
+};
+
+struct NcclWorld;  // transport_nccl.cpp
+std::unique_ptr<Comm> make_nccl_comm(NcclWorld* w, int color, int key, int size, int pos,
+                                     tp_status* st);
+NcclWorld* nccl_world_create(int world, int rank, const void* id128, tp_status* st);
+void nccl_world_destroy(NcclWorld* w);
+tp_status nccl_unique_id(void* id128);
+
+std::unique_ptr<Comm> make_local_comm(const void* id128, int world, const std::vector<int>& members,
+                                      int pos, int device, tp_status* st);
+tp_status local_unique_id(void* id128);
+
+}  // namespace tp
+
+// ---- the grid -----------------------------------------------------------------------------
+struct tp_grid {
+  tp_mode mode = TP_1D;
+  int world = 1, rank = 0, q = 1, d = 1;
+  int ndims = 1;
+  int dims[3] = {1, 1, 1};
+  int coords[3] = {0, 0, 0};
+  int device = 0;
+  tp_transport transport = TP_TRANSPORT_NONE;
+  tp::NcclWorld* nccl = nullptr;
+  std::unique_ptr<tp::Comm> axis[3];  // line along each axis (nullptr if size 1 or NONE)
+  cudaStream_t comm_stream = nullptr;
+  static constexpr int kEvents = 64;
+  cudaEvent_t events[kEvents] = {};
+  int next_event = 0;
+  cudaEvent_t ev() {  // round-robin event pool (timing disabled)
+    cudaEvent_t e = events[next_event];
+    next_event = (next_event + 1) % kEvents;
+    return e;
+  }
+  std::vector<int> group_members(int axis) const;
+};

@@ -1,0 +1,128 @@
+// NCCL transport: one communicator for the world (ncclCommInitRank on the caller-shared
+// unique id), one per grid line via ncclCommSplit ("only incur communication on a
+// sub-group"). On an NVSwitch B200 node every pair of GPUs has full NVLink 5 bandwidth, so
+// the row/column/depth communicators need no placement (contrast P:L155-157).
+#include <nccl.h>
+
+#include <cstring>
+
+#include "tp_internal.h"
+
+namespace tp {
+
+struct NcclWorld {
+  ncclComm_t world = nullptr;
+  int size = 0, rank = 0;
+};
+
+namespace {
+
+tp_status nccl_fail(ncclResult_t r, const char* what) {
+  return fail(TP_ERR_NCCL, std::string(what) + ": " + ncclGetErrorString(r));
+}
+
+#define TP_NCCL(call)                                \
+  do {                                               \
+    ncclResult_t r_ = (call);                        \
+    if (r_ != ncclSuccess) return nccl_fail(r_, #call); \
+  } while (0)
+
+ncclDataType_t nt(tp_dtype d) { return d == TP_BF16 ? ncclBfloat16 : ncclFloat32; }
+
+class NcclComm final : public Comm {
+ public:
+  NcclComm(ncclComm_t c, int size, int pos) : c_(c), size_(size), pos_(pos) {}
+  ~NcclComm() override {
+    if (c_) ncclCommDestroy(c_);
+  }
+  int size() const override { return size_; }
+  int pos() const override { return pos_; }
+  tp_status bcast(void* buf, size_t count, tp_dtype dt, int root, cudaStream_t s) override {
+    if (!count) return TP_OK;
+    TP_NCCL(ncclBroadcast(buf, buf, count, nt(dt), root, c_, s));
+    return TP_OK;
+  }
+  tp_status reduce(const void* send, void* recv, size_t count, tp_dtype dt, int root,
+                   cudaStream_t s) override {
+    if (!count) return TP_OK;
+    TP_NCCL(ncclReduce(send, recv, count, nt(dt), ncclSum, root, c_, s));
+    return TP_OK;
+  }
+  tp_status allreduce(const void* send, void* recv, size_t count, tp_dtype dt,
+                      cudaStream_t s) override {
+    if (!count) return TP_OK;
+    TP_NCCL(ncclAllReduce(send, recv, count, nt(dt), ncclSum, c_, s));
+    return TP_OK;
+  }
+  tp_status allgather(const void* send, void* recv, size_t count, tp_dtype dt,
+                      cudaStream_t s) override {
+    if (!count) return TP_OK;
+    TP_NCCL(ncclAllGather(send, recv, count, nt(dt), c_, s));
+    return TP_OK;
+  }
+  tp_status reducescatter(const void* send, void* recv, size_t count, tp_dtype dt,
+                          cudaStream_t s) override {
+    if (!count) return TP_OK;
+    TP_NCCL(ncclReduceScatter(send, recv, count, nt(dt), ncclSum, c_, s));
+    return TP_OK;
+  }
+  tp_status group_start() override {
+    TP_NCCL(ncclGroupStart());
+    return TP_OK;
+  }
+  tp_status group_end() override {
+    TP_NCCL(ncclGroupEnd());
+    return TP_OK;
+  }
+
+ private:
+  ncclComm_t c_;
+  int size_, pos_;
+};
+
+}  // namespace
+
+tp_status nccl_unique_id(void* id128) {
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  ncclUniqueId id;
+  TP_NCCL(ncclGetUniqueId(&id));
+  std::memcpy(id128, &id, sizeof(id));
+  return TP_OK;
+}
+
+NcclWorld* nccl_world_create(int world, int rank, const void* id128, tp_status* st) {
+  ncclUniqueId id;
+  std::memcpy(&id, id128, sizeof(id));
+  auto* w = new NcclWorld();
+  w->size = world;
+  w->rank = rank;
+  ncclResult_t r = ncclCommInitRank(&w->world, world, id, rank);
+  if (r != ncclSuccess) {
+    *st = nccl_fail(r, "ncclCommInitRank");
+    delete w;
+    return nullptr;
+  }
+  *st = TP_OK;
+  return w;
+}
+
+void nccl_world_destroy(NcclWorld* w) {
+  if (!w) return;
+  if (w->world) ncclCommDestroy(w->world);
+  delete w;
+}
+
+// Collective over the world communicator: every rank calls it once per axis.
+std::unique_ptr<Comm> make_nccl_comm(NcclWorld* w, int color, int key, int size, int pos,
+                                     tp_status* st) {
+  ncclComm_t c = nullptr;
+  ncclResult_t r = ncclCommSplit(w->world, color, key, &c, nullptr);
+  if (r != ncclSuccess) {
+    *st = nccl_fail(r, "ncclCommSplit");
+    return nullptr;
+  }
+  *st = TP_OK;
+  return std::make_unique<NcclComm>(c, size, pos);
+}
+
+}  // namespace tp

@@ -1,0 +1,177 @@
+"""Single-GPU parity of the library's kernels against the oracle / the shared generator.
+
+Tolerances: bf16 output rel-Frobenius <= 1e-2 (north star),
+fp32 output of bf16 operands <= 2e-5 (fp32 accumulation only), fp32 mode <= 1e-5;
+exact-integer inputs and every index / copy / generator path: bit-exact.
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import dense
+from oracle.grid import build_grid
+from oracle.shards import LayerSpec, extent as oextent
+
+from tp_harness import TORCH_DT, rel_fro, to_dev, to_np
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def api():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2110_14883_b200 import api
+    return api
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+@pytest.mark.parametrize("kind,scale", [("uniform", 0.0625), ("uniform", 0.37), ("ternary", 1.0)])
+def test_fill_bit_exact_vs_synth(api, dtype, kind, scale):
+    rows, cols, r0, c0, gcols = 37, 129, 5, 11, 200
+    ref = synth.tensor(42, 17, 64, gcols, kind, scale, dtype, row0=r0, nrows=rows, col0=c0, ncols=cols)
+    out = torch.empty(rows, cols + 3, device="cuda", dtype=TORCH_DT[dtype])
+    api.tp_fill(out, dtype, rows, cols, cols + 3, 42, 17, kind, scale, r0, c0, gcols)
+    torch.cuda.synchronize()
+    got = out[:, :cols].float().cpu().numpy()
+    assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("mode,p,d,kw", [
+    ("1d", 8, 1, dict(split_1d=0)), ("1d", 4, 1, dict(split_1d=1)), ("2d", 4, 1, {}),
+    ("2d", 9, 1, {}), ("2.5d", 8, 2, {}), ("2.5d", 8, 2, dict(flags=1)), ("3d", 8, 1, dict(parity_3d=1)),
+    ("3d", 27, 1, {})])
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_pack_unpack_bit_exact(api, mode, p, d, kw, dtype):
+    og = build_grid(mode, p, d)
+    unit = {"1d": p, "2d": og.q, "2.5d": og.q * og.d, "3d": og.q * og.q}[mode]
+    M, K, N = 3 * unit, 8 * unit, 5 * unit
+    spec = LayerSpec(M, K, N, split_1d="row" if kw.get("split_1d") == 1 else "col",
+                     parity=kw.get("parity_3d", 0), w_depth_sharded=bool(kw.get("flags", 0) & 1))
+    ds = api.desc(M, K, N, dtype, **kw)
+    for t, shp in (("X", (M, K)), ("W", (K, N)), ("Y", (M, N))):
+        G = torch.arange(np.prod(shp), device="cuda", dtype=torch.float32).reshape(shp)
+        G = (G % 251).to(TORCH_DT[dtype])          # exact in bf16
+        back = torch.full_like(G, -1)
+        for r in range(p):
+            g = api.tp_grid_init(mode, p, r, 0, d)
+            e = api.tp_shard_extent(g, ds, t)
+            sh = torch.empty(e[1], e[3], device="cuda", dtype=G.dtype)
+            api.tp_pack(g, ds, t, G, sh)
+            oe = oextent(og, spec, r, t)
+            ref = G[oe.row0:oe.row0 + oe.rows, oe.col0:oe.col0 + oe.cols]
+            torch.cuda.synchronize()
+            assert torch.equal(sh, ref)
+            api.tp_unpack(g, ds, t, sh, back)
+            api.tp_grid_destroy(g)
+        torch.cuda.synchronize()
+        assert torch.equal(back, G)
+
+
+def _gemm_case(api, ta, tb, M, N, K, in_dt, out_dt, seed, alpha=1.0, with_c=False, with_bias=False,
+               kind="uniform", pad=0):
+    A = synth.tensor(seed, 0, K if ta else M, M if ta else K, kind, 1.0, in_dt)
+    B = synth.tensor(seed, 1, N if tb else K, K if tb else N, kind, 0.5, in_dt)
+    Cm = synth.tensor(seed, 2, M, N, "uniform", 1.0, "fp32") if with_c else None
+    bias = synth.tensor(seed, 3, 1, N, "uniform", 1.0, in_dt)[0] if with_bias else None
+    lda = A.shape[1] + pad
+    ldb = B.shape[1] + pad
+    dA = torch.zeros(A.shape[0], lda, device="cuda", dtype=TORCH_DT[in_dt])
+    dA[:, :A.shape[1]] = to_dev(A, in_dt)
+    dB = torch.zeros(B.shape[0], ldb, device="cuda", dtype=TORCH_DT[in_dt])
+    dB[:, :B.shape[1]] = to_dev(B, in_dt)
+    dC = to_dev(Cm, "fp32") if with_c else None
+    db = to_dev(bias[None, :], in_dt)[0].contiguous() if with_bias else None
+    D = torch.full((M, N), float("nan"), device="cuda", dtype=TORCH_DT[out_dt])
+    api.tp_gemm(ta, tb, M, N, K, in_dt, dA, lda, dB, ldb, dC, N, D, N, out_dt, alpha, db)
+    torch.cuda.synchronize()
+    opA = A.T if ta else A
+    opB = B.T if tb else B
+    ref = dense.matmul(opA, opB)
+    if with_c:
+        ref = ref + Cm
+    ref = alpha * ref
+    if with_bias:
+        ref = ref + bias[None, :]
+    return to_np(D), ref
+
+
+@pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (200, 136, 72), (384, 520, 256), (16, 64, 32),
+                                   (1000, 1304, 328)])
+def test_gemm_bf16_vs_oracle(api, ta, tb, M, N, K):
+    got, ref = _gemm_case(api, ta, tb, M, N, K, "bf16", "fp32", seed=M + N + K)
+    assert rel_fro(got, ref) <= 2e-5
+    got, ref = _gemm_case(api, ta, tb, M, N, K, "bf16", "bf16", seed=M + N + K)
+    assert rel_fro(got, ref) <= 1e-2 and np.isfinite(got).all()
+
+
+@pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
+def test_gemm_bf16_exact_integer_bit_equal(api, ta, tb):
+    """Ternary operands, K <= 256: exact products and sums, bf16-exact outputs (|y| <= 256)."""
+    for (M, N, K) in [(128, 256, 256), (72, 40, 200), (304, 520, 136)]:
+        got, ref = _gemm_case(api, ta, tb, M, N, K, "bf16", "bf16", seed=7, kind="ternary")
+        assert np.array_equal(got, ref)
+        got, ref = _gemm_case(api, ta, tb, M, N, K, "bf16", "fp32", seed=8, kind="ternary")
+        assert np.array_equal(got, ref)
+
+
+def test_gemm_bf16_wide_tile_path(api):
+    """Enough 128x256 tiles to take the BN=256 persistent path (> #SMs tiles), multi-tile per CTA."""
+    for ta, tb in [(0, 0), (0, 1), (1, 0)]:
+        got, ref = _gemm_case(api, ta, tb, 2048, 4096, 512, "bf16", "fp32", seed=3)
+        assert rel_fro(got, ref) <= 2e-5
+
+
+@pytest.mark.parametrize("ta,tb", [(0, 0), (1, 1)])
+def test_gemm_epilogue_alpha_c_bias_and_padding(api, ta, tb):
+    got, ref = _gemm_case(api, ta, tb, 264, 200, 136, "bf16", "fp32", seed=5, alpha=0.75,
+                          with_c=True, with_bias=True, pad=8)
+    assert rel_fro(got, ref) <= 2e-5
+    got, ref = _gemm_case(api, ta, tb, 264, 200, 136, "bf16", "bf16", seed=5, alpha=-1.5,
+                          with_c=True, with_bias=True)
+    assert rel_fro(got, ref) <= 1e-2
+
+
+@pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("M,N,K", [(16, 64, 64), (67, 45, 33), (130, 70, 260)])
+def test_gemm_fp32_mode_vs_oracle(api, ta, tb, M, N, K):
+    got, ref = _gemm_case(api, ta, tb, M, N, K, "fp32", "fp32", seed=11, alpha=0.5, with_c=True,
+                          with_bias=True)
+    assert rel_fro(got, ref) <= 1e-5
+
+
+def test_gemm_degenerate_shapes(api):
+    # K == 0: D = alpha * C + bias ; M == 0 / N == 0: nothing
+    got, ref = _gemm_case(api, 0, 0, 32, 48, 0, "bf16", "fp32", seed=1, alpha=2.0, with_c=True,
+                          with_bias=True)
+    assert np.allclose(got, ref, rtol=1e-6, atol=1e-6)
+    D = torch.zeros(4, 4, device="cuda")
+    api.tp_gemm(0, 0, 0, 4, 8, "bf16", None, 8, None, 8, None, 4, D, 4, "fp32")
+    with pytest.raises(api.TPError) as e:     # TMA stride rule: lda must be a multiple of 8
+        A = torch.zeros(8, 12, device="cuda", dtype=torch.bfloat16)
+        api.tp_gemm(0, 0, 8, 8, 12, "bf16", A, 12, A, 8, None, 8, D, 8, "fp32")
+    assert e.value.status == 3
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_colsum_vs_oracle(api, dtype):
+    for rows, cols in [(1000, 136), (7, 3), (4096, 520)]:
+        Y = synth.tensor(9, 2, rows, cols, "uniform", 1.0, dtype)
+        out = torch.empty(cols, device="cuda", dtype=TORCH_DT[dtype])
+        api.tp_colsum(to_dev(Y, dtype), rows, cols, cols, dtype, out)
+        torch.cuda.synchronize()
+        ref = np.asarray(Y, np.float64).sum(axis=0)
+        assert rel_fro(to_np(out), ref) <= (1e-2 if dtype == "bf16" else 1e-5)
+
+
+def test_instrumentation_counts_launches_and_times_gemms(api):
+    api.tp_prof_reset()
+    api.tp_prof_enable(True)
+    n0 = api.tp_launch_count()
+    _gemm_case(api, 0, 0, 256, 256, 256, "bf16", "fp32", seed=2)
+    api.tp_prof_enable(False)
+    ms, n, fl = api.tp_prof_read(0)
+    assert n == 1 and ms > 0 and fl == 2.0 * 256 ** 3
+    assert api.tp_launch_count() - n0 >= 1
+    api.tp_prof_reset()
