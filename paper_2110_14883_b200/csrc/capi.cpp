@@ -446,7 +446,7 @@ tp_status tp_colsum(const void* src, int64_t rows, int64_t cols, int64_t ld, tp_
   thread_local int64_t cap = 0;
   if (cap < cols) {
     if (scratch) cudaFree(scratch);
-    TP_CUDA(cudaMalloc(&scratch, std::max<int64_t>(cols, 1024) * sizeof(float)));
+    TP_CUDA(cudaMalloc(&scratch, kColsumSlabs * std::max<int64_t>(cols, 1024) * sizeof(float)));
     cap = std::max<int64_t>(cols, 1024);
   }
   return launch_colsum(src, rows, cols, ld, dtype, dst, scratch, static_cast<cudaStream_t>(stream));

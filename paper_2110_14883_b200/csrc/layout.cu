@@ -39,11 +39,12 @@ __global__ void copy2d_scalar(const T* __restrict__ src, int64_t sld, T* __restr
 }
 
 // ---- column sums: db = 1^T dY --------------------------------------------------------------
-// Block (x: 64 column pairs, y: row slab). Each thread sums a column pair over its slab in
-// fp32, then one atomicAdd per column into the fp32 scratch.
+// Deterministic two-pass reduction (replicas of db on different ranks must be bit-equal):
+// pass 1, block (x: 128 columns, y: row slab) sums its slab per column in fp32 into
+// part[slab][col]; pass 2 sums the slabs in ascending order.
 template <typename T>
 __global__ void colsum_partial(const T* __restrict__ src, int64_t rows, int64_t cols, int64_t ld,
-                               int64_t rows_per_slab, float* __restrict__ acc) {
+                               int64_t rows_per_slab, float* __restrict__ part) {
   const int64_t c = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x);
   if (c >= cols) return;
   const int64_t r0 = blockIdx.y * rows_per_slab;
@@ -55,17 +56,20 @@ __global__ void colsum_partial(const T* __restrict__ src, int64_t rows, int64_t 
     else
       s += src[r * ld + c];
   }
-  atomicAdd(&acc[c], s);
+  part[blockIdx.y * cols + c] = s;
 }
 
 template <typename T>
-__global__ void store_f32(const float* __restrict__ acc, T* __restrict__ dst, int64_t n) {
+__global__ void colsum_final(const float* __restrict__ part, int slabs, T* __restrict__ dst,
+                             int64_t n) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
+    float s = 0.f;
+    for (int k = 0; k < slabs; ++k) s += part[k * n + i];
     if constexpr (sizeof(T) == 2)
-      dst[i] = __float2bfloat16_rn(acc[i]);
+      dst[i] = __float2bfloat16_rn(s);
     else
-      dst[i] = acc[i];
+      dst[i] = s;
   }
 }
 
@@ -164,13 +168,13 @@ tp_status launch_copy2d(const void* src, int64_t src_ld, void* dst, int64_t dst_
 tp_status launch_colsum(const void* src, int64_t rows, int64_t cols, int64_t ld, tp_dtype dt,
                         void* dst, float* scratch, cudaStream_t s) {
   if (cols <= 0) return TP_OK;
-  TP_CUDA(cudaMemsetAsync(scratch, 0, cols * sizeof(float), s));
+  int64_t slabs = 0;
   if (rows > 0) {
     const int64_t colblocks = (cols + 127) / 128;
-    int64_t slabs = (148 * 4 + colblocks - 1) / colblocks;
+    slabs = (148 * 4 + colblocks - 1) / colblocks;
     if (slabs > rows) slabs = rows;
     if (slabs < 1) slabs = 1;
-    if (slabs > 65535) slabs = 65535;
+    if (slabs > kColsumSlabs) slabs = kColsumSlabs;
     const int64_t per = (rows + slabs - 1) / slabs;
     slabs = (rows + per - 1) / per;
     dim3 grid(static_cast<unsigned>(colblocks), static_cast<unsigned>(slabs));
@@ -183,10 +187,11 @@ tp_status launch_colsum(const void* src, int64_t rows, int64_t cols, int64_t ld,
     count_launch();
   }
   if (dt == TP_BF16)
-    store_f32<__nv_bfloat16><<<blocks_for(cols, 256), 256, 0, s>>>(
-        scratch, static_cast<__nv_bfloat16*>(dst), cols);
+    colsum_final<__nv_bfloat16><<<blocks_for(cols, 256), 256, 0, s>>>(
+        scratch, static_cast<int>(slabs), static_cast<__nv_bfloat16*>(dst), cols);
   else
-    store_f32<float><<<blocks_for(cols, 256), 256, 0, s>>>(scratch, static_cast<float*>(dst), cols);
+    colsum_final<float><<<blocks_for(cols, 256), 256, 0, s>>>(scratch, static_cast<int>(slabs),
+                                                              static_cast<float*>(dst), cols);
   count_launch();
   TP_CUDA(cudaGetLastError());
   return TP_OK;

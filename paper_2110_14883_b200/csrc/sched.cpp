@@ -60,6 +60,7 @@ struct Ctx {
     return gemm(a, R.s);
   }
   // column sums of a [rows, cols] shard into out (dtype dt); fp32 scratch from ws
+  float* colsum_scratch(int64_t cols) { return static_cast<float*>(ws(size_t(kColsumSlabs) * cols, 4)); }
   tp_status colsum(const void* src, int64_t rows, int64_t cols, void* out, float* scratch) {
     return launch_colsum(src, rows, cols, cols, dt, out, scratch, R.s);
   }
@@ -195,7 +196,7 @@ tp_status bwd_1d(Ctx& C, const void* dy, const void* x, const void* w, void* dx,
   if (d->split_1d == 0) {
     const int64_t Nl = N / p;
     void* P = (dx && p > 1) ? C.ws(M * K) : dx;
-    float* scratch = dbias ? static_cast<float*>(C.ws(Nl, 4)) : nullptr;
+    float* scratch = dbias ? C.colsum_scratch(Nl) : nullptr;
     if (C.R.plan) return TP_OK;
     if (dx) {  // dX = AR_p(dY_r . W_r^T): the column split's only collective
       TP_TRY(C.mm(M, K, Nl, dy, false, w, true, P, C.dt, d->alpha, nullptr, nullptr));
@@ -210,7 +211,7 @@ tp_status bwd_1d(Ctx& C, const void* dy, const void* x, const void* w, void* dx,
     return TP_OK;
   }
   const int64_t Kl = K / p;
-  float* scratch = dbias ? static_cast<float*>(C.ws(N, 4)) : nullptr;
+  float* scratch = dbias ? C.colsum_scratch(N) : nullptr;
   if (C.R.plan) return TP_OK;
   if (dx) TP_TRY(C.mm(M, Kl, N, dy, false, w, true, dx, C.dt, d->alpha, nullptr, nullptr));
   TP_TRY(C.mm(Kl, N, M, x, true, dy, false, dw, C.dt, d->alpha, nullptr, nullptr));
@@ -372,7 +373,7 @@ tp_status bwd_2d(Ctx& C, const void* dy, const void* x, const void* w, const voi
   const void* W = sharded ? saved : w;
   const bool depth = P.d > 1;
   void* dwt = depth ? C.ws(P.kq * P.nq) : dw;
-  float* scratch = dbias ? static_cast<float*>(C.ws(P.nq, 4)) : nullptr;
+  float* scratch = dbias ? C.colsum_scratch(P.nq) : nullptr;
   void* db_t[2] = {dbias ? C.ws(P.nq) : nullptr, dbias ? C.ws(P.nq) : nullptr};
   // the two SUMMA chains carve separate buffers so both pipelines can stay in flight
   if (dx) TP_TRY(summa_abt(C, P, dy, W, dx));
@@ -456,7 +457,7 @@ tp_status bwd_3d(Ctx& C, const void* dy, const void* x, const void* w, const voi
   Cube Q = cube_of(C);
   const float alpha = C.d->alpha;
   if (Q.l == 1) {
-    float* scratch = dbias ? static_cast<float*>(C.ws(C.d->N, 4)) : nullptr;
+    float* scratch = dbias ? C.colsum_scratch(C.d->N) : nullptr;
     if (C.R.plan) return TP_OK;
     const int64_t M = C.d->M, K = C.d->K, N = C.d->N;
     if (dx) TP_TRY(C.mm(M, K, N, dy, false, w, true, dx, C.dt, alpha, nullptr, nullptr));
@@ -470,7 +471,7 @@ tp_status bwd_3d(Ctx& C, const void* dy, const void* x, const void* w, const voi
   void* dYg = C.ws(Q.ml * Q.nl);
   void* Px = dx ? C.ws(Q.ml * Q.kl) : nullptr;
   void* Pw = C.ws(Q.kl * Q.nl);
-  float* scratch = dbias ? static_cast<float*>(C.ws(Q.nl, 4)) : nullptr;
+  float* scratch = dbias ? C.colsum_scratch(Q.nl) : nullptr;
   void* dbt = dbias ? C.ws(Q.nl) : nullptr;
   if (C.R.plan) return TP_OK;
   TP_TRY(Q.cy->allgather(dy, dYg, Q.mb * Q.nl, C.dt, C.R.cs));  // dY[a,c]

@@ -43,6 +43,8 @@ void prof_end(int token, cudaStream_t s);
 // ---- kernels (layout.cu) ------------------------------------------------------------------
 tp_status launch_copy2d(const void* src, int64_t src_ld, void* dst, int64_t dst_ld, int64_t rows,
                         int64_t cols, size_t esz, cudaStream_t s);
+// Deterministic two-pass column sums; scratch holds kColsumSlabs * cols floats.
+constexpr int kColsumSlabs = 32;
 tp_status launch_colsum(const void* src, int64_t rows, int64_t cols, int64_t ld, tp_dtype dt,
                         void* dst, float* scratch, cudaStream_t s);
 tp_status launch_fill(void* dst, tp_dtype dt, int64_t rows, int64_t cols, int64_t ld,

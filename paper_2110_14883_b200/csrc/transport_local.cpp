@@ -98,6 +98,10 @@ class LocalComm final : public Comm {
     grp_ = get_group(id_, members_);
   }
   ~LocalComm() override {
+    // Destruction is collective (like ncclCommDestroy): a peer may still be enqueuing a
+    // wait on our `done` event from the last exchange, so nobody frees events before all
+    // members got here.
+    if (grp_) grp_->barrier();
     if (ready_) cudaEventDestroy(ready_);
     if (done_) cudaEventDestroy(done_);
     grp_.reset();
