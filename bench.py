@@ -139,10 +139,7 @@ def run_ours(a):
     tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
 
     if world > 1:
-        uid = api.tp_get_unique_id(api.TP_TRANSPORT_NCCL) if rank == 0 else b"\0" * 128
-        t = torch.tensor(list(uid), dtype=torch.uint8, device="cuda")
-        dist.broadcast(t, 0)
-        uid = bytes(t.cpu().tolist())
+        uid = api.share_unique_id(api.TP_TRANSPORT_NCCL)
         g = api.tp_grid_init(mode, world, rank, 0, depth, local, api.TP_TRANSPORT_NCCL, uid)
     else:
         g = api.tp_grid_init(mode, 1, 0, 0, 1, local, api.TP_TRANSPORT_NONE)

@@ -67,6 +67,19 @@ def tp_get_unique_id(transport: int) -> bytes:
     return buf.raw
 
 
+def share_unique_id(transport: int, src: int = 0) -> bytes:
+    """Rank `src` creates the 128-byte id, torch.distributed broadcasts it (rendezvous
+    plumbing only; works with the nccl and gloo backends)."""
+    import torch
+    import torch.distributed as dist
+    rank = dist.get_rank()
+    uid = tp_get_unique_id(transport) if rank == src else b"\0" * 128
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor(list(uid), dtype=torch.uint8, device=dev)
+    dist.broadcast(t, src)
+    return bytes(t.cpu().tolist())
+
+
 def tp_grid_init(mode, world, rank, q=0, d=1, device=0, transport=TP_TRANSPORT_NONE,
                  uid: bytes | None = None):
     m = MODES[mode] if isinstance(mode, str) else int(mode)
