@@ -161,13 +161,17 @@ tp_status tp_unpack(const tp_grid* grid, const tp_linear_desc* desc, tp_tensor t
  * op(A) = A [M,K] row-major (lda >= K) if trans_a == 0, else A is stored [K,M] (lda >= M);
  * op(B) = B [K,N] row-major (ldb >= N) if trans_b == 0, else B is stored [N,K] (ldb >= K).
  * C: fp32 [M,N] (ldc) or NULL; bias: in_dtype [N] or NULL; D: out_dtype, ldd.
- * TP_BF16 inputs run the tcgen05/TMEM/TMA kernel (bf16 x bf16 -> fp32), TP_FP32 inputs
- * the SIMT fp32 kernel. bf16 operands need lda, ldb multiples of 8 and 16-byte aligned
- * bases (TMA), else TP_ERR_SHAPE. D may alias C (in-place accumulate). */
+ * TP_BF16 inputs run the tcgen05/TMEM/TMA kernels (bf16 x bf16 -> fp32; CTA-pair
+ * cta_group::2 tiles when M > 128), TP_FP32 inputs the SIMT fp32 kernel. bf16 operands need
+ * lda, ldb multiples of 8 and 16-byte aligned bases (TMA), else TP_ERR_SHAPE. D may alias C
+ * (in-place accumulate). ws: optional device scratch (ws_bytes >= tp_gemm_ws_bytes() enables
+ * split-K for grids with fewer tiles than SM pairs); NULL/0 disables split-K. */
 tp_status tp_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, tp_dtype in_dtype,
                   const void* A, int64_t lda, const void* B, int64_t ldb, const float* C,
                   int64_t ldc, void* D, int64_t ldd, tp_dtype out_dtype, float alpha,
-                  const void* bias, void* stream);
+                  const void* bias, void* ws, size_t ws_bytes, void* stream);
+/* Scratch bytes that enable split-K in tp_gemm for any shape. */
+size_t tp_gemm_ws_bytes(void);
 
 /* db = 1^T dY: column sums of a [rows, cols] row-major matrix (ld), fp32 accumulate. */
 tp_status tp_colsum(const void* src, int64_t rows, int64_t cols, int64_t ld, tp_dtype dtype,

@@ -32,6 +32,7 @@ EXPORTED = [
     "tp_status_string", "tp_last_error", "tp_version", "tp_get_unique_id", "tp_grid_init",
     "tp_grid_coords", "tp_grid_dims", "tp_grid_group", "tp_grid_destroy", "tp_shard_extent",
     "tp_workspace_size", "tp_linear_fwd", "tp_linear_bwd", "tp_pack", "tp_unpack", "tp_gemm",
+    "tp_gemm_ws_bytes",
     "tp_colsum", "tp_fill", "tp_l2_flush", "tp_prof_enable", "tp_prof_reset", "tp_prof_read",
     "tp_launch_count",
 ]
@@ -64,7 +65,8 @@ _sigs = {
     "tp_pack": (_i, [_vp, C.POINTER(tp_linear_desc), _i, _vp, _vp, _vp]),
     "tp_unpack": (_i, [_vp, C.POINTER(tp_linear_desc), _i, _vp, _vp, _vp]),
     "tp_gemm": (_i, [_i, _i, _i64, _i64, _i64, _i, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64,
-                     _i, _f, _vp, _vp]),
+                     _i, _f, _vp, _vp, _sz, _vp]),
+    "tp_gemm_ws_bytes": (_sz, []),
     "tp_colsum": (_i, [_vp, _i64, _i64, _i64, _i, _vp, _vp]),
     "tp_fill": (_i, [_vp, _i, _i64, _i64, _i64, C.c_uint64, _i, _i, _f, _i64, _i64, _i64, _vp]),
     "tp_l2_flush": (_i, [_vp, _sz, _vp]),

@@ -157,12 +157,16 @@ def tp_unpack(g, d, tensor, shard, global_, stream=None):
 
 
 def tp_gemm(trans_a, trans_b, M, N, K, in_dtype, A, lda, B, ldb, Cm, ldc, D, ldd, out_dtype,
-            alpha=1.0, bias=None, stream=None):
+            alpha=1.0, bias=None, stream=None, ws=None):
     idt = DTYPES[in_dtype] if isinstance(in_dtype, str) else int(in_dtype)
     odt = DTYPES[out_dtype] if isinstance(out_dtype, str) else int(out_dtype)
     _check(lib.tp_gemm(int(trans_a), int(trans_b), M, N, K, idt, _ptr(A), lda, _ptr(B), ldb,
-                       _ptr(Cm), ldc, _ptr(D), ldd, odt, float(alpha), _ptr(bias),
-                       _stream(stream)), "tp_gemm")
+                       _ptr(Cm), ldc, _ptr(D), ldd, odt, float(alpha), _ptr(bias), _ptr(ws),
+                       _nbytes(ws), _stream(stream)), "tp_gemm")
+
+
+def tp_gemm_ws_bytes() -> int:
+    return int(lib.tp_gemm_ws_bytes())
 
 
 def tp_colsum(src, rows, cols, ld, dtype, dst, stream=None):

@@ -413,7 +413,7 @@ tp_status tp_unpack(const tp_grid* g, const tp_linear_desc* d, tp_tensor t, cons
 tp_status tp_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, tp_dtype in_dtype,
                   const void* A, int64_t lda, const void* B, int64_t ldb, const float* C,
                   int64_t ldc, void* D, int64_t ldd, tp_dtype out_dtype, float alpha,
-                  const void* bias, void* stream) {
+                  const void* bias, void* ws, size_t ws_bytes, void* stream) {
   if (in_dtype != TP_BF16 && in_dtype != TP_FP32) return fail(TP_ERR_ARG, "in_dtype");
   if (out_dtype != TP_BF16 && out_dtype != TP_FP32) return fail(TP_ERR_ARG, "out_dtype");
   GemmArgs a;
@@ -434,8 +434,12 @@ tp_status tp_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, tp_
   a.out_dtype = out_dtype;
   a.alpha = alpha;
   a.bias = bias;
+  a.ws = ws;
+  a.ws_bytes = ws ? ws_bytes : 0;
   return gemm(a, static_cast<cudaStream_t>(stream));
 }
+
+size_t tp_gemm_ws_bytes(void) { return gemm_tc2_ws_bytes(); }
 
 tp_status tp_colsum(const void* src, int64_t rows, int64_t cols, int64_t ld, tp_dtype dtype,
                     void* dst, void* stream) {

@@ -4,6 +4,8 @@
 // misses (reading A12). Also the GEMM dispatcher and the K == 0 epilogue.
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "tp_internal.h"
 
 namespace tp {
@@ -149,6 +151,13 @@ tp_status gemm(const GemmArgs& g, cudaStream_t s) {
     return fail(TP_ERR_SHAPE,
                 "gemm(bf16): TMA needs 16-byte aligned A/B and row strides that are multiples "
                 "of 8 elements (lda=" + std::to_string(g.lda) + ", ldb=" + std::to_string(g.ldb) + ")");
+  // Kernel choice: the CTA-pair kernel unless the problem is a single 128-row strip or the
+  // output cannot take TMA stores; TP_GEMM_KERNEL=1|2 forces one (A/B measurements).
+  static const int force = [] {
+    const char* e = std::getenv("TP_GEMM_KERNEL");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (force != 1 && gemm_tc2_supported(g)) return gemm_tc2_bf16(g, s);
   return gemm_tc_bf16(g, s);
 }
 

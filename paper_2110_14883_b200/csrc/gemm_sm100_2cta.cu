@@ -1,0 +1,608 @@
+// CTA-pair (tcgen05 cta_group::2) bf16 GEMM for sm_100a — the main local-GEMM kernel of every
+// TP mode:   D[M,N] = alpha * (op(A).op(B) + C) + bias[col].
+//
+// Why a pair (profiles/r01_gemm_v1_summary.md): on one SM, shared memory feeds both the TMA
+// writes and the UMMA operand reads. A 1-CTA 128x128 K=16 step moves 8 KB in + 8 KB out per 64
+// MMA cycles (2x the ~128 B/clk port) and measured 47% tensor-pipe activity. A CTA pair
+// computes a 256x256 tile: each CTA stages its own 128 rows of A and 128 of the 256 columns of
+// B, the leader issues M=256 N=256 MMAs that read both CTAs' smem, each CTA keeps its 128
+// accumulator rows (256 fp32 columns) in its own TMEM. Per CTA: 8 KB read + 8 KB written per
+// 128 MMA cycles = the port's rate.
+//
+//   * cluster (2,1,1); persistent over pair-tiles (grouped raster), 192 threads per CTA:
+//     warp 0 TMA producer (both CTAs; bytes signalled on the leader's `full` barrier),
+//     warp 1 TMEM allocator (both) + MMA issuer (leader), warps 2..5 epilogue (both);
+//   * 6-stage smem ring (32 KB/stage/CTA), BK = 64 with 128-byte swizzle; K-major or MN-major
+//     operands by descriptor (no transposes); TMEM accumulator double-buffered (2 x 256 cols);
+//   * split-K for grids with fewer pair-tiles than SM pairs (e.g. M = 512): every split writes
+//     an fp32 partial tile, the last split to arrive (per-tile counter) sums the partials in
+//     split order (deterministic) and runs the epilogue;
+//   * epilogue: TMEM -> registers -> alpha / C / bias / cast -> 128-byte-swizzled smem staging
+//     -> TMA bulk tensor store (full-line writes, asynchronous).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+#include <mutex>
+
+#include "sm100_ptx.cuh"
+#include "tp_internal.h"
+
+namespace tp {
+namespace {
+
+using namespace ptx;
+
+constexpr int kBM = 128;  // A rows per CTA (pair tile: 256 rows)
+constexpr int kBK = 64;
+constexpr int kABytes = kBM * kBK * 2;
+constexpr int kOutBytes = 32 * 128;  // per epilogue warp: 32 rows x 128 B staging
+constexpr int kThreads = 192;
+
+// Pair-tile width BNP (256 or 128): B columns per CTA, ring depth, TMEM, smem.
+template <int BNP>
+struct PC {
+  static constexpr int BNC = BNP / 2;
+  static constexpr int Stages = BNP == 256 ? 6 : 8;
+  static constexpr int BBytes = BNC * kBK * 2;
+  static constexpr int StageBytes = kABytes + BBytes;
+  static constexpr int TmemCols = 2 * BNP;
+  static constexpr int Smem = Stages * StageBytes + 4 * kOutBytes + 1024 + 256;
+  static constexpr int TileElems = 256 * BNP;
+};
+
+struct Epi2 {
+  const float* C;
+  const void* bias;
+  float* part;
+  int* counters;
+  int64_t ldc;
+  float alpha;
+  int out_bf16;
+  int M, N;
+  int splits, kb_per_split;
+  int c_vec;     // C rows 16-byte aligned
+  int prefetch;  // L2 prefetch distance in k-blocks (0 = off)
+};
+
+__device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb, int& nb) {
+  constexpr int G = 8;  // pair-tile rows per raster band
+  const int band = t / (G * num_n);
+  const int m_start = band * G;
+  const int band_m = min(G, num_m - m_start);
+  const int idx = t - band * G * num_n;
+  mb = m_start + idx % band_m;
+  nb = idx / band_m;
+}
+
+// alpha*(acc + C) + bias for `cw` consecutive columns starting at col0 of one row.
+template <int CW>
+__device__ __forceinline__ void finish_vals(const Epi2& ep, float (&v)[CW], int64_t row, int64_t col0) {
+  const bool in_row = row < ep.M;
+  const bool full = col0 + CW <= ep.N;
+  if (ep.C && in_row) {
+    const float* c = ep.C + row * ep.ldc + col0;
+    if (full && ep.c_vec) {
+#pragma unroll
+      for (int i = 0; i < CW / 4; ++i) {
+        float4 x = reinterpret_cast<const float4*>(c)[i];
+        v[4 * i] += x.x;
+        v[4 * i + 1] += x.y;
+        v[4 * i + 2] += x.z;
+        v[4 * i + 3] += x.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < CW; ++i)
+        if (col0 + i < ep.N) v[i] += c[i];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < CW; ++i) v[i] *= ep.alpha;
+  if (ep.bias) {
+    const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(ep.bias) + col0;
+#pragma unroll
+    for (int i = 0; i < CW; ++i)
+      if (col0 + i < ep.N) v[i] += __bfloat162float(b[i]);
+  }
+}
+
+// Stage one 32-row x 128-byte box (row = lane) with the 128-byte swizzle the TMA store expects.
+template <int CW>
+__device__ __forceinline__ void stage_row(uint8_t* stg, int lane, const float (&v)[CW], int out_bf16) {
+  uint8_t* rowp = stg + lane * 128;
+  if (out_bf16) {  // CW == 64
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      uint4 u;
+      __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) h[k] = __floats2bfloat162_rn(v[8 * j + 2 * k], v[8 * j + 2 * k + 1]);
+      *reinterpret_cast<uint4*>(rowp + ((j ^ (lane & 7)) << 4)) = u;
+    }
+  } else {  // CW == 32
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      *reinterpret_cast<float4*>(rowp + ((j ^ (lane & 7)) << 4)) =
+          make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+  }
+}
+
+template <int CW>
+__device__ __forceinline__ void store_box(const CUtensorMap* tmD, uint8_t* stg, int lane,
+                                          float (&v)[CW], const Epi2& ep, int64_t row, int64_t col0,
+                                          int64_t row0) {
+  finish_vals<CW>(ep, v, row, col0);
+  if (lane == 0) bulk_wait_read0();  // previous box of this warp has left the staging buffer
+  __syncwarp();
+  stage_row<CW>(stg, lane, v, ep.out_bf16);
+  fence_proxy_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    tma_store_2d(tmD, stg, static_cast<int>(col0), static_cast<int>(row0));
+    bulk_commit();
+  }
+}
+
+template <int BNP, bool A_MN, bool B_MN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const __grid_constant__ CUtensorMap tmD, const Epi2 ep, int K, int num_m,
+                    int num_n) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + PC<BNP>::Stages * kABytes;
+  uint8_t* sOut = sB + PC<BNP>::Stages * PC<BNP>::BBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sOut + 4 * kOutBytes);
+  uint64_t* empty = full + PC<BNP>::Stages;
+  uint64_t* tfull = empty + PC<BNP>::Stages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* sflag = reinterpret_cast<int*>(tslot + 1);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int cid = blockIdx.x / 2, ncl = gridDim.x / 2;
+  const int num_tiles = num_m * num_n;
+  const int num_units = num_tiles * ep.splits;
+  const int num_k = (K + kBK - 1) / kBK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    tma_prefetch(&tmD);
+    for (int s = 0; s < PC<BNP>::Stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is the one used)
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_cg2(tslot, PC<BNP>::TmemCols);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===== TMA producer (both CTAs) =====
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = cid; u < num_units; u += ncl) {
+        const int tile = u / ep.splits, split = u % ep.splits;
+        int mb, nb;
+        tile_coords(tile, num_m, num_n, mb, nb);
+        const int kb0 = split * ep.kb_per_split;
+        const int kb1 = min(num_k, kb0 + ep.kb_per_split);
+        const int m0 = mb * 256 + static_cast<int>(rank) * kBM;
+        const int n0 = nb * BNP + static_cast<int>(rank) * PC<BNP>::BNC;
+        // L2 prefetch runs `pf` k-blocks ahead of the smem ring (deeper effective pipeline
+        // for operands that stream from HBM once, e.g. W when M is small)
+        const int pf = ep.prefetch;
+        for (int kb = kb0; kb < min(kb1, kb0 + pf); ++kb) {
+          if (!A_MN) tma_prefetch_2d(&tmA, kb * kBK, m0);
+          else for (int c = 0; c < kBM / 64; ++c) tma_prefetch_2d(&tmA, m0 + c * 64, kb * kBK);
+          if (!B_MN) tma_prefetch_2d(&tmB, kb * kBK, n0);
+          else for (int c = 0; c < PC<BNP>::BNC / 64; ++c) tma_prefetch_2d(&tmB, n0 + c * 64, kb * kBK);
+        }
+        for (int kb = kb0; kb < kb1; ++kb) {
+          if (pf && kb + pf < kb1) {
+            const int kp = kb + pf;
+            if (!A_MN) tma_prefetch_2d(&tmA, kp * kBK, m0);
+            else for (int c = 0; c < kBM / 64; ++c) tma_prefetch_2d(&tmA, m0 + c * 64, kp * kBK);
+            if (!B_MN) tma_prefetch_2d(&tmB, kp * kBK, n0);
+            else for (int c = 0; c < PC<BNP>::BNC / 64; ++c) tma_prefetch_2d(&tmB, n0 + c * 64, kp * kBK);
+          }
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) mbar_expect_tx(&full[stage], 2 * PC<BNP>::StageBytes);
+          uint8_t* a_dst = sA + stage * kABytes;
+          uint8_t* b_dst = sB + stage * PC<BNP>::BBytes;
+          if (!A_MN) {
+            tma_load_2d_pair(&tmA, &full[stage], a_dst, kb * kBK, m0);
+          } else {
+#pragma unroll
+            for (int c = 0; c < kBM / 64; ++c)
+              tma_load_2d_pair(&tmA, &full[stage], a_dst + c * (kBK * 128), m0 + c * 64, kb * kBK);
+          }
+          if (!B_MN) {
+            tma_load_2d_pair(&tmB, &full[stage], b_dst, kb * kBK, n0);
+          } else {
+#pragma unroll
+            for (int c = 0; c < PC<BNP>::BNC / 64; ++c)
+              tma_load_2d_pair(&tmB, &full[stage], b_dst + c * (kBK * 128), n0 + c * 64, kb * kBK);
+          }
+          if (++stage == PC<BNP>::Stages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      // ===== MMA issuer (leader) =====
+      constexpr uint32_t idesc = idesc_bf16_f32(256, BNP, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int u = cid; u < num_units; u += ncl) {
+        const int split = u % ep.splits;
+        const int kb0 = split * ep.kb_per_split;
+        const int kb1 = min(num_k, kb0 + ep.kb_per_split);
+        mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BNP);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(sA + stage * kABytes);
+          const uint32_t b_base = smem_u32(sB + stage * PC<BNP>::BBytes);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) {
+            const uint64_t ad = A_MN ? sdesc_sw128(a_base + k * 2048, kBK * 128, 1024)
+                                     : sdesc_sw128(a_base + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? sdesc_sw128(b_base + k * 2048, kBK * 128, 1024)
+                                     : sdesc_sw128(b_base + k * 32, 16, 1024);
+            umma_bf16_cg2(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          }
+          umma_commit_cg2_mc(&empty[stage], 0x3);
+          if (++stage == PC<BNP>::Stages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_cg2_mc(&tfull[acc], 0x3);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ===== epilogue warps 2..5 (both CTAs): TMEM lane quadrant = warp % 4 =====
+    const int quad = warp & 3;
+    uint8_t* stg = sOut + (warp - 2) * kOutBytes;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int u = cid; u < num_units; u += ncl) {
+      const int tile = u / ep.splits;
+      int mb, nb;
+      tile_coords(tile, num_m, num_n, mb, nb);
+      const int64_t rloc = static_cast<int64_t>(rank) * kBM + quad * 32;  // row within pair tile
+      const int64_t row0 = static_cast<int64_t>(mb) * 256 + rloc;          // first row of warp
+      const int64_t row = row0 + lane;
+      const int64_t n0 = static_cast<int64_t>(nb) * BNP;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
+                             static_cast<uint32_t>(acc * BNP);
+      if (ep.splits == 1) {
+        if (ep.out_bf16) {
+#pragma unroll 1
+          for (int sub = 0; sub < BNP / 64; ++sub) {
+            uint32_t r0[32], r1[32];
+            tmem_ld32(t_row + sub * 64, r0);
+            tmem_ld32(t_row + sub * 64 + 32, r1);
+            tmem_wait_ld();
+            float v[64];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              v[i] = __uint_as_float(r0[i]);
+              v[32 + i] = __uint_as_float(r1[i]);
+            }
+            store_box<64>(&tmD, stg, lane, v, ep, row, n0 + sub * 64, row0);
+          }
+        } else {
+#pragma unroll 1
+          for (int sub = 0; sub < BNP / 32; ++sub) {
+            uint32_t r0[32];
+            tmem_ld32(t_row + sub * 32, r0);
+            tmem_wait_ld();
+            float v[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r0[i]);
+            store_box<32>(&tmD, stg, lane, v, ep, row, n0 + sub * 32, row0);
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(&tempty[acc], 0);
+      } else {
+        // ---- split-K: publish this split's fp32 partial, the last split reduces ----
+        // partial layout per CTA half: float4 slot f (column/4) major, row minor, so a
+        // warp's 32 rows of one slot are 512 contiguous bytes (coalesced store and reload)
+        float4* mypart = reinterpret_cast<float4*>(ep.part + static_cast<int64_t>(u) * PC<BNP>::TileElems +
+                                                   rank * (kBM * BNP)) + quad * 32 + lane;
+#pragma unroll 1
+        for (int ch = 0; ch < BNP / 32; ++ch) {
+          uint32_t r0[32];
+          tmem_ld32(t_row + ch * 32, r0);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            mypart[(ch * 8 + i) * kBM] =
+                make_float4(__uint_as_float(r0[4 * i]), __uint_as_float(r0[4 * i + 1]),
+                            __uint_as_float(r0[4 * i + 2]), __uint_as_float(r0[4 * i + 3]));
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(&tempty[acc], 0);  // TMEM free for the next unit
+        __threadfence();
+        named_barrier_sync(1, 128);
+        if (threadIdx.x == 64) {
+          int* cnt = ep.counters + tile * 2 + rank;
+          const int old = atomicAdd(cnt, 1);
+          const int last = old == ep.splits - 1;
+          if (last) *cnt = 0;  // ready for the next launch
+          *sflag = last;
+        }
+        named_barrier_sync(1, 128);
+        const int last = *sflag;
+        named_barrier_sync(1, 128);
+        if (last) {
+          __threadfence();
+          const float4* base =
+              reinterpret_cast<const float4*>(ep.part + static_cast<int64_t>(tile) * ep.splits * PC<BNP>::TileElems +
+                                              rank * (kBM * BNP)) + quad * 32 + lane;
+          constexpr int kSplitStride4 = PC<BNP>::TileElems / 4;
+          constexpr int CWB = 64;
+          if (ep.out_bf16) {
+#pragma unroll 1
+            for (int sub = 0; sub < BNP / CWB; ++sub) {
+              float v[CWB];
+#pragma unroll
+              for (int i = 0; i < CWB; ++i) v[i] = 0.f;
+              for (int s = 0; s < ep.splits; ++s) {
+                const float4* p = base + s * kSplitStride4 + (sub * (CWB / 4)) * kBM;
+#pragma unroll
+                for (int i = 0; i < CWB / 4; ++i) {
+                  float4 x = __ldcg(p + i * kBM);
+                  v[4 * i] += x.x;
+                  v[4 * i + 1] += x.y;
+                  v[4 * i + 2] += x.z;
+                  v[4 * i + 3] += x.w;
+                }
+              }
+              store_box<CWB>(&tmD, stg, lane, v, ep, row, n0 + sub * CWB, row0);
+            }
+          } else {
+#pragma unroll 1
+            for (int sub = 0; sub < BNP / 32; ++sub) {
+              float v[32];
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = 0.f;
+              for (int s = 0; s < ep.splits; ++s) {
+                const float4* p = base + s * kSplitStride4 + (sub * 8) * kBM;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                  float4 x = __ldcg(p + i * kBM);
+                  v[4 * i] += x.x;
+                  v[4 * i + 1] += x.y;
+                  v[4 * i + 2] += x.z;
+                  v[4 * i + 3] += x.w;
+                }
+              }
+              store_box<32>(&tmD, stg, lane, v, ep, row, n0 + sub * 32, row0);
+            }
+          }
+        }
+      }
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+    if (lane == 0) bulk_wait0();
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_cg2(tmem_base, PC<BNP>::TmemCols);
+  }
+}
+
+// ------------------------------------------------------------------------------ host side
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+tp_status make_map2(CUtensorMap* m, CUtensorMapDataType dt, size_t esz, const void* base,
+                    uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_inner,
+                    uint32_t box_outer) {
+  auto fn = encode_fn();
+  if (!fn) return fail(TP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld * esz};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(TP_ERR_SHAPE, "cuTensorMapEncodeTiled (pair kernel) failed: " + std::to_string(int(r)));
+  return TP_OK;
+}
+
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+struct Plan2 {
+  int num_m, num_n, splits, kbps, grid;
+};
+
+template <int BNP>
+Plan2 plan2(const GemmArgs& g, size_t ws_bytes) {
+  Plan2 p;
+  p.num_m = static_cast<int>((g.M + 255) / 256);
+  p.num_n = static_cast<int>((g.N + BNP - 1) / BNP);
+  const int tiles = p.num_m * p.num_n;
+  const int num_k = static_cast<int>((g.K + kBK - 1) / kBK);
+  const int pairs = sm_count() / 2;
+  int S = 1;
+  static const int allow_split = [] {
+    const char* e = std::getenv("TP_GEMM_SPLITK");
+    return e ? std::atoi(e) : 1;
+  }();
+  // split-K only when the grid would leave more than half of the SM pairs idle
+  for (int s = 2; s <= 4 && allow_split; ++s) {
+    const size_t need = size_t(tiles) * s * PC<BNP>::TileElems * 4 + size_t(tiles) * 2 * 4 + 256;
+    if (2 * tiles <= pairs && tiles * s <= pairs && num_k >= 4 * s && need <= ws_bytes) S = s;
+  }
+  int kbps = (num_k + S - 1) / S;
+  S = (num_k + kbps - 1) / kbps;  // no empty split
+  if (S < 1) S = 1;
+  p.splits = S;
+  p.kbps = S > 1 ? kbps : num_k;
+  const int units = tiles * S;
+  p.grid = 2 * (units < pairs ? units : pairs);
+  return p;
+}
+
+template <int BNP, bool A_MN, bool B_MN>
+tp_status launch2(const GemmArgs& g, cudaStream_t s) {
+  using P = PC<BNP>;
+  Plan2 pl = plan2<BNP>(g, g.ws_bytes);
+  CUtensorMap ta, tb, td;
+  const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  if (!A_MN)
+    TP_TRY(make_map2(&ta, BF, 2, g.A, g.K, g.M, g.lda, kBK, kBM));
+  else
+    TP_TRY(make_map2(&ta, BF, 2, g.A, g.M, g.K, g.lda, 64, kBK));
+  if (!B_MN)
+    TP_TRY(make_map2(&tb, BF, 2, g.B, g.K, g.N, g.ldb, kBK, P::BNC));
+  else
+    TP_TRY(make_map2(&tb, BF, 2, g.B, g.N, g.K, g.ldb, 64, kBK));
+  if (g.out_dtype == TP_BF16)
+    TP_TRY(make_map2(&td, BF, 2, g.D, g.N, g.M, g.ldd, 64, 32));
+  else
+    TP_TRY(make_map2(&td, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, g.D, g.N, g.M, g.ldd, 32, 32));
+
+  auto kern = gemm_tc2_kernel<BNP, A_MN, B_MN>;
+  {
+    static std::mutex mu;
+    static bool done = false;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!done) {
+      TP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, P::Smem));
+      done = true;
+    }
+  }
+  Epi2 ep;
+  ep.C = g.C;
+  ep.bias = g.bias;
+  ep.ldc = g.ldc;
+  ep.alpha = g.alpha;
+  ep.out_bf16 = g.out_dtype == TP_BF16;
+  ep.M = static_cast<int>(g.M);
+  ep.N = static_cast<int>(g.N);
+  ep.splits = pl.splits;
+  ep.kb_per_split = pl.kbps;
+  ep.c_vec = !g.C || ((reinterpret_cast<uintptr_t>(g.C) % 16 == 0) && (g.ldc % 4 == 0));
+  ep.part = nullptr;
+  ep.counters = nullptr;
+  static const int pf_env = [] {
+    const char* e = std::getenv("TP_GEMM_PREFETCH");
+    return e ? std::atoi(e) : -1;
+  }();
+  ep.prefetch = pf_env >= 0 ? pf_env : 0;
+  if (pl.splits > 1) {
+    const int tiles = pl.num_m * pl.num_n;
+    char* w = static_cast<char*>(g.ws);
+    ep.counters = reinterpret_cast<int*>(w);
+    ep.part = reinterpret_cast<float*>(w + 256 * ((tiles * 2 * 4 + 255) / 256));
+    TP_CUDA(cudaMemsetAsync(ep.counters, 0, tiles * 2 * sizeof(int), s));
+  }
+  const int tok = prof_begin(0, s, 2.0 * double(g.M) * double(g.N) * double(g.K));
+  kern<<<pl.grid, kThreads, P::Smem, s>>>(ta, tb, td, ep, static_cast<int>(g.K), pl.num_m,
+                                          pl.num_n);
+  count_launch();
+  prof_end(tok, s);
+  TP_CUDA(cudaGetLastError());
+  return TP_OK;
+}
+
+template <int BNP>
+tp_status dispatch2(const GemmArgs& g, cudaStream_t s) {
+  const bool a_mn = g.trans_a;
+  const bool b_mn = !g.trans_b;
+  if (!a_mn && !b_mn) return launch2<BNP, false, false>(g, s);
+  if (!a_mn && b_mn) return launch2<BNP, false, true>(g, s);
+  if (a_mn && !b_mn) return launch2<BNP, true, false>(g, s);
+  return launch2<BNP, true, true>(g, s);
+}
+
+}  // namespace
+
+bool gemm_tc2_supported(const GemmArgs& g) {
+  const size_t osz = dtype_size(g.out_dtype);
+  return g.M > 128 && (reinterpret_cast<uintptr_t>(g.D) % 16 == 0) && ((g.ldd * osz) % 16 == 0) &&
+         (!g.bias || reinterpret_cast<uintptr_t>(g.bias) % 2 == 0);
+}
+
+size_t gemm_tc2_ws_bytes() {
+  // split-K scratch upper bound: tiles*splits <= #SM pairs (74 on B200), 256x256 fp32 each
+  return size_t(74) * PC<256>::TileElems * 4 + 74 * 2 * 4 * 4 + 1024;
+}
+
+tp_status gemm_tc2_bf16(const GemmArgs& g, cudaStream_t s) {
+  // 256x256 pair tiles when they fill the SM pairs, else 256x128 (twice the tiles)
+  static const int force_bn = [] {
+    const char* e = std::getenv("TP_GEMM_BN");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int64_t tiles256 = ((g.M + 255) / 256) * ((g.N + 255) / 256);
+  const int pairs = sm_count() / 2;
+  const bool wide = force_bn ? force_bn == 256 : tiles256 >= pairs;
+  return wide ? dispatch2<256>(g, s) : dispatch2<128>(g, s);
+}
+
+}  // namespace tp

@@ -57,7 +57,17 @@ struct Ctx {
     a.out_dtype = out;
     a.alpha = alpha;
     a.bias = bias;
+    a.ws = gws;
+    a.ws_bytes = gws_bytes;
     return gemm(a, R.s);
+  }
+  // split-K scratch shared by this schedule's GEMMs (they run in order on `s`)
+  void* gws = nullptr;
+  size_t gws_bytes = 0;
+  void carve_gemm_scratch() {
+    if (dt != TP_BF16) return;
+    gws_bytes = gemm_tc2_ws_bytes();
+    gws = R.ws.take(gws_bytes);
   }
   // column sums of a [rows, cols] shard into out (dtype dt); fp32 scratch from ws
   float* colsum_scratch(int64_t cols) { return static_cast<float*>(ws(size_t(kColsumSlabs) * cols, 4)); }
@@ -493,6 +503,7 @@ tp_status bwd_3d(Ctx& C, const void* dy, const void* x, const void* w, const voi
 
 tp_status sched_fwd(Run& R, const void* x, const void* w, const void* bias, void* y) {
   Ctx C(R);
+  C.carve_gemm_scratch();
   switch (R.g->mode) {
     case TP_1D: return fwd_1d(C, x, w, bias, y);
     case TP_2D:
@@ -505,6 +516,7 @@ tp_status sched_fwd(Run& R, const void* x, const void* w, const void* bias, void
 tp_status sched_bwd(Run& R, const void* dy, const void* x, const void* w, void* dx, void* dw,
                     void* dbias) {
   Ctx C(R);
+  C.carve_gemm_scratch();
   const void* saved = R.saved.base;
   switch (R.g->mode) {
     case TP_1D: return bwd_1d(C, dy, x, w, dx, dw, dbias);

@@ -72,9 +72,14 @@ struct GemmArgs {
   tp_dtype out_dtype = TP_BF16;
   float alpha = 1.f;
   const void* bias = nullptr;
+  void* ws = nullptr;    // split-K scratch (optional; no split-K without it)
+  size_t ws_bytes = 0;
 };
 tp_status gemm(const GemmArgs& a, cudaStream_t s);         // dispatch + validation
-tp_status gemm_tc_bf16(const GemmArgs& a, cudaStream_t s);  // tcgen05
+tp_status gemm_tc_bf16(const GemmArgs& a, cudaStream_t s);  // tcgen05, 1 CTA per tile
+tp_status gemm_tc2_bf16(const GemmArgs& a, cudaStream_t s); // tcgen05 cta_group::2 pair tiles
+bool gemm_tc2_supported(const GemmArgs& a);
+size_t gemm_tc2_ws_bytes();                                 // split-K scratch upper bound
 tp_status gemm_simt_f32(const GemmArgs& a, cudaStream_t s); // FFMA
 tp_status gemm_k0(const GemmArgs& a, cudaStream_t s);       // K == 0 epilogue only
 

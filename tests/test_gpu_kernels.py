@@ -68,8 +68,17 @@ def test_pack_unpack_bit_exact(api, mode, p, d, kw, dtype):
         assert torch.equal(back, G)
 
 
+_WS = {}
+
+
+def _gemm_ws(api):
+    if "ws" not in _WS:
+        _WS["ws"] = torch.empty(api.tp_gemm_ws_bytes(), device="cuda", dtype=torch.uint8)
+    return _WS["ws"]
+
+
 def _gemm_case(api, ta, tb, M, N, K, in_dt, out_dt, seed, alpha=1.0, with_c=False, with_bias=False,
-               kind="uniform", pad=0):
+               kind="uniform", pad=0, split_k=True):
     A = synth.tensor(seed, 0, K if ta else M, M if ta else K, kind, 1.0, in_dt)
     B = synth.tensor(seed, 1, N if tb else K, K if tb else N, kind, 0.5, in_dt)
     Cm = synth.tensor(seed, 2, M, N, "uniform", 1.0, "fp32") if with_c else None
@@ -83,7 +92,8 @@ def _gemm_case(api, ta, tb, M, N, K, in_dt, out_dt, seed, alpha=1.0, with_c=Fals
     dC = to_dev(Cm, "fp32") if with_c else None
     db = to_dev(bias[None, :], in_dt)[0].contiguous() if with_bias else None
     D = torch.full((M, N), float("nan"), device="cuda", dtype=TORCH_DT[out_dt])
-    api.tp_gemm(ta, tb, M, N, K, in_dt, dA, lda, dB, ldb, dC, N, D, N, out_dt, alpha, db)
+    api.tp_gemm(ta, tb, M, N, K, in_dt, dA, lda, dB, ldb, dC, N, D, N, out_dt, alpha, db,
+                ws=_gemm_ws(api) if split_k else None)
     torch.cuda.synchronize()
     opA = A.T if ta else A
     opB = B.T if tb else B
@@ -114,6 +124,45 @@ def test_gemm_bf16_exact_integer_bit_equal(api, ta, tb):
         assert np.array_equal(got, ref)
         got, ref = _gemm_case(api, ta, tb, M, N, K, "bf16", "fp32", seed=8, kind="ternary")
         assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("M,N,K", [(512, 4096, 4096), (304, 600, 1024), (264, 520, 2048)])
+@pytest.mark.parametrize("split_k", [True, False])
+def test_gemm_pair_kernel_split_k(api, ta, tb, M, N, K, split_k):
+    """CTA-pair kernel with (and without) split-K: few 256x256 tiles, long K (C2 shapes)."""
+    got, ref = _gemm_case(api, ta, tb, M, N, K, "bf16", "fp32", seed=13, split_k=split_k)
+    assert rel_fro(got, ref) <= 2e-5
+    got, ref = _gemm_case(api, ta, tb, M, N, K, "bf16", "bf16", seed=13, alpha=0.5, with_c=True,
+                          with_bias=True, split_k=split_k)
+    assert rel_fro(got, ref) <= 1e-2
+
+
+def test_gemm_split_k_is_deterministic(api):
+    A = to_dev(synth.tensor(1, 0, 512, 4096), "bf16")
+    B = to_dev(synth.tensor(1, 1, 4096, 4096, scale=0.03), "bf16")
+    outs = []
+    for _ in range(3):
+        D = torch.empty(512, 4096, device="cuda", dtype=torch.float32)
+        api.tp_gemm(0, 0, 512, 4096, 4096, "bf16", A, 4096, B, 4096, None, 4096, D, 4096, "fp32",
+                    ws=_gemm_ws(api))
+        outs.append(D)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+
+
+def test_gemm_single_cta_kernel_forced(api):
+    """TP_GEMM_KERNEL=1 forces the 1-CTA kernel for every bf16 shape (A/B comparisons);
+    run its parity tests in a child process (the choice is read once per process)."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, TP_GEMM_KERNEL="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "tests/test_gpu_kernels.py",
+                        "-k", "bf16_vs_oracle or exact_integer or wide_tile or epilogue"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
 def test_gemm_bf16_wide_tile_path(api):
