@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--seed", type=int, default=42)
+    ap.add_argument("--eager", action="store_true", help="time eager launches instead of a CUDA graph")
     return ap.parse_args()
 
 
@@ -108,6 +109,28 @@ class Clocks:
         reasons = sorted({n for r in self.rows for n, v in zip(names, r[5:9]) if v.strip() == "Active"})
         return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
                 "samples": len(self.rows)}
+
+
+def traffic_of(workload, world):
+    """DRAM bytes (read + write) per GEMM launch from the committed ncu capture of this workload
+    (tools/ncu_traffic.py writes profiles/traffic_<workload>_p<N>.json), else None."""
+    p = os.path.join(ROOT, "profiles", f"traffic_{workload}_p{world}.json")
+    try:
+        with open(p) as f:
+            return json.load(f)["dram_bytes_per_gemm_launch"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
+def alg_bytes_per_gemm(M, layers, world, mode):
+    """Algorithmic HBM bytes per GEMM launch at p = 1: each operand read once, output written
+    once (bf16), averaged over the step's 3 GEMMs per layer (fwd, dX, dW)."""
+    if world != 1:
+        return None
+    tot = 0
+    for K, N in layers:
+        tot += 2 * (M * K + K * N + M * N) * 3
+    return tot // (3 * len(layers))
 
 
 # ------------------------------------------------------------------------------- our arm
@@ -198,25 +221,66 @@ def run_ours(a):
         step()
     barrier()
     stream = torch.cuda.current_stream()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(a.steps)]
+
+    # ---- pass 1 (instrumented): CUDA events around every GEMM launch on its launching stream
+    # (captured into the step's graph as external event nodes) -> the dominant kernel's
+    # achieved TFLOP/s for the roofline; kernel launches per step
     api.tp_prof_reset()
     n0 = api.tp_launch_count()
     api.tp_prof_enable(True)
+    gemm_ms = gemm_flops = simt_ms = simt_flops = 0.0
+    gemm_n = simt_n = 0
+    if not a.eager:
+        gprof = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gprof):
+            step()
+        api.tp_prof_enable(False)
+        launches_per_step = api.tp_launch_count() - n0
+        for k in range(a.steps):
+            api.tp_l2_flush(flush)
+            gprof.replay()
+            torch.cuda.synchronize()
+            m_, n_, f_ = api.tp_prof_read(0)
+            gemm_ms, gemm_n, gemm_flops = gemm_ms + m_, gemm_n + n_, gemm_flops + f_
+            m_, n_, f_ = api.tp_prof_read(1)
+            simt_ms, simt_n, simt_flops = simt_ms + m_, simt_n + n_, simt_flops + f_
+        del gprof
+    else:
+        for k in range(a.steps):
+            api.tp_l2_flush(flush)
+            torch.cuda._sleep(2_000_000)   # host runs ahead: events bracket device time only
+            step()
+            torch.cuda.synchronize()
+        api.tp_prof_enable(False)
+        launches_per_step = (api.tp_launch_count() - n0) // a.steps
+        gemm_ms, gemm_n, gemm_flops = api.tp_prof_read(0)
+        simt_ms, simt_n, simt_flops = api.tp_prof_read(1)
+    barrier()
+    api.tp_prof_reset()
+
+    # ---- pass 2 (timed): the step captured once as a CUDA graph (all of its kernels and
+    # collectives, no host work per step), replayed K times, L2 flushed between replays
+    graph = None
+    if not a.eager:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        for _ in range(a.warmup):
+            graph.replay()
+        barrier()
+    run_step = graph.replay if graph is not None else step
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(a.steps)]
     with Clocks(local) as clk:
         t_wall = time.perf_counter()
         for k in range(a.steps):
             api.tp_l2_flush(flush)
             ev[k][0].record(stream)
-            step()
+            run_step()
             ev[k][1].record(stream)
         barrier()
         t_wall = time.perf_counter() - t_wall
-    api.tp_prof_enable(False)
-    launches = api.tp_launch_count() - n0 - a.steps * 0
-    gemm_ms, gemm_n, gemm_flops = api.tp_prof_read(0)
-    simt_ms, simt_n, simt_flops = api.tp_prof_read(1)
-    api.tp_prof_reset()
+    launches = launches_per_step * a.steps
     ms = sum(s.elapsed_time(e) for s, e in ev) / a.steps
     if world > 1:
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
@@ -266,8 +330,12 @@ def run_ours(a):
         roof = {"bound": "tensor", "kernel": "gemm_tc_kernel (tcgen05, bf16->fp32)",
                 "achieved": round(ach, 2) if ach else None, "peak": peak, "unit": "TFLOP/s",
                 "frac": round(ach / peak, 4) if ach else None, "peak_source": src + " bf16_tflops (burst)",
-                "traffic": None, "launches_timed": gemm_n,
-                "gemm_share_of_step": round(gemm_ms / a.steps / ms, 3) if ms > 0 else None}
+                "traffic": traffic_of(a.workload, world), "traffic_unit": "bytes/launch (ncu)",
+                "alg_bytes_per_launch": alg_bytes_per_gemm(M, layers, world, mode),
+                "launches_timed": gemm_n,
+                "gemm_share_of_step": round(gemm_ms / a.steps / ms, 3) if ms > 0 else None,
+                "timing": "per-GEMM CUDA events on the launching stream, recorded inside the "
+                          "step graph (external event nodes), K instrumented replays"}
     else:
         peak = 148 * 128 * 2 * 1.965  # fp32 FFMA: SMs x lanes x 2 flop x GHz (GFLOP/s->TFLOP/s /1e3)
         peak = peak / 1e3
@@ -292,6 +360,7 @@ def run_ours(a):
                    "parallelism": f"tp-{mode}x{world}"},
         "per_gpu_tflops": round(value / world, 3),
         "wall_s": round(t_wall, 3),
+        "launch": "cuda-graph replay" if graph is not None else "eager",
         "gpu_launches": launches,
         "roofline": roof,
         "clocks": clk.summary(),

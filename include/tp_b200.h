@@ -197,6 +197,11 @@ tp_status tp_prof_reset(void);
 tp_status tp_prof_read(int kernel_class, double* total_ms, int64_t* launches, double* flops);
 /* Number of kernels this library has launched since load (all classes). */
 int64_t tp_launch_count(void);
+/* Diagnostics: when buf (device, >= 8 x uint64 per CTA of the largest grid) is non-NULL, the
+ * CTA-pair GEMM writes per-CTA clock64 counters: [0] producer wait on free slots, [1] producer
+ * total, [2] MMA wait on loaded stages, [3] MMA wait on a free accumulator, [4] MMA total,
+ * [5] epilogue wait on accumulators, [6] epilogue total. NULL disables (default). */
+tp_status tp_gemm_trace(unsigned long long* buf);
 
 #ifdef __cplusplus
 }

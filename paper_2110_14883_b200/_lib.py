@@ -34,7 +34,7 @@ EXPORTED = [
     "tp_workspace_size", "tp_linear_fwd", "tp_linear_bwd", "tp_pack", "tp_unpack", "tp_gemm",
     "tp_gemm_ws_bytes",
     "tp_colsum", "tp_fill", "tp_l2_flush", "tp_prof_enable", "tp_prof_reset", "tp_prof_read",
-    "tp_launch_count",
+    "tp_launch_count", "tp_gemm_trace",
 ]
 
 
@@ -74,6 +74,7 @@ _sigs = {
     "tp_prof_reset": (_i, []),
     "tp_prof_read": (_i, [_i, C.POINTER(C.c_double), _P64, C.POINTER(C.c_double)]),
     "tp_launch_count": (_i64, []),
+    "tp_gemm_trace": (_i, [_vp]),
 }
 
 for _name, (_res, _args) in _sigs.items():

@@ -203,3 +203,7 @@ def tp_prof_read(kernel_class=0):
 
 def tp_launch_count() -> int:
     return int(lib.tp_launch_count())
+
+
+def tp_gemm_trace(buf=None):
+    _check(lib.tp_gemm_trace(_ptr(buf)), "tp_gemm_trace")

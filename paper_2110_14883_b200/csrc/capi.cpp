@@ -34,12 +34,22 @@ std::atomic<bool> g_prof_on{false};
 
 bool prof_on() { return g_prof_on.load(std::memory_order_relaxed); }
 
+// Under CUDA-graph capture the record becomes an external event node, so the timestamps are
+// taken on every replay of the graph (read them after each replay).
+static void record_timing_event(cudaEvent_t e, cudaStream_t s) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &st) == cudaSuccess && st == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+  else
+    cudaEventRecord(e, s);
+}
+
 int prof_begin(int cls, cudaStream_t s, double flops) {
   if (!prof_on()) return -1;
   ProfRec r{cls, flops, nullptr, nullptr};
   cudaEventCreate(&r.a);
   cudaEventCreate(&r.b);
-  cudaEventRecord(r.a, s);
+  record_timing_event(r.a, s);
   std::lock_guard<std::mutex> lk(g_prof_mu);
   g_prof.push_back(r);
   return static_cast<int>(g_prof.size()) - 1;
@@ -53,7 +63,7 @@ void prof_end(int token, cudaStream_t s) {
     if (token >= static_cast<int>(g_prof.size())) return;
     b = g_prof[token].b;
   }
-  cudaEventRecord(b, s);
+  record_timing_event(b, s);
 }
 
 }  // namespace tp
@@ -511,5 +521,10 @@ tp_status tp_prof_read(int cls, double* total_ms, int64_t* launches, double* flo
 }
 
 int64_t tp_launch_count(void) { return g_launches.load(); }
+
+tp_status tp_gemm_trace(unsigned long long* buf) {
+  tp::g_gemm_trace = buf;
+  return TP_OK;
+}
 
 }  // extern "C"

@@ -157,7 +157,20 @@ tp_status gemm(const GemmArgs& g, cudaStream_t s) {
     const char* e = std::getenv("TP_GEMM_KERNEL");
     return e ? std::atoi(e) : 0;
   }();
-  if (force != 1 && gemm_tc2_supported(g)) return gemm_tc2_bf16(g, s);
+  // The pair kernel needs enough 256x256 pair tiles to occupy the SM pairs; below that, the
+  // streaming-bound small-M shapes run faster as 1-CTA tiles (measured, see
+  // profiles/r01_gemm_v2_summary.md).
+  static int sms_cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& sms = sms_cache[dev & 63];
+  if (!sms) {
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const int64_t pair_tiles = ((g.M + 255) / 256) * ((g.N + 255) / 256);
+  const bool pair_ok = force == 2 || (force == 0 && pair_tiles >= sms / 2);
+  if (force != 1 && pair_ok && gemm_tc2_supported(g)) return gemm_tc2_bf16(g, s);
   return gemm_tc_bf16(g, s);
 }
 

@@ -21,6 +21,7 @@
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "tp_internal.h"
@@ -514,7 +515,12 @@ tp_status gemm_tc_bf16(const GemmArgs& g, cudaStream_t s) {
   int dev = 0;
   TP_CUDA(cudaGetDevice(&dev));
   const int64_t tiles256 = ((g.M + BM - 1) / BM) * ((g.N + 255) / 256);
-  const bool wide = tiles256 >= num_sms(dev);
+  static const int force_bn = [] {
+    const char* e = std::getenv("TP_GEMM_V1_BN");
+    return e ? std::atoi(e) : 0;
+  }();
+  // measured (profiles/r01_gemm_v2_summary.md): 128x256 tiles win once ~120+ of them exist
+  const bool wide = force_bn ? force_bn == 256 : tiles256 >= (num_sms(dev) * 13) / 16;
   if (wide) {
     if (!a_mn && !b_mn) return launch<256, false, false>(g, s);
     if (!a_mn && b_mn) return launch<256, false, true>(g, s);

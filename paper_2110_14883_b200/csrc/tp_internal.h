@@ -34,6 +34,7 @@ inline size_t dtype_size(tp_dtype t) { return t == TP_BF16 ? 2 : 4; }
 
 // ---- instrumentation ------------------------------------------------------------------
 extern std::atomic<int64_t> g_launches;
+extern unsigned long long* g_gemm_trace;
 inline void count_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 bool prof_on();
 // Opens a timed region for kernel class `cls` on `s`; returns a token for prof_end.

@@ -151,17 +151,26 @@ def test_gemm_split_k_is_deterministic(api):
     assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
 
 
-def test_gemm_single_cta_kernel_forced(api):
-    """TP_GEMM_KERNEL=1 forces the 1-CTA kernel for every bf16 shape (A/B comparisons);
-    run its parity tests in a child process (the choice is read once per process)."""
+@pytest.mark.parametrize("env", [
+    {"TP_GEMM_KERNEL": "1"},                                   # 1-CTA kernel everywhere
+    {"TP_GEMM_KERNEL": "2"},                                   # CTA-pair kernel (M > 128)
+    {"TP_GEMM_KERNEL": "2", "TP_GEMM_MC": "2"},                # + A multicast over 2 pairs
+    {"TP_GEMM_KERNEL": "2", "TP_GEMM_MC": "3"},                # + B multicast over 2 pairs
+    {"TP_GEMM_KERNEL": "2", "TP_GEMM_BN": "128"},              # 256x128 pair tiles
+    {"TP_GEMM_KERNEL": "2", "TP_GEMM_BN": "256", "TP_GEMM_SPLITK": "0"},
+], ids=lambda e: "-".join(f"{k[8:]}{v}" for k, v in e.items()))
+def test_gemm_kernel_variants_forced(api, env):
+    """Every kernel variant the dispatcher can pick, forced for every shape of the GEMM parity
+    tests; run in a child process (the choice is read once per process)."""
     import os
     import subprocess
     import sys
-    env = dict(os.environ, TP_GEMM_KERNEL="1")
+    env = dict(os.environ, **env)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "tests/test_gpu_kernels.py",
-                        "-k", "bf16_vs_oracle or exact_integer or wide_tile or epilogue"],
-                       cwd=root, env=env, capture_output=True, text=True, timeout=600)
+                        "-k", "bf16_vs_oracle or exact_integer or wide_tile or epilogue or pair_kernel"
+                              " or deterministic"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 

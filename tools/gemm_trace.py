@@ -1,0 +1,55 @@
+"""Where does the CTA-pair GEMM spend its cycles?  Runs one tp_gemm with the clock64 trace on
+and prints per-role wait fractions (averaged over CTAs).
+
+    python tools/gemm_trace.py 512x4096x4096 NN
+"""
+import json
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2110_14883_b200 import api  # noqa: E402
+
+OPS = {"NN": (0, 0), "NT": (0, 1), "TN": (1, 0), "TT": (1, 1)}
+
+
+def main():
+    shp = sys.argv[1] if len(sys.argv) > 1 else "512x4096x4096"
+    op = sys.argv[2] if len(sys.argv) > 2 else "NN"
+    M, N, K = map(int, shp.split("x"))
+    ta, tb = OPS[op]
+    A = torch.randn((K, M) if ta else (M, K), device="cuda").to(torch.bfloat16)
+    B = torch.randn((N, K) if tb else (K, N), device="cuda").to(torch.bfloat16)
+    D = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    ws = torch.empty(api.tp_gemm_ws_bytes(), device="cuda", dtype=torch.uint8)
+    flush = torch.empty(256 << 20, device="cuda", dtype=torch.uint8)
+    tr = torch.zeros(300 * 8, device="cuda", dtype=torch.int64)
+    run = lambda: api.tp_gemm(ta, tb, M, N, K, "bf16", A, A.shape[1], B, B.shape[1], None, N, D, N,
+                              "bf16", ws=ws)
+    run()
+    api.tp_gemm_trace(tr)
+    api.tp_l2_flush(flush)
+    torch.cuda._sleep(1_000_000)
+    run()
+    torch.cuda.synchronize()
+    api.tp_gemm_trace(None)
+    t = tr.view(-1, 8).cpu().double()
+    live = t[:, 1] > 0
+    t = t[live]
+    names = ["prod_wait_empty", "prod_total", "mma_wait_full", "mma_wait_tmem", "mma_total",
+             "epi_wait_tfull", "epi_total"]
+    out = {"shape": shp, "op": op, "ctas": int(live.sum())}
+    for i, n in enumerate(names):
+        col = t[:, i]
+        nz = col[col > 0] if i in (2, 3, 4) else col
+        out[n] = round(float(nz.mean()), 0) if len(nz) else 0
+    out["mma_full_wait_frac"] = round(out["mma_wait_full"] / max(out["mma_total"], 1), 3)
+    out["prod_wait_frac"] = round(out["prod_wait_empty"] / max(out["prod_total"], 1), 3)
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
