@@ -1,0 +1,124 @@
+"""Parity at the BASELINE.json full sizes, in the launch configurations bench.py times.
+
+* configs[1] (C2: two layers, batch 512, hidden 4096): the bench's N=1 program (1D p=1 chain),
+  the N=4 program (2D q=2) and the N=8 program (3D l=2), the latter two on 4 / 8 in-process
+  ranks of one GPU - every output compared element by element with the dense fp64 oracle.
+* configs[2] HEAD (M = h = 16384) and configs[4] (GPT fc1 16384 x 8192 -> 32768): one layer at
+  p = 1, 1024 sampled entries of each of Y, dX, dW recomputed one by one by oracle/sampled.py.
+* configs[2] literal (batch 64, hidden 16384): 3D l=2 on 8 in-process ranks, full compare.
+Inputs are generated on the device by tp_fill (bit-exact with synth, see test_gpu_kernels).
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import dense, sampled
+from oracle.grid import build_grid
+from oracle.shards import LayerSpec, gather_full
+
+from tp_harness import rel_fro, run_ranks, to_np
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def api():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2110_14883_b200 import api
+    return api
+
+
+def chain_inputs(seed, M, layers):
+    X = synth.tensor(seed, synth.layer_tid(0, 0), M, layers[0][0]).astype(np.float64)
+    Ws = [synth.tensor(seed, synth.layer_tid(i, 1), K, N, scale=synth.xavier_scale(K, N))
+          .astype(np.float64) for i, (K, N) in enumerate(layers)]
+    dY = synth.tensor(seed, synth.layer_tid(len(layers) - 1, 2), M, layers[-1][1]).astype(np.float64)
+    return X, Ws, dY
+
+
+def oracle_chain(X, Ws, dY):
+    acts = [X]
+    for W in Ws:
+        acts.append(dense.linear_fwd(acts[-1], W))
+    dWs = [None] * len(Ws)
+    d = dY
+    for i in reversed(range(len(Ws))):
+        dX, dWs[i], _ = dense.linear_bwd(d, acts[i], Ws[i])
+        d = dX
+    return acts[-1], d, dWs
+
+
+def run_chain(api, mode, p, d, M, layers, seed=42):
+    from paper_2110_14883_b200.mlp import TPMLP
+    transport = api.TP_TRANSPORT_LOCAL if p > 1 else api.TP_TRANSPORT_NONE
+    uid = api.tp_get_unique_id(transport)
+
+    def rank_fn(r):
+        g = api.tp_grid_init(mode, p, r, 0, d, 0, transport, uid)
+        s = torch.cuda.Stream()
+        try:
+            with torch.cuda.stream(s):
+                m = TPMLP(g, M, layers, seed=seed)
+                m.step()
+            s.synchronize()
+            return {"Y": to_np(m.Y[-1]), "dX": to_np(m.dX[0]), "dW": [to_np(w) for w in m.dW]}
+        finally:
+            s.synchronize()
+            api.tp_grid_destroy(g)
+
+    return run_ranks(p, rank_fn, timeout=900)
+
+
+@pytest.mark.parametrize("mode,p,d", [("1d", 1, 1), ("2d", 4, 1), ("3d", 8, 1), ("1d", 8, 1),
+                                      ("2.5d", 8, 2)])
+def test_c2_two_layer_chain_full(api, mode, p, d):
+    M, layers = 512, [(4096, 4096), (4096, 4096)]
+    per = run_chain(api, mode, p, d, M, layers)
+    X, Ws, dY = chain_inputs(42, M, layers)
+    Yr, dXr, dWr = oracle_chain(X, Ws, dY)
+    g = build_grid(mode, p, d)
+    specs = [LayerSpec(M, K, N, split_1d="row" if i % 2 else "col", parity=i % 2)
+             for i, (K, N) in enumerate(layers)]
+    Y = gather_full(g, specs[-1], {r: per[r]["Y"] for r in range(p)}, "Y")
+    dXg = gather_full(g, specs[0], {r: per[r]["dX"] for r in range(p)}, "X")
+    assert rel_fro(Y, Yr) <= 1e-2
+    assert rel_fro(dXg, dXr) <= 1e-2
+    for i in range(len(layers)):
+        dWg = gather_full(g, specs[i], {r: per[r]["dW"][i] for r in range(p)}, "W")
+        assert rel_fro(dWg, dWr[i]) <= 1e-2
+
+
+@pytest.mark.parametrize("name,M,K,N", [("c3head", 16384, 16384, 16384),
+                                        ("c5_fc1", 16384, 8192, 32768)])
+def test_single_layer_full_size_sampled(api, name, M, K, N):
+    from paper_2110_14883_b200.mlp import TPMLP
+    g = api.tp_grid_init("1d", 1, 0)
+    try:
+        m = TPMLP(g, M, [(K, N)], seed=7)
+        m.step()
+        torch.cuda.synchronize()
+        spec = sampled.layer_spec(7, M, K, N)
+        r, c, k = sampled.sample_indices(3, 1024, M, N, K)
+        rt, ct, kt = (torch.from_numpy(v).cuda() for v in (r, c, k))
+        got_y = m.Y[0][rt, ct].float().cpu().numpy()
+        got_dx = m.dX[0][rt, kt].float().cpu().numpy()
+        got_dw = m.dW[0][kt, ct].float().cpu().numpy()
+    finally:
+        api.tp_grid_destroy(g)
+    assert rel_fro(got_y, sampled.y_entries(spec, r, c)) <= 1e-2
+    assert rel_fro(got_dx, sampled.dx_entries(spec, r, k)) <= 1e-2
+    assert rel_fro(got_dw, sampled.dw_entries(spec, k, c)) <= 1e-2
+
+
+def test_c3_literal_3d_8ranks_full(api):
+    """configs[2] literal: batch 64 x hidden 16384, one layer, 3D l=2 (the NVLink-bound corner)."""
+    M, layers = 64, [(16384, 16384)]
+    per = run_chain(api, "3d", 8, 1, M, layers, seed=11)
+    X, Ws, dY = chain_inputs(11, M, layers)
+    Yr, dXr, dWr = oracle_chain(X, Ws, dY)
+    g = build_grid("3d", 8, 1)
+    spec = LayerSpec(M, 16384, 16384, parity=0)
+    assert rel_fro(gather_full(g, spec, {r: per[r]["Y"] for r in range(8)}, "Y"), Yr) <= 1e-2
+    assert rel_fro(gather_full(g, spec, {r: per[r]["dX"] for r in range(8)}, "X"), dXr) <= 1e-2
+    assert rel_fro(gather_full(g, spec, {r: per[r]["dW"][0] for r in range(8)}, "W"), dWr[0]) <= 1e-2

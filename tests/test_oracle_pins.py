@@ -463,3 +463,21 @@ def test_memory_reductions_match_paper_range_test():
         x = (2 / p - (1 - R) * 2 / p) / ((1 - R) * (2 + 1 / p) - 3 / p)
         pred25 = 1 - (3 * x / p + 2 * 2 / p) / ((2 + 1 / p) * x + 2 / p)
         assert abs(pred25 - case["reduction_25d"]) < 0.03
+
+
+# ----------------------------------------------------------------------------- sampled oracle
+
+def test_sampled_entries_equal_dense_definition():
+    """oracle/sampled.py (entry-by-entry, used at full BASELINE sizes) == the dense oracle on the
+    same generator-defined inputs, for every output kind."""
+    from oracle import sampled
+    M, K, N = 48, 40, 56
+    spec = sampled.layer_spec(42, M, K, N)
+    X, W, dY, b = (np.asarray(a, np.float64) for a in synth.layer_inputs(42, M, K, N, with_bias=True))
+    Y = dense.linear_fwd(X, W, b, 0.5)
+    dX, dW, db = dense.linear_bwd(dY, X, W, 0.5)
+    r, c, k = sampled.sample_indices(1, 64, M, N, K)
+    assert np.allclose(sampled.y_entries(spec, r, c, 0.5, with_bias=True), Y[r, c], rtol=1e-13, atol=1e-13)
+    assert np.allclose(sampled.dx_entries(spec, r, k, 0.5), dX[r, k], rtol=1e-13, atol=1e-13)
+    assert np.allclose(sampled.dw_entries(spec, k, c, 0.5), dW[k, c], rtol=1e-13, atol=1e-13)
+    assert np.allclose(sampled.db_entries(spec, c), db[c], rtol=1e-13, atol=1e-13)
