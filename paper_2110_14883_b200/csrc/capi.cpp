@@ -34,6 +34,14 @@ std::atomic<bool> g_prof_on{false};
 
 bool prof_on() { return g_prof_on.load(std::memory_order_relaxed); }
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("TP_PDL");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 // Under CUDA-graph capture the record becomes an external event node, so the timestamps are
 // taken on every replay of the graph (read them after each replay).
 static void record_timing_event(cudaEvent_t e, cudaStream_t s) {

@@ -175,3 +175,33 @@ tp_status gemm(const GemmArgs& g, cudaStream_t s) {
 }
 
 }  // namespace tp
+
+namespace tp {
+
+// Two independent GEMMs (e.g. a layer's dX and dW). When both are bf16 tensor-core problems
+// the CTA-pair kernel takes them in ONE persistent launch, so the tiles of a small-M product
+// (few tiles, long K) and of a short-K product (many tiles) share the machine instead of
+// each leaving SMs idle; otherwise (or with TP_GEMM_KERNEL=1 / TP_GEMM_GROUP=0) two launches.
+tp_status gemm_pair(const GemmArgs& a, const GemmArgs& b, cudaStream_t s) {
+  static const int force = [] {
+    const char* e = std::getenv("TP_GEMM_KERNEL");
+    return e ? std::atoi(e) : 0;
+  }();
+  static const int group_env = [] {
+    const char* e = std::getenv("TP_GEMM_GROUP");
+    return e ? std::atoi(e) : 1;
+  }();
+  auto eligible = [](const GemmArgs& g) {
+    return g.in_dtype == TP_BF16 && g.M > 0 && g.N > 0 && g.K > 0 && g.A && g.B && g.D &&
+           g.ldd >= g.N && (!g.C || g.ldc >= g.N) && g.lda >= (g.trans_a ? g.M : g.K) &&
+           g.ldb >= (g.trans_b ? g.K : g.N) && g.M <= INT32_MAX && g.N <= INT32_MAX &&
+           g.K <= INT32_MAX && (reinterpret_cast<uintptr_t>(g.A) % 16) == 0 &&
+           (reinterpret_cast<uintptr_t>(g.B) % 16) == 0 && (g.lda % 8) == 0 && (g.ldb % 8) == 0 &&
+           gemm_tc2_supported(g);
+  };
+  if (force != 1 && group_env && eligible(a) && eligible(b)) return gemm_tc2_group(a, b, s);
+  TP_TRY(gemm(a, s));
+  return gemm(b, s);
+}
+
+}  // namespace tp

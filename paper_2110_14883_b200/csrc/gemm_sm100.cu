@@ -293,6 +293,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tslot;
+  // programmatic dependent launch: prologue above overlaps the previous kernel's tail
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp == 0) {
     if (lane == 0) {
@@ -498,8 +501,9 @@ tp_status launch(const GemmArgs& g, cudaStream_t s) {
               (!g.C || (((reinterpret_cast<uintptr_t>(g.C) % 16) == 0) && ((g.ldc * 4) % 16 == 0))) &&
               (!g.bias || (reinterpret_cast<uintptr_t>(g.bias) % 16) == 0);
   const int tok = prof_begin(0, s, 2.0 * double(g.M) * double(g.N) * double(g.K));
-  kern<<<grid, kThreads, C::kSmem, s>>>(ta, tb, ep, static_cast<int>(g.M), static_cast<int>(g.N),
-                                        static_cast<int>(g.K), num_m, num_n);
+  TP_CUDA(launch_pdl(kern, dim3(grid), dim3(kThreads), C::kSmem, s, ta, tb, ep,
+                     static_cast<int>(g.M), static_cast<int>(g.N), static_cast<int>(g.K), num_m,
+                     num_n));
   count_launch();
   prof_end(tok, s);
   TP_CUDA(cudaGetLastError());

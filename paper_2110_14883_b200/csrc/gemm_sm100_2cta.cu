@@ -1,28 +1,30 @@
 // CTA-pair (tcgen05 cta_group::2) bf16 GEMM for sm_100a — the main local-GEMM kernel of every
-// TP mode:   D[M,N] = alpha * (op(A).op(B) + C) + bias[col].
+// TP mode:   D[M,N] = alpha * (op(A).op(B) + C) + bias[col],
+// for ONE problem or a GROUP of two independent problems in one persistent launch (e.g. the
+// backward's dX = dY.W^T and dW = X^T.dY, whose tiles together fill the machine).
 //
-// Why a pair (profiles/r01_gemm_v1_summary.md): on one SM, shared memory feeds both the TMA
-// writes and the UMMA operand reads. A 1-CTA 128x128 K=16 step moves 8 KB in + 8 KB out per 64
-// MMA cycles (2x the ~128 B/clk port) and measured 47% tensor-pipe activity. A CTA pair
-// computes a 256x256 tile: each CTA stages its own 128 rows of A and 128 of the 256 columns of
-// B, the leader issues M=256 N=256 MMAs that read both CTAs' smem, each CTA keeps its 128
-// accumulator rows (256 fp32 columns) in its own TMEM. Per CTA: 8 KB read + 8 KB written per
-// 128 MMA cycles = the port's rate.
-//
-//   * cluster (2,1,1); persistent over pair-tiles (grouped raster), 192 threads per CTA:
-//     warp 0 TMA producer (both CTAs; bytes signalled on the leader's `full` barrier),
-//     warp 1 TMEM allocator (both) + MMA issuer (leader), warps 2..5 epilogue (both);
-//   * 6-stage smem ring (32 KB/stage/CTA), BK = 64 with 128-byte swizzle; K-major or MN-major
-//     operands by descriptor (no transposes); TMEM accumulator double-buffered (2 x 256 cols);
-//   * split-K for grids with fewer pair-tiles than SM pairs (e.g. M = 512): every split writes
-//     an fp32 partial tile, the last split to arrive (per-tile counter) sums the partials in
-//     split order (deterministic) and runs the epilogue;
+// Design (profiles/r01_gemm_v1_summary.md, r01_gemm_v2_summary.md):
+//   * a CTA pair computes a 256 x BNP tile (BNP 256 or 128): each CTA stages its 128 rows of
+//     A and BNP/2 of the B columns, the leader issues M=256 N=BNP MMAs reading both CTAs'
+//     shared memory, each CTA keeps its 128 accumulator rows in its own TMEM;
+//   * cluster of 1 pair, or 2 pairs sharing an operand by TMA multicast (MC 2: pairs side by
+//     side in N share A; MC 3: pairs stacked in M share B);
+//   * persistent over units (problem, pair-tile, K split), 192 threads per CTA: warp 0 TMA
+//     producer (both CTAs; bytes land on the pair leader's `full` barrier), warp 1 TMEM
+//     allocator (both) + MMA issuer (leader), warps 2..5 epilogue (both);
+//   * 6-8 stage smem ring, BK = 64 with 128-byte swizzle; operand majorness (K- or MN-major)
+//     is per problem at run time (descriptors + instruction descriptor), so transposes are
+//     never copies; TMEM accumulator double-buffered so the epilogue overlaps the next unit;
+//   * split-K when a single problem has too few tiles: every split writes an fp32 partial,
+//     the last split to arrive sums the partials in split order (deterministic);
 //   * epilogue: TMEM -> registers -> alpha / C / bias / cast -> 128-byte-swizzled smem staging
-//     -> TMA bulk tensor store (full-line writes, asynchronous).
+//     (two buffers per warp) -> TMA bulk tensor store;
+//   * programmatic dependent launch: the prologue overlaps the previous kernel's tail.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <mutex>
 
@@ -38,8 +40,9 @@ using namespace ptx;
 constexpr int kBM = 128;  // A rows per CTA (pair tile: 256 rows)
 constexpr int kBK = 64;
 constexpr int kABytes = kBM * kBK * 2;
-constexpr int kOutBytes = 32 * 128;  // per epilogue warp: 32 rows x 128 B staging
+constexpr int kOutBytes = 32 * 128;  // per epilogue warp and buffer: 32 rows x 128 B staging
 constexpr int kThreads = 192;
+constexpr int kMaxProbs = 2;
 
 // Pair-tile width BNP (256 or 128): B columns per CTA, ring depth, TMEM, smem.
 template <int BNP>
@@ -53,7 +56,8 @@ struct PC {
   static constexpr int TileElems = 256 * BNP;
 };
 
-struct Epi2 {
+struct Prob {
+  CUtensorMap tmA, tmB, tmD;
   const float* C;
   const void* bias;
   float* part;
@@ -61,11 +65,19 @@ struct Epi2 {
   int64_t ldc;
   float alpha;
   int out_bf16;
-  int M, N;
+  int M, N, K;
+  int a_mn, b_mn;
+  int num_m, num_n;
   int splits, kb_per_split;
-  int c_vec;     // C rows 16-byte aligned
-  int prefetch;  // L2 prefetch distance in k-blocks (0 = off)
-  unsigned long long* trace;  // optional per-CTA wait-cycle counters (TP_GEMM_TRACE)
+  int c_vec;
+  int unit0;  // first unit of this problem in the launch's unit space
+};
+
+struct Group {
+  Prob p[kMaxProbs];
+  int nprob;
+  int total_units;
+  unsigned long long* trace;  // optional per-CTA wait-cycle counters (tp_gemm_trace)
 };
 
 __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb, int& nb) {
@@ -78,9 +90,43 @@ __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb
   nb = idx / band_m;
 }
 
-// alpha*(acc + C) + bias for `cw` consecutive columns starting at col0 of one row.
+// Cluster shapes (MC): 1 = one CTA pair; 2 = two pairs side by side in N sharing their A rows;
+// 3 = two pairs stacked in M sharing their B columns. A "super tile" = the cluster's tiles.
+__host__ __device__ constexpr int pairs_of(int MC) { return MC == 1 ? 1 : 2; }
+__host__ __device__ constexpr int super_tiles(int MC, int num_m, int num_n) {
+  return MC == 1 ? num_m * num_n
+                 : MC == 2 ? num_m * ((num_n + 1) / 2) : ((num_m + 1) / 2) * num_n;
+}
+
+struct Unit {
+  int prob, mb, nb, split, ptile;
+};
+
+template <int MC>
+__device__ __forceinline__ Unit unit_of(const Group& G, int u, int pair) {
+  Unit x;
+  x.prob = (G.nprob > 1 && u >= G.p[1].unit0) ? 1 : 0;
+  const Prob& P = G.p[x.prob];
+  const int lu = u - P.unit0;
+  const int st = lu / P.splits;
+  x.split = lu % P.splits;
+  if (MC == 3) {
+    int mbs;
+    tile_coords(st, (P.num_m + 1) / 2, P.num_n, mbs, x.nb);
+    x.mb = mbs * 2 + pair;
+  } else {
+    const int num_ns = (P.num_n + MC - 1) / MC;
+    int nbs;
+    tile_coords(st, P.num_m, num_ns, x.mb, nbs);
+    x.nb = nbs * MC + pair;
+  }
+  x.ptile = st * pairs_of(MC) + pair;  // dense pair-tile id (split-K partials / counters)
+  return x;
+}
+
+// alpha*(acc + C) + bias for CW consecutive columns starting at col0 of one row.
 template <int CW>
-__device__ __forceinline__ void finish_vals(const Epi2& ep, float (&v)[CW], int64_t row, int64_t col0) {
+__device__ __forceinline__ void finish_vals(const Prob& ep, float (&v)[CW], int64_t row, int64_t col0) {
   const bool in_row = row < ep.M;
   const bool full = col0 + CW <= ep.N;
   if (ep.C && in_row) {
@@ -112,9 +158,9 @@ __device__ __forceinline__ void finish_vals(const Epi2& ep, float (&v)[CW], int6
 
 // Stage one 32-row x 128-byte box (row = lane) with the 128-byte swizzle the TMA store expects.
 template <int CW>
-__device__ __forceinline__ void stage_row(uint8_t* stg, int lane, const float (&v)[CW], int out_bf16) {
+__device__ __forceinline__ void stage_row(uint8_t* stg, int lane, const float (&v)[CW]) {
   uint8_t* rowp = stg + lane * 128;
-  if (out_bf16) {  // CW == 64
+  if (CW == 64) {  // bf16
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       uint4 u;
@@ -123,7 +169,7 @@ __device__ __forceinline__ void stage_row(uint8_t* stg, int lane, const float (&
       for (int k = 0; k < 4; ++k) h[k] = __floats2bfloat162_rn(v[8 * j + 2 * k], v[8 * j + 2 * k + 1]);
       *reinterpret_cast<uint4*>(rowp + ((j ^ (lane & 7)) << 4)) = u;
     }
-  } else {  // CW == 32
+  } else {  // fp32, CW == 32
 #pragma unroll
     for (int j = 0; j < 8; ++j)
       *reinterpret_cast<float4*>(rowp + ((j ^ (lane & 7)) << 4)) =
@@ -131,196 +177,229 @@ __device__ __forceinline__ void stage_row(uint8_t* stg, int lane, const float (&
   }
 }
 
-// Each epilogue warp owns two 4 KB staging buffers used alternately: before refilling one,
-// wait until at most one bulk store (the other buffer's) is still reading shared memory.
+// Two staging buffers per warp used alternately: before refilling one, wait until at most one
+// bulk store (the other buffer's) is still reading shared memory.
 template <int CW>
-__device__ __forceinline__ void store_box(const CUtensorMap* tmD, uint8_t* stg, int& nbox, int lane,
-                                          float (&v)[CW], const Epi2& ep, int64_t row, int64_t col0,
-                                          int64_t row0) {
+__device__ __forceinline__ void store_box(const Prob& ep, uint8_t* stg, int& nbox, int lane,
+                                          float (&v)[CW], int64_t row, int64_t col0, int64_t row0) {
   finish_vals<CW>(ep, v, row, col0);
   uint8_t* buf = stg + (nbox & 1) * kOutBytes;
   if (lane == 0) bulk_wait_read1();
   __syncwarp();
-  stage_row<CW>(buf, lane, v, ep.out_bf16);
+  stage_row<CW>(buf, lane, v);
   fence_proxy_async_smem();
   __syncwarp();
   if (lane == 0) {
-    tma_store_2d(tmD, buf, static_cast<int>(col0), static_cast<int>(row0));
+    tma_store_2d(&ep.tmD, buf, static_cast<int>(col0), static_cast<int>(row0));
     bulk_commit();
   }
   ++nbox;
 }
 
-// Unit u of a cluster -> (pair-tile row mb, pair-tile column nb of this CTA's pair, K split).
-// Cluster shapes (MC): 1 = one CTA pair; 2 = two pairs side by side in N sharing (multicasting)
-// their A rows; 3 = two pairs stacked in M sharing their B columns. A "super tile" is the
-// cluster's pair-tiles.
-constexpr int pairs_of(int MC) { return MC == 1 ? 1 : 2; }
-struct Unit {
-  int mb, nb, split, ptile;
-};
-template <int MC>
-__device__ __forceinline__ Unit unit_of(int u, int splits, int num_m, int num_n, int pair) {
-  Unit x;
-  const int st = u / splits;
-  x.split = u % splits;
-  if (MC == 3) {
-    int mbs;
-    tile_coords(st, (num_m + 1) / 2, num_n, mbs, x.nb);
-    x.mb = mbs * 2 + pair;
+// CW output columns (sub-chunk `sub`) of this thread's row, straight from TMEM.
+template <int CW>
+__device__ __forceinline__ void tmem_cols(uint32_t t_row, int sub, float (&v)[CW]) {
+  uint32_t r0[32];
+  tmem_ld32(t_row + sub * CW, r0);
+  if (CW == 64) {
+    uint32_t r1[32];
+    tmem_ld32(t_row + sub * CW + 32, r1);
+    tmem_wait_ld();
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      v[i] = __uint_as_float(r0[i]);
+      v[(CW == 64 ? 32 : 0) + i] = __uint_as_float(r1[i]);
+    }
   } else {
-    const int num_ns = (num_n + MC - 1) / MC;
-    int nbs;
-    tile_coords(st, num_m, num_ns, x.mb, nbs);
-    x.nb = nbs * MC + pair;
+    tmem_wait_ld();
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r0[i]);
   }
-  x.ptile = st * pairs_of(MC) + pair;  // dense pair-tile id (split-K partials / counters)
-  return x;
-}
-__host__ __device__ constexpr int super_tiles(int MC, int num_m, int num_n) {
-  return MC == 1 ? num_m * num_n
-                 : MC == 2 ? num_m * ((num_n + 1) / 2) : ((num_m + 1) / 2) * num_n;
 }
 
-template <int BNP, int MC, bool A_MN, bool B_MN>
+// Last split: sum the S fp32 partials of this thread's row for sub-chunk `sub`, split order.
+template <int CW>
+__device__ __forceinline__ void sum_partials(const float4* base, int splits, int split_stride4,
+                                             int sub, float (&v)[CW]) {
+#pragma unroll
+  for (int i = 0; i < CW; ++i) v[i] = 0.f;
+  if (splits == 2) {
+    float4 x0[CW / 4], x1[CW / 4];
+    const float4* p0 = base + (sub * (CW / 4)) * kBM;
+    const float4* p1 = p0 + split_stride4;
+#pragma unroll
+    for (int i = 0; i < CW / 4; ++i) {
+      x0[i] = __ldcg(p0 + i * kBM);
+      x1[i] = __ldcg(p1 + i * kBM);
+    }
+#pragma unroll
+    for (int i = 0; i < CW / 4; ++i) {
+      v[4 * i] = x0[i].x + x1[i].x;
+      v[4 * i + 1] = x0[i].y + x1[i].y;
+      v[4 * i + 2] = x0[i].z + x1[i].z;
+      v[4 * i + 3] = x0[i].w + x1[i].w;
+    }
+  } else {
+    for (int s = 0; s < splits; ++s) {
+      const float4* p = base + s * split_stride4 + (sub * (CW / 4)) * kBM;
+      float4 x[CW / 4];
+#pragma unroll
+      for (int i = 0; i < CW / 4; ++i) x[i] = __ldcg(p + i * kBM);
+#pragma unroll
+      for (int i = 0; i < CW / 4; ++i) {
+        v[4 * i] += x[i].x;
+        v[4 * i + 1] += x[i].y;
+        v[4 * i + 2] += x[i].z;
+        v[4 * i + 3] += x[i].w;
+      }
+    }
+  }
+}
+
+template <int BNP, int MC>
 __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThreads, 1)
-    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    const __grid_constant__ CUtensorMap tmD, const Epi2 ep, int K, int num_m,
-                    int num_n) {
+    gemm_tc2_kernel(const __grid_constant__ Group G) {
+  using P = PC<BNP>;
+  constexpr int NP = pairs_of(MC);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = sA + PC<BNP>::Stages * kABytes;
-  uint8_t* sOut = sB + PC<BNP>::Stages * PC<BNP>::BBytes;
+  uint8_t* sB = sA + P::Stages * kABytes;
+  uint8_t* sOut = sB + P::Stages * P::BBytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(sOut + 8 * kOutBytes);
-  uint64_t* empty = full + PC<BNP>::Stages;
-  uint64_t* tfull = empty + PC<BNP>::Stages;
+  uint64_t* empty = full + P::Stages;
+  uint64_t* tfull = empty + P::Stages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
   int* sflag = reinterpret_cast<int*>(tslot + 1);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t crank = cluster_rank();
-  const uint32_t rank = crank & 1;        // position in the CTA pair
+  const uint32_t rank = crank & 1;   // position in the CTA pair
   const int pair = static_cast<int>(crank >> 1);
-  const uint32_t lead = crank & ~1u;      // this pair's leader (issues the MMAs)
+  const uint32_t lead = crank & ~1u;  // this pair's leader (issues the MMAs)
   const bool leader = rank == 0;
-  constexpr int NP = pairs_of(MC);
   const int cid = blockIdx.x / (2 * NP), ncl = gridDim.x / (2 * NP);
-  const int num_units = super_tiles(MC, num_m, num_n) * ep.splits;
-  const int num_k = (K + kBK - 1) / kBK;
   constexpr uint16_t kAllMask = static_cast<uint16_t>((1u << (2 * NP)) - 1);
   const uint16_t pair_mask = static_cast<uint16_t>(0x3u << (2 * pair));
+  const uint16_t xmask = static_cast<uint16_t>((1u << rank) | (1u << (2 + rank)));
 
   if (warp == 0 && lane == 0) {
-    tma_prefetch(&tmA);
-    tma_prefetch(&tmB);
-    tma_prefetch(&tmD);
-    for (int s = 0; s < PC<BNP>::Stages; ++s) {
+    for (int i = 0; i < G.nprob; ++i) {
+      tma_prefetch(&G.p[i].tmA);
+      tma_prefetch(&G.p[i].tmB);
+      tma_prefetch(&G.p[i].tmD);
+    }
+    for (int s = 0; s < P::Stages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], pairs_of(MC));  // free once every pair's MMAs read it (multicast)
+      mbar_init(&empty[s], NP);  // free once every pair's MMAs have read it (multicast)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is the one used)
+      mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs (the pair leader's copy is used)
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc_cg2(tslot, PC<BNP>::TmemCols);
+  if (warp == 1) tmem_alloc_cg2(tslot, P::TmemCols);
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tslot;
+  // the prologue above overlaps the previous kernel's tail (PDL); operands, C and outputs are
+  // touched only once the previous kernel's results are visible
+  pdl_launch_dependents();
+  pdl_wait();
 
   if (warp == 0) {
     if (lane == 0) {
-      // ===== TMA producer (both CTAs) =====
+      // ===== TMA producer (both CTAs of every pair) =====
       int stage = 0;
       uint32_t phase = 0;
       unsigned long long t_wait = 0, t_begin = clock64();
-      for (int u = cid; u < num_units; u += ncl) {
-        const Unit t = unit_of<MC>(u, ep.splits, num_m, num_n, pair);
-        const int kb0 = t.split * ep.kb_per_split;
-        const int kb1 = min(num_k, kb0 + ep.kb_per_split);
+      for (int u = cid; u < G.total_units; u += ncl) {
+        const Unit t = unit_of<MC>(G, u, pair);
+        const Prob& pr = G.p[t.prob];
+        const int num_k = (pr.K + kBK - 1) / kBK;
+        const int kb0 = t.split * pr.kb_per_split;
+        const int kb1 = min(num_k, kb0 + pr.kb_per_split);
         const int m0 = t.mb * 256 + static_cast<int>(rank) * kBM;
-        const int n0 = t.nb * BNP + static_cast<int>(rank) * PC<BNP>::BNC;
+        const int n0 = t.nb * BNP + static_cast<int>(rank) * P::BNC;
         for (int kb = kb0; kb < kb1; ++kb) {
           {
             const unsigned long long t0 = clock64();
             mbar_wait(&empty[stage], phase ^ 1);
             t_wait += clock64() - t0;
           }
-          if (leader) mbar_expect_tx(&full[stage], 2 * PC<BNP>::StageBytes);
+          if (leader) mbar_expect_tx(&full[stage], 2 * P::StageBytes);
           uint8_t* a_dst = sA + stage * kABytes;
-          uint8_t* b_dst = sB + stage * PC<BNP>::BBytes;
-          const uint16_t xmask = static_cast<uint16_t>((1u << rank) | (1u << (2 + rank)));
+          uint8_t* b_dst = sB + stage * P::BBytes;
+          // ---- A: this CTA's 128 rows (K-major: one box; MN-major: two 64-wide chunks)
           if (MC != 2) {
-            if (!A_MN) {
-              tma_load_2d_pair(&tmA, &full[stage], a_dst, kb * kBK, m0);
+            if (!pr.a_mn) {
+              tma_load_2d_pair(&pr.tmA, &full[stage], a_dst, kb * kBK, m0);
             } else {
-#pragma unroll
               for (int c = 0; c < kBM / 64; ++c)
-                tma_load_2d_pair(&tmA, &full[stage], a_dst + c * (kBK * 128), m0 + c * 64, kb * kBK);
+                tma_load_2d_pair(&pr.tmA, &full[stage], a_dst + c * (kBK * 128), m0 + c * 64, kb * kBK);
             }
-          } else {
-            // A rows are the same for both pairs of the cluster: pair p fetches the p-th 64-row
-            // half of this CTA's 128-row A tile and multicasts it to the same-rank CTA of every
-            // pair (halves the TMA issue and L2 reads of A)
-            if (!A_MN)
-              tma_load_2d_pair_mc(&tmA, &full[stage], a_dst + pair * 64 * 128, kb * kBK,
+          } else {  // pair p fetches the p-th half and multicasts it to the same-rank CTAs
+            if (!pr.a_mn)
+              tma_load_2d_pair_mc(&pr.tmA, &full[stage], a_dst + pair * 64 * 128, kb * kBK,
                                   m0 + pair * 64, xmask);
             else
-              tma_load_2d_pair_mc(&tmA, &full[stage], a_dst + pair * (kBK * 128), m0 + pair * 64,
-                                  kb * kBK, xmask);
+              tma_load_2d_pair_mc(&pr.tmA, &full[stage], a_dst + pair * (kBK * 128),
+                                  m0 + pair * 64, kb * kBK, xmask);
           }
+          // ---- B: this CTA's BNP/2 columns
           if (MC != 3) {
-            if (!B_MN) {
-              tma_load_2d_pair(&tmB, &full[stage], b_dst, kb * kBK, n0);
+            if (!pr.b_mn) {
+              tma_load_2d_pair(&pr.tmB, &full[stage], b_dst, kb * kBK, n0);
             } else {
-#pragma unroll
-              for (int c = 0; c < PC<BNP>::BNC / 64; ++c)
-                tma_load_2d_pair(&tmB, &full[stage], b_dst + c * (kBK * 128), n0 + c * 64, kb * kBK);
+              for (int c = 0; c < P::BNC / 64; ++c)
+                tma_load_2d_pair(&pr.tmB, &full[stage], b_dst + c * (kBK * 128), n0 + c * 64, kb * kBK);
             }
-          } else {
-            // B columns are the same for both pairs (stacked in M): pair p fetches half of this
-            // CTA's B tile and multicasts it to the same-rank CTA of both pairs
-            constexpr int BNC = PC<BNP>::BNC;
-            if (!B_MN) {  // stored [N,K]: half the N rows
-              tma_load_2d_pair_mc(&tmB, &full[stage], b_dst + pair * (BNC / 2) * 128, kb * kBK,
+          } else {  // pairs stacked in M share B: pair p fetches half and multicasts it
+            constexpr int BNC = P::BNC;
+            if (!pr.b_mn)
+              tma_load_2d_pair_mc(&pr.tmB, &full[stage], b_dst + pair * (BNC / 2) * 128, kb * kBK,
                                   n0 + pair * (BNC / 2), xmask);
-            } else if (BNC >= 128) {  // stored [K,N]: one of the 64-column chunks
-              tma_load_2d_pair_mc(&tmB, &full[stage], b_dst + pair * (kBK * 128), n0 + pair * 64,
+            else if (BNC >= 128)
+              tma_load_2d_pair_mc(&pr.tmB, &full[stage], b_dst + pair * (kBK * 128), n0 + pair * 64,
                                   kb * kBK, xmask);
-            } else {  // a single 64-column chunk: half of its K rows
-              tma_load_2d_pair_mc(&tmB, &full[stage], b_dst + pair * (kBK / 2) * 128, n0,
+            else
+              tma_load_2d_pair_mc(&pr.tmB, &full[stage], b_dst + pair * (kBK / 2) * 128, n0,
                                   kb * kBK + pair * (kBK / 2), xmask);
-            }
           }
-          if (++stage == PC<BNP>::Stages) {
+          if (++stage == P::Stages) {
             stage = 0;
             phase ^= 1;
           }
         }
       }
-      if (ep.trace) {
-        ep.trace[blockIdx.x * 8 + 0] = t_wait;
-        ep.trace[blockIdx.x * 8 + 1] = clock64() - t_begin;
+      if (G.trace) {
+        G.trace[blockIdx.x * 8 + 0] = t_wait;
+        G.trace[blockIdx.x * 8 + 1] = clock64() - t_begin;
       }
     }
   } else if (warp == 1) {
     if (leader && lane == 0) {
-      // ===== MMA issuer (leader) =====
-      constexpr uint32_t idesc = idesc_bf16_f32(256, BNP, A_MN, B_MN);
+      // ===== MMA issuer (pair leader) =====
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
       unsigned long long t_full = 0, t_temp = 0, t_begin = clock64();
-      for (int u = cid; u < num_units; u += ncl) {
-        const int split = u % ep.splits;  // same K range for every pair of the cluster
-        const int kb0 = split * ep.kb_per_split;
-        const int kb1 = min(num_k, kb0 + ep.kb_per_split);
+      for (int u = cid; u < G.total_units; u += ncl) {
+        const Unit t = unit_of<MC>(G, u, pair);
+        const Prob& pr = G.p[t.prob];
+        const int num_k = (pr.K + kBK - 1) / kBK;
+        const int kb0 = t.split * pr.kb_per_split;
+        const int kb1 = min(num_k, kb0 + pr.kb_per_split);
+        const uint32_t idesc = idesc_bf16_f32(256, BNP, pr.a_mn != 0, pr.b_mn != 0);
+        // K-major: +32 B per 16-element K step inside the 128 B swizzle atom (SBO = 8 rows).
+        // MN-major: +16 rows x 128 B per K step; LBO = one 64-wide MN chunk (BK rows).
+        const uint32_t a_step = pr.a_mn ? 2048u : 32u, a_lbo = pr.a_mn ? kBK * 128 : 16;
+        const uint32_t b_step = pr.b_mn ? 2048u : 32u, b_lbo = pr.b_mn ? kBK * 128 : 16;
         {
           const unsigned long long t0 = clock64();
           mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
@@ -336,31 +415,29 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
           }
           tc_fence_after();
           const uint32_t a_base = smem_u32(sA + stage * kABytes);
-          const uint32_t b_base = smem_u32(sB + stage * PC<BNP>::BBytes);
+          const uint32_t b_base = smem_u32(sB + stage * P::BBytes);
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k) {
-            const uint64_t ad = A_MN ? sdesc_sw128(a_base + k * 2048, kBK * 128, 1024)
-                                     : sdesc_sw128(a_base + k * 32, 16, 1024);
-            const uint64_t bd = B_MN ? sdesc_sw128(b_base + k * 2048, kBK * 128, 1024)
-                                     : sdesc_sw128(b_base + k * 32, 16, 1024);
+            const uint64_t ad = sdesc_sw128(a_base + k * a_step, a_lbo, 1024);
+            const uint64_t bd = sdesc_sw128(b_base + k * b_step, b_lbo, 1024);
             umma_bf16_cg2(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           }
-          umma_commit_cg2_mc(&empty[stage], kAllMask);
-          if (++stage == PC<BNP>::Stages) {
+          umma_commit_cg2_mc(&empty[stage], kAllMask);  // slot free once these MMAs retire
+          if (++stage == P::Stages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit_cg2_mc(&tfull[acc], pair_mask);
+        umma_commit_cg2_mc(&tfull[acc], pair_mask);  // accumulator ready for the epilogue
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
         }
       }
-      if (ep.trace) {
-        ep.trace[blockIdx.x * 8 + 2] = t_full;
-        ep.trace[blockIdx.x * 8 + 3] = t_temp;
-        ep.trace[blockIdx.x * 8 + 4] = clock64() - t_begin;
+      if (G.trace) {
+        G.trace[blockIdx.x * 8 + 2] = t_full;
+        G.trace[blockIdx.x * 8 + 3] = t_temp;
+        G.trace[blockIdx.x * 8 + 4] = clock64() - t_begin;
       }
     }
   } else {
@@ -370,14 +447,14 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
     int nbox = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    unsigned long long t_tf = 0, t_part = 0, t_begin = clock64();
-    for (int u = cid; u < num_units; u += ncl) {
-      const Unit t = unit_of<MC>(u, ep.splits, num_m, num_n, pair);
-      const int tile = t.ptile, mb = t.mb, nb = t.nb;
+    unsigned long long t_tf = 0, t_begin = clock64();
+    for (int u = cid; u < G.total_units; u += ncl) {
+      const Unit t = unit_of<MC>(G, u, pair);
+      const Prob& pr = G.p[t.prob];
       const int64_t rloc = static_cast<int64_t>(rank) * kBM + quad * 32;  // row within pair tile
-      const int64_t row0 = static_cast<int64_t>(mb) * 256 + rloc;          // first row of warp
+      const int64_t row0 = static_cast<int64_t>(t.mb) * 256 + rloc;       // first row of warp
       const int64_t row = row0 + lane;
-      const int64_t n0 = static_cast<int64_t>(nb) * BNP;
+      const int64_t n0 = static_cast<int64_t>(t.nb) * BNP;
       {
         const unsigned long long t0 = clock64();
         mbar_wait(&tfull[acc], acc_phase);
@@ -386,32 +463,20 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
       tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
                              static_cast<uint32_t>(acc * BNP);
-      if (ep.splits == 1) {
-        if (ep.out_bf16) {
+      if (pr.splits == 1) {
+        if (pr.out_bf16) {
 #pragma unroll 1
           for (int sub = 0; sub < BNP / 64; ++sub) {
-            uint32_t r0[32], r1[32];
-            tmem_ld32(t_row + sub * 64, r0);
-            tmem_ld32(t_row + sub * 64 + 32, r1);
-            tmem_wait_ld();
             float v[64];
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              v[i] = __uint_as_float(r0[i]);
-              v[32 + i] = __uint_as_float(r1[i]);
-            }
-            store_box<64>(&tmD, stg, nbox, lane, v, ep, row, n0 + sub * 64, row0);
+            tmem_cols<64>(t_row, sub, v);
+            store_box<64>(pr, stg, nbox, lane, v, row, n0 + sub * 64, row0);
           }
         } else {
 #pragma unroll 1
           for (int sub = 0; sub < BNP / 32; ++sub) {
-            uint32_t r0[32];
-            tmem_ld32(t_row + sub * 32, r0);
-            tmem_wait_ld();
             float v[32];
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r0[i]);
-            store_box<32>(&tmD, stg, nbox, lane, v, ep, row, n0 + sub * 32, row0);
+            tmem_cols<32>(t_row, sub, v);
+            store_box<32>(pr, stg, nbox, lane, v, row, n0 + sub * 32, row0);
           }
         }
         tc_fence_before();
@@ -419,12 +484,14 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
         if (lane == 0) mbar_arrive_cluster(&tempty[acc], lead);
       } else {
         // ---- split-K: publish this split's fp32 partial, the last split reduces ----
-        // partial layout per CTA half: float4 slot f (column/4) major, row minor, so a
-        // warp's 32 rows of one slot are 512 contiguous bytes (coalesced store and reload)
-        float4* mypart = reinterpret_cast<float4*>(ep.part + static_cast<int64_t>(tile * ep.splits + t.split) *
-                                                                 PC<BNP>::TileElems +
-                                                   rank * (kBM * BNP)) + quad * 32 + lane;
-        const unsigned long long tp0 = clock64();
+        // partial layout per CTA half: float4 slot f (column/4) major, row minor, so a warp's
+        // 32 rows of one slot are 512 contiguous bytes (coalesced store and reload)
+        const int tile = t.ptile;
+        float4* mypart =
+            reinterpret_cast<float4*>(pr.part + static_cast<int64_t>(tile * pr.splits + t.split) *
+                                                    P::TileElems +
+                                      rank * (kBM * BNP)) +
+            quad * 32 + lane;
 #pragma unroll 1
         for (int ch = 0; ch < BNP / 32; ++ch) {
           uint32_t r0[32];
@@ -441,11 +508,10 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
         if (lane == 0) mbar_arrive_cluster(&tempty[acc], lead);  // TMEM free for the next unit
         __threadfence();
         named_barrier_sync(1, 128);
-        t_part += clock64() - tp0;
         if (threadIdx.x == 64) {
-          int* cnt = ep.counters + tile * 2 + rank;
+          int* cnt = pr.counters + tile * 2 + rank;
           const int old = atomicAdd(cnt, 1);
-          const int last = old == ep.splits - 1;
+          const int last = old == pr.splits - 1;
           if (last) *cnt = 0;  // ready for the next launch
           *sflag = last;
         }
@@ -455,67 +521,23 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
         if (last) {
           __threadfence();
           const float4* base =
-              reinterpret_cast<const float4*>(ep.part + static_cast<int64_t>(tile) * ep.splits * PC<BNP>::TileElems +
-                                              rank * (kBM * BNP)) + quad * 32 + lane;
-          constexpr int kSplitStride4 = PC<BNP>::TileElems / 4;
-          constexpr int CWB = 64;
-          if (ep.out_bf16) {
+              reinterpret_cast<const float4*>(pr.part + static_cast<int64_t>(tile) * pr.splits * P::TileElems +
+                                              rank * (kBM * BNP)) +
+              quad * 32 + lane;
+          constexpr int kSplitStride4 = P::TileElems / 4;
+          if (pr.out_bf16) {
 #pragma unroll 1
-            for (int sub = 0; sub < BNP / CWB; ++sub) {
-              float v[CWB];
-#pragma unroll
-              for (int i = 0; i < CWB; ++i) v[i] = 0.f;
-              if (ep.splits == 2) {
-                float4 x0[CWB / 4], x1[CWB / 4];
-                const float4* p0 = base + (sub * (CWB / 4)) * kBM;
-                const float4* p1 = p0 + kSplitStride4;
-#pragma unroll
-                for (int i = 0; i < CWB / 4; ++i) {
-                  x0[i] = __ldcg(p0 + i * kBM);
-                  x1[i] = __ldcg(p1 + i * kBM);
-                }
-#pragma unroll
-                for (int i = 0; i < CWB / 4; ++i) {
-                  v[4 * i] = x0[i].x + x1[i].x;
-                  v[4 * i + 1] = x0[i].y + x1[i].y;
-                  v[4 * i + 2] = x0[i].z + x1[i].z;
-                  v[4 * i + 3] = x0[i].w + x1[i].w;
-                }
-              } else {
-                for (int s = 0; s < ep.splits; ++s) {
-                  const float4* p = base + s * kSplitStride4 + (sub * (CWB / 4)) * kBM;
-                  float4 x[CWB / 4];
-#pragma unroll
-                  for (int i = 0; i < CWB / 4; ++i) x[i] = __ldcg(p + i * kBM);
-#pragma unroll
-                  for (int i = 0; i < CWB / 4; ++i) {
-                    v[4 * i] += x[i].x;
-                    v[4 * i + 1] += x[i].y;
-                    v[4 * i + 2] += x[i].z;
-                    v[4 * i + 3] += x[i].w;
-                  }
-                }
-              }
-              store_box<CWB>(&tmD, stg, nbox, lane, v, ep, row, n0 + sub * CWB, row0);
+            for (int sub = 0; sub < BNP / 64; ++sub) {
+              float v[64];
+              sum_partials<64>(base, pr.splits, kSplitStride4, sub, v);
+              store_box<64>(pr, stg, nbox, lane, v, row, n0 + sub * 64, row0);
             }
           } else {
 #pragma unroll 1
             for (int sub = 0; sub < BNP / 32; ++sub) {
               float v[32];
-#pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] = 0.f;
-              for (int s = 0; s < ep.splits; ++s) {
-                const float4* p = base + s * kSplitStride4 + (sub * 8) * kBM;
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                  float4 x = __ldcg(p + i * kBM);
-                  v[4 * i] += x.x;
-                  v[4 * i + 1] += x.y;
-                  v[4 * i + 2] += x.z;
-                  v[4 * i + 3] += x.w;
-                }
-              }
-              store_box<32>(&tmD, stg, nbox, lane, v, ep, row, n0 + sub * 32, row0);
+              sum_partials<32>(base, pr.splits, kSplitStride4, sub, v);
+              store_box<32>(pr, stg, nbox, lane, v, row, n0 + sub * 32, row0);
             }
           }
         }
@@ -526,10 +548,9 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
       }
     }
     if (lane == 0) bulk_wait0();
-    if (ep.trace && warp == 2 && lane == 0) {
-      ep.trace[blockIdx.x * 8 + 5] = t_tf;
-      ep.trace[blockIdx.x * 8 + 6] = clock64() - t_begin;
-      ep.trace[blockIdx.x * 8 + 7] = t_part;
+    if (G.trace && warp == 2 && lane == 0) {
+      G.trace[blockIdx.x * 8 + 5] = t_tf;
+      G.trace[blockIdx.x * 8 + 6] = clock64() - t_begin;
     }
   }
 
@@ -537,7 +558,7 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
   cluster_sync();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc_cg2(tmem_base, PC<BNP>::TmemCols);
+    tmem_dealloc_cg2(tmem_base, P::TmemCols);
   }
 }
 
@@ -584,11 +605,7 @@ int sm_count() {
   return n;
 }
 
-struct Plan2 {
-  int num_m, num_n, splits, kbps, grid;
-};
-
-// Max co-resident clusters of a kernel (cluster size 4 may strand SMs on some GPCs).
+// Max co-resident clusters of a kernel (clusters of 4 may strand SMs on some GPCs).
 template <typename Kern>
 int max_clusters(Kern kern, int csize, int smem) {
   cudaLaunchConfig_t cfg{};
@@ -610,38 +627,75 @@ int max_clusters(Kern kern, int csize, int smem) {
   return n;
 }
 
+// Fill one problem's maps, epilogue params and its split-K choice.
 template <int BNP, int MC>
-Plan2 plan2(const GemmArgs& g, size_t ws_bytes, int clusters) {
-  Plan2 p;
-  p.num_m = static_cast<int>((g.M + 255) / 256);
-  p.num_n = static_cast<int>((g.N + BNP - 1) / BNP);
-  const int supers = super_tiles(MC, p.num_m, p.num_n);
+tp_status setup_prob(const GemmArgs& g, Prob& pr, int clusters, bool allow_split, char*& ws,
+                     size_t& ws_left, cudaStream_t s) {
+  using P = PC<BNP>;
+  const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  pr.a_mn = g.trans_a ? 1 : 0;
+  pr.b_mn = g.trans_b ? 0 : 1;
+  // multicast halves: MC 2 loads half of the A rows per pair, MC 3 half of the B tile
+  if (!pr.a_mn)
+    TP_TRY(make_map2(&pr.tmA, BF, 2, g.A, g.K, g.M, g.lda, kBK, MC == 2 ? kBM / 2 : kBM));
+  else
+    TP_TRY(make_map2(&pr.tmA, BF, 2, g.A, g.M, g.K, g.lda, 64, kBK));
+  if (!pr.b_mn)
+    TP_TRY(make_map2(&pr.tmB, BF, 2, g.B, g.K, g.N, g.ldb, kBK, MC == 3 ? P::BNC / 2 : P::BNC));
+  else
+    TP_TRY(make_map2(&pr.tmB, BF, 2, g.B, g.N, g.K, g.ldb, 64,
+                     (MC == 3 && P::BNC < 128) ? kBK / 2 : kBK));
+  if (g.out_dtype == TP_BF16)
+    TP_TRY(make_map2(&pr.tmD, BF, 2, g.D, g.N, g.M, g.ldd, 64, 32));
+  else
+    TP_TRY(make_map2(&pr.tmD, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, g.D, g.N, g.M, g.ldd, 32, 32));
+  pr.C = g.C;
+  pr.bias = g.bias;
+  pr.ldc = g.ldc;
+  pr.alpha = g.alpha;
+  pr.out_bf16 = g.out_dtype == TP_BF16;
+  pr.M = static_cast<int>(g.M);
+  pr.N = static_cast<int>(g.N);
+  pr.K = static_cast<int>(g.K);
+  pr.num_m = static_cast<int>((g.M + 255) / 256);
+  pr.num_n = static_cast<int>((g.N + BNP - 1) / BNP);
+  pr.c_vec = !g.C || ((reinterpret_cast<uintptr_t>(g.C) % 16 == 0) && (g.ldc % 4 == 0));
+  pr.part = nullptr;
+  pr.counters = nullptr;
+  const int supers = super_tiles(MC, pr.num_m, pr.num_n);
   const int ptiles = supers * pairs_of(MC);
-  const int num_k = static_cast<int>((g.K + kBK - 1) / kBK);
+  const int num_k = (pr.K + kBK - 1) / kBK;
   int S = 1;
-  static const int allow_split = [] {
+  static const int env_split = [] {
     const char* e = std::getenv("TP_GEMM_SPLITK");
     return e ? std::atoi(e) : 1;
   }();
   // split-K only when the grid would leave more than half of the clusters idle
-  for (int s = 2; s <= 4 && allow_split; ++s) {
-    const size_t need = size_t(ptiles) * s * PC<BNP>::TileElems * 4 + size_t(ptiles) * 2 * 4 + 256;
-    if (2 * supers <= clusters && supers * s <= clusters && num_k >= 4 * s && need <= ws_bytes) S = s;
+  for (int sp = 2; sp <= 4 && allow_split && env_split; ++sp) {
+    const size_t need = size_t(ptiles) * sp * P::TileElems * 4 + 256 * ((ptiles * 8 + 255) / 256);
+    if (2 * supers <= clusters && supers * sp <= clusters && num_k >= 4 * sp && need <= ws_left) S = sp;
   }
   int kbps = (num_k + S - 1) / S;
   S = (num_k + kbps - 1) / kbps;  // no empty split
   if (S < 1) S = 1;
-  p.splits = S;
-  p.kbps = S > 1 ? kbps : num_k;
-  const int units = supers * S;
-  p.grid = 2 * pairs_of(MC) * (units < clusters ? units : clusters);
-  return p;
+  pr.splits = S;
+  pr.kb_per_split = S > 1 ? kbps : num_k;
+  if (S > 1) {
+    const size_t cbytes = 256 * ((ptiles * 8 + 255) / 256);
+    pr.counters = reinterpret_cast<int*>(ws);
+    pr.part = reinterpret_cast<float*>(ws + cbytes);
+    const size_t used = cbytes + size_t(ptiles) * S * P::TileElems * 4;
+    ws += used;
+    ws_left -= used;
+    TP_CUDA(cudaMemsetAsync(pr.counters, 0, ptiles * 2 * sizeof(int), s));
+  }
+  return TP_OK;
 }
 
-template <int BNP, int MC, bool A_MN, bool B_MN>
-tp_status launch2(const GemmArgs& g, cudaStream_t s) {
+template <int BNP, int MC>
+tp_status launch2(const GemmArgs* gs, int n, cudaStream_t s) {
   using P = PC<BNP>;
-  auto kern = gemm_tc2_kernel<BNP, MC, A_MN, B_MN>;
+  auto kern = gemm_tc2_kernel<BNP, MC>;
   static int clusters = 0;
   {
     static std::mutex mu;
@@ -651,64 +705,29 @@ tp_status launch2(const GemmArgs& g, cudaStream_t s) {
       clusters = max_clusters(kern, 2 * pairs_of(MC), P::Smem);
     }
   }
-  Plan2 pl = plan2<BNP, MC>(g, g.ws_bytes, clusters);
-  CUtensorMap ta, tb, td;
-  const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
-  // multicast halves: MC 2 loads half of the A rows per pair, MC 3 half of the B tile
-  const uint32_t a_rows = MC == 2 ? kBM / 2 : kBM;
-  if (!A_MN)
-    TP_TRY(make_map2(&ta, BF, 2, g.A, g.K, g.M, g.lda, kBK, a_rows));
-  else
-    TP_TRY(make_map2(&ta, BF, 2, g.A, g.M, g.K, g.lda, 64, kBK));
-  if (!B_MN)
-    TP_TRY(make_map2(&tb, BF, 2, g.B, g.K, g.N, g.ldb, kBK, MC == 3 ? P::BNC / 2 : P::BNC));
-  else
-    TP_TRY(make_map2(&tb, BF, 2, g.B, g.N, g.K, g.ldb, 64,
-                     (MC == 3 && P::BNC < 128) ? kBK / 2 : kBK));
-  if (g.out_dtype == TP_BF16)
-    TP_TRY(make_map2(&td, BF, 2, g.D, g.N, g.M, g.ldd, 64, 32));
-  else
-    TP_TRY(make_map2(&td, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, g.D, g.N, g.M, g.ldd, 32, 32));
-
-  Epi2 ep;
-  ep.C = g.C;
-  ep.bias = g.bias;
-  ep.ldc = g.ldc;
-  ep.alpha = g.alpha;
-  ep.out_bf16 = g.out_dtype == TP_BF16;
-  ep.M = static_cast<int>(g.M);
-  ep.N = static_cast<int>(g.N);
-  ep.splits = pl.splits;
-  ep.kb_per_split = pl.kbps;
-  ep.c_vec = !g.C || ((reinterpret_cast<uintptr_t>(g.C) % 16 == 0) && (g.ldc % 4 == 0));
-  ep.part = nullptr;
-  ep.counters = nullptr;
-  ep.prefetch = 0;
-  ep.trace = g_gemm_trace;
-  if (pl.splits > 1) {
-    const int ptiles = super_tiles(MC, pl.num_m, pl.num_n) * pairs_of(MC);
-    char* w = static_cast<char*>(g.ws);
-    ep.counters = reinterpret_cast<int*>(w);
-    ep.part = reinterpret_cast<float*>(w + 256 * ((ptiles * 2 * 4 + 255) / 256));
-    TP_CUDA(cudaMemsetAsync(ep.counters, 0, ptiles * 2 * sizeof(int), s));
+  Group G;
+  G.nprob = n;
+  G.trace = g_gemm_trace;
+  char* ws = static_cast<char*>(gs[0].ws);
+  size_t ws_left = ws ? gs[0].ws_bytes : 0;
+  int units = 0;
+  double flops = 0;
+  for (int i = 0; i < n; ++i) {
+    // no split-K inside a group: measured slower (the partial round trip outweighs the balance
+    // gain on the C2 backward, 0.135 vs 0.126 ms/step)
+    TP_TRY((setup_prob<BNP, MC>(gs[i], G.p[i], clusters, n == 1, ws, ws_left, s)));
+    G.p[i].unit0 = units;
+    units += super_tiles(MC, G.p[i].num_m, G.p[i].num_n) * G.p[i].splits;
+    flops += 2.0 * double(gs[i].M) * double(gs[i].N) * double(gs[i].K);
   }
-  const int tok = prof_begin(0, s, 2.0 * double(g.M) * double(g.N) * double(g.K));
-  kern<<<pl.grid, kThreads, P::Smem, s>>>(ta, tb, td, ep, static_cast<int>(g.K), pl.num_m,
-                                          pl.num_n);
+  G.total_units = units;
+  const int grid = 2 * pairs_of(MC) * (units < clusters ? units : clusters);
+  const int tok = prof_begin(0, s, flops);
+  TP_CUDA(launch_pdl(kern, dim3(grid), dim3(kThreads), P::Smem, s, G));
   count_launch();
   prof_end(tok, s);
   TP_CUDA(cudaGetLastError());
   return TP_OK;
-}
-
-template <int BNP, int MC>
-tp_status dispatch2(const GemmArgs& g, cudaStream_t s) {
-  const bool a_mn = g.trans_a;
-  const bool b_mn = !g.trans_b;
-  if (!a_mn && !b_mn) return launch2<BNP, MC, false, false>(g, s);
-  if (!a_mn && b_mn) return launch2<BNP, MC, false, true>(g, s);
-  if (a_mn && !b_mn) return launch2<BNP, MC, true, false>(g, s);
-  return launch2<BNP, MC, true, true>(g, s);
 }
 
 }  // namespace
@@ -720,14 +739,14 @@ bool gemm_tc2_supported(const GemmArgs& g) {
 }
 
 size_t gemm_tc2_ws_bytes() {
-  // split-K scratch upper bound: pair-tiles*splits <= #SMs/2 (74 on B200, +1 ragged super
+  // split-K scratch upper bound: pair-tiles*splits <= #SMs/2 (74 on B200, + a ragged super
   // tile), 256x256 fp32 each, plus counters
-  return size_t(76) * PC<256>::TileElems * 4 + 76 * 2 * 4 * 4 + 1024;
+  return size_t(76) * PC<256>::TileElems * 4 + 4096;
 }
 
 tp_status gemm_tc2_bf16(const GemmArgs& g, cudaStream_t s) {
   // Pair tile 256x256 when those tiles fill the SM pairs, else 256x128 (twice the tiles).
-  // Two pairs per cluster (A multicast) whenever there are >= 2 pair-tile columns.
+  // TP_GEMM_BN / TP_GEMM_MC force a width / cluster shape (tests, A/B measurements).
   static const int force_bn = [] {
     const char* e = std::getenv("TP_GEMM_BN");
     return e ? std::atoi(e) : 0;
@@ -739,20 +758,25 @@ tp_status gemm_tc2_bf16(const GemmArgs& g, cudaStream_t s) {
   const int64_t tiles256 = ((g.M + 255) / 256) * ((g.N + 255) / 256);
   const int pairs = sm_count() / 2;
   const bool wide = force_bn ? force_bn == 256 : tiles256 >= pairs;
-  // cluster shape: share the operand that is re-read more (B when few pair-tile rows)
   const int64_t nrows = (g.M + 255) / 256;
   const int64_t ncols = wide ? (g.N + 255) / 256 : (g.N + 127) / 128;
-  int mc = 1;
-  if (force_mc) mc = force_mc;
-  else if (!wide && nrows >= 2 && nrows <= 4) mc = 3;
+  const int mc = force_mc ? force_mc : 1;
   if (wide) {
-    if (mc == 2 && ncols >= 2) return dispatch2<256, 2>(g, s);
-    if (mc == 3 && nrows >= 2) return dispatch2<256, 3>(g, s);
-    return dispatch2<256, 1>(g, s);
+    if (mc == 2 && ncols >= 2) return launch2<256, 2>(&g, 1, s);
+    if (mc == 3 && nrows >= 2) return launch2<256, 3>(&g, 1, s);
+    return launch2<256, 1>(&g, 1, s);
   }
-  if (mc == 2 && ncols >= 2) return dispatch2<128, 2>(g, s);
-  if (mc == 3 && nrows >= 2) return dispatch2<128, 3>(g, s);
-  return dispatch2<128, 1>(g, s);
+  if (mc == 2 && ncols >= 2) return launch2<128, 2>(&g, 1, s);
+  if (mc == 3 && nrows >= 2) return launch2<128, 3>(&g, 1, s);
+  return launch2<128, 1>(&g, 1, s);
+}
+
+// Two independent problems in one launch, 256x256 pair tiles; the problem with more K blocks
+// per tile goes first so the round-robin unit assignment front-loads the long units.
+tp_status gemm_tc2_group(const GemmArgs& a, const GemmArgs& b, cudaStream_t s) {
+  GemmArgs gs[2] = {a, b};
+  if (b.K > a.K) std::swap(gs[0], gs[1]);
+  return launch2<256, 1>(gs, 2, s);
 }
 
 }  // namespace tp

@@ -39,6 +39,12 @@ struct Ctx {
   // D[M,N] = alpha * (op(A).op(B) + C) + bias
   tp_status mm(int64_t M, int64_t N, int64_t K, const void* A, bool ta, const void* B, bool tb,
                void* D, tp_dtype out, float alpha, const float* C, const void* bias) {
+    return gemm(args(M, N, K, A, ta, B, tb, D, out, alpha, C, bias), R.s);
+  }
+  // two independent products (a layer's dX and dW) -> one grouped launch when possible
+  tp_status mm2(const GemmArgs& a, const GemmArgs& b) { return gemm_pair(a, b, R.s); }
+  GemmArgs args(int64_t M, int64_t N, int64_t K, const void* A, bool ta, const void* B, bool tb,
+                void* D, tp_dtype out, float alpha, const float* C, const void* bias) {
     GemmArgs a;
     a.M = M;
     a.N = N;
@@ -59,7 +65,7 @@ struct Ctx {
     a.bias = bias;
     a.ws = gws;
     a.ws_bytes = gws_bytes;
-    return gemm(a, R.s);
+    return a;
   }
   // split-K scratch shared by this schedule's GEMMs (they run in order on `s`)
   void* gws = nullptr;
@@ -208,6 +214,12 @@ tp_status bwd_1d(Ctx& C, const void* dy, const void* x, const void* w, void* dx,
     void* P = (dx && p > 1) ? C.ws(M * K) : dx;
     float* scratch = dbias ? C.colsum_scratch(Nl) : nullptr;
     if (C.R.plan) return TP_OK;
+    if (dx && p == 1) {  // no collective to overlap: dX and dW as one grouped launch
+      TP_TRY(C.mm2(C.args(M, K, Nl, dy, false, w, true, dx, C.dt, d->alpha, nullptr, nullptr),
+                   C.args(K, Nl, M, x, true, dy, false, dw, C.dt, d->alpha, nullptr, nullptr)));
+      if (dbias) TP_TRY(C.colsum(dy, M, Nl, dbias, scratch));
+      return TP_OK;
+    }
     if (dx) {  // dX = AR_p(dY_r . W_r^T): the column split's only collective
       TP_TRY(C.mm(M, K, Nl, dy, false, w, true, P, C.dt, d->alpha, nullptr, nullptr));
       if (p > 1) {
@@ -223,8 +235,11 @@ tp_status bwd_1d(Ctx& C, const void* dy, const void* x, const void* w, void* dx,
   const int64_t Kl = K / p;
   float* scratch = dbias ? C.colsum_scratch(N) : nullptr;
   if (C.R.plan) return TP_OK;
-  if (dx) TP_TRY(C.mm(M, Kl, N, dy, false, w, true, dx, C.dt, d->alpha, nullptr, nullptr));
-  TP_TRY(C.mm(Kl, N, M, x, true, dy, false, dw, C.dt, d->alpha, nullptr, nullptr));
+  const GemmArgs gw = C.args(Kl, N, M, x, true, dy, false, dw, C.dt, d->alpha, nullptr, nullptr);
+  if (dx)  // row-parallel backward is communication-free: dX_r and dW_r in one launch
+    TP_TRY(C.mm2(C.args(M, Kl, N, dy, false, w, true, dx, C.dt, d->alpha, nullptr, nullptr), gw));
+  else
+    TP_TRY(gemm(gw, C.R.s));
   if (dbias) TP_TRY(C.colsum(dy, M, N, dbias, scratch));
   return TP_OK;
 }
@@ -386,8 +401,14 @@ tp_status bwd_2d(Ctx& C, const void* dy, const void* x, const void* w, const voi
   float* scratch = dbias ? C.colsum_scratch(P.nq) : nullptr;
   void* db_t[2] = {dbias ? C.ws(P.nq) : nullptr, dbias ? C.ws(P.nq) : nullptr};
   // the two SUMMA chains carve separate buffers so both pipelines can stay in flight
-  if (dx) TP_TRY(summa_abt(C, P, dy, W, dx));
-  TP_TRY(summa_atb(C, P, x, dy, dwt));
+  if (P.q == 1 && dx) {  // one-rank plane: both products local and independent
+    if (!C.R.plan)
+      TP_TRY(C.mm2(C.args(P.mb, P.kq, P.nq, dy, false, W, true, dx, C.dt, C.d->alpha, nullptr, nullptr),
+                   C.args(P.kq, P.nq, P.mb, x, true, dy, false, dwt, C.dt, C.d->alpha, nullptr, nullptr)));
+  } else {
+    if (dx) TP_TRY(summa_abt(C, P, dy, W, dx));
+    TP_TRY(summa_atb(C, P, x, dy, dwt));
+  }
   if (C.R.plan) return TP_OK;
   if (depth) {  // 2.5D: sum the planes' dW partials over depth (a-8)
     TP_TRY(C.order(C.R.s, C.R.cs));
@@ -470,8 +491,11 @@ tp_status bwd_3d(Ctx& C, const void* dy, const void* x, const void* w, const voi
     float* scratch = dbias ? C.colsum_scratch(C.d->N) : nullptr;
     if (C.R.plan) return TP_OK;
     const int64_t M = C.d->M, K = C.d->K, N = C.d->N;
-    if (dx) TP_TRY(C.mm(M, K, N, dy, false, w, true, dx, C.dt, alpha, nullptr, nullptr));
-    TP_TRY(C.mm(K, N, M, x, true, dy, false, dw, C.dt, alpha, nullptr, nullptr));
+    const GemmArgs gw = C.args(K, N, M, x, true, dy, false, dw, C.dt, alpha, nullptr, nullptr);
+    if (dx)
+      TP_TRY(C.mm2(C.args(M, K, N, dy, false, w, true, dx, C.dt, alpha, nullptr, nullptr), gw));
+    else
+      TP_TRY(gemm(gw, C.R.s));
     if (dbias) TP_TRY(C.colsum(dy, M, N, dbias, scratch));
     return TP_OK;
   }

@@ -41,6 +41,25 @@ bool prof_on();
 int prof_begin(int cls, cudaStream_t s, double flops);
 void prof_end(int token, cudaStream_t s);
 
+// Launch with programmatic stream serialization (PDL): the kernel may start while its
+// predecessor drains and must call griddepcontrol.wait before touching dependent memory.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 // ---- kernels (layout.cu) ------------------------------------------------------------------
 tp_status launch_copy2d(const void* src, int64_t src_ld, void* dst, int64_t dst_ld, int64_t rows,
                         int64_t cols, size_t esz, cudaStream_t s);
@@ -77,6 +96,9 @@ struct GemmArgs {
   size_t ws_bytes = 0;
 };
 tp_status gemm(const GemmArgs& a, cudaStream_t s);         // dispatch + validation
+// Two independent GEMMs: one grouped CTA-pair launch when both qualify, else two launches.
+tp_status gemm_pair(const GemmArgs& a, const GemmArgs& b, cudaStream_t s);
+tp_status gemm_tc2_group(const GemmArgs& a, const GemmArgs& b, cudaStream_t s);
 tp_status gemm_tc_bf16(const GemmArgs& a, cudaStream_t s);  // tcgen05, 1 CTA per tile
 tp_status gemm_tc2_bf16(const GemmArgs& a, cudaStream_t s); // tcgen05 cta_group::2 pair tiles
 bool gemm_tc2_supported(const GemmArgs& a);
