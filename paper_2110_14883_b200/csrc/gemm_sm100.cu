@@ -487,7 +487,9 @@ tp_status launch(const GemmArgs& g, cudaStream_t s) {
   const int num_m = static_cast<int>((g.M + BM - 1) / BM);
   const int num_n = static_cast<int>((g.N + BN - 1) / BN);
   const int tiles = num_m * num_n;
-  const int grid = tiles < num_sms(dev) ? tiles : num_sms(dev);
+  int cap = num_sms(dev);
+  if (g.reserve_sms > 0) cap = std::max(1, cap - g.reserve_sms);  // room for concurrent NCCL
+  const int grid = tiles < cap ? tiles : cap;
   EpiParams ep;
   ep.D = g.D;
   ep.C = g.C;

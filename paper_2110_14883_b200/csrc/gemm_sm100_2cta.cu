@@ -721,7 +721,12 @@ tp_status launch2(const GemmArgs* gs, int n, cudaStream_t s) {
     flops += 2.0 * double(gs[i].M) * double(gs[i].N) * double(gs[i].K);
   }
   G.total_units = units;
-  const int grid = 2 * pairs_of(MC) * (units < clusters ? units : clusters);
+  // persistent grid; when a collective runs concurrently (SUMMA panel broadcast under this
+  // GEMM) leave SMs for its kernels, else the NCCL CTAs cannot be resident until we finish
+  int cap = clusters;
+  if (gs[0].reserve_sms > 0)
+    cap = std::max(1, std::min(cap, (sm_count() - gs[0].reserve_sms) / (2 * pairs_of(MC))));
+  const int grid = 2 * pairs_of(MC) * (units < cap ? units : cap);
   const int tok = prof_begin(0, s, flops);
   TP_CUDA(launch_pdl(kern, dim3(grid), dim3(kThreads), P::Smem, s, G));
   count_launch();

@@ -7,6 +7,8 @@
 // finished with, so step t+1's transfer overlaps step t's GEMM; the reduce of step k's
 // partial overlaps step k+1's GEMM. In 3D the reduce-scatter of dX overlaps the dW GEMM.
 // Every collective's root uses its own shard in place (no staging copy).
+#include <cstdlib>
+
 #include "sched.h"
 
 namespace tp {
@@ -65,7 +67,17 @@ struct Ctx {
     a.bias = bias;
     a.ws = gws;
     a.ws_bytes = gws_bytes;
+    a.reserve_sms = comm_sms();
     return a;
+  }
+  // SMs left to the collectives that run on `cs` under the GEMMs (TP_COMM_SMS, default 16)
+  int comm_sms() const {
+    if (g->world == 1 || R.cs == R.s) return 0;
+    static const int n = [] {
+      const char* e = std::getenv("TP_COMM_SMS");
+      return e ? std::atoi(e) : 16;
+    }();
+    return n;
   }
   // split-K scratch shared by this schedule's GEMMs (they run in order on `s`)
   void* gws = nullptr;

@@ -94,6 +94,7 @@ struct GemmArgs {
   const void* bias = nullptr;
   void* ws = nullptr;    // split-K scratch (optional; no split-K without it)
   size_t ws_bytes = 0;
+  int reserve_sms = 0;  // leave this many SMs free (a collective runs concurrently)
 };
 tp_status gemm(const GemmArgs& a, cudaStream_t s);         // dispatch + validation
 // Two independent GEMMs: one grouped CTA-pair launch when both qualify, else two launches.
