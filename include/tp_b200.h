@@ -155,6 +155,19 @@ tp_status tp_pack(const tp_grid* grid, const tp_linear_desc* desc, tp_tensor ten
 tp_status tp_unpack(const tp_grid* grid, const tp_linear_desc* desc, tp_tensor tensor,
                     const void* shard, void* global, void* stream);
 
+/* ---- fused peer-memory path ----------------------------------------- */
+/* Registers a SYMMETRIC buffer: every rank of the grid calls this collectively, in the same
+ * order, with its own copy of the same logical buffer (same size). Afterwards, for a pointer
+ * p inside the buffer at offset o, the library can address every rank's p + o directly: raw
+ * pointers for ranks of the same process (TP_TRANSPORT_LOCAL), CUDA IPC mappings across
+ * processes (TP_TRANSPORT_NCCL, NVLink peer access). With TP_FLAG_PEER_FUSED, a 2D / 2.5D
+ * layer whose x, w (and dy) shards lie in registered buffers at the same offsets on all ranks
+ * runs as panel GEMMs that read the peers' shards with TMA (no broadcast, no reduce).
+ * The buffer must stay allocated until tp_deregister_all / tp_grid_destroy. */
+tp_status tp_register_buffer(tp_grid* grid, void* ptr, size_t bytes);
+tp_status tp_deregister_all(tp_grid* grid);
+#define TP_FLAG_PEER_FUSED 0x4u /* tp_linear_desc.flags: fused peer-panel SUMMA (2D, 2.5D) */
+
 /* ---- kernels exposed for parity tests and benchmarks ----------------------------------- */
 /* Local GEMM, the per-step shard product of every mode:
  *   D[M,N] = alpha * (op(A) . op(B) + C) + bias[col]

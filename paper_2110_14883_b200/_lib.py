@@ -27,6 +27,7 @@ TP_TRANSPORT_NCCL, TP_TRANSPORT_LOCAL, TP_TRANSPORT_NONE = 0, 1, 2
 TP_TENSOR_X, TP_TENSOR_W, TP_TENSOR_Y, TP_TENSOR_BIAS = 0, 1, 2, 3
 TP_FLAG_W25_DEPTH_SHARDED = 0x1
 TP_FLAG_SERIAL = 0x2
+TP_FLAG_PEER_FUSED = 0x4
 
 EXPORTED = [
     "tp_status_string", "tp_last_error", "tp_version", "tp_get_unique_id", "tp_grid_init",
@@ -34,7 +35,7 @@ EXPORTED = [
     "tp_workspace_size", "tp_linear_fwd", "tp_linear_bwd", "tp_pack", "tp_unpack", "tp_gemm",
     "tp_gemm_ws_bytes",
     "tp_colsum", "tp_fill", "tp_l2_flush", "tp_prof_enable", "tp_prof_reset", "tp_prof_read",
-    "tp_launch_count", "tp_gemm_trace",
+    "tp_launch_count", "tp_gemm_trace", "tp_register_buffer", "tp_deregister_all",
 ]
 
 
@@ -75,6 +76,8 @@ _sigs = {
     "tp_prof_read": (_i, [_i, C.POINTER(C.c_double), _P64, C.POINTER(C.c_double)]),
     "tp_launch_count": (_i64, []),
     "tp_gemm_trace": (_i, [_vp]),
+    "tp_register_buffer": (_i, [_vp, _vp, _sz]),
+    "tp_deregister_all": (_i, [_vp]),
 }
 
 for _name, (_res, _args) in _sigs.items():

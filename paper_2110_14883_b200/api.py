@@ -10,6 +10,7 @@ import ctypes as C
 
 from . import _lib as L
 from ._lib import (TP_1D, TP_2D, TP_2P5D, TP_3D, TP_BF16, TP_FP32, TP_FLAG_SERIAL,  # noqa: F401
+                   TP_FLAG_PEER_FUSED,
                    TP_FLAG_W25_DEPTH_SHARDED, TP_TENSOR_BIAS, TP_TENSOR_W, TP_TENSOR_X,
                    TP_TENSOR_Y, TP_TRANSPORT_LOCAL, TP_TRANSPORT_NCCL, TP_TRANSPORT_NONE,
                    tp_linear_desc)
@@ -207,3 +208,12 @@ def tp_launch_count() -> int:
 
 def tp_gemm_trace(buf=None):
     _check(lib.tp_gemm_trace(_ptr(buf)), "tp_gemm_trace")
+
+
+def tp_register_buffer(g, t):
+    """Collective: register this rank's copy of a symmetric buffer (torch tensor)."""
+    _check(lib.tp_register_buffer(g, _ptr(t), _nbytes(t)), "tp_register_buffer")
+
+
+def tp_deregister_all(g):
+    _check(lib.tp_deregister_all(g), "tp_deregister_all")

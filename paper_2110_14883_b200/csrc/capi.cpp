@@ -1,5 +1,10 @@
 // The C ABI (include/tp_b200.h): argument validation, the grid / parallel context
 // ("parallel context manager"), and dispatch into the per-mode schedules.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <unistd.h>
+
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -266,6 +271,19 @@ tp_status tp_grid_init(tp_grid** out, tp_mode mode, int world, int rank, int q, 
       return st;
     }
   }
+  if (world > 1) {  // all ranks: barriers of the fused peer-memory path, buffer registration
+    if (transport == TP_TRANSPORT_NCCL) {
+      g->all = make_nccl_world_comm(g->nccl);
+    } else {
+      std::vector<int> everyone(world);
+      for (int r = 0; r < world; ++r) everyone[r] = r;
+      g->all = make_local_comm(id128, world, everyone, rank, cuda_device, &st);
+      if (st != TP_OK) {
+        tp_grid_destroy(g.release());
+        return st;
+      }
+    }
+  }
   *out = g.release();
   return TP_OK;
 }
@@ -294,7 +312,11 @@ tp_status tp_grid_group(const tp_grid* g, int axis, int* members) {
 tp_status tp_grid_destroy(tp_grid* g) {
   if (!g) return TP_OK;
   if (g->comm_stream) cudaStreamSynchronize(g->comm_stream);
+  for (auto& kv : g->ipc_cache) cudaIpcCloseMemHandle(kv.second);
+  g->ipc_cache.clear();
+  g->regs.clear();
   for (auto& a : g->axis) a.reset();
+  g->all.reset();
   if (g->nccl) nccl_world_destroy(g->nccl);
   for (auto& e : g->events)
     if (e) cudaEventDestroy(e);
@@ -529,6 +551,94 @@ tp_status tp_prof_read(int cls, double* total_ms, int64_t* launches, double* flo
 }
 
 int64_t tp_launch_count(void) { return g_launches.load(); }
+
+// ---- symmetric buffer registration (fused peer-memory path) ------------------------------
+namespace {
+struct RegRecord {
+  cudaIpcMemHandle_t handle;
+  uint64_t offset;  // ptr - allocation base
+  uint64_t ptr;     // raw pointer (usable as-is by ranks of the same process)
+  int64_t pid;
+  int32_t device;
+  int32_t pad;
+};
+
+tp_status alloc_range(const void* ptr, void** base) {
+  static PFN_cuMemGetAddressRange_v3020 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(p);
+  });
+  if (!fn) return fail(TP_ERR_CUDA, "cuMemGetAddressRange unavailable");
+  CUdeviceptr b = 0;
+  size_t sz = 0;
+  if (fn(&b, &sz, reinterpret_cast<CUdeviceptr>(ptr)) != CUDA_SUCCESS)
+    return fail(TP_ERR_ARG, "tp_register_buffer: not a device allocation");
+  *base = reinterpret_cast<void*>(b);
+  return TP_OK;
+}
+}  // namespace
+
+tp_status tp_register_buffer(tp_grid* g, void* ptr, size_t bytes) {
+  if (!g || !ptr || !bytes) return fail(TP_ERR_ARG, "tp_register_buffer: null argument");
+  tp_grid::RegBuf rb;
+  rb.base = static_cast<char*>(ptr);
+  rb.bytes = bytes;
+  rb.peer.assign(g->world, nullptr);
+  rb.peer[g->rank] = rb.base;
+  if (g->world > 1) {
+    if (!g->all) return fail(TP_ERR_ARG, "tp_register_buffer: grid has no transport");
+    TP_CUDA(cudaSetDevice(g->device));
+    RegRecord mine{};
+    mine.ptr = reinterpret_cast<uint64_t>(ptr);
+    mine.pid = static_cast<int64_t>(getpid());
+    mine.device = g->device;
+    if (g->transport == TP_TRANSPORT_NCCL) {
+      void* base = nullptr;
+      TP_TRY(alloc_range(ptr, &base));
+      TP_CUDA(cudaIpcGetMemHandle(&mine.handle, base));
+      mine.offset = static_cast<uint64_t>(static_cast<char*>(ptr) - static_cast<char*>(base));
+    }
+    std::vector<RegRecord> all(g->world);
+    TP_TRY(g->all->host_allgather(&mine, sizeof(RegRecord), all.data()));
+    for (int r = 0; r < g->world; ++r) {
+      if (r == g->rank) continue;
+      if (all[r].pid == mine.pid) {  // same process (LOCAL transport / threads): share directly
+        rb.peer[r] = reinterpret_cast<char*>(all[r].ptr);
+        if (all[r].device != g->device) {
+          cudaError_t e = cudaDeviceEnablePeerAccess(all[r].device, 0);
+          if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+            return fail(TP_ERR_CUDA, std::string("peer access: ") + cudaGetErrorString(e));
+          cudaGetLastError();
+        }
+        continue;
+      }
+      std::string key = std::to_string(r) + ":" +
+                        std::string(reinterpret_cast<const char*>(&all[r].handle), sizeof(cudaIpcMemHandle_t));
+      void* mapped = nullptr;
+      for (auto& kv : g->ipc_cache)
+        if (kv.first == key) mapped = kv.second;
+      if (!mapped) {
+        TP_CUDA(cudaIpcOpenMemHandle(&mapped, all[r].handle, cudaIpcMemLazyEnablePeerAccess));
+        g->ipc_cache.emplace_back(key, mapped);
+      }
+      rb.peer[r] = static_cast<char*>(mapped) + all[r].offset;
+    }
+  }
+  g->regs.push_back(std::move(rb));
+  return TP_OK;
+}
+
+tp_status tp_deregister_all(tp_grid* g) {
+  if (!g) return fail(TP_ERR_ARG, "grid is null");
+  if (g->comm_stream) cudaStreamSynchronize(g->comm_stream);
+  g->regs.clear();  // IPC mappings stay cached until tp_grid_destroy (cheap re-registration)
+  return TP_OK;
+}
 
 tp_status tp_gemm_trace(unsigned long long* buf) {
   tp::g_gemm_trace = buf;

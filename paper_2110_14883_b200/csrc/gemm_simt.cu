@@ -144,6 +144,15 @@ tp_status gemm(const GemmArgs& g, cudaStream_t s) {
   if (g.ldb < (g.trans_b ? g.K : g.N)) return fail(TP_ERR_SHAPE, "gemm: ldb too small");
   if (g.M > INT32_MAX || g.N > INT32_MAX || g.K > INT32_MAX)
     return fail(TP_ERR_UNSUPPORTED, "gemm: dims must fit int32");
+  if (g.npanels > 1) {  // fused peer-panel product: CTA-pair kernel only
+    if (g.in_dtype != TP_BF16 || g.npanels > 4 || !gemm_tc2_supported(g))
+      return fail(TP_ERR_UNSUPPORTED, "gemm: K-panels need bf16, <= 4 panels and M > 128");
+    for (int p = 0; p < g.npanels; ++p)
+      if (!g.Ap[p] || !g.Bp[p] || (reinterpret_cast<uintptr_t>(g.Ap[p]) % 16) ||
+          (reinterpret_cast<uintptr_t>(g.Bp[p]) % 16) || (g.lda % 8) || (g.ldb % 8))
+        return fail(TP_ERR_SHAPE, "gemm: K-panel operands need 16-byte aligned bases / strides");
+    return gemm_tc2_bf16(g, s);
+  }
   if (g.in_dtype == TP_FP32) return gemm_simt_f32(g, s);
   // TMA: 16-byte aligned bases and row strides (bf16: multiples of 8 elements)
   if ((reinterpret_cast<uintptr_t>(g.A) % 16) || (reinterpret_cast<uintptr_t>(g.B) % 16) ||

@@ -43,6 +43,7 @@ constexpr int kABytes = kBM * kBK * 2;
 constexpr int kOutBytes = 32 * 128;  // per epilogue warp and buffer: 32 rows x 128 B staging
 constexpr int kThreads = 192;
 constexpr int kMaxProbs = 2;
+constexpr int kMaxPanels = 4;  // K-panels per problem (peer shards of a fused SUMMA)
 
 // Pair-tile width BNP (256 or 128): B columns per CTA, ring depth, TMEM, smem.
 template <int BNP>
@@ -57,7 +58,7 @@ struct PC {
 };
 
 struct Prob {
-  CUtensorMap tmA, tmB, tmD;
+  CUtensorMap tmA[kMaxPanels], tmB[kMaxPanels], tmD;  // one A/B map per K-panel
   const float* C;
   const void* bias;
   float* part;
@@ -70,6 +71,7 @@ struct Prob {
   int num_m, num_n;
   int splits, kb_per_split;
   int c_vec;
+  int npanels, kb_panel, num_kb;  // K = npanels panels of kb_panel 64-wide k-blocks
   int unit0;  // first unit of this problem in the launch's unit space
 };
 
@@ -287,8 +289,10 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < G.nprob; ++i) {
-      tma_prefetch(&G.p[i].tmA);
-      tma_prefetch(&G.p[i].tmB);
+      for (int k = 0; k < G.p[i].npanels; ++k) {
+        tma_prefetch(&G.p[i].tmA[k]);
+        tma_prefetch(&G.p[i].tmB[k]);
+      }
       tma_prefetch(&G.p[i].tmD);
     }
     for (int s = 0; s < P::Stages; ++s) {
@@ -320,7 +324,7 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
       for (int u = cid; u < G.total_units; u += ncl) {
         const Unit t = unit_of<MC>(G, u, pair);
         const Prob& pr = G.p[t.prob];
-        const int num_k = (pr.K + kBK - 1) / kBK;
+        const int num_k = pr.num_kb;
         const int kb0 = t.split * pr.kb_per_split;
         const int kb1 = min(num_k, kb0 + pr.kb_per_split);
         const int m0 = t.mb * 256 + static_cast<int>(rank) * kBM;
@@ -332,43 +336,47 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
             t_wait += clock64() - t0;
           }
           if (leader) mbar_expect_tx(&full[stage], 2 * P::StageBytes);
+          // k-block kb lives in K-panel kb / kb_panel (its own tensor maps: e.g. a peer's shard)
+          const CUtensorMap* mA = &pr.tmA[kb / pr.kb_panel];
+          const CUtensorMap* mB = &pr.tmB[kb / pr.kb_panel];
+          const int kc = (kb % pr.kb_panel) * kBK;
           uint8_t* a_dst = sA + stage * kABytes;
           uint8_t* b_dst = sB + stage * P::BBytes;
           // ---- A: this CTA's 128 rows (K-major: one box; MN-major: two 64-wide chunks)
           if (MC != 2) {
             if (!pr.a_mn) {
-              tma_load_2d_pair(&pr.tmA, &full[stage], a_dst, kb * kBK, m0);
+              tma_load_2d_pair(mA, &full[stage], a_dst, kc, m0);
             } else {
               for (int c = 0; c < kBM / 64; ++c)
-                tma_load_2d_pair(&pr.tmA, &full[stage], a_dst + c * (kBK * 128), m0 + c * 64, kb * kBK);
+                tma_load_2d_pair(mA, &full[stage], a_dst + c * (kBK * 128), m0 + c * 64, kc);
             }
           } else {  // pair p fetches the p-th half and multicasts it to the same-rank CTAs
             if (!pr.a_mn)
-              tma_load_2d_pair_mc(&pr.tmA, &full[stage], a_dst + pair * 64 * 128, kb * kBK,
+              tma_load_2d_pair_mc(mA, &full[stage], a_dst + pair * 64 * 128, kc,
                                   m0 + pair * 64, xmask);
             else
-              tma_load_2d_pair_mc(&pr.tmA, &full[stage], a_dst + pair * (kBK * 128),
-                                  m0 + pair * 64, kb * kBK, xmask);
+              tma_load_2d_pair_mc(mA, &full[stage], a_dst + pair * (kBK * 128),
+                                  m0 + pair * 64, kc, xmask);
           }
           // ---- B: this CTA's BNP/2 columns
           if (MC != 3) {
             if (!pr.b_mn) {
-              tma_load_2d_pair(&pr.tmB, &full[stage], b_dst, kb * kBK, n0);
+              tma_load_2d_pair(mB, &full[stage], b_dst, kc, n0);
             } else {
               for (int c = 0; c < P::BNC / 64; ++c)
-                tma_load_2d_pair(&pr.tmB, &full[stage], b_dst + c * (kBK * 128), n0 + c * 64, kb * kBK);
+                tma_load_2d_pair(mB, &full[stage], b_dst + c * (kBK * 128), n0 + c * 64, kc);
             }
           } else {  // pairs stacked in M share B: pair p fetches half and multicasts it
             constexpr int BNC = P::BNC;
             if (!pr.b_mn)
-              tma_load_2d_pair_mc(&pr.tmB, &full[stage], b_dst + pair * (BNC / 2) * 128, kb * kBK,
+              tma_load_2d_pair_mc(mB, &full[stage], b_dst + pair * (BNC / 2) * 128, kc,
                                   n0 + pair * (BNC / 2), xmask);
             else if (BNC >= 128)
-              tma_load_2d_pair_mc(&pr.tmB, &full[stage], b_dst + pair * (kBK * 128), n0 + pair * 64,
-                                  kb * kBK, xmask);
+              tma_load_2d_pair_mc(mB, &full[stage], b_dst + pair * (kBK * 128), n0 + pair * 64,
+                                  kc, xmask);
             else
-              tma_load_2d_pair_mc(&pr.tmB, &full[stage], b_dst + pair * (kBK / 2) * 128, n0,
-                                  kb * kBK + pair * (kBK / 2), xmask);
+              tma_load_2d_pair_mc(mB, &full[stage], b_dst + pair * (kBK / 2) * 128, n0,
+                                  kc + pair * (kBK / 2), xmask);
           }
           if (++stage == P::Stages) {
             stage = 0;
@@ -392,7 +400,7 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
       for (int u = cid; u < G.total_units; u += ncl) {
         const Unit t = unit_of<MC>(G, u, pair);
         const Prob& pr = G.p[t.prob];
-        const int num_k = (pr.K + kBK - 1) / kBK;
+        const int num_k = pr.num_kb;
         const int kb0 = t.split * pr.kb_per_split;
         const int kb1 = min(num_k, kb0 + pr.kb_per_split);
         const uint32_t idesc = idesc_bf16_f32(256, BNP, pr.a_mn != 0, pr.b_mn != 0);
@@ -636,15 +644,23 @@ tp_status setup_prob(const GemmArgs& g, Prob& pr, int clusters, bool allow_split
   pr.a_mn = g.trans_a ? 1 : 0;
   pr.b_mn = g.trans_b ? 0 : 1;
   // multicast halves: MC 2 loads half of the A rows per pair, MC 3 half of the B tile
-  if (!pr.a_mn)
-    TP_TRY(make_map2(&pr.tmA, BF, 2, g.A, g.K, g.M, g.lda, kBK, MC == 2 ? kBM / 2 : kBM));
-  else
-    TP_TRY(make_map2(&pr.tmA, BF, 2, g.A, g.M, g.K, g.lda, 64, kBK));
-  if (!pr.b_mn)
-    TP_TRY(make_map2(&pr.tmB, BF, 2, g.B, g.K, g.N, g.ldb, kBK, MC == 3 ? P::BNC / 2 : P::BNC));
-  else
-    TP_TRY(make_map2(&pr.tmB, BF, 2, g.B, g.N, g.K, g.ldb, 64,
-                     (MC == 3 && P::BNC < 128) ? kBK / 2 : kBK));
+  pr.npanels = g.npanels > 1 ? g.npanels : 1;
+  if (pr.npanels > kMaxPanels) return fail(TP_ERR_UNSUPPORTED, "gemm: more than 4 K-panels");
+  for (int k = 0; k < pr.npanels; ++k) {
+    const void* A = pr.npanels > 1 ? g.Ap[k] : g.A;
+    const void* B = pr.npanels > 1 ? g.Bp[k] : g.B;
+    if (!pr.a_mn)
+      TP_TRY(make_map2(&pr.tmA[k], BF, 2, A, g.K, g.M, g.lda, kBK, MC == 2 ? kBM / 2 : kBM));
+    else
+      TP_TRY(make_map2(&pr.tmA[k], BF, 2, A, g.M, g.K, g.lda, 64, kBK));
+    if (!pr.b_mn)
+      TP_TRY(make_map2(&pr.tmB[k], BF, 2, B, g.K, g.N, g.ldb, kBK, MC == 3 ? P::BNC / 2 : P::BNC));
+    else
+      TP_TRY(make_map2(&pr.tmB[k], BF, 2, B, g.N, g.K, g.ldb, 64,
+                       (MC == 3 && P::BNC < 128) ? kBK / 2 : kBK));
+  }
+  pr.kb_panel = static_cast<int>((g.K + kBK - 1) / kBK);
+  pr.num_kb = pr.kb_panel * pr.npanels;
   if (g.out_dtype == TP_BF16)
     TP_TRY(make_map2(&pr.tmD, BF, 2, g.D, g.N, g.M, g.ldd, 64, 32));
   else
@@ -664,7 +680,7 @@ tp_status setup_prob(const GemmArgs& g, Prob& pr, int clusters, bool allow_split
   pr.counters = nullptr;
   const int supers = super_tiles(MC, pr.num_m, pr.num_n);
   const int ptiles = supers * pairs_of(MC);
-  const int num_k = (pr.K + kBK - 1) / kBK;
+  const int num_k = pr.num_kb;
   int S = 1;
   static const int env_split = [] {
     const char* e = std::getenv("TP_GEMM_SPLITK");
@@ -718,7 +734,7 @@ tp_status launch2(const GemmArgs* gs, int n, cudaStream_t s) {
     TP_TRY((setup_prob<BNP, MC>(gs[i], G.p[i], clusters, n == 1, ws, ws_left, s)));
     G.p[i].unit0 = units;
     units += super_tiles(MC, G.p[i].num_m, G.p[i].num_n) * G.p[i].splits;
-    flops += 2.0 * double(gs[i].M) * double(gs[i].N) * double(gs[i].K);
+    flops += 2.0 * double(gs[i].M) * double(gs[i].N) * double(gs[i].K) * G.p[i].npanels;
   }
   G.total_units = units;
   // persistent grid; when a collective runs concurrently (SUMMA panel broadcast under this

@@ -388,8 +388,94 @@ tp_status summa_atb(Ctx& C, const Plane& P, const void* x, const void* dy, void*
   return TP_OK;
 }
 
+// =========================================================================== fused peer SUMMA
+// TP_FLAG_PEER_FUSED. Owner computes: every output block is ONE panel
+// GEMM whose q K-panels are TMA-loaded straight from the shards of the ranks that own them
+// (registered symmetric buffers, NVLink peer memory across GPUs):
+//   Y[i,j]  = sum_t X[i,t] . W[t,j]        panels from ranks (i,t) and (t,j)
+//   dX[i,j] = sum_n dY[i,n] . W[j,n]^T     panels from ranks (i,n) and (j,n)
+//   dW[i,j] = sum_m X[m,i]^T . dY[m,j]     panels from ranks (m,i) and (m,j)
+// SUMMA's q broadcasts become TMA reads inside the GEMM and its q reduces disappear (the
+// whole contraction accumulates in TMEM); two stream-ordered barriers bracket the reads.
+int plane_rank(const tp_grid* g, const Plane& P, int i, int j) {
+  const int base = g->mode == TP_2P5D ? g->coords[0] * P.q * P.q : 0;
+  return base + i * P.q + j;
+}
+
+bool fused_ok(Ctx& C, const Plane& P, std::initializer_list<const void*> shards,
+              std::initializer_list<int64_t> rows) {
+  if (!(C.d->flags & TP_FLAG_PEER_FUSED) || C.dt != TP_BF16 || !C.g->all) return false;
+  if (C.g->mode == TP_2P5D && (C.d->flags & TP_FLAG_W25_DEPTH_SHARDED)) return false;
+  if (P.q < 2 || P.q > 4) return false;
+  if (P.kq % 8 || P.nq % 8) return false;  // TMA row strides
+  for (int64_t r : rows)
+    if (r <= 128) return false;  // CTA-pair kernel only (panels)
+  for (const void* s : shards)
+    if (!s || !C.g->peer_ptr(C.g->rank, s)) return false;
+  return true;
+}
+
+tp_status fused_barrier(Ctx& C) { return C.g->all->barrier(C.R.s); }
+
+GemmArgs panel_args(Ctx& C, const Plane& P, int64_t M, int64_t N, int64_t K, bool ta, bool tb,
+                    void* D, float alpha, const void* bias, const void* A_shard,
+                    const void* B_shard, int (*a_owner)(const Plane&, int), int (*b_owner)(const Plane&, int),
+                    const Plane& Pp) {
+  (void)Pp;
+  GemmArgs a = C.args(M, N, K, nullptr, ta, nullptr, tb, D, C.dt, alpha, nullptr, bias);
+  a.reserve_sms = 0;
+  a.ws = nullptr;
+  a.ws_bytes = 0;
+  a.npanels = P.q;
+  for (int t = 0; t < P.q; ++t) {
+    a.Ap[t] = C.g->peer_ptr(a_owner(P, t), A_shard);
+    a.Bp[t] = C.g->peer_ptr(b_owner(P, t), B_shard);
+  }
+  a.A = a.Ap[0];
+  a.B = a.Bp[0];
+  return a;
+}
+
+// owners of panel t, as global ranks, for the three products (P carries this rank's i, j)
+thread_local const tp_grid* t_grid = nullptr;
+int own_x_it(const Plane& P, int t) { return plane_rank(t_grid, P, P.i, t); }   // X[i,t]
+int own_w_tj(const Plane& P, int t) { return plane_rank(t_grid, P, t, P.j); }   // W[t,j]
+int own_dy_it(const Plane& P, int t) { return plane_rank(t_grid, P, P.i, t); }  // dY[i,t]
+int own_w_jt(const Plane& P, int t) { return plane_rank(t_grid, P, P.j, t); }   // W[j,t]
+int own_x_ti(const Plane& P, int t) { return plane_rank(t_grid, P, t, P.i); }   // X[t,i]
+int own_dy_tj(const Plane& P, int t) { return plane_rank(t_grid, P, t, P.j); }  // dY[t,j]
+
+tp_status fused_ab(Ctx& C, const Plane& P, const void* x, const void* w, const void* bias, void* y) {
+  if (C.R.plan) return TP_OK;
+  t_grid = C.g;
+  GemmArgs a = panel_args(C, P, P.mb, P.nq, P.kq, false, false, y, C.d->alpha, bias, x, w, own_x_it,
+                          own_w_tj, P);
+  TP_TRY(fused_barrier(C));  // every owner's shards are written
+  TP_TRY(gemm(a, C.R.s));
+  return fused_barrier(C);   // every reader is done before anyone overwrites its shards
+}
+
+tp_status fused_abt_atb(Ctx& C, const Plane& P, const void* dy, const void* x, const void* w,
+                        void* dx, void* dwt) {
+  if (C.R.plan) return TP_OK;
+  t_grid = C.g;
+  const float alpha = C.d->alpha;
+  GemmArgs gw = panel_args(C, P, P.kq, P.nq, P.mb, true, false, dwt, alpha, nullptr, x, dy,
+                           own_x_ti, own_dy_tj, P);
+  TP_TRY(fused_barrier(C));
+  if (dx) {
+    GemmArgs gx = panel_args(C, P, P.mb, P.kq, P.nq, false, true, dx, alpha, nullptr, dy, w,
+                             own_dy_it, own_w_jt, P);
+    TP_TRY(gemm_pair(gx, gw, C.R.s));  // both products in one grouped launch
+  } else {
+    TP_TRY(gemm(gw, C.R.s));
+  }
+  return fused_barrier(C);
+}
+
 tp_status fwd_2d(Ctx& C, const void* x, const void* w, const void* bias, void* y) {
   Plane P = plane_of(C);
+  if (fused_ok(C, P, {x, w}, {P.mb})) return fused_ab(C, P, x, w, bias, y);
   const void* W = w;
   if (C.g->mode == TP_2P5D && (C.d->flags & TP_FLAG_W25_DEPTH_SHARDED) && P.d > 1) {
     // depth-sharded W: all-gather the depth pieces of W[i,j] (row-contiguous) into `saved`
@@ -413,7 +499,9 @@ tp_status bwd_2d(Ctx& C, const void* dy, const void* x, const void* w, const voi
   float* scratch = dbias ? C.colsum_scratch(P.nq) : nullptr;
   void* db_t[2] = {dbias ? C.ws(P.nq) : nullptr, dbias ? C.ws(P.nq) : nullptr};
   // the two SUMMA chains carve separate buffers so both pipelines can stay in flight
-  if (P.q == 1 && dx) {  // one-rank plane: both products local and independent
+  if (!sharded && fused_ok(C, P, {x, w, dy}, {P.mb, P.kq})) {
+    TP_TRY(fused_abt_atb(C, P, dy, x, w, dx, dwt));
+  } else if (P.q == 1 && dx) {  // one-rank plane: both products local and independent
     if (!C.R.plan)
       TP_TRY(C.mm2(C.args(P.mb, P.kq, P.nq, dy, false, W, true, dx, C.dt, C.d->alpha, nullptr, nullptr),
                    C.args(P.kq, P.nq, P.mb, x, true, dy, false, dwt, C.dt, C.d->alpha, nullptr, nullptr)));

@@ -95,6 +95,12 @@ struct GemmArgs {
   void* ws = nullptr;    // split-K scratch (optional; no split-K without it)
   size_t ws_bytes = 0;
   int reserve_sms = 0;  // leave this many SMs free (a collective runs concurrently)
+  // K-panels (fused peer SUMMA): the contraction runs over npanels panels of K each; panel p
+  // reads A from Ap[p] and B from Bp[p] (same lda / ldb), accumulating in TMEM. npanels == 1
+  // uses A / B. Only the CTA-pair kernel takes npanels > 1.
+  int npanels = 1;
+  const void* Ap[4] = {};
+  const void* Bp[4] = {};
 };
 tp_status gemm(const GemmArgs& a, cudaStream_t s);         // dispatch + validation
 // Two independent GEMMs: one grouped CTA-pair launch when both qualify, else two launches.
@@ -129,12 +135,18 @@ class Comm {
                                   cudaStream_t s) = 0;
   virtual tp_status group_start() { return TP_OK; }
   virtual tp_status group_end() { return TP_OK; }
+  // Stream-ordered barrier: work after it on `s` starts only once every member's work before
+  // it (on their streams) has completed.
+  virtual tp_status barrier(cudaStream_t s) = 0;
+  // Host-side all-gather of `bytes` per member (setup only: buffer registration).
+  virtual tp_status host_allgather(const void* in, size_t bytes, void* out) = 0;
 };
 
 struct NcclWorld;  // transport_nccl.cpp
 std::unique_ptr<Comm> make_nccl_comm(NcclWorld* w, int color, int key, int size, int pos,
                                      tp_status* st);
 NcclWorld* nccl_world_create(int world, int rank, const void* id128, tp_status* st);
+std::unique_ptr<Comm> make_nccl_world_comm(NcclWorld* w);
 void nccl_world_destroy(NcclWorld* w);
 tp_status nccl_unique_id(void* id128);
 
@@ -155,6 +167,25 @@ struct tp_grid {
   tp_transport transport = TP_TRANSPORT_NONE;
   tp::NcclWorld* nccl = nullptr;
   std::unique_ptr<tp::Comm> axis[3];  // line along each axis (nullptr if size 1 or NONE)
+  std::unique_ptr<tp::Comm> all;      // every rank (barriers, registration); nullptr if p == 1
+  // Symmetric registered buffers (tp_register_buffer): this rank's range and every rank's
+  // pointer to its own copy, directly dereferenceable here (same process or CUDA IPC).
+  struct RegBuf {
+    char* base = nullptr;
+    size_t bytes = 0;
+    std::vector<char*> peer;
+    std::vector<void*> ipc_opened;  // IPC mappings to close on deregistration
+  };
+  std::vector<RegBuf> regs;
+  std::vector<std::pair<std::string, void*>> ipc_cache;  // (peer rank + IPC handle) -> mapping
+  // Pointer on `peer_rank` corresponding to `mine` (same offset in the same registered buffer),
+  // or nullptr if `mine` is not inside a registered buffer.
+  const void* peer_ptr(int peer_rank, const void* mine) const {
+    const char* p = static_cast<const char*>(mine);
+    for (const auto& r : regs)
+      if (p >= r.base && p < r.base + r.bytes) return r.peer[peer_rank] + (p - r.base);
+    return nullptr;
+  }
   cudaStream_t comm_stream = nullptr;
   static constexpr int kEvents = 64;
   cudaEvent_t events[kEvents] = {};

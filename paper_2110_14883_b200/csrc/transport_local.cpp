@@ -162,6 +162,19 @@ class LocalComm final : public Comm {
       return launch_sum_n(in.data(), size(), recv, count, dt, s);
     });
   }
+  tp_status barrier(cudaStream_t s) override {
+    return exchange(nullptr, nullptr, s, [](std::vector<Slot>&) -> tp_status { return TP_OK; });
+  }
+  tp_status host_allgather(const void* in, size_t bytes, void* out) override {
+    auto& sl = grp_->slots[calls_ & 1];
+    ++calls_;
+    sl[pos_].src = in;
+    grp_->barrier();
+    for (int m = 0; m < size(); ++m)
+      std::memcpy(static_cast<char*>(out) + m * bytes, sl[m].src, bytes);
+    grp_->barrier();
+    return TP_OK;
+  }
 
  private:
   template <typename Body>

@@ -31,9 +31,11 @@ ncclDataType_t nt(tp_dtype d) { return d == TP_BF16 ? ncclBfloat16 : ncclFloat32
 
 class NcclComm final : public Comm {
  public:
-  NcclComm(ncclComm_t c, int size, int pos) : c_(c), size_(size), pos_(pos) {}
+  NcclComm(ncclComm_t c, int size, int pos, bool owns = true)
+      : c_(c), size_(size), pos_(pos), owns_(owns) {}
   ~NcclComm() override {
-    if (c_) ncclCommDestroy(c_);
+    if (scratch_) cudaFree(scratch_);
+    if (c_ && owns_) ncclCommDestroy(c_);
   }
   int size() const override { return size_; }
   int pos() const override { return pos_; }
@@ -74,10 +76,39 @@ class NcclComm final : public Comm {
     TP_NCCL(ncclGroupEnd());
     return TP_OK;
   }
+  // a 4-byte all-reduce: stream-ordered, completes on each member only after every member's
+  // prior work on its stream
+  tp_status barrier(cudaStream_t s) override {
+    if (!scratch_) TP_CUDA(cudaMalloc(&scratch_, 256));
+    TP_NCCL(ncclAllReduce(scratch_, scratch_, 1, ncclInt32, ncclSum, c_, s));
+    return TP_OK;
+  }
+  tp_status host_allgather(const void* in, size_t bytes, void* out) override {
+    char* d = nullptr;
+    cudaStream_t st = nullptr;
+    TP_CUDA(cudaMalloc(&d, bytes * (size_ + 1)));
+    TP_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    tp_status rc = TP_OK;
+    if (cudaMemcpyAsync(d, in, bytes, cudaMemcpyHostToDevice, st) != cudaSuccess) rc = TP_ERR_CUDA;
+    if (rc == TP_OK) {
+      ncclResult_t r = ncclAllGather(d, d + bytes, bytes, ncclChar, c_, st);
+      if (r != ncclSuccess) rc = nccl_fail(r, "ncclAllGather (registration)");
+    }
+    if (rc == TP_OK && cudaMemcpyAsync(out, d + bytes, bytes * size_, cudaMemcpyDeviceToHost, st) !=
+                           cudaSuccess)
+      rc = TP_ERR_CUDA;
+    if (cudaStreamSynchronize(st) != cudaSuccess && rc == TP_OK) rc = TP_ERR_CUDA;
+    cudaStreamDestroy(st);
+    cudaFree(d);
+    if (rc == TP_ERR_CUDA) return fail(TP_ERR_CUDA, "host_allgather: CUDA copy failed");
+    return rc;
+  }
 
  private:
   ncclComm_t c_;
   int size_, pos_;
+  bool owns_;
+  int* scratch_ = nullptr;
 };
 
 }  // namespace
@@ -123,6 +154,11 @@ std::unique_ptr<Comm> make_nccl_comm(NcclWorld* w, int color, int key, int size,
   }
   *st = TP_OK;
   return std::make_unique<NcclComm>(c, size, pos);
+}
+
+// Non-owning view of the world communicator (destroyed with the NcclWorld).
+std::unique_ptr<Comm> make_nccl_world_comm(NcclWorld* w) {
+  return std::make_unique<NcclComm>(w->world, w->size, w->rank, /*owns=*/false);
 }
 
 }  // namespace tp

@@ -42,6 +42,11 @@ class TPMLP:
         self.ws = torch.empty(max(max(s[0] for s in sizes), 256), device="cuda", dtype=torch.uint8)
         self.saved = [torch.empty(s[1], device="cuda", dtype=torch.uint8) if s[1] else None
                       for s in sizes]
+        if flags & api.TP_FLAG_PEER_FUSED:
+            # every tensor a peer may read is a symmetric registered buffer (collective, same
+            # order on all ranks): layer inputs X / Y_i, weights W_i, gradients dY / dX_i
+            for t in [self.x, *self.W, *self.Y, self.dY, *self.dX]:
+                api.tp_register_buffer(self.g, t)
         if fill:
             self.fill_inputs()
 
