@@ -31,6 +31,11 @@
 #include "sm100_ptx.cuh"
 #include "tp_internal.h"
 
+// per-k-block clock64 instrumentation of the main loops (tools/gemm_trace.py); off by default
+#ifndef TP_LOOP_CLOCKS
+#define TP_LOOP_CLOCKS 0
+#endif
+
 namespace tp {
 unsigned long long* g_gemm_trace = nullptr;  // set by tp_gemm_trace (tools only)
 namespace {
@@ -94,10 +99,15 @@ __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb
 
 // Cluster shapes (MC): 1 = one CTA pair; 2 = two pairs side by side in N sharing their A rows;
 // 3 = two pairs stacked in M sharing their B columns. A "super tile" = the cluster's tiles.
-__host__ __device__ constexpr int pairs_of(int MC) { return MC == 1 ? 1 : 2; }
+// 4 = 2x2 pairs (cluster of 8): A shared along N and B along M, both by multicast.
+__host__ __device__ constexpr int pairs_of(int MC) { return MC == 1 ? 1 : MC == 4 ? 4 : 2; }
+__host__ __device__ constexpr bool mc_a(int MC) { return MC == 2 || MC == 4; }  // A multicast
+__host__ __device__ constexpr bool mc_b(int MC) { return MC == 3 || MC == 4; }  // B multicast
 __host__ __device__ constexpr int super_tiles(int MC, int num_m, int num_n) {
-  return MC == 1 ? num_m * num_n
-                 : MC == 2 ? num_m * ((num_n + 1) / 2) : ((num_m + 1) / 2) * num_n;
+  return MC == 1   ? num_m * num_n
+         : MC == 2 ? num_m * ((num_n + 1) / 2)
+         : MC == 3 ? ((num_m + 1) / 2) * num_n
+                   : ((num_m + 1) / 2) * ((num_n + 1) / 2);
 }
 
 struct Unit {
@@ -112,7 +122,12 @@ __device__ __forceinline__ Unit unit_of(const Group& G, int u, int pair) {
   const int lu = u - P.unit0;
   const int st = lu / P.splits;
   x.split = lu % P.splits;
-  if (MC == 3) {
+  if (MC == 4) {
+    int mbs, nbs;
+    tile_coords(st, (P.num_m + 1) / 2, (P.num_n + 1) / 2, mbs, nbs);
+    x.mb = mbs * 2 + (pair >> 1);
+    x.nb = nbs * 2 + (pair & 1);
+  } else if (MC == 3) {
     int mbs;
     tile_coords(st, (P.num_m + 1) / 2, P.num_n, mbs, x.nb);
     x.mb = mbs * 2 + pair;
@@ -277,6 +292,10 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
   int* sflag = reinterpret_cast<int*>(tslot + 1);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (G.trace && threadIdx.x == 0) {  // entry timestamps (tools only)
+    G.trace[blockIdx.x * 16 + 7] = globaltimer();
+    G.trace[blockIdx.x * 16 + 10] = clock64();
+  }
   const uint32_t crank = cluster_rank();
   const uint32_t rank = crank & 1;   // position in the CTA pair
   const int pair = static_cast<int>(crank >> 1);
@@ -285,7 +304,16 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
   const int cid = blockIdx.x / (2 * NP), ncl = gridDim.x / (2 * NP);
   constexpr uint16_t kAllMask = static_cast<uint16_t>((1u << (2 * NP)) - 1);
   const uint16_t pair_mask = static_cast<uint16_t>(0x3u << (2 * pair));
-  const uint16_t xmask = static_cast<uint16_t>((1u << rank) | (1u << (2 + rank)));
+  // multicast partners (same rank in the pair): MC 2/3 the other pair; MC 4 (pair = 2*pm + pn)
+  // A goes to the pairs of the same pair-row pm, B to the pairs of the same pair-column pn
+  const int a_idx = MC == 4 ? (pair & 1) : pair;   // which half of the shared A box this pair loads
+  const int b_idx = MC == 4 ? (pair >> 1) : pair;  // which half of the shared B box
+  const uint16_t xmask_a = static_cast<uint16_t>(
+      MC == 4 ? (1u << (4 * (pair >> 1) + rank)) | (1u << (4 * (pair >> 1) + 2 + rank))
+              : (1u << rank) | (1u << (2 + rank)));
+  const uint16_t xmask_b = static_cast<uint16_t>(
+      MC == 4 ? (1u << (2 * (pair & 1) + rank)) | (1u << (4 + 2 * (pair & 1) + rank))
+              : (1u << rank) | (1u << (2 + rank)));
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < G.nprob; ++i) {
@@ -314,89 +342,115 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
   // touched only once the previous kernel's results are visible
   pdl_launch_dependents();
   pdl_wait();
+  if (G.trace && threadIdx.x == 0) G.trace[blockIdx.x * 16 + 8] = globaltimer();
 
   if (warp == 0) {
-    if (lane == 0) {
+    {
       // ===== TMA producer (both CTAs of every pair) =====
+      // The whole warp runs the loop (its values stay warp-uniform, in uniform registers) and
+      // one elected lane issues: a single thread's instruction latency would otherwise pace
+      // the pipeline (profiles/r01_gemm_v3_summary.md).
       int stage = 0;
       uint32_t phase = 0;
       unsigned long long t_wait = 0, t_begin = clock64();
       for (int u = cid; u < G.total_units; u += ncl) {
         const Unit t = unit_of<MC>(G, u, pair);
         const Prob& pr = G.p[t.prob];
-        const int num_k = pr.num_kb;
         const int kb0 = t.split * pr.kb_per_split;
-        const int kb1 = min(num_k, kb0 + pr.kb_per_split);
+        const int kb1 = min(pr.num_kb, kb0 + pr.kb_per_split);
         const int m0 = t.mb * 256 + static_cast<int>(rank) * kBM;
         const int n0 = t.nb * BNP + static_cast<int>(rank) * P::BNC;
+        // k-block kb lives in K-panel kb / kb_panel (its own tensor maps, e.g. a peer's shard);
+        // the panel and in-panel column advance incrementally (no division in the loop: the
+        // single producer thread's instruction latency is on the pipeline's critical path)
+        const int kc_end = pr.kb_panel * kBK;
+        int panel = kb0 / pr.kb_panel;
+        int kc = (kb0 - panel * pr.kb_panel) * kBK;
+        const CUtensorMap* mA = &pr.tmA[panel];
+        const CUtensorMap* mB = &pr.tmB[panel];
+        // copies: the asm "memory" clobbers below would otherwise force param-space reloads
+        const bool a_mn = pr.a_mn != 0, b_mn = pr.b_mn != 0;
+        const CUtensorMap* const tmA = pr.tmA;
+        const CUtensorMap* const tmB = pr.tmB;
         for (int kb = kb0; kb < kb1; ++kb) {
+#if TP_LOOP_CLOCKS
           {
             const unsigned long long t0 = clock64();
             mbar_wait(&empty[stage], phase ^ 1);
             t_wait += clock64() - t0;
           }
+#else
+          mbar_wait(&empty[stage], phase ^ 1);
+#endif
+          if (elect_one()) {
           if (leader) mbar_expect_tx(&full[stage], 2 * P::StageBytes);
-          // k-block kb lives in K-panel kb / kb_panel (its own tensor maps: e.g. a peer's shard)
-          const CUtensorMap* mA = &pr.tmA[kb / pr.kb_panel];
-          const CUtensorMap* mB = &pr.tmB[kb / pr.kb_panel];
-          const int kc = (kb % pr.kb_panel) * kBK;
           uint8_t* a_dst = sA + stage * kABytes;
           uint8_t* b_dst = sB + stage * P::BBytes;
           // ---- A: this CTA's 128 rows (K-major: one box; MN-major: two 64-wide chunks)
-          if (MC != 2) {
-            if (!pr.a_mn) {
+          if (!mc_a(MC)) {
+            if (!a_mn) {
               tma_load_2d_pair(mA, &full[stage], a_dst, kc, m0);
             } else {
               for (int c = 0; c < kBM / 64; ++c)
                 tma_load_2d_pair(mA, &full[stage], a_dst + c * (kBK * 128), m0 + c * 64, kc);
             }
-          } else {  // pair p fetches the p-th half and multicasts it to the same-rank CTAs
-            if (!pr.a_mn)
-              tma_load_2d_pair_mc(mA, &full[stage], a_dst + pair * 64 * 128, kc,
-                                  m0 + pair * 64, xmask);
+          } else {  // this pair fetches half a_idx and multicasts it to the A-sharing CTAs
+            if (!a_mn)
+              tma_load_2d_pair_mc(mA, &full[stage], a_dst + a_idx * 64 * 128, kc,
+                                  m0 + a_idx * 64, xmask_a);
             else
-              tma_load_2d_pair_mc(mA, &full[stage], a_dst + pair * (kBK * 128),
-                                  m0 + pair * 64, kc, xmask);
+              tma_load_2d_pair_mc(mA, &full[stage], a_dst + a_idx * (kBK * 128),
+                                  m0 + a_idx * 64, kc, xmask_a);
           }
           // ---- B: this CTA's BNP/2 columns
-          if (MC != 3) {
-            if (!pr.b_mn) {
+          if (!mc_b(MC)) {
+            if (!b_mn) {
               tma_load_2d_pair(mB, &full[stage], b_dst, kc, n0);
             } else {
               for (int c = 0; c < P::BNC / 64; ++c)
                 tma_load_2d_pair(mB, &full[stage], b_dst + c * (kBK * 128), n0 + c * 64, kc);
             }
-          } else {  // pairs stacked in M share B: pair p fetches half and multicasts it
+          } else {  // pairs stacked in M share B: this pair fetches half b_idx, multicasts it
             constexpr int BNC = P::BNC;
-            if (!pr.b_mn)
-              tma_load_2d_pair_mc(mB, &full[stage], b_dst + pair * (BNC / 2) * 128, kc,
-                                  n0 + pair * (BNC / 2), xmask);
+            if (!b_mn)
+              tma_load_2d_pair_mc(mB, &full[stage], b_dst + b_idx * (BNC / 2) * 128, kc,
+                                  n0 + b_idx * (BNC / 2), xmask_b);
             else if (BNC >= 128)
-              tma_load_2d_pair_mc(mB, &full[stage], b_dst + pair * (kBK * 128), n0 + pair * 64,
-                                  kc, xmask);
+              tma_load_2d_pair_mc(mB, &full[stage], b_dst + b_idx * (kBK * 128), n0 + b_idx * 64,
+                                  kc, xmask_b);
             else
-              tma_load_2d_pair_mc(mB, &full[stage], b_dst + pair * (kBK / 2) * 128, n0,
-                                  kc + pair * (kBK / 2), xmask);
+              tma_load_2d_pair_mc(mB, &full[stage], b_dst + b_idx * (kBK / 2) * 128, n0,
+                                  kc + b_idx * (kBK / 2), xmask_b);
           }
+          }
+          __syncwarp();
           if (++stage == P::Stages) {
             stage = 0;
             phase ^= 1;
           }
+          kc += kBK;
+          if (kc == kc_end) {
+            kc = 0;
+            ++panel;
+            mA = &tmA[panel];
+            mB = &tmB[panel];
+          }
         }
       }
-      if (G.trace) {
-        G.trace[blockIdx.x * 8 + 0] = t_wait;
-        G.trace[blockIdx.x * 8 + 1] = clock64() - t_begin;
+      if (G.trace && lane == 0) {
+        G.trace[blockIdx.x * 16 + 0] = t_wait;
+        G.trace[blockIdx.x * 16 + 1] = clock64() - t_begin;
       }
     }
   } else if (warp == 1) {
-    if (leader && lane == 0) {
-      // ===== MMA issuer (pair leader) =====
+    if (leader) {
+      // ===== MMA issuer (pair leader; whole warp, one elected lane issues) =====
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      unsigned long long t_full = 0, t_temp = 0, t_begin = clock64();
+      unsigned long long t_full = 0, t_temp = 0, t_first = 0, t_unit0 = 0, t_steady = 0, n_steady = 0,
+                         t_begin = clock64();
       for (int u = cid; u < G.total_units; u += ncl) {
         const Unit t = unit_of<MC>(G, u, pair);
         const Prob& pr = G.p[t.prob];
@@ -406,46 +460,70 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
         const uint32_t idesc = idesc_bf16_f32(256, BNP, pr.a_mn != 0, pr.b_mn != 0);
         // K-major: +32 B per 16-element K step inside the 128 B swizzle atom (SBO = 8 rows).
         // MN-major: +16 rows x 128 B per K step; LBO = one 64-wide MN chunk (BK rows).
-        const uint32_t a_step = pr.a_mn ? 2048u : 32u, a_lbo = pr.a_mn ? kBK * 128 : 16;
-        const uint32_t b_step = pr.b_mn ? 2048u : 32u, b_lbo = pr.b_mn ? kBK * 128 : 16;
+        // Descriptors are built once per unit; per k-block / K step only the 16-byte-granular
+        // start-address field (low 14 bits, no carry: smem < 256 KB) advances.
+        const uint32_t a_step4 = pr.a_mn ? 2048u / 16 : 32u / 16;
+        const uint32_t b_step4 = pr.b_mn ? 2048u / 16 : 32u / 16;
+        const uint64_t a_desc0 = sdesc_sw128(smem_u32(sA), pr.a_mn ? kBK * 128 : 16, 1024);
+        const uint64_t b_desc0 = sdesc_sw128(smem_u32(sB), pr.b_mn ? kBK * 128 : 16, 1024);
         {
           const unsigned long long t0 = clock64();
           mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
           t_temp += clock64() - t0;
         }
+        __syncwarp();
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BNP);
         for (int kb = kb0; kb < kb1; ++kb) {
+#if TP_LOOP_CLOCKS
           {
             const unsigned long long t0 = clock64();
             mbar_wait(&full[stage], phase);
-            t_full += clock64() - t0;
+            const unsigned long long t1 = clock64();
+            const unsigned long long dt = t1 - t0;
+            t_full += dt;
+            if (kb == kb0) {
+              t_first += dt;
+              t_unit0 = t1;
+            }
+            if (kb == kb1 - 1) {  // steady-state cycles per k-block inside this unit
+              t_steady += t1 - t_unit0;
+              n_steady += kb1 - kb0 - 1;
+            }
           }
+#else
+          mbar_wait(&full[stage], phase);
+#endif
           tc_fence_after();
-          const uint32_t a_base = smem_u32(sA + stage * kABytes);
-          const uint32_t b_base = smem_u32(sB + stage * P::BBytes);
+          const uint64_t ad = a_desc0 + static_cast<uint32_t>(stage * (kABytes / 16));
+          const uint64_t bd = b_desc0 + static_cast<uint32_t>(stage * (P::BBytes / 16));
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k) {
-            const uint64_t ad = sdesc_sw128(a_base + k * a_step, a_lbo, 1024);
-            const uint64_t bd = sdesc_sw128(b_base + k * b_step, b_lbo, 1024);
-            umma_bf16_cg2(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < kBK / 16; ++k)
+              umma_bf16_cg2(d_tmem, ad + k * a_step4, bd + k * b_step4, idesc,
+                            (kb > kb0 || k > 0) ? 1u : 0u);
+            umma_commit_cg2_mc(&empty[stage], kAllMask);  // slot free once these MMAs retire
           }
-          umma_commit_cg2_mc(&empty[stage], kAllMask);  // slot free once these MMAs retire
+          __syncwarp();
           if (++stage == P::Stages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit_cg2_mc(&tfull[acc], pair_mask);  // accumulator ready for the epilogue
+        if (elect_one()) umma_commit_cg2_mc(&tfull[acc], pair_mask);  // accumulator ready
+        __syncwarp();
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
         }
       }
-      if (G.trace) {
-        G.trace[blockIdx.x * 8 + 2] = t_full;
-        G.trace[blockIdx.x * 8 + 3] = t_temp;
-        G.trace[blockIdx.x * 8 + 4] = clock64() - t_begin;
+      if (G.trace && lane == 0) {
+        G.trace[blockIdx.x * 16 + 2] = t_full;
+        G.trace[blockIdx.x * 16 + 3] = t_temp;
+        G.trace[blockIdx.x * 16 + 4] = clock64() - t_begin;
+        G.trace[blockIdx.x * 16 + 12] = t_first;
+        G.trace[blockIdx.x * 16 + 13] = t_steady;
+        G.trace[blockIdx.x * 16 + 14] = n_steady;
       }
     }
   } else {
@@ -464,8 +542,11 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
       const int64_t row = row0 + lane;
       const int64_t n0 = static_cast<int64_t>(t.nb) * BNP;
       {
+        // one lane polls, the rest park at the warp barrier: 4 warps x 32 lanes spinning on
+        // try_wait for the whole main loop would contend with the TMA/MMA smem traffic
         const unsigned long long t0 = clock64();
-        mbar_wait(&tfull[acc], acc_phase);
+        if (lane == 0) mbar_wait_sleep(&tfull[acc], acc_phase, 200);
+        __syncwarp();
         t_tf += clock64() - t0;
       }
       tc_fence_after();
@@ -557,16 +638,21 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
     }
     if (lane == 0) bulk_wait0();
     if (G.trace && warp == 2 && lane == 0) {
-      G.trace[blockIdx.x * 8 + 5] = t_tf;
-      G.trace[blockIdx.x * 8 + 6] = clock64() - t_begin;
+      G.trace[blockIdx.x * 16 + 5] = t_tf;
+      G.trace[blockIdx.x * 16 + 6] = clock64() - t_begin;
     }
   }
 
   tc_fence_before();
+  __syncthreads();  // reconverge every warp (idle lanes park here) before the .aligned barrier
   cluster_sync();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc_cg2(tmem_base, P::TmemCols);
+  }
+  if (G.trace && threadIdx.x == 0) {
+    G.trace[blockIdx.x * 16 + 9] = globaltimer();
+    G.trace[blockIdx.x * 16 + 11] = clock64();
   }
 }
 
@@ -650,14 +736,14 @@ tp_status setup_prob(const GemmArgs& g, Prob& pr, int clusters, bool allow_split
     const void* A = pr.npanels > 1 ? g.Ap[k] : g.A;
     const void* B = pr.npanels > 1 ? g.Bp[k] : g.B;
     if (!pr.a_mn)
-      TP_TRY(make_map2(&pr.tmA[k], BF, 2, A, g.K, g.M, g.lda, kBK, MC == 2 ? kBM / 2 : kBM));
+      TP_TRY(make_map2(&pr.tmA[k], BF, 2, A, g.K, g.M, g.lda, kBK, mc_a(MC) ? kBM / 2 : kBM));
     else
       TP_TRY(make_map2(&pr.tmA[k], BF, 2, A, g.M, g.K, g.lda, 64, kBK));
     if (!pr.b_mn)
-      TP_TRY(make_map2(&pr.tmB[k], BF, 2, B, g.K, g.N, g.ldb, kBK, MC == 3 ? P::BNC / 2 : P::BNC));
+      TP_TRY(make_map2(&pr.tmB[k], BF, 2, B, g.K, g.N, g.ldb, kBK, mc_b(MC) ? P::BNC / 2 : P::BNC));
     else
       TP_TRY(make_map2(&pr.tmB[k], BF, 2, B, g.N, g.K, g.ldb, 64,
-                       (MC == 3 && P::BNC < 128) ? kBK / 2 : kBK));
+                       (mc_b(MC) && P::BNC < 128) ? kBK / 2 : kBK));
   }
   pr.kb_panel = static_cast<int>((g.K + kBK - 1) / kBK);
   pr.num_kb = pr.kb_panel * pr.npanels;
@@ -783,10 +869,12 @@ tp_status gemm_tc2_bf16(const GemmArgs& g, cudaStream_t s) {
   const int64_t ncols = wide ? (g.N + 255) / 256 : (g.N + 127) / 128;
   const int mc = force_mc ? force_mc : 1;
   if (wide) {
+    if (mc == 4 && ncols >= 2 && nrows >= 2) return launch2<256, 4>(&g, 1, s);
     if (mc == 2 && ncols >= 2) return launch2<256, 2>(&g, 1, s);
     if (mc == 3 && nrows >= 2) return launch2<256, 3>(&g, 1, s);
     return launch2<256, 1>(&g, 1, s);
   }
+  if (mc == 4 && ncols >= 2 && nrows >= 2) return launch2<128, 4>(&g, 1, s);
   if (mc == 2 && ncols >= 2) return launch2<128, 2>(&g, 1, s);
   if (mc == 3 && nrows >= 2) return launch2<128, 3>(&g, 1, s);
   return launch2<128, 1>(&g, 1, s);

@@ -1,0 +1,1 @@
+TP_GEMM_KERNEL=2 python tools/gemm_bench.py --shapes 8192x8192x8192,4096x4096x4096,512x4096x4096 --ops NN,NT --hot-graph 2>&1 | cut -c1-250
