@@ -24,6 +24,7 @@
 #include <cstdlib>
 #include <mutex>
 
+#include "sm100_ptx.cuh"
 #include "tp_internal.h"
 
 namespace tp {
@@ -298,8 +299,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ===== TMA producer =====
+    {
+      // ===== TMA producer: whole warp, one elected lane issues (warp-uniform values stay in
+      // uniform registers; a lone thread's instruction latency would pace the pipeline) =====
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
@@ -307,6 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tile_coords(t, num_m, num_n, mb, nb);
         for (int kb = 0; kb < num_k; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
+          if (ptx::elect_one()) {
           mbar_expect_tx(&full[stage], C::kStageBytes);
           uint8_t* a_dst = sA + stage * C::kABytes;
           uint8_t* b_dst = sB + stage * C::kBBytes;
@@ -324,6 +327,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int c = 0; c < BN / 64; ++c)
               tma_load_2d(&tmB, &full[stage], b_dst + c * (BK * 128), nb * BN + c * 64, kb * BK);
           }
+          }
+          __syncwarp();
           if (++stage == C::kStages) {
             stage = 0;
             phase ^= 1;
@@ -332,8 +337,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ===== MMA issuer =====
+    {
+      // ===== MMA issuer (whole warp, one elected lane issues) =====
       constexpr uint32_t idesc = idesc_bf16(BM, BN, A_MN, B_MN);
       int stage = 0;
       uint32_t phase = 0;
@@ -341,6 +346,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t acc_phase = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
+        __syncwarp();
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
         for (int kb = 0; kb < num_k; ++kb) {
@@ -348,23 +354,27 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
           const uint32_t a_base = smem_u32(sA + stage * C::kABytes);
           const uint32_t b_base = smem_u32(sB + stage * C::kBBytes);
+          if (ptx::elect_one()) {
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            // K-major: +32 B per 16-element K step inside the 128 B swizzle atom (SBO = 8 rows).
-            // MN-major: +16 rows x 128 B per K step; LBO = one 64-wide MN chunk (BK rows).
-            const uint64_t ad = A_MN ? sdesc(a_base + k * 2048, BK * 128, 1024)
-                                     : sdesc(a_base + k * 32, 16, 1024);
-            const uint64_t bd = B_MN ? sdesc(b_base + k * 2048, BK * 128, 1024)
-                                     : sdesc(b_base + k * 32, 16, 1024);
-            umma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+            for (int k = 0; k < BK / 16; ++k) {
+              // K-major: +32 B per 16-element K step inside the 128 B swizzle atom (SBO = 8
+              // rows). MN-major: +16 rows x 128 B per K step; LBO = one 64-wide MN chunk.
+              const uint64_t ad = A_MN ? sdesc(a_base + k * 2048, BK * 128, 1024)
+                                       : sdesc(a_base + k * 32, 16, 1024);
+              const uint64_t bd = B_MN ? sdesc(b_base + k * 2048, BK * 128, 1024)
+                                       : sdesc(b_base + k * 32, 16, 1024);
+              umma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+            }
+            umma_commit(&empty[stage]);  // smem slot free once these MMAs retire
           }
-          umma_commit(&empty[stage]);  // smem slot free once these MMAs retire
+          __syncwarp();
           if (++stage == C::kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        if (ptx::elect_one()) umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        __syncwarp();
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -379,7 +389,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       int mb, nb;
       tile_coords(t, num_m, num_n, mb, nb);
-      mbar_wait(&tfull[acc], acc_phase);
+      if (lane == 0) mbar_wait(&tfull[acc], acc_phase);  // one poller per warp
+      __syncwarp();
       tc_fence_after();
       const int64_t row = static_cast<int64_t>(mb) * BM + quad * 32 + lane;
 #pragma unroll 1

@@ -76,6 +76,7 @@ struct Prob {
   int num_m, num_n;
   int splits, kb_per_split;
   int c_vec;
+  int owner_wait;  // split-K: split 0 keeps its tile in TMEM and waits for the other splits
   int npanels, kb_panel, num_kb;  // K = npanels panels of kb_panel 64-wide k-blocks
   int unit0;  // first unit of this problem in the launch's unit space
 };
@@ -269,6 +270,26 @@ __device__ __forceinline__ void sum_partials(const float4* base, int splits, int
         v[4 * i + 2] += x[i].z;
         v[4 * i + 3] += x[i].w;
       }
+    }
+  }
+}
+
+// v += partials of splits 1..S-1 (split order) for sub-chunk `sub` of this thread's row. All
+// loads of one split are issued before use (memory-level parallelism: the partials are L2-hot).
+template <int CW>
+__device__ __forceinline__ void add_partials(const float4* base, int splits, int split_stride4,
+                                             int sub, float (&v)[CW]) {
+  for (int sp = 1; sp < splits; ++sp) {
+    const float4* p = base + sp * split_stride4 + (sub * (CW / 4)) * kBM;
+    float4 x[CW / 4];
+#pragma unroll
+    for (int i = 0; i < CW / 4; ++i) x[i] = __ldcg(p + i * kBM);
+#pragma unroll
+    for (int i = 0; i < CW / 4; ++i) {
+      v[4 * i] += x[i].x;
+      v[4 * i + 1] += x[i].y;
+      v[4 * i + 2] += x[i].z;
+      v[4 * i + 3] += x[i].w;
     }
   }
 }
@@ -571,8 +592,46 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(&tempty[acc], lead);
+      } else if (pr.owner_wait && t.split == 0) {
+        // ---- split-K, owner: every split is co-resident (one unit per cluster), so split 0
+        // keeps its accumulator in TMEM, waits for the other splits' partials and adds them
+        // in split order (deterministic), then stores the tile
+        const int tile = t.ptile;
+        const float4* base =
+            reinterpret_cast<const float4*>(pr.part + static_cast<int64_t>(tile) * pr.splits * P::TileElems +
+                                            rank * (kBM * BNP)) +
+            quad * 32 + lane;
+        constexpr int kSplitStride4 = P::TileElems / 4;
+        if (threadIdx.x == 64) {
+          volatile int* cnt = pr.counters + tile * 2 + rank;
+          while (*cnt < pr.splits - 1) __nanosleep(64);
+          __threadfence();
+          *cnt = 0;  // ready for the next launch
+        }
+        named_barrier_sync(1, 128);
+        if (pr.out_bf16) {
+#pragma unroll 1
+          for (int sub = 0; sub < BNP / 64; ++sub) {
+            float v[64];
+            tmem_cols<64>(t_row, sub, v);
+            add_partials<64>(base, pr.splits, kSplitStride4, sub, v);
+            store_box<64>(pr, stg, nbox, lane, v, row, n0 + sub * 64, row0);
+          }
+        } else {
+#pragma unroll 1
+          for (int sub = 0; sub < BNP / 32; ++sub) {
+            float v[32];
+            tmem_cols<32>(t_row, sub, v);
+            add_partials<32>(base, pr.splits, kSplitStride4, sub, v);
+            store_box<32>(pr, stg, nbox, lane, v, row, n0 + sub * 32, row0);
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(&tempty[acc], lead);
       } else {
-        // ---- split-K: publish this split's fp32 partial, the last split reduces ----
+        // ---- split-K: publish this split's fp32 partial; with owner_wait split 0 adds it,
+        // otherwise the last split to arrive reduces all partials ----
         // partial layout per CTA half: float4 slot f (column/4) major, row minor, so a warp's
         // 32 rows of one slot are 512 contiguous bytes (coalesced store and reload)
         const int tile = t.ptile;
@@ -597,7 +656,9 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
         if (lane == 0) mbar_arrive_cluster(&tempty[acc], lead);  // TMEM free for the next unit
         __threadfence();
         named_barrier_sync(1, 128);
-        if (threadIdx.x == 64) {
+        if (pr.owner_wait) {
+          if (threadIdx.x == 64) atomicAdd(pr.counters + tile * 2 + rank, 1);
+        } else if (threadIdx.x == 64) {
           int* cnt = pr.counters + tile * 2 + rank;
           const int old = atomicAdd(cnt, 1);
           const int last = old == pr.splits - 1;
@@ -605,7 +666,7 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
           *sflag = last;
         }
         named_barrier_sync(1, 128);
-        const int last = *sflag;
+        const int last = pr.owner_wait ? 0 : *sflag;
         named_barrier_sync(1, 128);
         if (last) {
           __threadfence();
@@ -764,6 +825,7 @@ tp_status setup_prob(const GemmArgs& g, Prob& pr, int clusters, bool allow_split
   pr.c_vec = !g.C || ((reinterpret_cast<uintptr_t>(g.C) % 16 == 0) && (g.ldc % 4 == 0));
   pr.part = nullptr;
   pr.counters = nullptr;
+  pr.owner_wait = 0;
   const int supers = super_tiles(MC, pr.num_m, pr.num_n);
   const int ptiles = supers * pairs_of(MC);
   const int num_k = pr.num_kb;
@@ -817,7 +879,11 @@ tp_status launch2(const GemmArgs* gs, int n, cudaStream_t s) {
   for (int i = 0; i < n; ++i) {
     // no split-K inside a group: measured slower (the partial round trip outweighs the balance
     // gain on the C2 backward, 0.135 vs 0.126 ms/step)
-    TP_TRY((setup_prob<BNP, MC>(gs[i], G.p[i], clusters, n == 1, ws, ws_left, s)));
+    static const int group_split = [] {
+      const char* e = std::getenv("TP_GEMM_GROUP_SPLIT");
+      return e ? std::atoi(e) : 0;
+    }();
+    TP_TRY((setup_prob<BNP, MC>(gs[i], G.p[i], clusters, n == 1 || group_split, ws, ws_left, s)));
     G.p[i].unit0 = units;
     units += super_tiles(MC, G.p[i].num_m, G.p[i].num_n) * G.p[i].splits;
     flops += 2.0 * double(gs[i].M) * double(gs[i].N) * double(gs[i].K) * G.p[i].npanels;
@@ -829,6 +895,13 @@ tp_status launch2(const GemmArgs* gs, int n, cudaStream_t s) {
   if (gs[0].reserve_sms > 0)
     cap = std::max(1, std::min(cap, (sm_count() - gs[0].reserve_sms) / (2 * pairs_of(MC))));
   const int grid = 2 * pairs_of(MC) * (units < cap ? units : cap);
+  // split 0 may wait for its sibling splits only when every unit has its own resident cluster
+  static const int env_owner = [] {
+    const char* e = std::getenv("TP_GEMM_SPLIT_OWNER");
+    return e ? std::atoi(e) : 1;
+  }();
+  for (int i = 0; i < n; ++i)
+    G.p[i].owner_wait = (env_owner && G.p[i].splits > 1 && units <= grid / (2 * pairs_of(MC))) ? 1 : 0;
   const int tok = prof_begin(0, s, flops);
   TP_CUDA(launch_pdl(kern, dim3(grid), dim3(kThreads), P::Smem, s, G));
   count_launch();
