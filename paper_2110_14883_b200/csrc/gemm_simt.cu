@@ -191,7 +191,25 @@ namespace tp {
 // the CTA-pair kernel takes them in ONE persistent launch, so the tiles of a small-M product
 // (few tiles, long K) and of a short-K product (many tiles) share the machine instead of
 // each leaving SMs idle; otherwise (or with TP_GEMM_KERNEL=1 / TP_GEMM_GROUP=0) two launches.
-tp_status gemm_pair(const GemmArgs& a, const GemmArgs& b, cudaStream_t s) {
+namespace {
+bool group_eligible(const GemmArgs& g) {
+  if (g.in_dtype != TP_BF16 || g.M <= 0 || g.N <= 0 || g.K <= 0 || !g.A || !g.B || !g.D ||
+      g.ldd < g.N || (g.C && g.ldc < g.N) || g.lda < (g.trans_a ? g.M : g.K) ||
+      g.ldb < (g.trans_b ? g.K : g.N) || g.M > INT32_MAX || g.N > INT32_MAX || g.K > INT32_MAX ||
+      (g.lda % 8) || (g.ldb % 8) || g.npanels > 4 || !gemm_tc2_supported(g))
+    return false;
+  const int np = g.npanels > 1 ? g.npanels : 1;
+  for (int p = 0; p < np; ++p) {
+    const void* A = g.npanels > 1 ? g.Ap[p] : g.A;
+    const void* B = g.npanels > 1 ? g.Bp[p] : g.B;
+    if (!A || !B || (reinterpret_cast<uintptr_t>(A) % 16) || (reinterpret_cast<uintptr_t>(B) % 16))
+      return false;
+  }
+  return true;
+}
+}  // namespace
+
+tp_status gemm_group(const GemmArgs* gs, int n, cudaStream_t s) {
   static const int force = [] {
     const char* e = std::getenv("TP_GEMM_KERNEL");
     return e ? std::atoi(e) : 0;
@@ -200,17 +218,16 @@ tp_status gemm_pair(const GemmArgs& a, const GemmArgs& b, cudaStream_t s) {
     const char* e = std::getenv("TP_GEMM_GROUP");
     return e ? std::atoi(e) : 1;
   }();
-  auto eligible = [](const GemmArgs& g) {
-    return g.in_dtype == TP_BF16 && g.M > 0 && g.N > 0 && g.K > 0 && g.A && g.B && g.D &&
-           g.ldd >= g.N && (!g.C || g.ldc >= g.N) && g.lda >= (g.trans_a ? g.M : g.K) &&
-           g.ldb >= (g.trans_b ? g.K : g.N) && g.M <= INT32_MAX && g.N <= INT32_MAX &&
-           g.K <= INT32_MAX && (reinterpret_cast<uintptr_t>(g.A) % 16) == 0 &&
-           (reinterpret_cast<uintptr_t>(g.B) % 16) == 0 && (g.lda % 8) == 0 && (g.ldb % 8) == 0 &&
-           gemm_tc2_supported(g);
-  };
-  if (force != 1 && group_env && eligible(a) && eligible(b)) return gemm_tc2_group(a, b, s);
-  TP_TRY(gemm(a, s));
-  return gemm(b, s);
+  bool all = n >= 1 && n <= 4 && force != 1 && group_env;
+  for (int i = 0; all && i < n; ++i) all = group_eligible(gs[i]);
+  if (all && n > 1) return gemm_tc2_group(gs, n, s);
+  for (int i = 0; i < n; ++i) TP_TRY(gemm(gs[i], s));
+  return TP_OK;
+}
+
+tp_status gemm_pair(const GemmArgs& a, const GemmArgs& b, cudaStream_t s) {
+  const GemmArgs gs[2] = {a, b};
+  return gemm_group(gs, 2, s);
 }
 
 }  // namespace tp

@@ -47,7 +47,7 @@ constexpr int kBK = 64;
 constexpr int kABytes = kBM * kBK * 2;
 constexpr int kOutBytes = 32 * 128;  // per epilogue warp and buffer: 32 rows x 128 B staging
 constexpr int kThreads = 192;
-constexpr int kMaxProbs = 2;
+constexpr int kMaxProbs = 4;
 constexpr int kMaxPanels = 4;  // K-panels per problem (peer shards of a fused SUMMA)
 
 // Pair-tile width BNP (256 or 128): B columns per CTA, ring depth, TMEM, smem.
@@ -118,7 +118,10 @@ struct Unit {
 template <int MC>
 __device__ __forceinline__ Unit unit_of(const Group& G, int u, int pair) {
   Unit x;
-  x.prob = (G.nprob > 1 && u >= G.p[1].unit0) ? 1 : 0;
+  x.prob = 0;
+#pragma unroll
+  for (int i = 1; i < kMaxProbs; ++i)
+    if (i < G.nprob && u >= G.p[i].unit0) x.prob = i;
   const Prob& P = G.p[x.prob];
   const int lu = u - P.unit0;
   const int st = lu / P.splits;
@@ -953,12 +956,15 @@ tp_status gemm_tc2_bf16(const GemmArgs& g, cudaStream_t s) {
   return launch2<128, 1>(&g, 1, s);
 }
 
-// Two independent problems in one launch, 256x256 pair tiles; the problem with more K blocks
-// per tile goes first so the round-robin unit assignment front-loads the long units.
-tp_status gemm_tc2_group(const GemmArgs& a, const GemmArgs& b, cudaStream_t s) {
-  GemmArgs gs[2] = {a, b};
-  if (b.K > a.K) std::swap(gs[0], gs[1]);
-  return launch2<256, 1>(gs, 2, s);
+// Up to four independent problems in one launch, 256x256 pair tiles; problems with more K
+// blocks per tile go first so the round-robin unit assignment front-loads the long units.
+tp_status gemm_tc2_group(const GemmArgs* in, int n, cudaStream_t s) {
+  if (n < 1 || n > kMaxProbs) return fail(TP_ERR_UNSUPPORTED, "gemm group: 1..4 problems");
+  GemmArgs gs[kMaxProbs];
+  for (int i = 0; i < n; ++i) gs[i] = in[i];
+  auto kblocks = [](const GemmArgs& g) { return g.K * (g.npanels > 1 ? g.npanels : 1); };
+  std::stable_sort(gs, gs + n, [&](const GemmArgs& x, const GemmArgs& y) { return kblocks(x) > kblocks(y); });
+  return launch2<256, 1>(gs, n, s);
 }
 
 }  // namespace tp

@@ -560,9 +560,132 @@ Cube cube_of(Ctx& C) {
   return Q;
 }
 
+// ---- fused peer 3D (TP_FLAG_PEER_FUSED), owner computes, l = 2.
+// Write the rank as (a, u, v): a = coords[0] (the W axis), u = X's column-block coordinate
+// (b at parity 0, c at parity 1), v = the other. Then (extent table)
+//   X(a,u,v) = rows (a l + v) M/l^2, cols u K/l;  W(a,u,v) = rows (u l + a) K/l^2, cols v N/l;
+//   Y(a,u,v) = rows (a l + u) M/l^2, cols v N/l,
+// and every output shard is ONE GEMM over l^2 (or l) K-panels read from the owners' shards:
+//   Y  = sum_{u',a''} X(a,u',u)[:, a'' K/l^2 +: K/l^2] . W(a'',u',v)
+//   dX[:, a'' K/l^2 +: K/l^2] = sum_{v'} dY(a,v,v') . W(a'',u,v')^T        (l problems)
+//   dW = sum_{a',v'} X(a',u,v')[:, a K/l^2 +: K/l^2]^T . dY(a',v',v)
+// Balanced (M N K / l^3 flops per rank, as the collective schedule) and collective-free; it
+// reads (l-1)/l of X plus (l^2-1)/l^2 of the W column block -- more W bytes than AG+RS when
+// W dominates, fewer passes through HBM (no gathered copies, no partials).
+int cube_rank(const tp_grid* g, int parity, int a, int u, int v) {
+  const int l = g->q;
+  return parity == 0 ? (a * l + u) * l + v : (a * l + v) * l + u;
+}
+
+struct Cube3 {
+  int a, u, v, par;
+};
+
+Cube3 cube3_of(const Ctx& C) {
+  const tp_grid* g = C.g;
+  Cube3 r;
+  r.par = C.d->parity_3d;
+  r.a = g->coords[0];
+  r.u = r.par == 0 ? g->coords[1] : g->coords[2];
+  r.v = r.par == 0 ? g->coords[2] : g->coords[1];
+  return r;
+}
+
+bool fused3_ok(Ctx& C, const Cube& Q, std::initializer_list<const void*> shards) {
+  if (!(C.d->flags & TP_FLAG_PEER_FUSED) || C.dt != TP_BF16 || !C.g->all || Q.l != 2) return false;
+  if (Q.mb <= 128 || Q.kb <= 128) return false;           // CTA-pair kernel (fwd/dX and dW rows)
+  if (Q.kb % 8 || Q.nl % 8 || Q.kl % 8) return false;     // TMA bases / strides (16 bytes)
+  for (const void* s : shards)
+    if (!s || !C.g->peer_ptr(C.g->rank, s)) return false;
+  return true;
+}
+
+GemmArgs fused_args(Ctx& C, int64_t M, int64_t N, int64_t K, bool ta, bool tb, void* D,
+                    int64_t lda, int64_t ldb, int64_t ldd, const void* bias) {
+  GemmArgs a = C.args(M, N, K, nullptr, ta, nullptr, tb, D, C.dt, C.d->alpha, nullptr, bias);
+  a.lda = lda;
+  a.ldb = ldb;
+  a.ldd = ldd;
+  a.reserve_sms = 0;
+  a.ws = nullptr;
+  a.ws_bytes = 0;
+  return a;
+}
+
+const void* at_col(const void* p, int64_t col, size_t esz) {
+  return static_cast<const char*>(p) + col * static_cast<int64_t>(esz);
+}
+
+tp_status fused3_fwd(Ctx& C, const Cube& Q, const void* x, const void* w, const void* bias, void* y) {
+  if (C.R.plan) return TP_OK;
+  const tp_grid* g = C.g;
+  const Cube3 r = cube3_of(C);
+  const int l = static_cast<int>(Q.l);
+  GemmArgs a = fused_args(C, Q.mb, Q.nl, Q.kb, false, false, y, Q.kl, Q.nl, Q.nl, bias);
+  a.npanels = l * l;
+  for (int u2 = 0; u2 < l; ++u2)
+    for (int a2 = 0; a2 < l; ++a2) {
+      const int p = u2 * l + a2;
+      a.Ap[p] = at_col(g->peer_ptr(cube_rank(g, r.par, r.a, u2, r.u), x), a2 * Q.kb, C.esz);
+      a.Bp[p] = g->peer_ptr(cube_rank(g, r.par, a2, u2, r.v), w);
+    }
+  a.A = a.Ap[0];
+  a.B = a.Bp[0];
+  TP_TRY(fused_barrier(C));  // every owner's shards are written
+  TP_TRY(gemm(a, C.R.s));
+  return fused_barrier(C);   // every reader is done before anyone overwrites its shards
+}
+
+tp_status fused3_bwd(Ctx& C, const Cube& Q, const void* dy, const void* x, const void* w, void* dx,
+                     void* dw, void* dbias, float* scratch, void* db_t) {
+  if (C.R.plan) return TP_OK;
+  const tp_grid* g = C.g;
+  const Cube3 r = cube3_of(C);
+  const int l = static_cast<int>(Q.l);
+  GemmArgs gs[4];
+  int n = 0;
+  if (dx) {
+    for (int a2 = 0; a2 < l; ++a2) {  // dX column sub-block a2 needs W rows owned by (a2,u,*)
+      GemmArgs& d = gs[n++];
+      d = fused_args(C, Q.mb, Q.kb, Q.nl, false, true, static_cast<char*>(dx) + a2 * Q.kb * C.esz,
+                     Q.nl, Q.nl, Q.kl, nullptr);
+      d.npanels = l;
+      for (int v2 = 0; v2 < l; ++v2) {
+        d.Ap[v2] = g->peer_ptr(cube_rank(g, r.par, r.a, r.v, v2), dy);
+        d.Bp[v2] = g->peer_ptr(cube_rank(g, r.par, a2, r.u, v2), w);
+      }
+      d.A = d.Ap[0];
+      d.B = d.Bp[0];
+    }
+  }
+  GemmArgs& e = gs[n++];
+  e = fused_args(C, Q.kb, Q.nl, Q.mb, true, false, dw, Q.kl, Q.nl, Q.nl, nullptr);
+  e.npanels = l * l;
+  for (int a1 = 0; a1 < l; ++a1)
+    for (int v2 = 0; v2 < l; ++v2) {
+      const int p = a1 * l + v2;
+      e.Ap[p] = at_col(g->peer_ptr(cube_rank(g, r.par, a1, r.u, v2), x), r.a * Q.kb, C.esz);
+      e.Bp[p] = g->peer_ptr(cube_rank(g, r.par, a1, v2, r.v), dy);
+    }
+  e.A = e.Ap[0];
+  e.B = e.Bp[0];
+  TP_TRY(fused_barrier(C));
+  TP_TRY(gemm_group(gs, n, C.R.s));  // the dX sub-blocks and dW in one persistent launch
+  TP_TRY(fused_barrier(C));
+  if (dbias) {  // db[v] = sum over the l^2 ranks holding column block v (axes a and u)
+    void* db_u = static_cast<char*>(db_t) + ((Q.nl * C.esz + 255) & ~int64_t(255));
+    TP_TRY(C.colsum(dy, Q.mb, Q.nl, db_t, scratch));
+    TP_TRY(C.order(C.R.s, C.R.cs));
+    TP_TRY(Q.cy->allreduce(db_t, db_u, Q.nl, C.dt, C.R.cs));
+    TP_TRY(Q.cw->allreduce(db_u, dbias, Q.nl, C.dt, C.R.cs));
+  }
+  return TP_OK;
+}
+
 tp_status fwd_3d(Ctx& C, const void* x, const void* w, const void* bias, void* y) {
   Cube Q = cube_of(C);
   const float alpha = C.d->alpha;
+  if (Q.l > 1 && fused3_ok(C, Q, {x, w})) return fused3_fwd(C, Q, x, w, bias, y);
   if (Q.l == 1) {
     if (C.R.plan) return TP_OK;
     return C.mm(C.d->M, C.d->N, C.d->K, x, false, w, false, y, C.dt, alpha, nullptr, bias);
@@ -599,9 +722,21 @@ tp_status bwd_3d(Ctx& C, const void* dy, const void* x, const void* w, const voi
     if (dbias) TP_TRY(C.colsum(dy, M, N, dbias, scratch));
     return TP_OK;
   }
+  if (fused3_ok(C, Q, {x, w, dy})) {
+    float* scr = dbias ? C.colsum_scratch(Q.nl) : nullptr;
+    void* dbt = dbias ? C.ws(2 * ((Q.nl + 255) & ~int64_t(255))) : nullptr;  // two temporaries
+    return fused3_bwd(C, Q, dy, x, w, dx, dw, dbias, scr, dbt);
+  }
   const char* sv = static_cast<const char*>(saved);
   const void* Xg = sv;
   const void* Wg = sv ? sv + (((Q.ml * Q.kl * C.esz) + 255) & ~size_t(255)) : nullptr;
+  if (!C.R.plan && fused3_ok(C, Q, {x, w})) {
+    // the forward ran fused and left no gathered X / W in `saved`: gather them now
+    TP_TRY(Q.cx->group_start());
+    TP_TRY(Q.cx->allgather(x, const_cast<void*>(Xg), Q.mb * Q.kl, C.dt, C.R.cs));
+    TP_TRY(Q.cw->allgather(w, const_cast<void*>(Wg), Q.kb * Q.nl, C.dt, C.R.cs));
+    TP_TRY(Q.cx->group_end());
+  }
   void* dYg = C.ws(Q.ml * Q.nl);
   void* Px = dx ? C.ws(Q.ml * Q.kl) : nullptr;
   void* Pw = C.ws(Q.kl * Q.nl);

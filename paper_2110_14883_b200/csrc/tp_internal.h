@@ -105,7 +105,10 @@ struct GemmArgs {
 tp_status gemm(const GemmArgs& a, cudaStream_t s);         // dispatch + validation
 // Two independent GEMMs: one grouped CTA-pair launch when both qualify, else two launches.
 tp_status gemm_pair(const GemmArgs& a, const GemmArgs& b, cudaStream_t s);
-tp_status gemm_tc2_group(const GemmArgs& a, const GemmArgs& b, cudaStream_t s);
+// Up to 4 independent problems in one persistent CTA-pair launch (kernel level).
+tp_status gemm_tc2_group(const GemmArgs* gs, int n, cudaStream_t s);
+// Up to 4 independent GEMMs: one grouped launch when every problem is eligible, else in turn.
+tp_status gemm_group(const GemmArgs* gs, int n, cudaStream_t s);
 tp_status gemm_tc_bf16(const GemmArgs& a, cudaStream_t s);  // tcgen05, 1 CTA per tile
 tp_status gemm_tc2_bf16(const GemmArgs& a, cudaStream_t s); // tcgen05 cta_group::2 pair tiles
 bool gemm_tc2_supported(const GemmArgs& a);

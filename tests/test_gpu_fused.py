@@ -20,10 +20,13 @@ FUSED = 0x4  # TP_FLAG_PEER_FUSED
 # (mode, p, d, M, K, N): per-rank blocks > 128 rows with ragged tails, panels of K not a
 # multiple of the 64-wide k-block (the per-panel tensor map zero-fills the tail)
 CASES = [
-    ("2d", 4, 1, 520, 400, 656),     # q=2: 260 x 200 x 328 blocks
-    ("2d", 9, 1, 408, 432, 600),     # q=3: 136 x 144 x 200
-    ("2d", 16, 1, 576, 544, 544),    # q=4: 144 x 136 x 136 (four panels per product)
-    ("2.5d", 8, 2, 800, 272, 528),   # q=2, d=2 (replicated W): 200 x 136 x 264
+    ("2d", 4, 1, 520, 400, 656, 0),     # q=2: 260 x 200 x 328 blocks
+    ("2d", 9, 1, 408, 432, 600, 0),     # q=3: 136 x 144 x 200
+    ("2d", 16, 1, 576, 544, 544, 0),    # q=4: 144 x 136 x 136 (four panels per product)
+    ("2.5d", 8, 2, 800, 272, 528, 0),   # q=2, d=2 (replicated W): 200 x 136 x 264
+    # 3D l=2, both parities: shards [M/4, K/2] [K/4, N/2] [M/4, N/2] = 136 x 288, 144 x 200
+    ("3d", 8, 1, 544, 576, 400, 0),
+    ("3d", 8, 1, 544, 576, 400, 1),
 ]
 
 
@@ -35,17 +38,18 @@ def api():
 
 
 def _id(c):
-    return f"{c[0]}-p{c[1]}-d{c[2]}"
+    return f"{c[0]}-p{c[1]}-d{c[2]}-par{c[6]}"
 
 
 @pytest.mark.parametrize("case", CASES, ids=_id)
 @pytest.mark.parametrize("with_bias", [False, True])
 def test_fused_vs_oracle(api, case, with_bias):
-    mode, p, d, M, K, N = case
+    mode, p, d, M, K, N, par = case
     X, W, dY, b = synth.layer_inputs(11, M, K, N, with_bias=True)
     b = b if with_bias else None
-    per = tp_layer(api, mode, p, d, M, K, N, X, W, dY, b, "bf16", flags=FUSED, alpha=0.5)
-    spec = spec_of(M, K, N)
+    per = tp_layer(api, mode, p, d, M, K, N, X, W, dY, b, "bf16", parity=par, flags=FUSED,
+                   alpha=0.5)
+    spec = spec_of(M, K, N, parity=par)
     Yr, dXr, dWr, dbr = oracle_layer(mode, p, d, spec, X, W, dY, b, alpha=0.5)
     assert rel_fro(gather(mode, p, d, spec, per, "Y", "Y"), Yr) <= 1e-2
     assert rel_fro(gather(mode, p, d, spec, per, "dX", "X"), dXr) <= 1e-2
@@ -60,10 +64,10 @@ def test_fused_vs_oracle(api, case, with_bias):
 def test_fused_exact_integer_bit_equal(api, case):
     """Ternary inputs: every product is an exact small integer (|sum| <= K, M < 2^24) so the
     fused TMEM accumulation must be bit-equal to the oracle (A17)."""
-    mode, p, d, M, K, N = case
+    mode, p, d, M, K, N, par = case
     X, W, dY, _ = synth.layer_inputs(5, M, K, N, kind="ternary")
-    per = tp_layer(api, mode, p, d, M, K, N, X, W, dY, None, "bf16", flags=FUSED)
-    spec = spec_of(M, K, N)
+    per = tp_layer(api, mode, p, d, M, K, N, X, W, dY, None, "bf16", parity=par, flags=FUSED)
+    spec = spec_of(M, K, N, parity=par)
     Yr, dXr, dWr, dbr = oracle_layer(mode, p, d, spec, X, W, dY)
     for key, t, ref in (("Y", "Y", Yr), ("dX", "X", dXr), ("dW", "W", dWr), ("dB", "B", dbr)):
         assert np.array_equal(gather(mode, p, d, spec, per, key, t), ref), key
@@ -72,7 +76,7 @@ def test_fused_exact_integer_bit_equal(api, case):
 def test_fused_matches_collective_schedule(api):
     """Same inputs, both schedules: results agree to bf16 rounding of differently-ordered fp32
     sums (the collective path rounds each SUMMA partial to bf16; fused rounds once)."""
-    mode, p, d, M, K, N = CASES[0]
+    mode, p, d, M, K, N, _ = CASES[0]
     X, W, dY, b = synth.layer_inputs(3, M, K, N, with_bias=True)
     a = tp_layer(api, mode, p, d, M, K, N, X, W, dY, b, "bf16", flags=FUSED)
     c = tp_layer(api, mode, p, d, M, K, N, X, W, dY, b, "bf16", flags=0)
@@ -93,3 +97,49 @@ def test_fused_falls_back_on_small_blocks(api):
     assert np.array_equal(gather("2d", 4, 1, spec, per, "Y", "Y"), Yr)
     assert np.array_equal(gather("2d", 4, 1, spec, per, "dX", "X"), dXr)
     assert np.array_equal(gather("2d", 4, 1, spec, per, "dW", "W"), dWr)
+
+
+@pytest.mark.parametrize("par", [0, 1])
+def test_fused_3d_backward_after_unfused_dy(api, par):
+    """Fused forward (X, W registered) followed by a backward whose dY is NOT registered: the
+    backward falls back to the collective schedule and must first re-gather X and W (the fused
+    forward left nothing in `saved`)."""
+    import torch
+    from tp_harness import run_ranks, to_dev, to_np, TORCH_DT
+    M, K, N = 544, 576, 400
+    X, W, dY, _ = synth.layer_inputs(7, M, K, N, kind="ternary")
+    uid = api.tp_get_unique_id(api.TP_TRANSPORT_LOCAL)
+    gX, gW, gdY = to_dev(X, "bf16"), to_dev(W, "bf16"), to_dev(dY, "bf16")
+    torch.cuda.synchronize()
+
+    def rank_fn(r):
+        g = api.tp_grid_init("3d", 8, r, 0, 1, 0, api.TP_TRANSPORT_LOCAL, uid)
+        s = torch.cuda.Stream()
+        try:
+            with torch.cuda.stream(s):
+                ds = api.desc(M, K, N, "bf16", 0, par, FUSED)
+                ext = {t: api.tp_shard_extent(g, ds, t) for t in ("X", "W", "Y")}
+                mk = lambda t: torch.empty(ext[t][1], ext[t][3], device="cuda", dtype=torch.bfloat16)
+                x, w, y, dy = mk("X"), mk("W"), mk("Y"), mk("Y")
+                api.tp_register_buffer(g, x)
+                api.tp_register_buffer(g, w)
+                api.tp_pack(g, ds, "X", gX, x)
+                api.tp_pack(g, ds, "W", gW, w)
+                api.tp_pack(g, ds, "Y", gdY, dy)
+                wsb, svb = api.tp_workspace_size(g, ds)
+                ws = torch.empty(max(wsb, 1), device="cuda", dtype=torch.uint8)
+                sv = torch.empty(svb, device="cuda", dtype=torch.uint8)
+                api.tp_linear_fwd(g, ds, x, w, None, y, sv, ws)
+                dx, dw = torch.empty_like(x), torch.empty_like(w)
+                api.tp_linear_bwd(g, ds, dy, x, w, sv, dx, dw, None, ws)
+            s.synchronize()
+            return {"Y": to_np(y), "dX": to_np(dx), "dW": to_np(dw)}
+        finally:
+            s.synchronize()
+            api.tp_grid_destroy(g)
+
+    per = run_ranks(8, rank_fn)
+    spec = spec_of(M, K, N, parity=par)
+    Yr, dXr, dWr, _ = oracle_layer("3d", 8, 1, spec, X, W, dY)
+    for key, t, ref in (("Y", "Y", Yr), ("dX", "X", dXr), ("dW", "W", dWr)):
+        assert np.array_equal(gather("3d", 8, 1, spec, per, key, t), ref), key
