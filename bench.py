@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--eager", action="store_true", help="time eager launches instead of a CUDA graph")
+    ap.add_argument("--fused", action="store_true",
+                    help="N > 1: fused peer-panel schedule (TP_FLAG_PEER_FUSED; 2D / 2.5D / 3D l=2)")
     return ap.parse_args()
 
 
@@ -170,7 +172,9 @@ def run_ours(a):
         g = api.tp_grid_init(mode, 1, 0, 0, 1, local, api.TP_TRANSPORT_NONE)
     # ---- this rank's shards, generated in place by the library's seeded generator ----
     from paper_2110_14883_b200.mlp import TPMLP
-    model = TPMLP(g, M, layers, dtype=dtype, seed=a.seed)
+    fused = a.fused and world > 1
+    model = TPMLP(g, M, layers, dtype=dtype, seed=a.seed,
+                  flags=api.TP_FLAG_PEER_FUSED if fused else 0)
     x, ws_, dy_last, dacts, grads_w = model.x, model.W, model.dY, model.dX, model.dW
     flush = torch.empty(256 << 20, device="cuda", dtype=torch.uint8)
     step = model.step
@@ -326,7 +330,7 @@ def run_ours(a):
         "config": {"workload": a.workload, "desc": wl["desc"], "mode": mode, "depth": depth,
                    "grid": list(api.tp_grid_dims(g)), "M": M, "layers": layers,
                    "flops_per_step": flops, "l2": "flushed (256 MiB write) between timed steps",
-                   "parallelism": f"tp-{mode}x{world}"},
+                   "parallelism": f"tp-{mode}x{world}" + ("-fused" if fused else "")},
         "per_gpu_tflops": round(value / world, 3),
         "wall_s": round(t_wall, 3),
         "launch": "cuda-graph replay" if graph is not None else "eager",
