@@ -210,11 +210,35 @@ tp_status tp_prof_reset(void);
 tp_status tp_prof_read(int kernel_class, double* total_ms, int64_t* launches, double* flops);
 /* Number of kernels this library has launched since load (all classes). */
 int64_t tp_launch_count(void);
-/* Diagnostics: when buf (device, >= 8 x uint64 per CTA of the largest grid) is non-NULL, the
- * CTA-pair GEMM writes per-CTA clock64 counters: [0] producer wait on free slots, [1] producer
- * total, [2] MMA wait on loaded stages, [3] MMA wait on a free accumulator, [4] MMA total,
- * [5] epilogue wait on accumulators, [6] epilogue total. NULL disables (default). */
+/* Diagnostics: when buf (device, >= 16 x uint64 per CTA of the largest grid) is non-NULL, the
+ * CTA-pair GEMM writes per-CTA counters: [0] producer wait on free slots, [1] producer total,
+ * [2] MMA wait on loaded stages, [3] MMA wait on a free accumulator, [4] MMA total, [5]
+ * epilogue wait on accumulators, [6] epilogue total (clock64; [0],[2],[12..14] only in a
+ * TP_LOOP_CLOCKS=1 build), [7]/[8]/[9] globaltimer at entry / after the prologue / at exit,
+ * [10]/[11] clock64 at entry / exit. NULL disables (default). */
 tp_status tp_gemm_trace(unsigned long long* buf);
+
+/* ---- analytic cost model --------------------- */
+/* One linear layer, fwd+bwd, bias-free, on the grid (mode, world, q, d) with desc's M, K, N,
+ * dtype, split_1d and flags (TP_FLAG_W25_DEPTH_SHARDED). Host only, no device work.
+ *   paper_elems      the paper's Table tp-comm-vol row, evaluated verbatim (elements):
+ *                    1D 2(p-1)S_x (S_y for the row split), 2D 3(q-1)(S_x+S_w),
+ *                    2.5D 3(q-1)(S_x/d+S_w) (per plane), 3D 2(l-1)/l (S_x+S_w+S_y)
+ *   counted_elems    what this library's collective schedule moves, all ranks together, in
+ *                    SPEC's conventions (bcast/reduce (g-1)m, AR 2(g-1)m, AG/RS (g-1)m_total)
+ *   link_bytes       per-GPU bytes over NVLink = counted_elems / world * element size
+ *   flops            per-GPU flops = 6 M K N / world
+ *   mem_x/w/y        per-rank at-rest elements of the X, W and Y shards
+ *   t_tensor_us, t_link_us, t_roof_us   flops / peak_tflops, link_bytes / link_gbs, their max
+ * peak_tflops / link_gbs <= 0 leave the times at 0. Errors: TP_ERR_CONSTRAINT (grid),
+ * TP_ERR_INDIVISIBLE, TP_ERR_ARG (null pointers). */
+typedef struct {
+  double paper_elems, counted_elems, link_bytes, flops;
+  double mem_x, mem_w, mem_y;
+  double t_tensor_us, t_link_us, t_roof_us;
+} tp_cost;
+tp_status tp_cost_model(tp_mode mode, int world, int q, int d, const tp_linear_desc* desc,
+                        double peak_tflops, double link_gbs, tp_cost* out);
 
 #ifdef __cplusplus
 }

@@ -36,7 +36,14 @@ EXPORTED = [
     "tp_gemm_ws_bytes",
     "tp_colsum", "tp_fill", "tp_l2_flush", "tp_prof_enable", "tp_prof_reset", "tp_prof_read",
     "tp_launch_count", "tp_gemm_trace", "tp_register_buffer", "tp_deregister_all",
+    "tp_cost_model",
 ]
+
+
+class tp_cost(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("paper_elems", "counted_elems", "link_bytes", "flops",
+                                          "mem_x", "mem_w", "mem_y", "t_tensor_us", "t_link_us",
+                                          "t_roof_us")]
 
 
 class tp_linear_desc(C.Structure):
@@ -78,6 +85,8 @@ _sigs = {
     "tp_gemm_trace": (_i, [_vp]),
     "tp_register_buffer": (_i, [_vp, _vp, _sz]),
     "tp_deregister_all": (_i, [_vp]),
+    "tp_cost_model": (_i, [_i, _i, _i, _i, C.POINTER(tp_linear_desc), C.c_double, C.c_double,
+                           C.POINTER(tp_cost)]),
 }
 
 for _name, (_res, _args) in _sigs.items():

@@ -13,7 +13,7 @@ from ._lib import (TP_1D, TP_2D, TP_2P5D, TP_3D, TP_BF16, TP_FP32, TP_FLAG_SERIA
                    TP_FLAG_PEER_FUSED,
                    TP_FLAG_W25_DEPTH_SHARDED, TP_TENSOR_BIAS, TP_TENSOR_W, TP_TENSOR_X,
                    TP_TENSOR_Y, TP_TRANSPORT_LOCAL, TP_TRANSPORT_NCCL, TP_TRANSPORT_NONE,
-                   tp_linear_desc)
+                   tp_cost, tp_linear_desc)
 
 lib = L.lib
 
@@ -217,3 +217,12 @@ def tp_register_buffer(g, t):
 
 def tp_deregister_all(g):
     _check(lib.tp_deregister_all(g), "tp_deregister_all")
+
+
+def tp_cost_model(mode, world, d_: tp_linear_desc, q=0, depth=1, peak_tflops=0.0, link_gbs=0.0):
+    """Analytic per-layer fwd+bwd cost (host only); returns a dict of the tp_cost fields."""
+    m = MODES[mode] if isinstance(mode, str) else int(mode)
+    c = tp_cost()
+    _check(lib.tp_cost_model(m, world, q, depth, C.byref(d_), float(peak_tflops), float(link_gbs),
+                             C.byref(c)), "tp_cost_model")
+    return {n: getattr(c, n) for n, _ in tp_cost._fields_}

@@ -646,3 +646,60 @@ tp_status tp_gemm_trace(unsigned long long* buf) {
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------------ analytic cost model
+// the paper's Table row next to what the library's schedules move,
+// per-GPU link bytes, flops and at-rest shard sizes, and the roofline times.
+// Written independently of oracle/closed_forms.py (tests compare the two).
+extern "C" tp_status tp_cost_model(tp_mode mode, int world, int q, int d, const tp_linear_desc* desc,
+                                   double peak_tflops, double link_gbs, tp_cost* out) {
+  if (!desc || !out) return tp::fail(TP_ERR_ARG, "tp_cost_model: null desc or out");
+  tp_grid g;
+  TP_TRY(plan_grid(&g, mode, world, 0, q, d));
+  TP_TRY(check_desc(&g, desc));
+  const double M = double(desc->M), K = double(desc->K), N = double(desc->N);
+  const double Sx = M * K, Sw = K * N, Sy = M * N, p = world;
+  const double e = desc->dtype == TP_BF16 ? 2.0 : 4.0;
+  const int j = g.q, dd = g.d;
+  const bool row = desc->split_1d != 0;
+  tp_cost c{};
+  switch (mode) {
+    case TP_1D:  // col: AR of dX in bwd; row: AR of Y in fwd (one ring AR per layer, A3)
+      c.paper_elems = 2.0 * (p - 1) * (row ? Sy : Sx);
+      c.counted_elems = c.paper_elems;
+      c.mem_x = row ? Sx / p : Sx;
+      c.mem_w = Sw / p;
+      c.mem_y = row ? Sy : Sy / p;
+      break;
+    case TP_2D:  // SUMMA: fwd bcast X,W; bwd bcast W + reduce dX, bcast X + reduce dW (A4)
+      c.paper_elems = 3.0 * (j - 1) * (Sx + Sw);
+      c.counted_elems = c.paper_elems;
+      c.mem_x = Sx / p;
+      c.mem_w = Sw / p;
+      c.mem_y = Sy / p;
+      break;
+    case TP_2P5D:  // d planes of SUMMA on S_x/d rows + depth AR(dW) or AG(W)+RS(dW) (A6, A11)
+      c.paper_elems = 3.0 * (j - 1) * (Sx / dd + Sw);
+      c.counted_elems = dd * 3.0 * (j - 1) * (Sx / dd + Sw) + 2.0 * (dd - 1) * Sw;
+      c.mem_x = Sx / p;
+      c.mem_w = (desc->flags & TP_FLAG_W25_DEPTH_SHARDED) ? Sw / p : Sw / (double(j) * j);
+      c.mem_y = Sy / p;
+      break;
+    case TP_3D:  // AG X, AG W, RS Y; AG dY, RS dX, RS dW: each tensor moves twice (A10)
+      c.paper_elems = 2.0 * (j - 1) / j * (Sx + Sw + Sy);
+      c.counted_elems = 2.0 * (j - 1) * (Sx + Sw + Sy);
+      c.mem_x = Sx / p;
+      c.mem_w = Sw / p;
+      c.mem_y = Sy / p;
+      break;
+    default:
+      return tp::fail(TP_ERR_ARG, "tp_cost_model: unknown mode");
+  }
+  c.link_bytes = c.counted_elems / p * e;
+  c.flops = 6.0 * M * K * N / p;
+  if (peak_tflops > 0) c.t_tensor_us = c.flops / (peak_tflops * 1e12) * 1e6;
+  if (link_gbs > 0) c.t_link_us = c.link_bytes / (link_gbs * 1e9) * 1e6;
+  c.t_roof_us = c.t_tensor_us > c.t_link_us ? c.t_tensor_us : c.t_link_us;
+  *out = c;
+  return TP_OK;
+}

@@ -1,0 +1,81 @@
+"""The library's analytic cost model (tp_cost_model, NEXT-4's comm-volume/scaling CLI) against
+the oracle's closed forms, which are themselves pinned to the paper's Table and to
+the simulated-collective ledger (tests/test_oracle_pins.py). Host only: runs without a GPU."""
+from fractions import Fraction
+
+import pytest
+
+from oracle import closed_forms as cf
+
+api = pytest.importorskip("paper_2110_14883_b200.api")
+
+GRIDS = [("1d", 1, 0, 1), ("1d", 2, 0, 1), ("1d", 4, 0, 1), ("1d", 8, 0, 1), ("1d", 6, 0, 1),
+         ("2d", 1, 1, 1), ("2d", 4, 2, 1), ("2d", 9, 3, 1), ("2d", 16, 4, 1),
+         ("2.5d", 4, 2, 1), ("2.5d", 8, 2, 2), ("2.5d", 18, 3, 2), ("2.5d", 32, 2, 8),
+         ("3d", 1, 1, 1), ("3d", 8, 2, 1), ("3d", 27, 3, 1)]
+SHAPES = [(144, 96, 72), (512, 4096, 4096), (16384, 8192, 24576), (72, 216, 144)]
+
+
+def _ok(mode, p, q, d, M, K, N, split):
+    if mode == "1d":
+        return (N if split == 0 else K) % p == 0
+    if mode == "2d":
+        return M % q == 0 and K % q == 0 and N % q == 0
+    if mode == "2.5d":
+        return M % (d * q) == 0 and K % q == 0 and N % q == 0
+    return M % (q * q) == 0 and K % (q * q) == 0 and N % q == 0
+
+
+@pytest.mark.parametrize("grid", GRIDS, ids=lambda g: f"{g[0]}-p{g[1]}-d{g[3]}")
+@pytest.mark.parametrize("shape", SHAPES, ids=lambda s: "x".join(map(str, s)))
+@pytest.mark.parametrize("split", [0, 1])
+def test_volumes_match_oracle(grid, shape, split):
+    mode, p, q, d = grid
+    M, K, N = shape
+    if mode != "1d" and split:
+        pytest.skip("split applies to 1D only")
+    if not _ok(mode, p, q, d, M, K, N, split):
+        pytest.skip("indivisible")
+    c = api.tp_cost_model(mode, p, api.desc(M, K, N, "bf16", split_1d=split), q=q, depth=d)
+    Sx, Sw, Sy = M * K, K * N, M * N
+    if mode == "1d":
+        paper = cf.paper_comm_volume("1d", Sy if split else Sx, Sw, p=p)
+    elif mode == "2d":
+        paper = cf.paper_comm_volume("2d", Sx, Sw, j=q)
+    elif mode == "2.5d":
+        paper = cf.paper_comm_volume("2.5d", Sx, Sw, k=q, d=d)
+    else:
+        paper = cf.paper_comm_volume("3d", Sx, Sw, Sy, l=q)
+    counted = cf.counted_volume(mode, M, K, N, p=p, q=q, d=d, split_1d="row" if split else "col")
+    assert c["paper_elems"] == pytest.approx(float(Fraction(paper)), rel=1e-12)
+    assert c["counted_elems"] == pytest.approx(float(counted), rel=1e-12)
+    assert c["link_bytes"] == pytest.approx(counted / p * 2, rel=1e-12)
+    assert c["flops"] == pytest.approx(6.0 * M * K * N / p, rel=1e-12)
+    mem = cf.memory_per_rank(mode, M, K, N, p, q=q, d=d, split_1d="row" if split else "col")
+    assert (c["mem_x"], c["mem_w"], c["mem_y"]) == (mem["X"], mem["W"], mem["Y"])
+
+
+def test_depth_sharded_weight_memory():
+    c = api.tp_cost_model("2.5d", 8, api.desc(512, 4096, 4096, "bf16", flags=1), q=2, depth=2)
+    assert c["mem_w"] == cf.memory_per_rank("2.5d", 512, 4096, 4096, 8, q=2, d=2,
+                                            w_depth_sharded=True)["W"]
+
+
+def test_roofline_times_and_survey_table():
+    """SURVEY 8(d) roofline rows for C2 (two square layers, M=512, h=4096, F = 1663.3 TF/s,
+    900 GB/s): per-GPU NVLink MB and the bound / max % of peak."""
+    from paper_2110_14883_b200 import costmodel
+    rows = {(r["grid"], r["gpus"]): r for p in (4, 8) for r in costmodel.model("c2", p)}
+    assert rows[("1d", 4)]["link_mb_per_gpu"] == 12.6
+    assert rows[("2d", 4)]["link_mb_per_gpu"] == 56.6 and rows[("2d", 4)]["bound"] == "link"
+    assert rows[("2.5d(d=2)", 8)]["link_mb_per_gpu"] == 70.3
+    assert rows[("3d", 8)]["link_mb_per_gpu"] == 21.0
+    assert rows[("3d", 8)]["max_pct_of_peak"] == 33.2
+    assert rows[("1d", 8)]["max_pct_of_peak"] == 47.5
+
+
+def test_errors():
+    with pytest.raises(api.TPError):
+        api.tp_cost_model("2d", 8, api.desc(16, 16, 16))  # 8 is not a square
+    with pytest.raises(api.TPError):
+        api.tp_cost_model("3d", 8, api.desc(6, 16, 16))  # M not divisible by l^2
