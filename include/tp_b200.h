@@ -218,6 +218,31 @@ int64_t tp_launch_count(void);
  * [10]/[11] clock64 at entry / exit. NULL disables (default). */
 tp_status tp_gemm_trace(unsigned long long* buf);
 
+/* ---- LayerNorm in the tensor-parallel layouts ------------------------ */
+/* LayerNorm over the hidden (column) dimension, per row r of the global activation A [M, H]:
+ *   mu = mean_c A[r,c], var = mean_c (A[r,c]-mu)^2, y = (A - mu)/sqrt(var + eps)*gamma + beta
+ * (textbook definition; the paper names the layer, without a formula).
+ * The activation is sharded as tensor `tensor` (TP_TENSOR_X: A = X [M, K]; TP_TENSOR_Y: A = Y
+ * [M, N]) of the layer `desc` on this grid: this rank passes its dense block [rows, cols] of
+ * tp_shard_extent(grid, desc, tensor) (row stride = cols). gamma / beta / dgamma / dbeta are
+ * the matching column block [cols] (tp_shard_extent(..., TP_TENSOR_BIAS) for Y; the X column
+ * block for X); NULL gamma = ones, NULL beta = zeros. dtype = desc->dtype.
+ * Row statistics are all-reduced (fp32) over the ranks holding the other column blocks of
+ * the same rows; dgamma / dbeta over the ranks holding the other row blocks of the same
+ * columns. stats: [rows, 2] fp32 (mean, rstd), written by fwd, read by bwd.
+ * Collective: every rank of the grid calls with identical desc / tensor / eps.
+ * Errors: TP_ERR_ARG (tensor not X/Y, null pointers), TP_ERR_WORKSPACE, TP_ERR_INDIVISIBLE. */
+tp_status tp_layernorm_ws_size(const tp_grid* grid, const tp_linear_desc* desc, tp_tensor tensor,
+                               size_t* ws_bytes);
+tp_status tp_layernorm_fwd(tp_grid* grid, const tp_linear_desc* desc, tp_tensor tensor, float eps,
+                           const void* x, const void* gamma, const void* beta, void* y,
+                           float* stats, void* ws, size_t ws_bytes, void* stream);
+/* dx may be NULL (skip), dgamma / dbeta may be NULL (skip). */
+tp_status tp_layernorm_bwd(tp_grid* grid, const tp_linear_desc* desc, tp_tensor tensor,
+                           const void* dy, const void* x, const void* gamma, const float* stats,
+                           void* dx, void* dgamma, void* dbeta, void* ws, size_t ws_bytes,
+                           void* stream);
+
 /* ---- analytic cost model --------------------- */
 /* One linear layer, fwd+bwd, bias-free, on the grid (mode, world, q, d) with desc's M, K, N,
  * dtype, split_1d and flags (TP_FLAG_W25_DEPTH_SHARDED). Host only, no device work.

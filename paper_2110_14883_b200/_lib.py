@@ -36,7 +36,7 @@ EXPORTED = [
     "tp_gemm_ws_bytes",
     "tp_colsum", "tp_fill", "tp_l2_flush", "tp_prof_enable", "tp_prof_reset", "tp_prof_read",
     "tp_launch_count", "tp_gemm_trace", "tp_register_buffer", "tp_deregister_all",
-    "tp_cost_model",
+    "tp_cost_model", "tp_layernorm_ws_size", "tp_layernorm_fwd", "tp_layernorm_bwd",
 ]
 
 
@@ -85,6 +85,11 @@ _sigs = {
     "tp_gemm_trace": (_i, [_vp]),
     "tp_register_buffer": (_i, [_vp, _vp, _sz]),
     "tp_deregister_all": (_i, [_vp]),
+    "tp_layernorm_ws_size": (_i, [_vp, C.POINTER(tp_linear_desc), _i, C.POINTER(_sz)]),
+    "tp_layernorm_fwd": (_i, [_vp, C.POINTER(tp_linear_desc), _i, _f, _vp, _vp, _vp, _vp, _vp, _vp,
+                              _sz, _vp]),
+    "tp_layernorm_bwd": (_i, [_vp, C.POINTER(tp_linear_desc), _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                              _vp, _sz, _vp]),
     "tp_cost_model": (_i, [_i, _i, _i, _i, C.POINTER(tp_linear_desc), C.c_double, C.c_double,
                            C.POINTER(tp_cost)]),
 }

@@ -226,3 +226,27 @@ def tp_cost_model(mode, world, d_: tp_linear_desc, q=0, depth=1, peak_tflops=0.0
     _check(lib.tp_cost_model(m, world, q, depth, C.byref(d_), float(peak_tflops), float(link_gbs),
                              C.byref(c)), "tp_cost_model")
     return {n: getattr(c, n) for n, _ in tp_cost._fields_}
+
+
+def tp_layernorm_ws_size(g, d, tensor):
+    t = TENSORS[tensor] if isinstance(tensor, str) else int(tensor)
+    n = C.c_size_t()
+    _check(lib.tp_layernorm_ws_size(g, C.byref(d), t, C.byref(n)), "tp_layernorm_ws_size")
+    return n.value
+
+
+def tp_layernorm_fwd(g, d, tensor, eps, x, gamma, beta, y, stats, ws, stream=None, ws_bytes=None):
+    t = TENSORS[tensor] if isinstance(tensor, str) else int(tensor)
+    wb = _nbytes(ws) if ws_bytes is None else ws_bytes
+    _check(lib.tp_layernorm_fwd(g, C.byref(d), t, float(eps), _ptr(x), _ptr(gamma), _ptr(beta),
+                                _ptr(y), _ptr(stats), _ptr(ws), wb, _stream(stream)),
+           "tp_layernorm_fwd")
+
+
+def tp_layernorm_bwd(g, d, tensor, dy, x, gamma, stats, dx, dgamma, dbeta, ws, stream=None,
+                     ws_bytes=None):
+    t = TENSORS[tensor] if isinstance(tensor, str) else int(tensor)
+    wb = _nbytes(ws) if ws_bytes is None else ws_bytes
+    _check(lib.tp_layernorm_bwd(g, C.byref(d), t, _ptr(dy), _ptr(x), _ptr(gamma), _ptr(stats),
+                                _ptr(dx), _ptr(dgamma), _ptr(dbeta), _ptr(ws), wb, _stream(stream)),
+           "tp_layernorm_bwd")

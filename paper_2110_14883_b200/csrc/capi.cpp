@@ -703,3 +703,31 @@ extern "C" tp_status tp_cost_model(tp_mode mode, int world, int q, int d, const 
   *out = c;
   return TP_OK;
 }
+
+// ------------------------------------------------------------------------------- LayerNorm
+extern "C" tp_status tp_layernorm_ws_size(const tp_grid* g, const tp_linear_desc* d, tp_tensor t,
+                                          size_t* ws_bytes) {
+  if (!g || !d || !ws_bytes) return tp::fail(TP_ERR_ARG, "tp_layernorm_ws_size: null argument");
+  return tp::layernorm_ws_bytes(g, d, t, ws_bytes);
+}
+
+extern "C" tp_status tp_layernorm_fwd(tp_grid* g, const tp_linear_desc* d, tp_tensor t, float eps,
+                                      const void* x, const void* gamma, const void* beta, void* y,
+                                      float* stats, void* ws, size_t ws_bytes, void* stream) {
+  if (!g || !d) return tp::fail(TP_ERR_ARG, "tp_layernorm_fwd: null grid or desc");
+  if (d->dtype != TP_BF16 && d->dtype != TP_FP32) return tp::fail(TP_ERR_ARG, "unknown dtype");
+  TP_CUDA(cudaSetDevice(g->device));
+  return tp::layernorm_fwd(g, d, t, eps, x, gamma, beta, y, stats, ws, ws_bytes,
+                           static_cast<cudaStream_t>(stream));
+}
+
+extern "C" tp_status tp_layernorm_bwd(tp_grid* g, const tp_linear_desc* d, tp_tensor t,
+                                      const void* dy, const void* x, const void* gamma,
+                                      const float* stats, void* dx, void* dgamma, void* dbeta,
+                                      void* ws, size_t ws_bytes, void* stream) {
+  if (!g || !d) return tp::fail(TP_ERR_ARG, "tp_layernorm_bwd: null grid or desc");
+  if (d->dtype != TP_BF16 && d->dtype != TP_FP32) return tp::fail(TP_ERR_ARG, "unknown dtype");
+  TP_CUDA(cudaSetDevice(g->device));
+  return tp::layernorm_bwd(g, d, t, dy, x, gamma, stats, dx, dgamma, dbeta, ws, ws_bytes,
+                           static_cast<cudaStream_t>(stream));
+}

@@ -34,6 +34,15 @@ struct Run {
   Carver ws, saved;
 };
 
+// LayerNorm over the columns of a TP activation shard (norm.cu; tensor = TP_TENSOR_X / _Y).
+tp_status layernorm_ws_bytes(const tp_grid* g, const tp_linear_desc* d, int tensor, size_t* bytes);
+tp_status layernorm_fwd(tp_grid* g, const tp_linear_desc* d, int tensor, float eps, const void* x,
+                        const void* gamma, const void* beta, void* y, float* stats, void* ws,
+                        size_t ws_bytes, cudaStream_t s);
+tp_status layernorm_bwd(tp_grid* g, const tp_linear_desc* d, int tensor, const void* dy,
+                        const void* x, const void* gamma, const float* stats, void* dx,
+                        void* dgamma, void* dbeta, void* ws, size_t ws_bytes, cudaStream_t s);
+
 tp_status sched_fwd(Run& R, const void* x, const void* w, const void* bias, void* y);
 tp_status sched_bwd(Run& R, const void* dy, const void* x, const void* w, void* dx, void* dw,
                     void* dbias);
