@@ -71,6 +71,10 @@ typedef enum { TP_TENSOR_X = 0, TP_TENSOR_W = 1, TP_TENSOR_Y = 2, TP_TENSOR_BIAS
 /* tp_linear_desc.flags */
 #define TP_FLAG_W25_DEPTH_SHARDED 0x1u /* 2.5D: W also split over depth (1/p at rest); AG in fwd, RS of dW */
 #define TP_FLAG_SERIAL 0x2u            /* debug: run collectives on the compute stream (no overlap) */
+/* Y = gelu(alpha X.W + b) (exact erf form; oracle/activation.py): the
+ * forward keeps the pre-activation Z (the Y shard) in `saved` after the mode's own content and
+ * tp_linear_bwd takes dL/dY, forming dZ = dY * gelu'(Z) in `ws` (tp_workspace_size counts both). */
+#define TP_FLAG_GELU 0x8u
 
 typedef struct tp_grid tp_grid; /* opaque; library-owned (communicators, streams, events) */
 
@@ -166,7 +170,7 @@ tp_status tp_unpack(const tp_grid* grid, const tp_linear_desc* desc, tp_tensor t
  * The buffer must stay allocated until tp_deregister_all / tp_grid_destroy. */
 tp_status tp_register_buffer(tp_grid* grid, void* ptr, size_t bytes);
 tp_status tp_deregister_all(tp_grid* grid);
-#define TP_FLAG_PEER_FUSED 0x4u /* tp_linear_desc.flags: fused peer-panel SUMMA (2D, 2.5D) */
+#define TP_FLAG_PEER_FUSED 0x4u /* tp_linear_desc.flags: fused owner-computes panel GEMMs (2D, 2.5D, 3D l=2) */
 
 /* ---- kernels exposed for parity tests and benchmarks ----------------------------------- */
 /* Local GEMM, the per-step shard product of every mode:

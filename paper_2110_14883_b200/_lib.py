@@ -28,6 +28,7 @@ TP_TENSOR_X, TP_TENSOR_W, TP_TENSOR_Y, TP_TENSOR_BIAS = 0, 1, 2, 3
 TP_FLAG_W25_DEPTH_SHARDED = 0x1
 TP_FLAG_SERIAL = 0x2
 TP_FLAG_PEER_FUSED = 0x4
+TP_FLAG_GELU = 0x8
 
 EXPORTED = [
     "tp_status_string", "tp_last_error", "tp_version", "tp_get_unique_id", "tp_grid_init",

@@ -183,7 +183,7 @@ tp_status check_desc(const tp_grid* g, const tp_linear_desc* d) {
   return check_divisible(g, d);
 }
 
-tp_status plan_sizes(tp_grid* g, const tp_linear_desc* d, size_t* ws, size_t* saved) {
+tp_status plan_mode_sizes(tp_grid* g, const tp_linear_desc* d, size_t* ws, size_t* saved) {
   Run R;
   R.g = g;
   R.d = d;
@@ -199,6 +199,37 @@ tp_status plan_sizes(tp_grid* g, const tp_linear_desc* d, size_t* ws, size_t* sa
   TP_TRY(sched_bwd(B, nullptr, nullptr, nullptr, &dummy, &dummy, &dummy));
   *ws = std::max(wf, B.ws.off);
   *saved = sf;
+  return TP_OK;
+}
+
+size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+
+// TP_FLAG_GELU: the pre-activation Z (Y shard) lives in `saved` after the mode's own content,
+// and the backward's dZ in `ws` after the mode's scratch.
+struct GeluLayout {
+  size_t saved_off = 0, ws_off = 0, bytes = 0, n = 0;
+};
+
+tp_status gelu_layout(tp_grid* g, const tp_linear_desc* d, GeluLayout* L) {
+  size_t ws = 0, sv = 0;
+  TP_TRY(plan_mode_sizes(g, d, &ws, &sv));
+  Ext e;
+  TP_TRY(extent(g, d, TP_TENSOR_Y, &e));
+  L->n = size_t(e.rows) * size_t(e.cols);
+  L->bytes = L->n * dtype_size(d->dtype);
+  L->saved_off = align256(sv);
+  L->ws_off = align256(ws);
+  return TP_OK;
+}
+
+tp_status plan_sizes(tp_grid* g, const tp_linear_desc* d, size_t* ws, size_t* saved) {
+  TP_TRY(plan_mode_sizes(g, d, ws, saved));
+  if (d->flags & TP_FLAG_GELU) {
+    GeluLayout L;
+    TP_TRY(gelu_layout(g, d, &L));
+    *ws = L.ws_off + L.bytes;
+    *saved = L.saved_off + L.bytes;
+  }
   return TP_OK;
 }
 
@@ -392,6 +423,11 @@ tp_status tp_linear_fwd(tp_grid* g, const tp_linear_desc* d, const void* x, cons
     cudaEventRecord(e, R.cs);
     cudaStreamWaitEvent(s, e, 0);
   }
+  if (st == TP_OK && (d->flags & TP_FLAG_GELU)) {  // Y = gelu(Z); Z kept for the backward
+    GeluLayout L;
+    TP_TRY(gelu_layout(g, d, &L));
+    if (L.n) TP_TRY(launch_gelu_fwd(y, static_cast<char*>(saved) + L.saved_off, L.n, d->dtype, s));
+  }
   return st;
 }
 
@@ -411,6 +447,20 @@ tp_status tp_linear_bwd(tp_grid* g, const tp_linear_desc* d, const void* dy, con
     cudaEvent_t e = g->ev();
     TP_CUDA(cudaEventRecord(e, s));
     TP_CUDA(cudaStreamWaitEvent(R.cs, e, 0));
+  }
+  if (d->flags & TP_FLAG_GELU) {  // dZ = dY * gelu'(Z), then the linear backward with dZ
+    GeluLayout L;
+    TP_TRY(gelu_layout(g, d, &L));
+    void* dz = static_cast<char*>(ws) + L.ws_off;
+    if (L.n)
+      TP_TRY(launch_gelu_bwd(dy, static_cast<const char*>(saved) + L.saved_off, dz, L.n,
+                             d->dtype, s));
+    dy = dz;
+    if (R.cs != s) {  // the comm stream must see dZ too
+      cudaEvent_t e = g->ev();
+      TP_CUDA(cudaEventRecord(e, s));
+      TP_CUDA(cudaStreamWaitEvent(R.cs, e, 0));
+    }
   }
   tp_status st = sched_bwd(R, dy, x, w, dx, dw, dbias);
   if (R.cs != s) {

@@ -235,4 +235,105 @@ tp_status launch_memset(void* dst, size_t bytes, cudaStream_t s) {
   return TP_OK;
 }
 
+
+// ------------------------------------------------------------------------------------ GeLU
+// gelu(z) = z Phi(z) = 0.5 z (1 + erf(z / sqrt 2)), gelu'(z) = Phi(z) + z phi(z) (fp32 math,
+// exact erf form; oracle/activation.py). Elementwise over the Y shard; 16-byte vectors.
+namespace {
+__device__ __forceinline__ float gelu_f(float z) { return 0.5f * z * (1.f + erff(z * 0.70710678118654752f)); }
+__device__ __forceinline__ float gelu_grad_f(float z) {
+  const float Phi = 0.5f * (1.f + erff(z * 0.70710678118654752f));
+  return Phi + z * 0.39894228040143268f * __expf(-0.5f * z * z);
+}
+template <typename T>
+__device__ __forceinline__ float to_f(T v) {
+  if constexpr (sizeof(T) == 2) return __bfloat162float(v);
+  else return v;
+}
+template <typename T>
+__device__ __forceinline__ T from_f(float v) {
+  if constexpr (sizeof(T) == 2) return __float2bfloat16_rn(v);
+  else return v;
+}
+
+template <typename T>
+__global__ void gelu_fwd_kernel(T* __restrict__ y, T* __restrict__ z, size_t n) {
+  constexpr int V = 16 / sizeof(T);
+  const size_t nv = n / V;
+  const size_t stride = size_t(gridDim.x) * blockDim.x;
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nv; i += stride) {
+    uint4 u = reinterpret_cast<const uint4*>(y)[i];
+    reinterpret_cast<uint4*>(z)[i] = u;
+    T* e = reinterpret_cast<T*>(&u);
+#pragma unroll
+    for (int j = 0; j < V; ++j) e[j] = from_f<T>(gelu_f(to_f(e[j])));
+    reinterpret_cast<uint4*>(y)[i] = u;
+  }
+  for (size_t i = nv * V + size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const T v = y[i];
+    z[i] = v;
+    y[i] = from_f<T>(gelu_f(to_f(v)));
+  }
+}
+
+template <typename T>
+__global__ void gelu_bwd_kernel(const T* __restrict__ dy, const T* __restrict__ z, T* __restrict__ dz,
+                                size_t n) {
+  constexpr int V = 16 / sizeof(T);
+  const size_t nv = n / V;
+  const size_t stride = size_t(gridDim.x) * blockDim.x;
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nv; i += stride) {
+    const uint4 a = reinterpret_cast<const uint4*>(dy)[i];
+    const uint4 b = reinterpret_cast<const uint4*>(z)[i];
+    uint4 o;
+    const T* ea = reinterpret_cast<const T*>(&a);
+    const T* eb = reinterpret_cast<const T*>(&b);
+    T* eo = reinterpret_cast<T*>(&o);
+#pragma unroll
+    for (int j = 0; j < V; ++j) eo[j] = from_f<T>(to_f(ea[j]) * gelu_grad_f(to_f(eb[j])));
+    reinterpret_cast<uint4*>(dz)[i] = o;
+  }
+  for (size_t i = nv * V + size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    dz[i] = from_f<T>(to_f(dy[i]) * gelu_grad_f(to_f(z[i])));
+}
+
+unsigned elem_grid(size_t n) {
+  const size_t b = (n / 8 + 255) / 256;
+  return static_cast<unsigned>(b < 148 * 16 ? (b > 0 ? b : 1) : 148 * 16);
+}
+}  // namespace
+
+tp_status launch_gelu_fwd(void* y, void* z, size_t n, tp_dtype dt, cudaStream_t s) {
+  if (!n) return TP_OK;
+  if ((reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(z)) % 16)
+    return fail(TP_ERR_SHAPE, "gelu: 16-byte aligned buffers required");
+  if (dt == TP_BF16)
+    gelu_fwd_kernel<__nv_bfloat16><<<elem_grid(n), 256, 0, s>>>(static_cast<__nv_bfloat16*>(y),
+                                                               static_cast<__nv_bfloat16*>(z), n);
+  else
+    gelu_fwd_kernel<float><<<elem_grid(n), 256, 0, s>>>(static_cast<float*>(y), static_cast<float*>(z), n);
+  count_launch();
+  TP_CUDA(cudaGetLastError());
+  return TP_OK;
+}
+
+tp_status launch_gelu_bwd(const void* dy, const void* z, void* dz, size_t n, tp_dtype dt,
+                          cudaStream_t s) {
+  if (!n) return TP_OK;
+  if ((reinterpret_cast<uintptr_t>(dy) | reinterpret_cast<uintptr_t>(z) |
+       reinterpret_cast<uintptr_t>(dz)) % 16)
+    return fail(TP_ERR_SHAPE, "gelu: 16-byte aligned buffers required");
+  if (dt == TP_BF16)
+    gelu_bwd_kernel<__nv_bfloat16><<<elem_grid(n), 256, 0, s>>>(
+        static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(z),
+        static_cast<__nv_bfloat16*>(dz), n);
+  else
+    gelu_bwd_kernel<float><<<elem_grid(n), 256, 0, s>>>(static_cast<const float*>(dy),
+                                                       static_cast<const float*>(z),
+                                                       static_cast<float*>(dz), n);
+  count_launch();
+  TP_CUDA(cudaGetLastError());
+  return TP_OK;
+}
+
 }  // namespace tp

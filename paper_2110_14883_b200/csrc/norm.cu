@@ -822,8 +822,8 @@ tp_status layernorm_bwd(tp_grid* g, const tp_linear_desc* d, int tensor, const v
     if (want_cols) {
       const int64_t nv = e.cols / (16 / int64_t(esz));
       // enough (slab x column-vector) threads to fill the machine, at most kLnColSlabs slabs
-      int64_t slabs = (65536 + nv - 1) / nv;
-      if (slabs < 64) slabs = 64;
+      int64_t slabs = (262144 + nv - 1) / nv;
+      if (slabs < 256) slabs = 256;
       if (slabs > kLnColSlabs) slabs = kLnColSlabs;
       if (slabs > e.rows) slabs = e.rows;
       const int64_t per = (e.rows + slabs - 1) / slabs;

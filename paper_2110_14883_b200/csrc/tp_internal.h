@@ -63,6 +63,10 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 // ---- kernels (layout.cu) ------------------------------------------------------------------
 tp_status launch_copy2d(const void* src, int64_t src_ld, void* dst, int64_t dst_ld, int64_t rows,
                         int64_t cols, size_t esz, cudaStream_t s);
+// GeLU (exact erf form) over n elements: fwd z = y, y = gelu(y); bwd dz = dy * gelu'(z).
+tp_status launch_gelu_fwd(void* y, void* z, size_t n, tp_dtype dt, cudaStream_t s);
+tp_status launch_gelu_bwd(const void* dy, const void* z, void* dz, size_t n, tp_dtype dt,
+                          cudaStream_t s);
 // Deterministic two-pass column sums; scratch holds kColsumSlabs * cols floats.
 constexpr int kColsumSlabs = 32;
 tp_status launch_colsum(const void* src, int64_t rows, int64_t cols, int64_t ld, tp_dtype dt,

@@ -25,12 +25,15 @@ def layer_tid(layer, tid):
 
 class TPMLP:
     def __init__(self, grid, M, layers, dtype="bf16", seed=42, flags=0, alpha=1.0,
-                 kind="uniform", fill=True):
+                 kind="uniform", fill=True, act=None):
         self.g, self.M, self.layers, self.dtype, self.seed = grid, M, list(layers), dtype, seed
         self.tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
         self.kind = kind
-        self.descs = [api.desc(M, K, N, dtype, split_1d=i % 2, parity_3d=i % 2, flags=flags,
-                               alpha=alpha) for i, (K, N) in enumerate(self.layers)]
+        # act="gelu": GeLU after every even layer (fc1 of each fc1 -> gelu -> fc2 pair)
+        gelu = lambda i: api.TP_FLAG_GELU if act == "gelu" and i % 2 == 0 and i + 1 < len(layers) else 0
+        self.descs = [api.desc(M, K, N, dtype, split_1d=i % 2, parity_3d=i % 2,
+                               flags=flags | gelu(i), alpha=alpha)
+                      for i, (K, N) in enumerate(self.layers)]
         L = len(self.layers)
         self.x = self._alloc(0, "X")
         self.W = [self._alloc(i, "W") for i in range(L)]
