@@ -787,7 +787,7 @@ int max_clusters(Kern kern, int csize, int smem) {
 
 // Fill one problem's maps, epilogue params and its split-K choice.
 template <int BNP, int MC>
-tp_status setup_prob(const GemmArgs& g, Prob& pr, int clusters, bool allow_split, char*& ws,
+tp_status setup_prob(const GemmArgs& g, Prob& pr, int clusters, int split_mode, char*& ws,
                      size_t& ws_left, cudaStream_t s) {
   using P = PC<BNP>;
   const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
@@ -837,10 +837,25 @@ tp_status setup_prob(const GemmArgs& g, Prob& pr, int clusters, bool allow_split
     const char* e = std::getenv("TP_GEMM_SPLITK");
     return e ? std::atoi(e) : 1;
   }();
-  // split-K only when the grid would leave more than half of the clusters idle
-  for (int sp = 2; sp <= 4 && allow_split && env_split; ++sp) {
-    const size_t need = size_t(ptiles) * sp * P::TileElems * 4 + 256 * ((ptiles * 8 + 255) / 256);
-    if (2 * supers <= clusters && supers * sp <= clusters && num_k >= 4 * sp && need <= ws_left) S = sp;
+  // split_mode > 0: a single problem -- split K only when the grid would leave more than half
+  // of the clusters idle (up to 16 ways, every split >= 4 k-blocks). split_mode < 0: a problem
+  // of a group whose tiles are far longer than the group's per-cluster share of work
+  // (-split_mode = that share in k-blocks): split so no unit exceeds ~ the share.
+  const auto need_of = [&](int sp) {
+    return size_t(ptiles) * sp * P::TileElems * 4 + 256 * ((ptiles * 8 + 255) / 256);
+  };
+  if (split_mode > 0 && env_split) {
+    for (int sp = 2; sp <= 16; ++sp)
+      if (2 * supers <= clusters && supers * sp <= clusters && num_k >= 4 * sp && need_of(sp) <= ws_left)
+        S = sp;
+  } else if (split_mode < 0 && env_split) {
+    const int share = -split_mode;
+    const int want = std::min(16, (num_k + share - 1) / share);
+    for (int sp = want; sp >= 2; --sp)
+      if (supers * sp <= clusters && num_k >= 4 * sp && need_of(sp) <= ws_left) {
+        S = sp;
+        break;
+      }
   }
   int kbps = (num_k + S - 1) / S;
   S = (num_k + kbps - 1) / kbps;  // no empty split
@@ -884,9 +899,23 @@ tp_status launch2(const GemmArgs* gs, int n, cudaStream_t s) {
     // gain on the C2 backward, 0.135 vs 0.126 ms/step)
     static const int group_split = [] {
       const char* e = std::getenv("TP_GEMM_GROUP_SPLIT");
-      return e ? std::atoi(e) : 0;
+      return e ? std::atoi(e) : 1;
     }();
-    TP_TRY((setup_prob<BNP, MC>(gs[i], G.p[i], clusters, n == 1 || group_split, ws, ws_left, s)));
+    int mode = n == 1 ? 1 : 0;
+    if (n > 1 && group_split) {
+      // per-cluster share of the group's work (tiles x k-blocks); a problem whose tiles are
+      // more than twice as long is split (e.g. a long-K dW next to many short dX tiles)
+      double work = 0;
+      for (int j = 0; j < n; ++j) {
+        const double tiles = double((gs[j].M + 255) / 256) * double((gs[j].N + BNP - 1) / BNP);
+        const double kb = double((gs[j].K + kBK - 1) / kBK) * (gs[j].npanels > 1 ? gs[j].npanels : 1);
+        work += tiles * kb;
+      }
+      const double share = work / clusters;
+      const double kb_i = double((gs[i].K + kBK - 1) / kBK) * (gs[i].npanels > 1 ? gs[i].npanels : 1);
+      if (kb_i > 2 * share && share >= 8) mode = -static_cast<int>(share);
+    }
+    TP_TRY((setup_prob<BNP, MC>(gs[i], G.p[i], clusters, mode, ws, ws_left, s)));
     G.p[i].unit0 = units;
     units += super_tiles(MC, G.p[i].num_m, G.p[i].num_n) * G.p[i].splits;
     flops += 2.0 * double(gs[i].M) * double(gs[i].N) * double(gs[i].K) * G.p[i].npanels;
