@@ -247,6 +247,28 @@ tp_status tp_layernorm_bwd(tp_grid* grid, const tp_linear_desc* desc, tp_tensor 
                            void* dx, void* dgamma, void* dbeta, void* ws, size_t ws_bytes,
                            void* stream);
 
+/* ---- Ring Self-Attention (sequence parallelism) ------------------------ */
+/* softmax(Q K^T * scale) V ("Attention(Q,K,V) = softmax(QK^T/sqrt(d_k))V") for
+ * `heads` independent (batch x head) problems, with Q, K, V split along the sequence over the
+ * p ranks of a TP_1D grid (the ring, "the input data is split along the sequence
+ * dimension"). This rank passes q, k, v and out as [heads, seq/p, d_k] row-major (rows
+ * [rank*seq/p, (rank+1)*seq/p) of every head). Pass 1 circulates K blocks around the ring
+ * (p-1 shifts; "transferred to the next device for N-1 times") and assembles the fp32
+ * score rows, a row softmax forms the probabilities, pass 2 circulates V blocks and
+ * accumulates the output. dtype TP_BF16 (tensor cores, fp32 accumulate) or
+ * TP_FP32. scale 0 means 1/sqrt(d_k). Collective over the ring.
+ * Errors: TP_ERR_CONSTRAINT (grid not 1D), TP_ERR_INDIVISIBLE (seq % p), TP_ERR_WORKSPACE. */
+typedef struct {
+  int64_t seq;    /* global sequence length s */
+  int64_t d_k;    /* head dimension of Q, K and V */
+  int64_t heads;  /* independent problems (batch x heads) */
+  tp_dtype dtype;
+  float scale;
+} tp_rsa_desc;
+tp_status tp_rsa_ws_size(const tp_grid* grid, const tp_rsa_desc* desc, size_t* ws_bytes);
+tp_status tp_rsa_fwd(tp_grid* grid, const tp_rsa_desc* desc, const void* q, const void* k,
+                     const void* v, void* out, void* ws, size_t ws_bytes, void* stream);
+
 /* ---- analytic cost model --------------------- */
 /* One linear layer, fwd+bwd, bias-free, on the grid (mode, world, q, d) with desc's M, K, N,
  * dtype, split_1d and flags (TP_FLAG_W25_DEPTH_SHARDED). Host only, no device work.

@@ -38,6 +38,7 @@ EXPORTED = [
     "tp_colsum", "tp_fill", "tp_l2_flush", "tp_prof_enable", "tp_prof_reset", "tp_prof_read",
     "tp_launch_count", "tp_gemm_trace", "tp_register_buffer", "tp_deregister_all",
     "tp_cost_model", "tp_layernorm_ws_size", "tp_layernorm_fwd", "tp_layernorm_bwd",
+    "tp_rsa_ws_size", "tp_rsa_fwd",
 ]
 
 
@@ -45,6 +46,11 @@ class tp_cost(C.Structure):
     _fields_ = [(n, C.c_double) for n in ("paper_elems", "counted_elems", "link_bytes", "flops",
                                           "mem_x", "mem_w", "mem_y", "t_tensor_us", "t_link_us",
                                           "t_roof_us")]
+
+
+class tp_rsa_desc(C.Structure):
+    _fields_ = [("seq", C.c_int64), ("d_k", C.c_int64), ("heads", C.c_int64), ("dtype", C.c_int),
+                ("scale", C.c_float)]
 
 
 class tp_linear_desc(C.Structure):
@@ -91,6 +97,8 @@ _sigs = {
                               _sz, _vp]),
     "tp_layernorm_bwd": (_i, [_vp, C.POINTER(tp_linear_desc), _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                               _vp, _sz, _vp]),
+    "tp_rsa_ws_size": (_i, [_vp, C.POINTER(tp_rsa_desc), C.POINTER(_sz)]),
+    "tp_rsa_fwd": (_i, [_vp, C.POINTER(tp_rsa_desc), _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "tp_cost_model": (_i, [_i, _i, _i, _i, C.POINTER(tp_linear_desc), C.c_double, C.c_double,
                            C.POINTER(tp_cost)]),
 }

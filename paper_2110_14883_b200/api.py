@@ -13,7 +13,7 @@ from ._lib import (TP_1D, TP_2D, TP_2P5D, TP_3D, TP_BF16, TP_FP32, TP_FLAG_SERIA
                    TP_FLAG_PEER_FUSED, TP_FLAG_GELU,
                    TP_FLAG_W25_DEPTH_SHARDED, TP_TENSOR_BIAS, TP_TENSOR_W, TP_TENSOR_X,
                    TP_TENSOR_Y, TP_TRANSPORT_LOCAL, TP_TRANSPORT_NCCL, TP_TRANSPORT_NONE,
-                   tp_cost, tp_linear_desc)
+                   tp_cost, tp_linear_desc, tp_rsa_desc)
 
 lib = L.lib
 
@@ -250,3 +250,20 @@ def tp_layernorm_bwd(g, d, tensor, dy, x, gamma, stats, dx, dgamma, dbeta, ws, s
     _check(lib.tp_layernorm_bwd(g, C.byref(d), t, _ptr(dy), _ptr(x), _ptr(gamma), _ptr(stats),
                                 _ptr(dx), _ptr(dgamma), _ptr(dbeta), _ptr(ws), wb, _stream(stream)),
            "tp_layernorm_bwd")
+
+
+def rsa_desc(seq, d_k, heads=1, dtype="bf16", scale=0.0) -> tp_rsa_desc:
+    dt = DTYPES[dtype] if isinstance(dtype, str) else int(dtype)
+    return tp_rsa_desc(int(seq), int(d_k), int(heads), dt, float(scale))
+
+
+def tp_rsa_ws_size(g, d: tp_rsa_desc) -> int:
+    n = C.c_size_t()
+    _check(lib.tp_rsa_ws_size(g, C.byref(d), C.byref(n)), "tp_rsa_ws_size")
+    return n.value
+
+
+def tp_rsa_fwd(g, d: tp_rsa_desc, q, k, v, out, ws, stream=None, ws_bytes=None):
+    wb = _nbytes(ws) if ws_bytes is None else ws_bytes
+    _check(lib.tp_rsa_fwd(g, C.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(ws), wb,
+                          _stream(stream)), "tp_rsa_fwd")

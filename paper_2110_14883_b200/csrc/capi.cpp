@@ -781,3 +781,16 @@ extern "C" tp_status tp_layernorm_bwd(tp_grid* g, const tp_linear_desc* d, tp_te
   return tp::layernorm_bwd(g, d, t, dy, x, gamma, stats, dx, dgamma, dbeta, ws, ws_bytes,
                            static_cast<cudaStream_t>(stream));
 }
+
+// ----------------------------------------------------------------------- Ring Self-Attention
+extern "C" tp_status tp_rsa_ws_size(const tp_grid* g, const tp_rsa_desc* d, size_t* ws_bytes) {
+  if (!ws_bytes) return tp::fail(TP_ERR_ARG, "tp_rsa_ws_size: null ws_bytes");
+  return tp::rsa_ws_bytes(g, d, ws_bytes);
+}
+
+extern "C" tp_status tp_rsa_fwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k,
+                                const void* v, void* out, void* ws, size_t ws_bytes, void* stream) {
+  if (!g || !d) return tp::fail(TP_ERR_ARG, "tp_rsa_fwd: null grid or desc");
+  TP_CUDA(cudaSetDevice(g->device));
+  return tp::rsa_fwd(g, d, q, k, v, out, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+}

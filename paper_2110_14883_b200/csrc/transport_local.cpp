@@ -162,6 +162,15 @@ class LocalComm final : public Comm {
       return launch_sum_n(in.data(), size(), recv, count, dt, s);
     });
   }
+  tp_status ring_shift(const void* send, void* recv, size_t count, tp_dtype dt,
+                       cudaStream_t s) override {
+    const size_t bytes = count * dtype_size(dt);
+    return exchange(send, recv, s, [&](std::vector<Slot>& sl) -> tp_status {
+      const void* src = sl[(pos_ + size() - 1) % size()].src;
+      if (bytes && recv != src) TP_CUDA(cudaMemcpyAsync(recv, src, bytes, cudaMemcpyDefault, s));
+      return TP_OK;
+    });
+  }
   tp_status barrier(cudaStream_t s) override {
     return exchange(nullptr, nullptr, s, [](std::vector<Slot>&) -> tp_status { return TP_OK; });
   }

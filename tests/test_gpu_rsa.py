@@ -1,0 +1,102 @@
+"""GPU parity of Ring Self-Attention (tp_rsa_fwd) against the oracle
+(oracle/ring_attention.py: dense attention + the rank-by-rank ring, pinned in
+tests/test_oracle_ring_attention.py). The ring ranks are in-process threads on cuda:0
+(LOCAL transport, 1D grid)."""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import ring_attention as rsa
+
+from tp_harness import TORCH_DT, rel_fro, run_ranks, to_np
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def api():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2110_14883_b200 import api
+    return api
+
+
+def inputs(seed, heads, s, d, dtype):
+    q = "bf16" if dtype == "bf16" else "fp32"
+    mk = lambda t: np.stack([synth.tensor(seed, 8 * h + t, s, d, dtype=q) for h in range(heads)]).astype(np.float64)
+    return mk(0), mk(1), mk(2)
+
+
+def run_rsa(api, p, heads, s, d, dtype, Q, K, V, scale=0.0):
+    transport = api.TP_TRANSPORT_LOCAL if p > 1 else api.TP_TRANSPORT_NONE
+    uid = api.tp_get_unique_id(transport)
+    b = s // p
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32)).cuda().to(TORCH_DT[dtype])
+
+    def rank_fn(r):
+        g = api.tp_grid_init("1d", p, r, 0, 1, 0, transport, uid)
+        st = torch.cuda.Stream()
+        try:
+            with torch.cuda.stream(st):
+                ds = api.rsa_desc(s, d, heads, dtype, scale)
+                q, k, v = (dev(X[:, r * b:(r + 1) * b, :]) for X in (Q, K, V))
+                out = torch.empty_like(q)
+                ws = torch.empty(api.tp_rsa_ws_size(g, ds), device="cuda", dtype=torch.uint8)
+                api.tp_rsa_fwd(g, ds, q, k, v, out, ws)
+            st.synchronize()
+            return to_np(out)
+        finally:
+            st.synchronize()
+            api.tp_grid_destroy(g)
+
+    per = run_ranks(p, rank_fn)
+    return np.concatenate(per, axis=1)
+
+
+def oracle_out(Q, K, V, scale=None):
+    return np.stack([rsa.attention(Q[h], K[h], V[h], scale)[0] for h in range(Q.shape[0])])
+
+
+@pytest.mark.parametrize("p", [1, 2, 4])
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_rsa_vs_oracle(api, p, dtype):
+    heads, s, d = 3, 1024, 64
+    Q, K, V = inputs(5, heads, s, d, dtype)
+    got = run_rsa(api, p, heads, s, d, dtype, Q, K, V)
+    ref = oracle_out(Q, K, V)
+    assert rel_fro(got, ref) <= (1e-2 if dtype == "bf16" else 1e-5)
+
+
+def test_rsa_ring_matches_oracle_ring_and_scale(api):
+    """Explicit scale, d_k = 128, and the oracle's own ring program as the reference."""
+    heads, s, d, p = 2, 768, 128, 3
+    Q, K, V = inputs(9, heads, s, d, "bf16")
+    got = run_rsa(api, p, heads, s, d, "bf16", Q, K, V, scale=0.05)
+    ref = np.stack([np.concatenate(list(rsa.ring_attention(rsa.shards(Q[h], p), rsa.shards(K[h], p),
+                                                           rsa.shards(V[h], p), scale=0.05)[0].values()),
+                                   axis=0) for h in range(heads)])
+    assert rel_fro(got, ref) <= 1e-2
+
+
+def test_rsa_parallel_degree_invariance(api):
+    heads, s, d = 2, 2048, 64
+    Q, K, V = inputs(3, heads, s, d, "bf16")
+    a = run_rsa(api, 2, heads, s, d, "bf16", Q, K, V)
+    b = run_rsa(api, 4, heads, s, d, "bf16", Q, K, V)
+    assert rel_fro(a, b) <= 1e-2
+    assert rel_fro(a, oracle_out(Q, K, V)) <= 1e-2
+
+
+def test_rsa_long_sequence(api):
+    """s = 8192 (row-resident softmax with 8 float4 per thread), two heads, ring of 2."""
+    heads, s, d = 2, 8192, 64
+    Q, K, V = inputs(1, heads, s, d, "bf16")
+    got = run_rsa(api, 2, heads, s, d, "bf16", Q, K, V)
+    assert rel_fro(got, oracle_out(Q, K, V)) <= 1e-2
+
+
+def test_rsa_zero_values(api):
+    heads, s, d = 1, 256, 64
+    Q, K, V = inputs(2, heads, s, d, "bf16")
+    got = run_rsa(api, 2, heads, s, d, "bf16", Q, K, 0 * V)
+    assert not got.any()

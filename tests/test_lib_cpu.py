@@ -169,3 +169,19 @@ def test_compute_on_none_transport_needs_world_1(api):
         assert e.value.status == 4
     finally:
         api.tp_grid_destroy(g)
+
+
+def test_rsa_and_layernorm_planning_errors():
+    """Host-side checks of the NEXT-2/3 entry points (nothing is enqueued on error)."""
+    from paper_2110_14883_b200 import api
+    g2 = api.tp_grid_init("2d", 4, 0, 0, 1, 0, api.TP_TRANSPORT_NONE)
+    with pytest.raises(api.TPError, match="1D"):
+        api.tp_rsa_ws_size(g2, api.rsa_desc(64, 16, 1))
+    with pytest.raises(api.TPError):
+        api.tp_layernorm_ws_size(g2, api.desc(8, 8, 8), "W")  # LayerNorm of a weight
+    api.tp_grid_destroy(g2)
+    g3 = api.tp_grid_init("1d", 3, 0, 0, 1, 0, api.TP_TRANSPORT_NONE)
+    with pytest.raises(api.TPError, match="divisible"):
+        api.tp_rsa_ws_size(g3, api.rsa_desc(100, 16, 1))
+    assert api.tp_rsa_ws_size(g3, api.rsa_desc(96, 16, 2)) > 2 * 32 * 96 * 4
+    api.tp_grid_destroy(g3)
