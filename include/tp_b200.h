@@ -75,6 +75,10 @@ typedef enum { TP_TENSOR_X = 0, TP_TENSOR_W = 1, TP_TENSOR_Y = 2, TP_TENSOR_BIAS
  * forward keeps the pre-activation Z (the Y shard) in `saved` after the mode's own content and
  * tp_linear_bwd takes dL/dY, forming dZ = dY * gelu'(Z) in `ws` (tp_workspace_size counts both). */
 #define TP_FLAG_GELU 0x8u
+/* 2D / 2.5D forward with Cannon's algorithm ("SUMMA and Cannon"; skew + unit cyclic
+ * shifts along the grid rows / columns) instead of SUMMA's broadcasts; same layouts and
+ * results. The backward keeps the SUMMA ABT / ATB schedule. */
+#define TP_FLAG_CANNON 0x10u
 
 typedef struct tp_grid tp_grid; /* opaque; library-owned (communicators, streams, events) */
 

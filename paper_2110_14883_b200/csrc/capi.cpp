@@ -724,6 +724,8 @@ extern "C" tp_status tp_cost_model(tp_mode mode, int world, int q, int d, const 
     case TP_2D:  // SUMMA: fwd bcast X,W; bwd bcast W + reduce dX, bcast X + reduce dW (A4)
       c.paper_elems = 3.0 * (j - 1) * (Sx + Sw);
       c.counted_elems = c.paper_elems;
+      // Cannon forward: skew (q-1)/q + (q-1) unit shifts of X and W (oracle/cannon.py)
+      if (desc->flags & TP_FLAG_CANNON) c.counted_elems += (j - 1) * (Sx + Sw) / j;
       c.mem_x = Sx / p;
       c.mem_w = Sw / p;
       c.mem_y = Sy / p;
@@ -731,6 +733,7 @@ extern "C" tp_status tp_cost_model(tp_mode mode, int world, int q, int d, const 
     case TP_2P5D:  // d planes of SUMMA on S_x/d rows + depth AR(dW) or AG(W)+RS(dW) (A6, A11)
       c.paper_elems = 3.0 * (j - 1) * (Sx / dd + Sw);
       c.counted_elems = dd * 3.0 * (j - 1) * (Sx / dd + Sw) + 2.0 * (dd - 1) * Sw;
+      if (desc->flags & TP_FLAG_CANNON) c.counted_elems += dd * (j - 1) * (Sx / dd + Sw) / j;
       c.mem_x = Sx / p;
       c.mem_w = (desc->flags & TP_FLAG_W25_DEPTH_SHARDED) ? Sw / p : Sw / (double(j) * j);
       c.mem_y = Sy / p;

@@ -288,7 +288,7 @@ tp_status rsa_fwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k
                               w.S + h * P.b * P.s + j * P.b, P.s, dt, TP_FP32, scale, nullptr, w));
       TP_TRY(run_heads(gs, s));
       if (t + 1 < P.p) {
-        TP_TRY(ring->ring_shift(cur, w.kv[nb], size_t(nh) * bd, dt, s));
+        TP_TRY(ring->shift(cur, w.kv[nb], size_t(nh) * bd, dt, -1, s));
         cur = w.kv[nb];
         nb ^= 1;
       }
@@ -312,7 +312,7 @@ tp_status rsa_fwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k
       }
       TP_TRY(run_heads(gs, s));
       if (!last) {
-        TP_TRY(ring->ring_shift(cur, w.kv[nb], size_t(nh) * bd, dt, s));
+        TP_TRY(ring->shift(cur, w.kv[nb], size_t(nh) * bd, dt, -1, s));
         cur = w.kv[nb];
         nb ^= 1;
       }

@@ -328,6 +328,60 @@ tp_status summa_ab(Ctx& C, const Plane& P, const void* x, const void* W, const v
   return TP_OK;
 }
 
+// Cannon's forward (TP_FLAG_CANNON; "SUMMA and Cannon"): skew
+// row i of X left by i and column j of W up by j, then q steps of (GEMM, shift X left by 1,
+// W up by 1). Each step's shifts run on the comm stream under the step's GEMM (double
+// buffers); oracle/cannon.py is the reference schedule.
+tp_status cannon_ab(Ctx& C, const Plane& P, const void* x, const void* W, const void* bias, void* y) {
+  const float alpha = C.d->alpha;
+  if (P.q == 1) {
+    if (C.R.plan) return TP_OK;
+    return C.mm(P.mb, P.nq, P.kq, x, false, W, false, y, C.dt, alpha, nullptr, bias);
+  }
+  void* bx[2] = {C.ws(P.mb * P.kq), C.ws(P.mb * P.kq)};
+  void* bw[2] = {C.ws(P.kq * P.nq), C.ws(P.kq * P.nq)};
+  float* acc = static_cast<float*>(C.ws(P.mb * P.nq, 4));
+  if (C.R.plan) return TP_OK;
+  // skew (every member of a row shares i, of a column shares j: collective-consistent)
+  TP_TRY(C.order(C.R.s, C.R.cs));
+  const void* cx = x;
+  const void* cw = W;
+  int ix = 0, iw = 0;
+  if (P.i) {
+    TP_TRY(P.row->shift(x, bx[0], P.mb * P.kq, C.dt, P.i, C.R.cs));
+    cx = bx[0];
+    ix = 1;
+  }
+  if (P.j) {
+    TP_TRY(P.col->shift(W, bw[0], P.kq * P.nq, C.dt, P.j, C.R.cs));
+    cw = bw[0];
+    iw = 1;
+  }
+  TP_TRY(C.order(C.R.cs, C.R.s));
+  for (int t = 0; t < P.q; ++t) {
+    const bool last = t == P.q - 1;
+    cudaEvent_t moved = nullptr;
+    void* nx = bx[ix];
+    void* nw = bw[iw];
+    if (!last) {  // next blocks move while this step's GEMM runs
+      TP_TRY(C.order(C.R.s, C.R.cs));  // the previous GEMM is done with the buffers we refill
+      TP_TRY(P.row->shift(cx, nx, P.mb * P.kq, C.dt, 1, C.R.cs));
+      TP_TRY(P.col->shift(cw, nw, P.kq * P.nq, C.dt, 1, C.R.cs));
+      moved = C.record(C.R.cs);
+    }
+    TP_TRY(C.mm(P.mb, P.nq, P.kq, cx, false, cw, false, last ? y : acc, last ? C.dt : TP_FP32,
+                last ? alpha : 1.f, t > 0 ? acc : nullptr, last ? bias : nullptr));
+    if (!last) {
+      TP_CUDA(cudaStreamWaitEvent(C.R.s, moved, 0));
+      cx = nx;
+      cw = nw;
+      ix ^= 1;
+      iw ^= 1;
+    }
+  }
+  return TP_OK;
+}
+
 // SUMMA "ABT" (a-6): dX[i,k] = reduce_row( dY[i,j] . W[k,j]^T ), W panels down the columns.
 tp_status summa_abt(Ctx& C, const Plane& P, const void* dy, const void* W, void* dx) {
   const float alpha = C.d->alpha;
@@ -486,6 +540,7 @@ tp_status fwd_2d(Ctx& C, const void* x, const void* w, const void* bias, void* y
     }
     W = Wfull;
   }
+  if (C.d->flags & TP_FLAG_CANNON) return cannon_ab(C, P, x, W, bias, y);
   return summa_ab(C, P, x, W, bias, y);
 }
 

@@ -140,10 +140,11 @@ class Comm {
   // recv [count] = slice `pos` of sum over members of send [size*count].
   virtual tp_status reducescatter(const void* send, void* recv, size_t count, tp_dtype dt,
                                   cudaStream_t s) = 0;
-  // Ring shift: recv [count] = send of member (pos - 1) mod size (every member sends to its
-  // successor); the Ring Self-Attention's K / V pass.
-  virtual tp_status ring_shift(const void* send, void* recv, size_t count, tp_dtype dt,
-                               cudaStream_t s) = 0;
+  // Cyclic shift along the line: recv [count] = send of member (pos + offset) mod size.
+  // offset -1: the Ring Self-Attention's K / V pass (every member sends to its successor,
+  // P:L606-612); offset +s: Cannon's "shift left / up by s". offset 0 copies.
+  virtual tp_status shift(const void* send, void* recv, size_t count, tp_dtype dt, int offset,
+                          cudaStream_t s) = 0;
   virtual tp_status group_start() { return TP_OK; }
   virtual tp_status group_end() { return TP_OK; }
   // Stream-ordered barrier: work after it on `s` starts only once every member's work before

@@ -162,11 +162,13 @@ class LocalComm final : public Comm {
       return launch_sum_n(in.data(), size(), recv, count, dt, s);
     });
   }
-  tp_status ring_shift(const void* send, void* recv, size_t count, tp_dtype dt,
-                       cudaStream_t s) override {
+  tp_status shift(const void* send, void* recv, size_t count, tp_dtype dt, int offset,
+                  cudaStream_t s) override {
     const size_t bytes = count * dtype_size(dt);
+    const int n = size();
+    const int off = ((offset % n) + n) % n;
     return exchange(send, recv, s, [&](std::vector<Slot>& sl) -> tp_status {
-      const void* src = sl[(pos_ + size() - 1) % size()].src;
+      const void* src = sl[(pos_ + off) % n].src;
       if (bytes && recv != src) TP_CUDA(cudaMemcpyAsync(recv, src, bytes, cudaMemcpyDefault, s));
       return TP_OK;
     });

@@ -68,17 +68,19 @@ class NcclComm final : public Comm {
     TP_NCCL(ncclReduceScatter(send, recv, count, nt(dt), ncclSum, c_, s));
     return TP_OK;
   }
-  tp_status ring_shift(const void* send, void* recv, size_t count, tp_dtype dt,
-                       cudaStream_t s) override {
+  tp_status shift(const void* send, void* recv, size_t count, tp_dtype dt, int offset,
+                  cudaStream_t s) override {
     if (!count) return TP_OK;
     const int n = size_;
-    if (n == 1) {
-      if (send != recv) TP_CUDA(cudaMemcpyAsync(recv, send, count * dtype_size(dt), cudaMemcpyDeviceToDevice, s));
+    const int off = ((offset % n) + n) % n;
+    if (off == 0) {
+      if (send != recv)
+        TP_CUDA(cudaMemcpyAsync(recv, send, count * dtype_size(dt), cudaMemcpyDeviceToDevice, s));
       return TP_OK;
     }
     TP_NCCL(ncclGroupStart());
-    TP_NCCL(ncclSend(send, count, nt(dt), (pos_ + 1) % n, c_, s));
-    TP_NCCL(ncclRecv(recv, count, nt(dt), (pos_ + n - 1) % n, c_, s));
+    TP_NCCL(ncclSend(send, count, nt(dt), (pos_ - off + n) % n, c_, s));
+    TP_NCCL(ncclRecv(recv, count, nt(dt), (pos_ + off) % n, c_, s));
     TP_NCCL(ncclGroupEnd());
     return TP_OK;
   }

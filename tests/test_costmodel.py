@@ -79,3 +79,25 @@ def test_errors():
         api.tp_cost_model("2d", 8, api.desc(16, 16, 16))  # 8 is not a square
     with pytest.raises(api.TPError):
         api.tp_cost_model("3d", 8, api.desc(6, 16, 16))  # M not divisible by l^2
+
+
+@pytest.mark.parametrize("q", [2, 3, 4])
+def test_cannon_volume_matches_oracle_ledger(q):
+    """Cannon's forward moves the SUMMA forward volume plus the skew: checked against the
+    message count of the oracle's Cannon program (oracle/cannon.py)."""
+    import numpy as np
+    from oracle import cannon
+    from oracle.fabric import Fabric
+    from oracle.grid import build_grid
+    from oracle.shards import LayerSpec, shard
+    M, K, N = 6 * q, 4 * q, 2 * q
+    grid = build_grid("2d", q * q)
+    spec = LayerSpec(M, K, N)
+    fab = Fabric()
+    X, W = np.ones((M, K)), np.ones((K, N))
+    cannon.cannon_fwd(grid, shard(grid, spec, X, "X"), shard(grid, spec, W, "W"), fab=fab)
+    fwd = fab.ledger.total()
+    c0 = api.tp_cost_model("2d", q * q, api.desc(M, K, N), q=q)
+    c1 = api.tp_cost_model("2d", q * q, api.desc(M, K, N, flags=0x10), q=q)
+    summa_fwd = cf.counted_volume("2d", M, K, N, q=q, part="fwd")
+    assert c1["counted_elems"] - c0["counted_elems"] == pytest.approx(fwd - summa_fwd)
