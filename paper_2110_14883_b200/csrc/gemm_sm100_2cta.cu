@@ -50,15 +50,18 @@ constexpr int kThreads = 192;
 constexpr int kMaxProbs = 4;
 constexpr int kMaxPanels = 4;  // K-panels per problem (peer shards of a fused SUMMA)
 
-// Pair-tile width BNP (256 or 128): B columns per CTA, ring depth, TMEM, smem.
-template <int BNP>
+// Pair-tile width BNP (256 or 128): B columns per CTA, ring depth, TMEM, smem. MC 5 (K-split
+// pair cluster) gives one ring stage to the 32 KB DSMEM receive buffer of the split reduction.
+constexpr int kRxBytes = 2 * 32 * kBM * 4;  // MC 5: two [32 cols][128 rows] fp32 chunks
+template <int BNP, int MC = 1>
 struct PC {
   static constexpr int BNC = BNP / 2;
-  static constexpr int Stages = BNP == 256 ? 6 : 8;
+  static constexpr int Stages = MC == 5 ? 5 : (BNP == 256 ? 6 : 8);
   static constexpr int BBytes = BNC * kBK * 2;
   static constexpr int StageBytes = kABytes + BBytes;
   static constexpr int TmemCols = 2 * BNP;
-  static constexpr int Smem = Stages * StageBytes + 8 * kOutBytes + 1024 + 256;
+  static constexpr int Rx = MC == 5 ? kRxBytes : 0;
+  static constexpr int Smem = Stages * StageBytes + 8 * kOutBytes + Rx + 1024 + 256;
   static constexpr int TileElems = 256 * BNP;
 };
 
@@ -101,11 +104,15 @@ __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb
 // Cluster shapes (MC): 1 = one CTA pair; 2 = two pairs side by side in N sharing their A rows;
 // 3 = two pairs stacked in M sharing their B columns. A "super tile" = the cluster's tiles.
 // 4 = 2x2 pairs (cluster of 8): A shared along N and B along M, both by multicast.
+// 5 = K-split pair cluster: both pairs compute the SAME tile, pair 0 over the first half of K,
+//     pair 1 over the second; pair 1 streams its fp32 accumulator into pair 0's shared memory
+//     (DSMEM, 32-column chunks, double-buffered) and pair 0 adds it and stores the tile. Fills
+//     the machine for few-tile (small-M) products without a global split-K round trip.
 __host__ __device__ constexpr int pairs_of(int MC) { return MC == 1 ? 1 : MC == 4 ? 4 : 2; }
 __host__ __device__ constexpr bool mc_a(int MC) { return MC == 2 || MC == 4; }  // A multicast
 __host__ __device__ constexpr bool mc_b(int MC) { return MC == 3 || MC == 4; }  // B multicast
 __host__ __device__ constexpr int super_tiles(int MC, int num_m, int num_n) {
-  return MC == 1   ? num_m * num_n
+  return (MC == 1 || MC == 5) ? num_m * num_n
          : MC == 2 ? num_m * ((num_n + 1) / 2)
          : MC == 3 ? ((num_m + 1) / 2) * num_n
                    : ((num_m + 1) / 2) * ((num_n + 1) / 2);
@@ -126,7 +133,12 @@ __device__ __forceinline__ Unit unit_of(const Group& G, int u, int pair) {
   const int lu = u - P.unit0;
   const int st = lu / P.splits;
   x.split = lu % P.splits;
-  if (MC == 4) {
+  if (MC == 5) {  // both pairs on the same tile; `split` = which half of K
+    tile_coords(st, P.num_m, P.num_n, x.mb, x.nb);
+    x.split = pair;
+    x.ptile = st;
+    return x;
+  } else if (MC == 4) {
     int mbs, nbs;
     tile_coords(st, (P.num_m + 1) / 2, (P.num_n + 1) / 2, mbs, nbs);
     x.mb = mbs * 2 + (pair >> 1);
@@ -300,7 +312,7 @@ __device__ __forceinline__ void add_partials(const float4* base, int splits, int
 template <int BNP, int MC>
 __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThreads, 1)
     gemm_tc2_kernel(const __grid_constant__ Group G) {
-  using P = PC<BNP>;
+  using P = PC<BNP, MC>;
   constexpr int NP = pairs_of(MC);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -308,11 +320,14 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
   uint8_t* sA = smem;
   uint8_t* sB = sA + P::Stages * kABytes;
   uint8_t* sOut = sB + P::Stages * P::BBytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sOut + 8 * kOutBytes);
+  float* rx = reinterpret_cast<float*>(sOut + 8 * kOutBytes);  // MC 5: [2][32 cols][128 rows]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sOut + 8 * kOutBytes + P::Rx);
   uint64_t* empty = full + P::Stages;
   uint64_t* tfull = empty + P::Stages;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* rxf = tempty + 2;  // MC 5, in pair 0: the sender's chunks landed (tx bytes)
+  uint64_t* rxe = rxf + 2;     // MC 5, in pair 1: the owner consumed them (4 owner warps)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(rxe + 2);
   int* sflag = reinterpret_cast<int*>(tslot + 1);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -349,11 +364,14 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
     }
     for (int s = 0; s < P::Stages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NP);  // free once every pair's MMAs have read it (multicast)
+      // free once every pair's MMAs have read it (multicast); MC 5 pairs share nothing
+      mbar_init(&empty[s], MC == 5 ? 1 : NP);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs (the pair leader's copy is used)
+      mbar_init(&rxf[a], 1);  // MC 5 owner: its own expect_tx arrive + the sender's bulk bytes
+      mbar_init(&rxe[a], 4);  // MC 5 sender: the owner's 4 epilogue warps
     }
     fence_barrier_init();
   }
@@ -380,7 +398,7 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
       for (int u = cid; u < G.total_units; u += ncl) {
         const Unit t = unit_of<MC>(G, u, pair);
         const Prob& pr = G.p[t.prob];
-        const int kb0 = t.split * pr.kb_per_split;
+        const int kb0 = t.split * pr.kb_per_split;  // MC 5: split = this pair's K half
         const int kb1 = min(pr.num_kb, kb0 + pr.kb_per_split);
         const int m0 = t.mb * 256 + static_cast<int>(rank) * kBM;
         const int n0 = t.nb * BNP + static_cast<int>(rank) * P::BNC;
@@ -526,7 +544,8 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
             for (int k = 0; k < kBK / 16; ++k)
               umma_bf16_cg2(d_tmem, ad + k * a_step4, bd + k * b_step4, idesc,
                             (kb > kb0 || k > 0) ? 1u : 0u);
-            umma_commit_cg2_mc(&empty[stage], kAllMask);  // slot free once these MMAs retire
+            // slot free once these MMAs retire (every sharing pair's CTAs; MC 5: own pair)
+            umma_commit_cg2_mc(&empty[stage], MC == 5 ? pair_mask : kAllMask);
           }
           __syncwarp();
           if (++stage == P::Stages) {
@@ -557,6 +576,7 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
     int nbox = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
+    uint32_t rx_round = 0;  // MC 5: DSMEM chunk rounds so far (both pairs count alike)
     unsigned long long t_tf = 0, t_begin = clock64();
     for (int u = cid; u < G.total_units; u += ncl) {
       const Unit t = unit_of<MC>(G, u, pair);
@@ -576,7 +596,73 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
       tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
                              static_cast<uint32_t>(acc * BNP);
-      if (pr.splits == 1) {
+      if (MC == 5) {
+        // ---- K-split pair: pair 1 streams its accumulator into pair 0's smem (DSMEM), pair 0
+        // adds it in column chunks of 64 (two 32-column buffers) and stores the tile
+        const uint32_t peer = crank ^ 2u;  // same rank, other pair
+        const int rrow = quad * 32 + lane;
+        if (pair == 1) {
+          // sender: TMEM -> own staging (conflict-free [col][row]) -> one bulk copy per 32-col
+          // chunk into the owner's buffer, completing as tx bytes on the owner's rxf
+#pragma unroll 1
+          for (int k = 0; k < BNP / 64; ++k, ++rx_round) {
+            mbar_wait_cluster(&rxe[0], (rx_round & 1) ^ 1);  // owner done with the last round
+            mbar_wait_cluster(&rxe[1], (rx_round & 1) ^ 1);
+            uint32_t r0[32], r1[32];
+            tmem_ld32(t_row + k * 64, r0);
+            tmem_ld32(t_row + k * 64 + 32, r1);
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              rx[j * kBM + rrow] = __uint_as_float(r0[j]);
+              rx[(32 + j) * kBM + rrow] = __uint_as_float(r1[j]);
+            }
+            fence_proxy_async_smem();
+            named_barrier_sync(1, 128);
+            if (threadIdx.x == 64) {
+              const uint32_t src = smem_u32(rx);
+              bulk_s2s(mapa(src, peer), src, 32 * kBM * 4, mapa(smem_u32(&rxf[0]), peer));
+              bulk_s2s(mapa(src + 32 * kBM * 4, peer), src + 32 * kBM * 4, 32 * kBM * 4,
+                       mapa(smem_u32(&rxf[1]), peer));
+            }
+          }
+        } else {
+#pragma unroll 1
+          for (int k = 0; k < BNP / 64; ++k, ++rx_round) {
+            if (threadIdx.x == 64) {  // this round's two chunks: 16 KB each
+              mbar_expect_tx(&rxf[0], 32 * kBM * 4);
+              mbar_expect_tx(&rxf[1], 32 * kBM * 4);
+            }
+            float v[64];
+            tmem_cols<64>(t_row, k, v);
+            mbar_wait(&rxf[0], rx_round & 1);
+            mbar_wait(&rxf[1], rx_round & 1);
+            const float* q0 = rx + rrow;
+#pragma unroll
+            for (int j = 0; j < 64; ++j) v[j] += q0[j * kBM];
+            __syncwarp();
+            if (lane == 0) {
+              mbar_arrive_cluster(&rxe[0], peer);
+              mbar_arrive_cluster(&rxe[1], peer);
+            }
+            if (pr.out_bf16) {
+              store_box<64>(pr, stg, nbox, lane, v, row, n0 + k * 64, row0);
+            } else {
+              float lo[32], hi[32];
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                lo[j] = v[j];
+                hi[j] = v[32 + j];
+              }
+              store_box<32>(pr, stg, nbox, lane, lo, row, n0 + k * 64, row0);
+              store_box<32>(pr, stg, nbox, lane, hi, row, n0 + k * 64 + 32, row0);
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(&tempty[acc], lead);
+      } else if (pr.splits == 1) {
         if (pr.out_bf16) {
 #pragma unroll 1
           for (int sub = 0; sub < BNP / 64; ++sub) {
@@ -789,7 +875,7 @@ int max_clusters(Kern kern, int csize, int smem) {
 template <int BNP, int MC>
 tp_status setup_prob(const GemmArgs& g, Prob& pr, int clusters, int split_mode, char*& ws,
                      size_t& ws_left, cudaStream_t s) {
-  using P = PC<BNP>;
+  using P = PC<BNP, MC>;
   const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   pr.a_mn = g.trans_a ? 1 : 0;
   pr.b_mn = g.trans_b ? 0 : 1;
@@ -857,6 +943,12 @@ tp_status setup_prob(const GemmArgs& g, Prob& pr, int clusters, int split_mode, 
         break;
       }
   }
+  if (MC == 5) {  // the cluster's two pairs split K in halves; no global split-K
+    if (num_k < 2) return fail(TP_ERR_UNSUPPORTED, "gemm: K-split pair cluster needs >= 2 k-blocks");
+    pr.splits = 1;
+    pr.kb_per_split = (num_k + 1) / 2;
+    return TP_OK;
+  }
   int kbps = (num_k + S - 1) / S;
   S = (num_k + kbps - 1) / kbps;  // no empty split
   if (S < 1) S = 1;
@@ -876,7 +968,7 @@ tp_status setup_prob(const GemmArgs& g, Prob& pr, int clusters, int split_mode, 
 
 template <int BNP, int MC>
 tp_status launch2(const GemmArgs* gs, int n, cudaStream_t s) {
-  using P = PC<BNP>;
+  using P = PC<BNP, MC>;
   auto kern = gemm_tc2_kernel<BNP, MC>;
   static int clusters = 0;
   {
@@ -973,6 +1065,8 @@ tp_status gemm_tc2_bf16(const GemmArgs& g, cudaStream_t s) {
   const int64_t nrows = (g.M + 255) / 256;
   const int64_t ncols = wide ? (g.N + 255) / 256 : (g.N + 127) / 128;
   const int mc = force_mc ? force_mc : 1;
+  const int64_t kblocks = (g.K + kBK - 1) / kBK * (g.npanels > 1 ? g.npanels : 1);
+  if (mc == 5 && kblocks >= 2) return force_bn == 128 ? launch2<128, 5>(&g, 1, s) : launch2<256, 5>(&g, 1, s);
   if (wide) {
     if (mc == 4 && ncols >= 2 && nrows >= 2) return launch2<256, 4>(&g, 1, s);
     if (mc == 2 && ncols >= 2) return launch2<256, 2>(&g, 1, s);

@@ -24,6 +24,22 @@ __device__ __forceinline__ uint32_t cluster_rank() {
   return r;
 }
 
+// store one fp32 to a shared::cluster address (DSMEM: another CTA of the cluster)
+__device__ __forceinline__ void st_cluster_f32(uint32_t addr, uint32_t bits) {
+  asm volatile("st.shared::cluster.b32 [%0], %1;" ::"r"(addr), "r"(bits) : "memory");
+}
+
+// bulk async copy of `bytes` from this CTA's smem to another CTA's smem (shared::cluster
+// addresses for dst and its mbarrier), completing as transaction bytes on that mbarrier
+__device__ __forceinline__ void bulk_s2s(uint32_t dst_cluster, uint32_t src_cta, uint32_t bytes,
+                                         uint32_t mbar_cluster) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          dst_cluster),
+      "r"(src_cta), "r"(bytes), "r"(mbar_cluster)
+      : "memory");
+}
+
 // true in exactly one (the leader) lane of the converged warp (elect.sync)
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;

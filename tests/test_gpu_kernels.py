@@ -158,6 +158,8 @@ def test_gemm_split_k_is_deterministic(api):
     {"TP_GEMM_KERNEL": "2", "TP_GEMM_MC": "3"},                # + B multicast over 2 pairs
     {"TP_GEMM_KERNEL": "2", "TP_GEMM_MC": "4"},                # 2x2 pairs, A and B multicast
     {"TP_GEMM_KERNEL": "2", "TP_GEMM_MC": "4", "TP_GEMM_BN": "128"},
+    {"TP_GEMM_KERNEL": "2", "TP_GEMM_MC": "5"},                # K-split pair cluster (DSMEM)
+    {"TP_GEMM_KERNEL": "2", "TP_GEMM_MC": "5", "TP_GEMM_BN": "128"},
     {"TP_GEMM_KERNEL": "2", "TP_GEMM_BN": "128"},              # 256x128 pair tiles
     {"TP_GEMM_KERNEL": "2", "TP_GEMM_BN": "256", "TP_GEMM_SPLITK": "0"},
 ], ids=lambda e: "-".join(f"{k[8:]}{v}" for k, v in e.items()))
