@@ -85,3 +85,75 @@ def ring_attention(Qs: dict, Ks: dict, Vs: dict, scale=None, ledger: Ledger | No
                     ledger.add("ring_v", group, r, (r + 1) % N, b * np.shape(Vs[0])[1])
             held = {r: held[(r - 1) % N] for r in range(N)}
     return O, S
+
+
+# ------------------------------------------------------------------------------- backward
+# The paper describes the forward only; the backward is the chain rule of the same definition
+# (reading N4), organised on the same ring:
+#   P = softmax(S), S = scale Q K^T, O = P V
+#   dV = P^T dO,  dP = dO V^T,  dS = P * (dP - rowsum(P * dP)),  dQ = scale dS K,
+#   dK = scale dS^T Q.
+# Rank r holds query rows r; it recomputes its score rows with the K ring (as the forward),
+# forms dP over the V ring, dQ over the K ring, and its contributions P_r[:, j]^T dO_r and
+# scale dS_r[:, j]^T Q_r to every key block j, which a reduce-scatter over the ring sums into
+# the owner of block j.
+
+
+def attention_bwd(Q, K, V, dO, scale=None):
+    """Dense gradients (dQ, dK, dV) of O = softmax(Q K^T scale) V, fp64."""
+    Q, K, V, dO = (np.asarray(a, np.float64) for a in (Q, K, V, dO))
+    scale = 1.0 / math.sqrt(Q.shape[1]) if scale is None else scale
+    _, P = attention(Q, K, V, scale)
+    dV = P.T @ dO
+    dP = dO @ V.T
+    dS = P * (dP - (P * dP).sum(axis=1, keepdims=True))
+    return scale * dS @ K, scale * dS.T @ Q, dV
+
+
+def ring_attention_bwd(Qs: dict, Ks: dict, Vs: dict, dOs: dict, scale=None,
+                       ledger: Ledger | None = None):
+    """Rank-by-rank RSA backward: ({r: dQ_r}, {r: dK_r}, {r: dV_r})."""
+    N = len(Qs)
+    b, d = np.shape(Qs[0])
+    s = b * N
+    scale = 1.0 / math.sqrt(d) if scale is None else scale
+    group = tuple(range(N))
+    _, S = ring_attention(Qs, Ks, Vs, scale, ledger)    # K ring (recompute) + V ring
+    P = {}
+    for r in range(N):
+        e = np.exp(S[r] - S[r].max(axis=1, keepdims=True))
+        P[r] = e / e.sum(axis=1, keepdims=True)
+    # dP rows over the V ring
+    held = {r: np.asarray(Vs[r], np.float64) for r in range(N)}
+    dP = {r: np.zeros((b, s)) for r in range(N)}
+    for t in range(N):
+        for r in range(N):
+            j = (r - t) % N
+            dP[r][:, j * b:(j + 1) * b] = np.asarray(dOs[r], np.float64) @ held[r].T
+        if t < N - 1:
+            if ledger is not None:
+                for r in range(N):
+                    ledger.add("ring_v", group, r, (r + 1) % N, b * d)
+            held = {r: held[(r - 1) % N] for r in range(N)}
+    dS = {r: P[r] * (dP[r] - (P[r] * dP[r]).sum(axis=1, keepdims=True)) for r in range(N)}
+    # dQ over the K ring
+    held = {r: np.asarray(Ks[r], np.float64) for r in range(N)}
+    dQ = {r: np.zeros((b, d)) for r in range(N)}
+    for t in range(N):
+        for r in range(N):
+            j = (r - t) % N
+            dQ[r] = dQ[r] + scale * dS[r][:, j * b:(j + 1) * b] @ held[r]
+        if t < N - 1:
+            if ledger is not None:
+                for r in range(N):
+                    ledger.add("ring_k", group, r, (r + 1) % N, b * d)
+            held = {r: held[(r - 1) % N] for r in range(N)}
+    # dK, dV: every rank's contribution to every key block, summed at the block's owner
+    dK = {j: sum(scale * dS[r][:, j * b:(j + 1) * b].T @ np.asarray(Qs[r], np.float64)
+                 for r in range(N)) for j in range(N)}
+    dV = {j: sum(P[r][:, j * b:(j + 1) * b].T @ np.asarray(dOs[r], np.float64)
+                 for r in range(N)) for j in range(N)}
+    if ledger is not None and N > 1:  # two reduce-scatters of N blocks of b x d
+        for r in range(N):
+            ledger.add("reduce_scatter", group, r, r, 2 * (N - 1) * b * d)
+    return dQ, dK, dV

@@ -88,3 +88,37 @@ def test_zero_values_and_indivisible():
     assert not gathered(out, 2).any()
     with pytest.raises(rsa.IndivisibleSequence):
         rsa.shards(Q, 3)
+
+
+def test_backward_matches_torch_autograd_and_ring():
+    Q, K, V = qkv(13, 32, 8)
+    dO = synth.tensor(13, 3, 32, 8, dtype="fp32").astype(np.float64)
+    tq, tk, tv = (torch.tensor(a, requires_grad=True) for a in (Q, K, V))
+    out = torch.nn.functional.scaled_dot_product_attention(tq[None, None], tk[None, None], tv[None, None])[0, 0]
+    out.backward(torch.tensor(dO))
+    dQ, dK, dV = rsa.attention_bwd(Q, K, V, dO)
+    assert np.allclose(dQ, tq.grad.numpy(), atol=1e-12)
+    assert np.allclose(dK, tk.grad.numpy(), atol=1e-12)
+    assert np.allclose(dV, tv.grad.numpy(), atol=1e-12)
+    for N in (1, 2, 4):
+        rq, rk, rv = rsa.ring_attention_bwd(rsa.shards(Q, N), rsa.shards(K, N), rsa.shards(V, N),
+                                            rsa.shards(dO, N))
+        assert np.allclose(gathered(rq, N), dQ, atol=1e-12)
+        assert np.allclose(gathered(rk, N), dK, atol=1e-12)
+        assert np.allclose(gathered(rv, N), dV, atol=1e-12)
+
+
+def test_backward_finite_differences():
+    Q, K, V = qkv(17, 8, 4)
+    dO = synth.tensor(17, 3, 8, 4, dtype="fp32").astype(np.float64)
+    dQ, dK, dV = rsa.attention_bwd(Q, K, V, dO)
+    loss = lambda Q_, K_, V_: float((rsa.attention(Q_, K_, V_)[0] * dO).sum())
+    h = 1e-6
+    for A, G, which in ((Q, dQ, 0), (K, dK, 1), (V, dV, 2)):
+        E = np.zeros_like(A)
+        E[3, 1] = h
+        args_p = [Q, K, V]
+        args_m = [Q, K, V]
+        args_p[which] = A + E
+        args_m[which] = A - E
+        assert abs((loss(*args_p) - loss(*args_m)) / (2 * h) - G[3, 1]) < 1e-7
