@@ -272,6 +272,14 @@ typedef struct {
 tp_status tp_rsa_ws_size(const tp_grid* grid, const tp_rsa_desc* desc, size_t* ws_bytes);
 tp_status tp_rsa_fwd(tp_grid* grid, const tp_rsa_desc* desc, const void* q, const void* k,
                      const void* v, void* out, void* ws, size_t ws_bytes, void* stream);
+/* Backward (the chain rule of the same definition; the paper describes the forward only):
+ * given dout = dL/dout [heads, seq/p, d_k] of this rank's rows, writes dq, dk, dv (same layout).
+ * Scores are recomputed with the K ring; dP uses the V ring, dq the K ring; every rank's
+ * contributions to each key block's dk / dv are reduce-scattered over the ring (fp32).
+ * Same workspace as the forward (tp_rsa_ws_size covers both). */
+tp_status tp_rsa_bwd(tp_grid* grid, const tp_rsa_desc* desc, const void* q, const void* k,
+                     const void* v, const void* dout, void* dq, void* dk, void* dv, void* ws,
+                     size_t ws_bytes, void* stream);
 
 /* ---- analytic cost model --------------------- */
 /* One linear layer, fwd+bwd, bias-free, on the grid (mode, world, q, d) with desc's M, K, N,

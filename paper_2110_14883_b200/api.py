@@ -267,3 +267,9 @@ def tp_rsa_fwd(g, d: tp_rsa_desc, q, k, v, out, ws, stream=None, ws_bytes=None):
     wb = _nbytes(ws) if ws_bytes is None else ws_bytes
     _check(lib.tp_rsa_fwd(g, C.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(ws), wb,
                           _stream(stream)), "tp_rsa_fwd")
+
+
+def tp_rsa_bwd(g, d: tp_rsa_desc, q, k, v, dout, dq, dk, dv, ws, stream=None, ws_bytes=None):
+    wb = _nbytes(ws) if ws_bytes is None else ws_bytes
+    _check(lib.tp_rsa_bwd(g, C.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(dout), _ptr(dq), _ptr(dk),
+                          _ptr(dv), _ptr(ws), wb, _stream(stream)), "tp_rsa_bwd")

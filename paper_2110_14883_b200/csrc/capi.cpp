@@ -797,3 +797,11 @@ extern "C" tp_status tp_rsa_fwd(tp_grid* g, const tp_rsa_desc* d, const void* q,
   TP_CUDA(cudaSetDevice(g->device));
   return tp::rsa_fwd(g, d, q, k, v, out, ws, ws_bytes, static_cast<cudaStream_t>(stream));
 }
+
+extern "C" tp_status tp_rsa_bwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k,
+                                const void* v, const void* dout, void* dq, void* dk, void* dv,
+                                void* ws, size_t ws_bytes, void* stream) {
+  if (!g || !d) return tp::fail(TP_ERR_ARG, "tp_rsa_bwd: null grid or desc");
+  TP_CUDA(cudaSetDevice(g->device));
+  return tp::rsa_bwd(g, d, q, k, v, dout, dq, dk, dv, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+}

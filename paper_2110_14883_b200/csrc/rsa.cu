@@ -162,6 +162,37 @@ tp_status launch_softmax(const float* S, int64_t rows, int64_t s, tp_dtype dt, v
   return TP_OK;
 }
 
+// dS = scale * P * (dP - rowsum(P * dP)) per row (in place over P); dP fp32.
+template <typename T>
+__global__ void rsa_dscore(T* __restrict__ P, const float* __restrict__ dP, int64_t rows, int64_t s,
+                           float scale) {
+  const int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  T* pr = P + r * s;
+  const float* dr = dP + r * s;
+  float dsum = 0.f;
+  for (int64_t c = lane; c < s; c += 32) {
+    float pv;
+    if constexpr (sizeof(T) == 2) pv = __bfloat162float(pr[c]);
+    else pv = pr[c];
+    dsum += pv * dr[c];
+  }
+  dsum = wsum(dsum);
+  for (int64_t c = lane; c < s; c += 32) {
+    float pv;
+    if constexpr (sizeof(T) == 2) pv = __bfloat162float(pr[c]);
+    else pv = pr[c];
+    st_out(pr + c, scale * pv * (dr[c] - dsum));
+  }
+}
+
+template <typename T>
+__global__ void rsa_cast(const float* __restrict__ src, int64_t n, T* __restrict__ dst) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) st_out(dst + i, src[i]);
+}
+
 struct RsaPlan {
   int p = 1, r = 0;
   int64_t s = 0, b = 0, d = 0, heads = 0, chunk = 1;
@@ -196,6 +227,8 @@ struct RsaWs {
   float* acc = nullptr;     // [chunk, b, d] fp32 output accumulator
   void* gemm_ws = nullptr;  // split-K scratch
   size_t gemm_ws_bytes = 0;
+  float *parts_k = nullptr, *parts_v = nullptr;  // backward: [p][chunk][b][d] fp32
+  float *red_k = nullptr, *red_v = nullptr;      // backward: [chunk][b][d] fp32
 };
 
 void rsa_carve(Carver& c, const RsaPlan& P, RsaWs* w) {
@@ -207,16 +240,22 @@ void rsa_carve(Carver& c, const RsaPlan& P, RsaWs* w) {
   w->acc = static_cast<float*>(c.take(ch * P.b * P.d * 4));
   w->gemm_ws_bytes = gemm_tc2_ws_bytes();
   w->gemm_ws = c.take(w->gemm_ws_bytes);
+  // backward: per-destination-block dK / dV contributions and their reduce-scattered sums
+  w->parts_k = static_cast<float*>(c.take(size_t(P.p) * ch * P.b * P.d * 4));
+  w->parts_v = static_cast<float*>(c.take(size_t(P.p) * ch * P.b * P.d * 4));
+  w->red_k = static_cast<float*>(c.take(ch * P.b * P.d * 4));
+  w->red_v = static_cast<float*>(c.take(ch * P.b * P.d * 4));
 }
 
 GemmArgs rsa_gemm(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, const void* B,
                   int64_t ldb, bool tb, void* D, int64_t ldd, tp_dtype in, tp_dtype out, float alpha,
-                  const float* C, const RsaWs& w) {
+                  const float* C, const RsaWs& w, bool ta = false) {
   GemmArgs a;
   a.M = M;
   a.N = N;
   a.K = K;
   a.A = A;
+  a.trans_a = ta;
   a.lda = lda;
   a.B = B;
   a.ldb = ldb;
@@ -317,6 +356,149 @@ tp_status rsa_fwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k
         nb ^= 1;
       }
     }
+  }
+  return TP_OK;
+}
+
+
+// Backward (reading N4; oracle/ring_attention.py ring_attention_bwd): per head chunk,
+//   K ring -> scores (recomputed) -> softmax P;  dV parts P_r[:, j]^T dO_r for every block j;
+//   V ring -> dP = dO V_j^T;  dS = scale P (dP - rowsum(P dP)) (over P);
+//   K ring -> dQ = sum_j dS[:, j] K_j;  dK parts dS[:, j]^T Q_r;
+//   reduce-scatter of the dK / dV parts over the ring -> this rank's blocks.
+tp_status rsa_bwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k, const void* v,
+                  const void* dout, void* dq, void* dk, void* dv, void* ws, size_t ws_bytes,
+                  cudaStream_t s) {
+  RsaPlan P;
+  TP_TRY(rsa_plan(g, d, &P));
+  size_t need = 0;
+  TP_TRY(rsa_ws_bytes(g, d, &need));
+  if (ws_bytes < need || !ws) return fail(TP_ERR_WORKSPACE, "rsa: workspace too small");
+  if (!P.heads || !P.b || !P.d) return TP_OK;
+  if (!q || !k || !v || !dout || !dq || !dk || !dv) return fail(TP_ERR_ARG, "rsa_bwd: null pointer");
+  Carver c;
+  c.base = static_cast<char*>(ws);
+  RsaWs w;
+  rsa_carve(c, P, &w);
+  Comm* ring = g->axis[0].get();
+  const tp_dtype dt = d->dtype;
+  const float scale = d->scale != 0.f ? d->scale : 1.f / std::sqrt(static_cast<float>(P.d));
+  const int64_t bd = P.b * P.d;
+  std::vector<GemmArgs> gs;
+  for (int64_t h0 = 0; h0 < P.heads; h0 += P.chunk) {
+    const int64_t nh = std::min<int64_t>(P.chunk, P.heads - h0);
+    const char* qc = static_cast<const char*>(q) + h0 * bd * P.esz;
+    const char* doc = static_cast<const char*>(dout) + h0 * bd * P.esz;
+    // ---- K ring: recompute the score rows, softmax
+    const void* cur = static_cast<const char*>(k) + h0 * bd * P.esz;
+    int nb = 0;
+    for (int t = 0; t < P.p; ++t) {
+      const int j = ((P.r - t) % P.p + P.p) % P.p;
+      gs.clear();
+      for (int64_t h = 0; h < nh; ++h)
+        gs.push_back(rsa_gemm(P.b, P.b, P.d, qc + h * bd * P.esz, P.d,
+                              static_cast<const char*>(cur) + h * bd * P.esz, P.d, true,
+                              w.S + h * P.b * P.s + j * P.b, P.s, dt, TP_FP32, scale, nullptr, w));
+      TP_TRY(run_heads(gs, s));
+      if (t + 1 < P.p) {
+        TP_TRY(ring->shift(cur, w.kv[nb], size_t(nh) * bd, dt, -1, s));
+        cur = w.kv[nb];
+        nb ^= 1;
+      }
+    }
+    TP_TRY(launch_softmax(w.S, nh * P.b, P.s, dt, w.Pm, s));
+    // ---- dV parts: block j <- P[:, j]^T dO (fp32, laid out [j][h][b][d] for the reduce-scatter)
+    gs.clear();
+    for (int j = 0; j < P.p; ++j)
+      for (int64_t h = 0; h < nh; ++h)
+        gs.push_back(rsa_gemm(P.b, P.d, P.b,
+                              static_cast<const char*>(w.Pm) + (h * P.b * P.s + j * P.b) * P.esz, P.s,
+                              doc + h * bd * P.esz, P.d, false,
+                              w.parts_v + (int64_t(j) * nh + h) * bd, P.d, dt, TP_FP32, 1.f, nullptr, w,
+                              true));
+    TP_TRY(run_heads(gs, s));
+    // ---- V ring: dP = dO V_j^T (over the score buffer)
+    cur = static_cast<const char*>(v) + h0 * bd * P.esz;
+    nb = 0;
+    for (int t = 0; t < P.p; ++t) {
+      const int j = ((P.r - t) % P.p + P.p) % P.p;
+      gs.clear();
+      for (int64_t h = 0; h < nh; ++h)
+        gs.push_back(rsa_gemm(P.b, P.b, P.d, doc + h * bd * P.esz, P.d,
+                              static_cast<const char*>(cur) + h * bd * P.esz, P.d, true,
+                              w.S + h * P.b * P.s + j * P.b, P.s, dt, TP_FP32, 1.f, nullptr, w));
+      TP_TRY(run_heads(gs, s));
+      if (t + 1 < P.p) {
+        TP_TRY(ring->shift(cur, w.kv[nb], size_t(nh) * bd, dt, -1, s));
+        cur = w.kv[nb];
+        nb ^= 1;
+      }
+    }
+    // ---- dS = scale P (dP - rowsum(P dP)), in place over P
+    {
+      const int64_t rows = nh * P.b;
+      const unsigned G = static_cast<unsigned>((rows * 32 + 255) / 256);
+      if (dt == TP_BF16)
+        rsa_dscore<__nv_bfloat16><<<G, 256, 0, s>>>(static_cast<__nv_bfloat16*>(w.Pm), w.S, rows, P.s, scale);
+      else
+        rsa_dscore<float><<<G, 256, 0, s>>>(static_cast<float*>(w.Pm), w.S, rows, P.s, scale);
+      count_launch();
+      TP_CUDA(cudaGetLastError());
+    }
+    // ---- dK parts: block j <- dS[:, j]^T Q
+    gs.clear();
+    for (int j = 0; j < P.p; ++j)
+      for (int64_t h = 0; h < nh; ++h)
+        gs.push_back(rsa_gemm(P.b, P.d, P.b,
+                              static_cast<const char*>(w.Pm) + (h * P.b * P.s + j * P.b) * P.esz, P.s,
+                              qc + h * bd * P.esz, P.d, false,
+                              w.parts_k + (int64_t(j) * nh + h) * bd, P.d, dt, TP_FP32, 1.f, nullptr, w,
+                              true));
+    TP_TRY(run_heads(gs, s));
+    // ---- K ring: dQ = sum_j dS[:, j] K_j (fp32 accumulator through C)
+    cur = static_cast<const char*>(k) + h0 * bd * P.esz;
+    nb = 0;
+    char* dqc = static_cast<char*>(dq) + h0 * bd * P.esz;
+    for (int t = 0; t < P.p; ++t) {
+      const int j = ((P.r - t) % P.p + P.p) % P.p;
+      const bool last = t + 1 == P.p;
+      gs.clear();
+      for (int64_t h = 0; h < nh; ++h) {
+        void* D = last ? static_cast<void*>(dqc + h * bd * P.esz) : static_cast<void*>(w.acc + h * bd);
+        gs.push_back(rsa_gemm(P.b, P.d, P.b,
+                              static_cast<const char*>(w.Pm) + (h * P.b * P.s + j * P.b) * P.esz, P.s,
+                              static_cast<const char*>(cur) + h * bd * P.esz, P.d, false, D, P.d, dt,
+                              last ? dt : TP_FP32, 1.f, t > 0 ? w.acc + h * bd : nullptr, w));
+      }
+      TP_TRY(run_heads(gs, s));
+      if (!last) {
+        TP_TRY(ring->shift(cur, w.kv[nb], size_t(nh) * bd, dt, -1, s));
+        cur = w.kv[nb];
+        nb ^= 1;
+      }
+    }
+    // ---- dK, dV: sum every rank's contribution at the block's owner
+    const int64_t n = nh * bd;
+    const float* rk = w.parts_k;
+    const float* rv = w.parts_v;
+    if (ring) {
+      TP_TRY(ring->reducescatter(w.parts_k, w.red_k, n, TP_FP32, s));
+      TP_TRY(ring->reducescatter(w.parts_v, w.red_v, n, TP_FP32, s));
+      rk = w.red_k;
+      rv = w.red_v;
+    }
+    const unsigned G = static_cast<unsigned>((n + 255) / 256);
+    char* dkc = static_cast<char*>(dk) + h0 * bd * P.esz;
+    char* dvc = static_cast<char*>(dv) + h0 * bd * P.esz;
+    if (dt == TP_BF16) {
+      rsa_cast<__nv_bfloat16><<<G, 256, 0, s>>>(rk, n, reinterpret_cast<__nv_bfloat16*>(dkc));
+      rsa_cast<__nv_bfloat16><<<G, 256, 0, s>>>(rv, n, reinterpret_cast<__nv_bfloat16*>(dvc));
+    } else {
+      rsa_cast<float><<<G, 256, 0, s>>>(rk, n, reinterpret_cast<float*>(dkc));
+      rsa_cast<float><<<G, 256, 0, s>>>(rv, n, reinterpret_cast<float*>(dvc));
+    }
+    count_launch(2);
+    TP_CUDA(cudaGetLastError());
   }
   return TP_OK;
 }

@@ -47,6 +47,9 @@ tp_status layernorm_bwd(tp_grid* g, const tp_linear_desc* d, int tensor, const v
 tp_status rsa_ws_bytes(const tp_grid* g, const tp_rsa_desc* d, size_t* bytes);
 tp_status rsa_fwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k, const void* v,
                   void* out, void* ws, size_t ws_bytes, cudaStream_t s);
+tp_status rsa_bwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k, const void* v,
+                  const void* dout, void* dq, void* dk, void* dv, void* ws, size_t ws_bytes,
+                  cudaStream_t s);
 
 tp_status sched_fwd(Run& R, const void* x, const void* w, const void* bias, void* y);
 tp_status sched_bwd(Run& R, const void* dy, const void* x, const void* w, void* dx, void* dw,

@@ -100,3 +100,44 @@ def test_rsa_zero_values(api):
     Q, K, V = inputs(2, heads, s, d, "bf16")
     got = run_rsa(api, 2, heads, s, d, "bf16", Q, K, 0 * V)
     assert not got.any()
+
+
+def run_rsa_bwd(api, p, heads, s, d, dtype, Q, K, V, dO, scale=0.0):
+    transport = api.TP_TRANSPORT_LOCAL if p > 1 else api.TP_TRANSPORT_NONE
+    uid = api.tp_get_unique_id(transport)
+    b = s // p
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32)).cuda().to(TORCH_DT[dtype])
+
+    def rank_fn(r):
+        g = api.tp_grid_init("1d", p, r, 0, 1, 0, transport, uid)
+        st = torch.cuda.Stream()
+        try:
+            with torch.cuda.stream(st):
+                ds = api.rsa_desc(s, d, heads, dtype, scale)
+                q, k, v, do = (dev(X[:, r * b:(r + 1) * b, :]) for X in (Q, K, V, dO))
+                dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+                ws = torch.empty(api.tp_rsa_ws_size(g, ds), device="cuda", dtype=torch.uint8)
+                api.tp_rsa_bwd(g, ds, q, k, v, do, dq, dk, dv, ws)
+            st.synchronize()
+            return to_np(dq), to_np(dk), to_np(dv)
+        finally:
+            st.synchronize()
+            api.tp_grid_destroy(g)
+
+    per = run_ranks(p, rank_fn)
+    return tuple(np.concatenate([x[i] for x in per], axis=1) for i in range(3))
+
+
+@pytest.mark.parametrize("p", [1, 2, 4])
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_rsa_backward_vs_oracle(api, p, dtype):
+    heads, s, d = 2, 512, 64
+    Q, K, V = inputs(23, heads, s, d, dtype)
+    q = "bf16" if dtype == "bf16" else "fp32"
+    dO = np.stack([synth.tensor(23, 8 * h + 3, s, d, dtype=q) for h in range(heads)]).astype(np.float64)
+    dq, dk, dv = run_rsa_bwd(api, p, heads, s, d, dtype, Q, K, V, dO)
+    ref = [rsa.attention_bwd(Q[h], K[h], V[h], dO[h]) for h in range(heads)]
+    tol = 2e-2 if dtype == "bf16" else 1e-5
+    for i, got in enumerate((dq, dk, dv)):
+        want = np.stack([ref[h][i] for h in range(heads)])
+        assert rel_fro(got, want) <= tol, ("dq", "dk", "dv")[i]
