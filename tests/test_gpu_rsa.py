@@ -137,7 +137,7 @@ def test_rsa_backward_vs_oracle(api, p, dtype):
     dO = np.stack([synth.tensor(23, 8 * h + 3, s, d, dtype=q) for h in range(heads)]).astype(np.float64)
     dq, dk, dv = run_rsa_bwd(api, p, heads, s, d, dtype, Q, K, V, dO)
     ref = [rsa.attention_bwd(Q[h], K[h], V[h], dO[h]) for h in range(heads)]
-    tol = 2e-2 if dtype == "bf16" else 1e-5
+    tol = 1e-2 if dtype == "bf16" else 1e-5  # measured ~3e-3 in bf16
     for i, got in enumerate((dq, dk, dv)):
         want = np.stack([ref[h][i] for h in range(heads)])
         assert rel_fro(got, want) <= tol, ("dq", "dk", "dv")[i]
