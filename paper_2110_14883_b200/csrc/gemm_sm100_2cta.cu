@@ -1087,6 +1087,11 @@ tp_status gemm_tc2_group(const GemmArgs* in, int n, cudaStream_t s) {
   for (int i = 0; i < n; ++i) gs[i] = in[i];
   auto kblocks = [](const GemmArgs& g) { return g.K * (g.npanels > 1 ? g.npanels : 1); };
   std::stable_sort(gs, gs + n, [&](const GemmArgs& x, const GemmArgs& y) { return kblocks(x) > kblocks(y); });
+  static const int group_bn = [] {
+    const char* e = std::getenv("TP_GEMM_GROUP_BN");
+    return e ? std::atoi(e) : 256;
+  }();
+  if (group_bn == 128) return launch2<128, 1>(gs, n, s);
   return launch2<256, 1>(gs, n, s);
 }
 
