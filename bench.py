@@ -26,6 +26,9 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# one metric string for both arms (BASELINE.json metric; value = whole-job TFLOP/s)
+METRIC = "TP linear fwd+bwd TFLOP/s (whole job; per-GPU in per_gpu_tflops) + % of roofline"
+
 # BASELINE.json configs -> (M tokens, hidden, layer widths)
 WORKLOADS = {
     "c1": dict(M=16, layers=[(64, 64), (64, 64)], dtype="fp32",
@@ -43,6 +46,30 @@ WORKLOADS = {
 }
 
 DEFAULT_MODE = {1: "1d", 2: "1d", 4: "2d", 8: "3d"}
+
+
+def grid_dims(mode, world, depth):
+    if mode == "1d":
+        return [world]
+    if mode == "2d":
+        q = round(world ** 0.5)
+        return [q, q]
+    if mode == "2.5d":
+        q = round((world // depth) ** 0.5)
+        return [depth, q, q]
+    l = round(world ** (1 / 3))
+    return [l, l, l]
+
+
+def config_of(workload, mode, depth, world, fused=False):
+    """The bench line's `config` (identical on both arms)."""
+    wl = WORKLOADS[workload]
+    M, layers = wl["M"], wl["layers"]
+    return {"workload": workload, "desc": wl["desc"], "mode": mode, "depth": depth,
+            "grid": grid_dims(mode, world, depth), "M": M, "layers": layers,
+            "flops_per_step": float(sum(6.0 * M * K * N for K, N in layers)),
+            "l2": "flushed (256 MiB write) between timed steps",
+            "parallelism": f"tp-{mode}x{world}" + ("-fused" if fused else "")}
 
 
 def parse():
@@ -322,15 +349,12 @@ def run_ours(a):
         cpu = cpu_baseline(a, mode, world, depth)
 
     line = {
-        "metric": "TP linear fwd+bwd TFLOP/s (whole job; per-GPU in per_gpu_tflops) + % of roofline",
+        "metric": METRIC,
         "value": round(value, 3), "unit": "TFLOP/s", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16" if dtype == "bf16" else "f32",
         "data": "synthetic (seeded SplitMix64, Xavier-uniform W, U(-1,1) X/dY; generated in HBM)",
-        "config": {"workload": a.workload, "desc": wl["desc"], "mode": mode, "depth": depth,
-                   "grid": list(api.tp_grid_dims(g)), "M": M, "layers": layers,
-                   "flops_per_step": flops, "l2": "flushed (256 MiB write) between timed steps",
-                   "parallelism": f"tp-{mode}x{world}" + ("-fused" if fused else "")},
+        "config": config_of(a.workload, mode, depth, world, fused),
         "per_gpu_tflops": round(value / world, 3),
         "wall_s": round(t_wall, 3),
         "launch": "cuda-graph replay" if graph is not None else "eager",
@@ -434,11 +458,11 @@ def run_reference(a):
         fl += oracle_step(wl, mode, world, depth, a.seed, M_run)
     dt = time.perf_counter() - t0
     v = fl / dt / 1e12
-    line = {"impl": "reference", "metric": "TP linear fwd+bwd TFLOP/s (whole job) + % of roofline",
+    line = {"impl": "reference", "metric": METRIC,
             "value": round(v, 6), "unit": "TFLOP/s", "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": round(dt / a.steps * 1e3, 3), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": a.workload, "mode": mode, "depth": depth, "M_sample": M_run},
+            "config": config_of(a.workload, mode, depth, world),
             "cpu_baseline": {"value": round(v, 6), "unit": "TFLOP/s", "kind": "oracle",
                              "cores": oracle_threads(),
                              "sample": f"M={M_run} of {M} rows per step, fp64 numpy oracle"},
