@@ -281,6 +281,25 @@ tp_status tp_rsa_bwd(tp_grid* grid, const tp_rsa_desc* desc, const void* q, cons
                      const void* v, const void* dout, void* dq, void* dk, void* dv, void* ws,
                      size_t ws_bytes, void* stream);
 
+/* ---- multi-head attention core in the TP layouts ---------------------- */
+/* Between a QKV linear (qkv_desc: M tokens = batch x seq, K = h, N = 3h) and the output
+ * projection: per sequence and head, softmax(Q K^T scale) V (scale 0 = 1/sqrt(d)).
+ * Head g occupies QKV columns [3 d g, 3 d (g+1)) as [q | k | v] (d = h / heads), so this
+ * rank's QKV output block (tp_shard_extent(grid, qkv_desc, TP_TENSOR_Y), row stride = cols)
+ * holds whole heads; its row extent must hold whole sequences. All work is local (no
+ * communication in any mode). out: [rows, heads_local d] = the X block of the output
+ * projection (1D row split, same 2D / 2.5D block, 3D parity + 1); backward takes dL/d(out)
+ * in that layout and writes dL/d(qkv) in the QKV block layout. Errors: TP_ERR_SHAPE (a
+ * block splits a head or a sequence, d % 8), TP_ERR_WORKSPACE. */
+tp_status tp_attention_ws_size(const tp_grid* grid, const tp_linear_desc* qkv_desc, int64_t seq,
+                               int64_t heads, size_t* ws_bytes);
+tp_status tp_attention_fwd(tp_grid* grid, const tp_linear_desc* qkv_desc, int64_t seq,
+                           int64_t heads, float scale, const void* qkv, void* out, void* ws,
+                           size_t ws_bytes, void* stream);
+tp_status tp_attention_bwd(tp_grid* grid, const tp_linear_desc* qkv_desc, int64_t seq,
+                           int64_t heads, float scale, const void* qkv, const void* dout,
+                           void* dqkv, void* ws, size_t ws_bytes, void* stream);
+
 /* ---- analytic cost model --------------------- */
 /* One linear layer, fwd+bwd, bias-free, on the grid (mode, world, q, d) with desc's M, K, N,
  * dtype, split_1d and flags (TP_FLAG_W25_DEPTH_SHARDED). Host only, no device work.

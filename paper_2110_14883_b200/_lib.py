@@ -39,7 +39,8 @@ EXPORTED = [
     "tp_colsum", "tp_fill", "tp_l2_flush", "tp_prof_enable", "tp_prof_reset", "tp_prof_read",
     "tp_launch_count", "tp_gemm_trace", "tp_register_buffer", "tp_deregister_all",
     "tp_cost_model", "tp_layernorm_ws_size", "tp_layernorm_fwd", "tp_layernorm_bwd",
-    "tp_rsa_ws_size", "tp_rsa_fwd", "tp_rsa_bwd",
+    "tp_rsa_ws_size", "tp_rsa_fwd", "tp_rsa_bwd", "tp_attention_ws_size", "tp_attention_fwd",
+    "tp_attention_bwd",
 ]
 
 
@@ -102,6 +103,11 @@ _sigs = {
     "tp_rsa_fwd": (_i, [_vp, C.POINTER(tp_rsa_desc), _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "tp_rsa_bwd": (_i, [_vp, C.POINTER(tp_rsa_desc), _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz,
                         _vp]),
+    "tp_attention_ws_size": (_i, [_vp, C.POINTER(tp_linear_desc), _i64, _i64, C.POINTER(_sz)]),
+    "tp_attention_fwd": (_i, [_vp, C.POINTER(tp_linear_desc), _i64, _i64, _f, _vp, _vp, _vp, _sz,
+                              _vp]),
+    "tp_attention_bwd": (_i, [_vp, C.POINTER(tp_linear_desc), _i64, _i64, _f, _vp, _vp, _vp, _vp,
+                              _sz, _vp]),
     "tp_cost_model": (_i, [_i, _i, _i, _i, C.POINTER(tp_linear_desc), C.c_double, C.c_double,
                            C.POINTER(tp_cost)]),
 }

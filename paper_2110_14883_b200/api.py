@@ -273,3 +273,23 @@ def tp_rsa_bwd(g, d: tp_rsa_desc, q, k, v, dout, dq, dk, dv, ws, stream=None, ws
     wb = _nbytes(ws) if ws_bytes is None else ws_bytes
     _check(lib.tp_rsa_bwd(g, C.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(dout), _ptr(dq), _ptr(dk),
                           _ptr(dv), _ptr(ws), wb, _stream(stream)), "tp_rsa_bwd")
+
+
+def tp_attention_ws_size(g, d, seq, heads) -> int:
+    n = C.c_size_t()
+    _check(lib.tp_attention_ws_size(g, C.byref(d), int(seq), int(heads), C.byref(n)),
+           "tp_attention_ws_size")
+    return n.value
+
+
+def tp_attention_fwd(g, d, seq, heads, qkv, out, ws, scale=0.0, stream=None, ws_bytes=None):
+    wb = _nbytes(ws) if ws_bytes is None else ws_bytes
+    _check(lib.tp_attention_fwd(g, C.byref(d), int(seq), int(heads), float(scale), _ptr(qkv),
+                                _ptr(out), _ptr(ws), wb, _stream(stream)), "tp_attention_fwd")
+
+
+def tp_attention_bwd(g, d, seq, heads, qkv, dout, dqkv, ws, scale=0.0, stream=None, ws_bytes=None):
+    wb = _nbytes(ws) if ws_bytes is None else ws_bytes
+    _check(lib.tp_attention_bwd(g, C.byref(d), int(seq), int(heads), float(scale), _ptr(qkv),
+                                _ptr(dout), _ptr(dqkv), _ptr(ws), wb, _stream(stream)),
+           "tp_attention_bwd")

@@ -805,3 +805,28 @@ extern "C" tp_status tp_rsa_bwd(tp_grid* g, const tp_rsa_desc* d, const void* q,
   TP_CUDA(cudaSetDevice(g->device));
   return tp::rsa_bwd(g, d, q, k, v, dout, dq, dk, dv, ws, ws_bytes, static_cast<cudaStream_t>(stream));
 }
+
+// ---------------------------------------------------------------- multi-head attention core
+extern "C" tp_status tp_attention_ws_size(const tp_grid* g, const tp_linear_desc* d, int64_t seq,
+                                          int64_t heads, size_t* ws_bytes) {
+  if (!ws_bytes) return tp::fail(TP_ERR_ARG, "tp_attention_ws_size: null ws_bytes");
+  return tp::attention_ws_bytes(g, d, seq, heads, ws_bytes);
+}
+
+extern "C" tp_status tp_attention_fwd(tp_grid* g, const tp_linear_desc* d, int64_t seq,
+                                      int64_t heads, float scale, const void* qkv, void* out,
+                                      void* ws, size_t ws_bytes, void* stream) {
+  if (!g) return tp::fail(TP_ERR_ARG, "tp_attention_fwd: null grid");
+  TP_CUDA(cudaSetDevice(g->device));
+  return tp::attention_fwd(g, d, seq, heads, scale, qkv, out, ws, ws_bytes,
+                           static_cast<cudaStream_t>(stream));
+}
+
+extern "C" tp_status tp_attention_bwd(tp_grid* g, const tp_linear_desc* d, int64_t seq,
+                                      int64_t heads, float scale, const void* qkv, const void* dout,
+                                      void* dqkv, void* ws, size_t ws_bytes, void* stream) {
+  if (!g) return tp::fail(TP_ERR_ARG, "tp_attention_bwd: null grid");
+  TP_CUDA(cudaSetDevice(g->device));
+  return tp::attention_bwd(g, d, seq, heads, scale, qkv, dout, dqkv, ws, ws_bytes,
+                           static_cast<cudaStream_t>(stream));
+}

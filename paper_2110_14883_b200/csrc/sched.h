@@ -51,6 +51,15 @@ tp_status rsa_bwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k
                   const void* dout, void* dq, void* dk, void* dv, void* ws, size_t ws_bytes,
                   cudaStream_t s);
 
+// Multi-head attention core in the TP layouts (attn.cu).
+tp_status attention_ws_bytes(const tp_grid* g, const tp_linear_desc* qd, int64_t seq, int64_t heads,
+                             size_t* bytes);
+tp_status attention_fwd(tp_grid* g, const tp_linear_desc* qd, int64_t seq, int64_t heads, float scale,
+                        const void* qkv, void* out, void* ws, size_t ws_bytes, cudaStream_t s);
+tp_status attention_bwd(tp_grid* g, const tp_linear_desc* qd, int64_t seq, int64_t heads, float scale,
+                        const void* qkv, const void* dout, void* dqkv, void* ws, size_t ws_bytes,
+                        cudaStream_t s);
+
 tp_status sched_fwd(Run& R, const void* x, const void* w, const void* bias, void* y);
 tp_status sched_bwd(Run& R, const void* dy, const void* x, const void* w, void* dx, void* dw,
                     void* dbias);
