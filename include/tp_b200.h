@@ -206,6 +206,10 @@ tp_status tp_fill(void* dst, tp_dtype dtype, int64_t rows, int64_t cols, int64_t
                   uint64_t seed, int tensor_id, int kind, float scale, int64_t g_row0,
                   int64_t g_col0, int64_t g_cols, void* stream);
 
+/* out[i] = a[i] + b[i] for n elements of dtype (a Transformer block's residual connections;
+ * out may alias a or b). 16-byte aligned buffers. */
+tp_status tp_add(const void* a, const void* b, void* out, size_t n, tp_dtype dtype, void* stream);
+
 /* Writes `bytes` to a scratch buffer (device) to evict L2 between timed steps. */
 tp_status tp_l2_flush(void* scratch, size_t bytes, void* stream);
 

@@ -40,7 +40,7 @@ EXPORTED = [
     "tp_launch_count", "tp_gemm_trace", "tp_register_buffer", "tp_deregister_all",
     "tp_cost_model", "tp_layernorm_ws_size", "tp_layernorm_fwd", "tp_layernorm_bwd",
     "tp_rsa_ws_size", "tp_rsa_fwd", "tp_rsa_bwd", "tp_attention_ws_size", "tp_attention_fwd",
-    "tp_attention_bwd",
+    "tp_attention_bwd", "tp_add",
 ]
 
 
@@ -108,6 +108,7 @@ _sigs = {
                               _vp]),
     "tp_attention_bwd": (_i, [_vp, C.POINTER(tp_linear_desc), _i64, _i64, _f, _vp, _vp, _vp, _vp,
                               _sz, _vp]),
+    "tp_add": (_i, [_vp, _vp, _vp, _sz, _i, _vp]),
     "tp_cost_model": (_i, [_i, _i, _i, _i, C.POINTER(tp_linear_desc), C.c_double, C.c_double,
                            C.POINTER(tp_cost)]),
 }

@@ -293,3 +293,9 @@ def tp_attention_bwd(g, d, seq, heads, qkv, dout, dqkv, ws, scale=0.0, stream=No
     _check(lib.tp_attention_bwd(g, C.byref(d), int(seq), int(heads), float(scale), _ptr(qkv),
                                 _ptr(dout), _ptr(dqkv), _ptr(ws), wb, _stream(stream)),
            "tp_attention_bwd")
+
+
+def tp_add(a, b, out, dtype=None, stream=None):
+    dt = DTYPES[dtype] if isinstance(dtype, str) else (int(dtype) if dtype is not None else
+                                                       (TP_BF16 if out.element_size() == 2 else TP_FP32))
+    _check(lib.tp_add(_ptr(a), _ptr(b), _ptr(out), out.numel(), dt, _stream(stream)), "tp_add")

@@ -830,3 +830,10 @@ extern "C" tp_status tp_attention_bwd(tp_grid* g, const tp_linear_desc* d, int64
   return tp::attention_bwd(g, d, seq, heads, scale, qkv, dout, dqkv, ws, ws_bytes,
                            static_cast<cudaStream_t>(stream));
 }
+
+extern "C" tp_status tp_add(const void* a, const void* b, void* out, size_t n, tp_dtype dt,
+                            void* stream) {
+  if (n && (!a || !b || !out)) return tp::fail(TP_ERR_ARG, "tp_add: null pointer");
+  if (dt != TP_BF16 && dt != TP_FP32) return tp::fail(TP_ERR_ARG, "tp_add: dtype");
+  return tp::launch_add(a, b, out, n, dt, static_cast<cudaStream_t>(stream));
+}

@@ -336,4 +336,44 @@ tp_status launch_gelu_bwd(const void* dy, const void* z, void* dz, size_t n, tp_
   return TP_OK;
 }
 
+
+// ------------------------------------------------------------------------------ residual add
+namespace {
+template <typename T>
+__global__ void add_kernel(const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ out, size_t n) {
+  constexpr int V = 16 / sizeof(T);
+  const size_t nv = n / V;
+  const size_t stride = size_t(gridDim.x) * blockDim.x;
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nv; i += stride) {
+    const uint4 x = reinterpret_cast<const uint4*>(a)[i];
+    const uint4 y = reinterpret_cast<const uint4*>(b)[i];
+    uint4 o;
+    const T* ex = reinterpret_cast<const T*>(&x);
+    const T* ey = reinterpret_cast<const T*>(&y);
+    T* eo = reinterpret_cast<T*>(&o);
+#pragma unroll
+    for (int j = 0; j < V; ++j) eo[j] = from_f<T>(to_f(ex[j]) + to_f(ey[j]));
+    reinterpret_cast<uint4*>(out)[i] = o;
+  }
+  for (size_t i = nv * V + size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = from_f<T>(to_f(a[i]) + to_f(b[i]));
+}
+}  // namespace
+
+tp_status launch_add(const void* a, const void* b, void* out, size_t n, tp_dtype dt, cudaStream_t s) {
+  if (!n) return TP_OK;
+  if ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) | reinterpret_cast<uintptr_t>(out)) % 16)
+    return fail(TP_ERR_SHAPE, "add: 16-byte aligned buffers required");
+  if (dt == TP_BF16)
+    add_kernel<__nv_bfloat16><<<elem_grid(n), 256, 0, s>>>(static_cast<const __nv_bfloat16*>(a),
+                                                          static_cast<const __nv_bfloat16*>(b),
+                                                          static_cast<__nv_bfloat16*>(out), n);
+  else
+    add_kernel<float><<<elem_grid(n), 256, 0, s>>>(static_cast<const float*>(a), static_cast<const float*>(b),
+                                                  static_cast<float*>(out), n);
+  count_launch();
+  TP_CUDA(cudaGetLastError());
+  return TP_OK;
+}
+
 }  // namespace tp

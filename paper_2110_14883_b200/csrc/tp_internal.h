@@ -65,6 +65,8 @@ tp_status launch_copy2d(const void* src, int64_t src_ld, void* dst, int64_t dst_
                         int64_t cols, size_t esz, cudaStream_t s);
 // GeLU (exact erf form) over n elements: fwd z = y, y = gelu(y); bwd dz = dy * gelu'(z).
 tp_status launch_gelu_fwd(void* y, void* z, size_t n, tp_dtype dt, cudaStream_t s);
+// out = a + b elementwise (residual connections); out may alias a or b.
+tp_status launch_add(const void* a, const void* b, void* out, size_t n, tp_dtype dt, cudaStream_t s);
 tp_status launch_gelu_bwd(const void* dy, const void* z, void* dz, size_t n, tp_dtype dt,
                           cudaStream_t s);
 // Deterministic two-pass column sums; scratch holds kColsumSlabs * cols floats.
