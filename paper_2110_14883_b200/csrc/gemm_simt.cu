@@ -144,6 +144,14 @@ tp_status gemm(const GemmArgs& g, cudaStream_t s) {
   if (g.ldb < (g.trans_b ? g.K : g.N)) return fail(TP_ERR_SHAPE, "gemm: ldb too small");
   if (g.M > INT32_MAX || g.N > INT32_MAX || g.K > INT32_MAX)
     return fail(TP_ERR_UNSUPPORTED, "gemm: dims must fit int32");
+  if (g.dpanels > 1) {  // fused 1D reduce-scatter: D row-panels, CTA-pair kernel only
+    if (g.in_dtype != TP_BF16 || g.npanels > 1 || !gemm_tc2_supported(g))
+      return fail(TP_ERR_UNSUPPORTED, "gemm: D row-panels need bf16, M > 128, d_rows % 32 == 0");
+    if ((reinterpret_cast<uintptr_t>(g.A) % 16) || (reinterpret_cast<uintptr_t>(g.B) % 16) ||
+        (g.lda % 8) || (g.ldb % 8))
+      return fail(TP_ERR_SHAPE, "gemm: TMA needs 16-byte aligned operands");
+    return gemm_tc2_bf16(g, s);
+  }
   if (g.npanels > 1) {  // fused peer-panel product: CTA-pair kernel only
     if (g.in_dtype != TP_BF16 || g.npanels > 4 || !gemm_tc2_supported(g))
       return fail(TP_ERR_UNSUPPORTED, "gemm: K-panels need bf16, <= 4 panels and M > 128");

@@ -49,6 +49,7 @@ constexpr int kOutBytes = 32 * 128;  // per epilogue warp and buffer: 32 rows x 
 constexpr int kThreads = 192;
 constexpr int kMaxProbs = 4;
 constexpr int kMaxPanels = 4;  // K-panels per problem (peer shards of a fused SUMMA)
+constexpr int kMaxDPanels = 8;  // D row-panels per problem (fused 1D reduce-scatter slots)
 
 // Pair-tile width BNP (256 or 128): B columns per CTA, ring depth, TMEM, smem. MC 5 (K-split
 // pair cluster) gives one ring stage to the 32 KB DSMEM receive buffer of the split reduction.
@@ -66,7 +67,9 @@ struct PC {
 };
 
 struct Prob {
-  CUtensorMap tmA[kMaxPanels], tmB[kMaxPanels], tmD;  // one A/B map per K-panel
+  CUtensorMap tmA[kMaxPanels], tmB[kMaxPanels];  // one A/B map per K-panel
+  CUtensorMap tmD[kMaxDPanels];                   // one D map per row-panel (usually 1)
+  int d_rows;                                      // rows per D panel (0: a single D)
   const float* C;
   const void* bias;
   float* part;
@@ -223,8 +226,12 @@ __device__ __forceinline__ void store_box(const Prob& ep, uint8_t* stg, int& nbo
   fence_proxy_async_smem();
   __syncwarp();
   if (lane == 0) {
-    tma_store_2d(&ep.tmD, buf, static_cast<int>(col0), static_cast<int>(row0));
-    bulk_commit();
+    const int pi = ep.d_rows ? static_cast<int>(row0 / ep.d_rows) : 0;
+    if (pi < kMaxDPanels) {
+      tma_store_2d(&ep.tmD[pi], buf, static_cast<int>(col0),
+                   static_cast<int>(row0 - int64_t(pi) * ep.d_rows));
+      bulk_commit();
+    }
   }
   ++nbox;
 }
@@ -360,7 +367,7 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
         tma_prefetch(&G.p[i].tmA[k]);
         tma_prefetch(&G.p[i].tmB[k]);
       }
-      tma_prefetch(&G.p[i].tmD);
+      tma_prefetch(&G.p[i].tmD[0]);
     }
     for (int s = 0; s < P::Stages; ++s) {
       mbar_init(&full[s], 1);
@@ -897,10 +904,17 @@ tp_status setup_prob(const GemmArgs& g, Prob& pr, int clusters, int split_mode, 
   }
   pr.kb_panel = static_cast<int>((g.K + kBK - 1) / kBK);
   pr.num_kb = pr.kb_panel * pr.npanels;
-  if (g.out_dtype == TP_BF16)
-    TP_TRY(make_map2(&pr.tmD, BF, 2, g.D, g.N, g.M, g.ldd, 64, 32));
-  else
-    TP_TRY(make_map2(&pr.tmD, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, g.D, g.N, g.M, g.ldd, 32, 32));
+  const int dp = g.dpanels > 1 ? g.dpanels : 1;
+  if (dp > kMaxDPanels) return fail(TP_ERR_UNSUPPORTED, "gemm: more than 8 D row-panels");
+  pr.d_rows = dp > 1 ? static_cast<int>(g.d_rows) : 0;
+  for (int i = 0; i < dp; ++i) {
+    void* D = dp > 1 ? g.Dp[i] : g.D;
+    const uint64_t rows = dp > 1 ? uint64_t(g.d_rows) : uint64_t(g.M);
+    if (g.out_dtype == TP_BF16)
+      TP_TRY(make_map2(&pr.tmD[i], BF, 2, D, g.N, rows, g.ldd, 64, 32));
+    else
+      TP_TRY(make_map2(&pr.tmD[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, D, g.N, rows, g.ldd, 32, 32));
+  }
   pr.C = g.C;
   pr.bias = g.bias;
   pr.ldc = g.ldc;
@@ -1038,8 +1052,13 @@ tp_status launch2(const GemmArgs* gs, int n, cudaStream_t s) {
 
 bool gemm_tc2_supported(const GemmArgs& g) {
   const size_t osz = dtype_size(g.out_dtype);
-  return g.M > 128 && (reinterpret_cast<uintptr_t>(g.D) % 16 == 0) && ((g.ldd * osz) % 16 == 0) &&
-         (!g.bias || reinterpret_cast<uintptr_t>(g.bias) % 2 == 0);
+  if (g.dpanels > 1) {
+    if (g.dpanels > kMaxDPanels || g.d_rows % 32 || g.d_rows * g.dpanels < g.M) return false;
+    for (int i = 0; i < g.dpanels; ++i)
+      if (!g.Dp[i] || reinterpret_cast<uintptr_t>(g.Dp[i]) % 16) return false;
+  }
+  return g.M > 128 && (g.dpanels > 1 || reinterpret_cast<uintptr_t>(g.D) % 16 == 0) &&
+         ((g.ldd * osz) % 16 == 0) && (!g.bias || reinterpret_cast<uintptr_t>(g.bias) % 2 == 0);
 }
 
 size_t gemm_tc2_ws_bytes() {

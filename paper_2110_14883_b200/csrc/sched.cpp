@@ -196,6 +196,53 @@ tp_status extent(const tp_grid* g, const tp_linear_desc* d, int tensor, Ext* e) 
 namespace {
 
 // =========================================================================== 1D (a-3, a-4)
+// ---- fused 1D reduce-scatter + all-gather over peer memory (TP_FLAG_PEER_FUSED, SURVEY
+// 8(f) NEXT-1 for 1D: "RS fused into the GEMM epilogue (partial tiles stored to the peer)").
+// The product whose partial sums the collective path all-reduces (1D column bwd: dX = sum_r
+// dY_r W_r^T; 1D row fwd: Y = sum_r X_r W_r) is computed in full on every rank, but the GEMM
+// epilogue stores the rows of block o straight into owner o's receive slot r (peer memory,
+// D row-panels); owner o sums its p slots in rank order (fp32) into its row block of the
+// output and every rank then copies the other row blocks from their owners. Moves the bytes
+// of a ring reduce-scatter + all-gather (= the all-reduce) without collective kernels; the
+// partials never round-trip through the sender's HBM. Needs `ws` (receive slots) and the
+// output registered (tp_register_buffer), 2 <= p <= 8, (rows / p) % 32 == 0.
+bool fused1d_ok(Ctx& C, const void* rx, const void* out, int64_t rows, int64_t cols) {
+  const int p = C.g->world;
+  if (!(C.d->flags & TP_FLAG_PEER_FUSED) || C.dt != TP_BF16 || !C.g->all || p < 2 || p > 8)
+    return false;
+  if (rows % p || (rows / p) % 32 || rows <= 128 || cols % 8) return false;
+  return rx && out && C.g->peer_ptr(C.g->rank, rx) && C.g->peer_ptr(C.g->rank, out);
+}
+
+tp_status fused_rs_ag(Ctx& C, GemmArgs a, const GemmArgs* other, void* rx, void* out, int64_t rows,
+                      int64_t cols) {
+  const tp_grid* g = C.g;
+  const int p = g->world, r = g->rank;
+  const int64_t b = rows / p;
+  const size_t blk = size_t(b) * cols * C.esz;
+  a.dpanels = p;
+  a.d_rows = b;
+  a.ldd = cols;
+  for (int o = 0; o < p; ++o)
+    a.Dp[o] = const_cast<char*>(static_cast<const char*>(g->peer_ptr(o, rx))) + r * blk;
+  a.D = a.Dp[0];
+  a.reserve_sms = 0;
+  TP_TRY(g->all->barrier(C.R.s));  // every owner's receive slots are free
+  if (other) TP_TRY(gemm_pair(a, *other, C.R.s));
+  else TP_TRY(gemm(a, C.R.s));
+  TP_TRY(g->all->barrier(C.R.s));  // every partial has landed
+  const void* in[8];
+  for (int o = 0; o < p; ++o) in[o] = static_cast<const char*>(rx) + o * blk;
+  TP_TRY(launch_sum_n(in, p, static_cast<char*>(out) + r * blk, size_t(b) * cols, C.dt, C.R.s));
+  TP_TRY(g->all->barrier(C.R.s));  // every owner has summed its block
+  for (int o = 0; o < p; ++o)
+    if (o != r)
+      TP_CUDA(cudaMemcpyAsync(static_cast<char*>(out) + o * blk,
+                              static_cast<const char*>(g->peer_ptr(o, out)) + o * blk, blk,
+                              cudaMemcpyDefault, C.R.s));
+  return g->all->barrier(C.R.s);   // nobody overwrites a block a peer still reads
+}
+
 tp_status fwd_1d(Ctx& C, const void* x, const void* w, const void* bias, void* y) {
   const tp_linear_desc* d = C.d;
   const int p = C.g->world, r = C.g->coords[0];
@@ -208,6 +255,9 @@ tp_status fwd_1d(Ctx& C, const void* x, const void* w, const void* bias, void* y
   const int64_t Kl = K / p;
   void* P = p > 1 ? C.ws(M * N) : y;
   if (C.R.plan) return TP_OK;
+  if (p > 1 && fused1d_ok(C, P, y, M, N))
+    return fused_rs_ag(C, C.args(M, N, Kl, x, false, w, false, nullptr, C.dt, d->alpha, nullptr,
+                                 r == 0 ? bias : nullptr), nullptr, P, y, M, N);
   TP_TRY(C.mm(M, N, Kl, x, false, w, false, P, C.dt, d->alpha, nullptr, r == 0 ? bias : nullptr));
   if (p > 1) {
     TP_TRY(C.order(C.R.s, C.R.cs));
@@ -229,6 +279,13 @@ tp_status bwd_1d(Ctx& C, const void* dy, const void* x, const void* w, void* dx,
     if (dx && p == 1) {  // no collective to overlap: dX and dW as one grouped launch
       TP_TRY(C.mm2(C.args(M, K, Nl, dy, false, w, true, dx, C.dt, d->alpha, nullptr, nullptr),
                    C.args(K, Nl, M, x, true, dy, false, dw, C.dt, d->alpha, nullptr, nullptr)));
+      if (dbias) TP_TRY(C.colsum(dy, M, Nl, dbias, scratch));
+      return TP_OK;
+    }
+    if (dx && fused1d_ok(C, P, dx, M, K)) {  // dX by the fused reduce-scatter + all-gather
+      const GemmArgs gw = C.args(K, Nl, M, x, true, dy, false, dw, C.dt, d->alpha, nullptr, nullptr);
+      TP_TRY(fused_rs_ag(C, C.args(M, K, Nl, dy, false, w, true, nullptr, C.dt, d->alpha, nullptr,
+                                   nullptr), &gw, P, dx, M, K));
       if (dbias) TP_TRY(C.colsum(dy, M, Nl, dbias, scratch));
       return TP_OK;
     }

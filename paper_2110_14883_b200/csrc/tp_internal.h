@@ -107,6 +107,12 @@ struct GemmArgs {
   int npanels = 1;
   const void* Ap[4] = {};
   const void* Bp[4] = {};
+  // D row-panels (fused 1D reduce-scatter): rows [p d_rows, (p+1) d_rows) of the product go
+  // to Dp[p] (row stride ldd), e.g. a slot in the owning rank's receive buffer. d_rows % 32 == 0.
+  // dpanels == 1 uses D. Only the CTA-pair kernel takes dpanels > 1.
+  int dpanels = 1;
+  int64_t d_rows = 0;
+  void* Dp[8] = {};
 };
 tp_status gemm(const GemmArgs& a, cudaStream_t s);         // dispatch + validation
 // Two independent GEMMs: one grouped CTA-pair launch when both qualify, else two launches.

@@ -143,3 +143,32 @@ def test_fused_3d_backward_after_unfused_dy(api, par):
     Yr, dXr, dWr, _ = oracle_layer("3d", 8, 1, spec, X, W, dY)
     for key, t, ref in (("Y", "Y", Yr), ("dX", "X", dXr), ("dW", "W", dWr)):
         assert np.array_equal(gather("3d", 8, 1, spec, per, key, t), ref), key
+
+
+@pytest.mark.parametrize("p,split", [(2, 0), (4, 0), (8, 0), (2, 1), (4, 1)])
+def test_fused_1d_reduce_scatter(api, p, split):
+    """1D: the all-reduced product (column split: dX in backward; row split: Y in forward) is
+    reduce-scattered by the GEMM epilogue into the owners' receive slots and all-gathered."""
+    M, K, N = 512, 384, 640
+    X, W, dY, b = synth.layer_inputs(29, M, K, N, with_bias=True)
+    per = tp_layer(api, "1d", p, 1, M, K, N, X, W, dY, b, "bf16", split, 0, FUSED, alpha=0.5)
+    spec = spec_of(M, K, N, split)
+    Yr, dXr, dWr, dbr = oracle_layer("1d", p, 1, spec, X, W, dY, b, alpha=0.5)
+    assert rel_fro(gather("1d", p, 1, spec, per, "Y", "Y"), Yr) <= 1e-2
+    assert rel_fro(gather("1d", p, 1, spec, per, "dX", "X"), dXr) <= 1e-2
+    assert rel_fro(gather("1d", p, 1, spec, per, "dW", "W"), dWr) <= 1e-2
+    assert rel_fro(gather("1d", p, 1, spec, per, "dB", "B"), dbr) <= 1e-2
+    if split == 1:  # the forward is one GEMM + the sum kernel per rank (+ peer copies)
+        assert per[0]["n_fwd"] == 2 * p
+
+
+def test_fused_1d_exact_integer(api):
+    M, K, N = 256, 128, 256
+    X, W, dY, _ = synth.layer_inputs(5, M, K, N, kind="ternary")
+    for split in (0, 1):
+        per = tp_layer(api, "1d", 4, 1, M, K, N, X, W, dY, None, "bf16", split, 0, FUSED)
+        spec = spec_of(M, K, N, split)
+        Yr, dXr, dWr, _ = oracle_layer("1d", 4, 1, spec, X, W, dY)
+        assert np.array_equal(gather("1d", 4, 1, spec, per, "Y", "Y"), Yr)
+        assert np.array_equal(gather("1d", 4, 1, spec, per, "dX", "X"), dXr)
+        assert np.array_equal(gather("1d", 4, 1, spec, per, "dW", "W"), dWr)

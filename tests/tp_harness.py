@@ -76,9 +76,13 @@ def tp_layer(api, mode, p, d, M, K, N, X, W, dY, b=None, dtype="bf16", split_1d=
                 ext = {t: api.tp_shard_extent(g, ds, t) for t in ("X", "W", "Y", "B")}
                 mk = lambda t: torch.empty(ext[t][1], ext[t][3], device="cuda", dtype=TORCH_DT[dtype])
                 x, w, y, dy = mk("X"), mk("W"), mk("Y"), mk("Y")
-                if flags & api.TP_FLAG_PEER_FUSED:  # peers read these shards directly
-                    for t in (x, w, dy):
-                        api.tp_register_buffer(g, t)
+                dx = torch.empty_like(x) if want_dx else None
+                wsb, svb = api.tp_workspace_size(g, ds)
+                ws = torch.empty(max(wsb, 1), device="cuda", dtype=torch.uint8)
+                if flags & api.TP_FLAG_PEER_FUSED:  # peers read / write these directly
+                    for t in (x, w, dy, y, dx, ws):
+                        if t is not None:
+                            api.tp_register_buffer(g, t)
                 api.tp_pack(g, ds, "X", gX, x)
                 api.tp_pack(g, ds, "W", gW, w)
                 api.tp_pack(g, ds, "Y", gdY, dy)
@@ -86,8 +90,6 @@ def tp_layer(api, mode, p, d, M, K, N, X, W, dY, b=None, dtype="bf16", split_1d=
                 if gb is not None:
                     bias = torch.empty(ext["B"][3], device="cuda", dtype=TORCH_DT[dtype])
                     api.tp_pack(g, ds, "B", gb, bias)
-                wsb, svb = api.tp_workspace_size(g, ds)
-                ws = torch.empty(max(wsb, 1), device="cuda", dtype=torch.uint8)
                 sv = torch.empty(svb, device="cuda", dtype=torch.uint8) if svb else None
                 s.synchronize()
                 bar.wait(120)  # count the launches of all ranks' forward calls (rank 0 reads)
@@ -96,7 +98,6 @@ def tp_layer(api, mode, p, d, M, K, N, X, W, dY, b=None, dtype="bf16", split_1d=
                 api.tp_linear_fwd(g, ds, x, w, bias, y, sv, ws)
                 bar.wait(120)
                 n_fwd = api.tp_launch_count() - n0
-                dx = torch.empty_like(x) if want_dx else None
                 dw = torch.empty_like(w)
                 db = torch.empty(ext["B"][3], device="cuda", dtype=TORCH_DT[dtype])
                 api.tp_linear_bwd(g, ds, dy, x, w, sv, dx, dw, db, ws)

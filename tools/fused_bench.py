@@ -20,7 +20,7 @@ sys.path.insert(0, ROOT)
 from paper_2110_14883_b200 import api  # noqa: E402
 from paper_2110_14883_b200.mlp import TPMLP  # noqa: E402
 
-GRIDS = {"2d": (4, 1), "2.5d": (8, 2), "3d": (8, 1)}
+GRIDS = {"1d": (4, 1), "2d": (4, 1), "2.5d": (8, 2), "3d": (8, 1)}
 
 
 def run(mode, M, h, steps, warmup, flags):
