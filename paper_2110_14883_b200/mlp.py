@@ -48,7 +48,8 @@ class TPMLP:
         if flags & api.TP_FLAG_PEER_FUSED:
             # every tensor a peer may read is a symmetric registered buffer (collective, same
             # order on all ranks): layer inputs X / Y_i, weights W_i, gradients dY / dX_i
-            for t in [self.x, *self.W, *self.Y, self.dY, *self.dX]:
+            # (and the workspace: the fused 1D reduce-scatter's receive slots live in it)
+            for t in [self.x, *self.W, *self.Y, self.dY, *self.dX, self.ws]:
                 api.tp_register_buffer(self.g, t)
         if fill:
             self.fill_inputs()
