@@ -46,7 +46,11 @@ constexpr int kBM = 128;  // A rows per CTA (pair tile: 256 rows)
 constexpr int kBK = 64;
 constexpr int kABytes = kBM * kBK * 2;
 constexpr int kOutBytes = 32 * 128;  // per epilogue warp and buffer: 32 rows x 128 B staging
-constexpr int kThreads = 192;
+// Epilogue warps: 4 (one per TMEM lane quadrant) or 8 (two per quadrant, each half of the
+// columns). 8 measured no faster on short-K tiles and costs a ring stage (r01_gemm_v3_summary).
+constexpr int kEpiWarps = 4;
+constexpr int kEpiThreads = kEpiWarps * 32;
+constexpr int kThreads = 64 + kEpiThreads;  // warp 0 TMA, warp 1 MMA, warps 2.. epilogue
 constexpr int kMaxProbs = 4;
 constexpr int kMaxPanels = 4;  // K-panels per problem (peer shards of a fused SUMMA)
 constexpr int kMaxDPanels = 8;  // D row-panels per problem (fused 1D reduce-scatter slots)
@@ -57,12 +61,13 @@ constexpr int kRxBytes = 2 * 32 * kBM * 4;  // MC 5: two [32 cols][128 rows] fp3
 template <int BNP, int MC = 1>
 struct PC {
   static constexpr int BNC = BNP / 2;
-  static constexpr int Stages = MC == 5 ? 5 : (BNP == 256 ? 6 : 8);
+  static constexpr int Stages = kEpiWarps == 8 ? (BNP == 256 ? (MC == 5 ? 4 : 5) : (MC == 5 ? 5 : 6))
+                                               : (BNP == 256 ? (MC == 5 ? 5 : 6) : (MC == 5 ? 6 : 8));
   static constexpr int BBytes = BNC * kBK * 2;
   static constexpr int StageBytes = kABytes + BBytes;
   static constexpr int TmemCols = 2 * BNP;
   static constexpr int Rx = MC == 5 ? kRxBytes : 0;
-  static constexpr int Smem = Stages * StageBytes + 8 * kOutBytes + Rx + 1024 + 256;
+  static constexpr int Smem = Stages * StageBytes + 2 * kEpiWarps * kOutBytes + Rx + 1024 + 256;
   static constexpr int TileElems = 256 * BNP;
 };
 
@@ -327,8 +332,8 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
   uint8_t* sA = smem;
   uint8_t* sB = sA + P::Stages * kABytes;
   uint8_t* sOut = sB + P::Stages * P::BBytes;
-  float* rx = reinterpret_cast<float*>(sOut + 8 * kOutBytes);  // MC 5: [2][32 cols][128 rows]
-  uint64_t* full = reinterpret_cast<uint64_t*>(sOut + 8 * kOutBytes + P::Rx);
+  float* rx = reinterpret_cast<float*>(sOut + 2 * kEpiWarps * kOutBytes);  // MC 5: [2][32][128]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sOut + 2 * kEpiWarps * kOutBytes + P::Rx);
   uint64_t* empty = full + P::Stages;
   uint64_t* tfull = empty + P::Stages;
   uint64_t* tempty = tfull + 2;
@@ -376,7 +381,7 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs (the pair leader's copy is used)
+      mbar_init(&tempty[a], 2 * kEpiWarps);  // epilogue warps x 2 CTAs (the leader's copy is used)
       mbar_init(&rxf[a], 1);  // MC 5 owner: its own expect_tx arrive + the sender's bulk bytes
       mbar_init(&rxe[a], 4);  // MC 5 sender: the owner's 4 epilogue warps
     }
@@ -577,8 +582,14 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
       }
     }
   } else {
-    // ===== epilogue warps 2..5 (both CTAs): TMEM lane quadrant = warp % 4 =====
+    // ===== epilogue warps 2..9 (both CTAs): TMEM lane quadrant = warp % 4; the two warps of a
+    // quadrant take the two halves of the tile's columns (`half`) =====
     const int quad = warp & 3;
+    const int half = (warp - 2) / 4;
+    constexpr int kHalves = kEpiWarps / 4;
+    constexpr int kSub64 = BNP / 64, kSub32 = BNP / 32;  // column sub-chunks per tile
+    const int s64_0 = half * (kSub64 / kHalves), s64_1 = s64_0 + kSub64 / kHalves;
+    const int s32_0 = half * (kSub32 / kHalves), s32_1 = s32_0 + kSub32 / kHalves;
     uint8_t* stg = sOut + (warp - 2) * 2 * kOutBytes;
     int nbox = 0;
     int acc = 0;
@@ -605,10 +616,13 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
                              static_cast<uint32_t>(acc * BNP);
       if (MC == 5) {
         // ---- K-split pair: pair 1 streams its accumulator into pair 0's smem (DSMEM), pair 0
-        // adds it in column chunks of 64 (two 32-column buffers) and stores the tile
+        // adds it in column chunks of 64 (two 32-column buffers) and stores the tile (the
+        // first four epilogue warps; the other four only release TMEM)
         const uint32_t peer = crank ^ 2u;  // same rank, other pair
         const int rrow = quad * 32 + lane;
-        if (pair == 1) {
+        if (half == 1) {
+          // nothing: the round protocol below runs on one warp per lane quadrant
+        } else if (pair == 1) {
           // sender: TMEM -> own staging (conflict-free [col][row]) -> one bulk copy per 32-col
           // chunk into the owner's buffer, completing as tx bytes on the owner's rxf
 #pragma unroll 1
@@ -625,7 +639,7 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
               rx[(32 + j) * kBM + rrow] = __uint_as_float(r1[j]);
             }
             fence_proxy_async_smem();
-            named_barrier_sync(1, 128);
+            named_barrier_sync(2, 128);  // the four working epilogue warps
             if (threadIdx.x == 64) {
               const uint32_t src = smem_u32(rx);
               bulk_s2s(mapa(src, peer), src, 32 * kBM * 4, mapa(smem_u32(&rxf[0]), peer));
@@ -672,14 +686,14 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
       } else if (pr.splits == 1) {
         if (pr.out_bf16) {
 #pragma unroll 1
-          for (int sub = 0; sub < BNP / 64; ++sub) {
+          for (int sub = s64_0; sub < s64_1; ++sub) {
             float v[64];
             tmem_cols<64>(t_row, sub, v);
             store_box<64>(pr, stg, nbox, lane, v, row, n0 + sub * 64, row0);
           }
         } else {
 #pragma unroll 1
-          for (int sub = 0; sub < BNP / 32; ++sub) {
+          for (int sub = s32_0; sub < s32_1; ++sub) {
             float v[32];
             tmem_cols<32>(t_row, sub, v);
             store_box<32>(pr, stg, nbox, lane, v, row, n0 + sub * 32, row0);
@@ -704,10 +718,10 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
           __threadfence();
           *cnt = 0;  // ready for the next launch
         }
-        named_barrier_sync(1, 128);
+        named_barrier_sync(1, kEpiThreads);
         if (pr.out_bf16) {
 #pragma unroll 1
-          for (int sub = 0; sub < BNP / 64; ++sub) {
+          for (int sub = s64_0; sub < s64_1; ++sub) {
             float v[64];
             tmem_cols<64>(t_row, sub, v);
             add_partials<64>(base, pr.splits, kSplitStride4, sub, v);
@@ -715,7 +729,7 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
           }
         } else {
 #pragma unroll 1
-          for (int sub = 0; sub < BNP / 32; ++sub) {
+          for (int sub = s32_0; sub < s32_1; ++sub) {
             float v[32];
             tmem_cols<32>(t_row, sub, v);
             add_partials<32>(base, pr.splits, kSplitStride4, sub, v);
@@ -737,7 +751,7 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
                                       rank * (kBM * BNP)) +
             quad * 32 + lane;
 #pragma unroll 1
-        for (int ch = 0; ch < BNP / 32; ++ch) {
+        for (int ch = s32_0; ch < s32_1; ++ch) {
           uint32_t r0[32];
           tmem_ld32(t_row + ch * 32, r0);
           tmem_wait_ld();
@@ -751,7 +765,7 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(&tempty[acc], lead);  // TMEM free for the next unit
         __threadfence();
-        named_barrier_sync(1, 128);
+        named_barrier_sync(1, kEpiThreads);
         if (pr.owner_wait) {
           if (threadIdx.x == 64) atomicAdd(pr.counters + tile * 2 + rank, 1);
         } else if (threadIdx.x == 64) {
@@ -761,9 +775,9 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
           if (last) *cnt = 0;  // ready for the next launch
           *sflag = last;
         }
-        named_barrier_sync(1, 128);
+        named_barrier_sync(1, kEpiThreads);
         const int last = pr.owner_wait ? 0 : *sflag;
-        named_barrier_sync(1, 128);
+        named_barrier_sync(1, kEpiThreads);
         if (last) {
           __threadfence();
           const float4* base =
@@ -773,14 +787,14 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
           constexpr int kSplitStride4 = P::TileElems / 4;
           if (pr.out_bf16) {
 #pragma unroll 1
-            for (int sub = 0; sub < BNP / 64; ++sub) {
+            for (int sub = s64_0; sub < s64_1; ++sub) {
               float v[64];
               sum_partials<64>(base, pr.splits, kSplitStride4, sub, v);
               store_box<64>(pr, stg, nbox, lane, v, row, n0 + sub * 64, row0);
             }
           } else {
 #pragma unroll 1
-            for (int sub = 0; sub < BNP / 32; ++sub) {
+            for (int sub = s32_0; sub < s32_1; ++sub) {
               float v[32];
               sum_partials<32>(base, pr.splits, kSplitStride4, sub, v);
               store_box<32>(pr, stg, nbox, lane, v, row, n0 + sub * 32, row0);
