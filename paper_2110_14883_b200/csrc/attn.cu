@@ -13,6 +13,9 @@
 // tensor cores, row softmax, PV GEMMs; backward by recomputation), and the scatter back.
 #include <cuda_bf16.h>
 
+#include <cmath>
+#include <cstdlib>
+
 #include "sched.h"
 #include "tp_internal.h"
 
@@ -142,7 +145,17 @@ tp_status attention_fwd(tp_grid* g, const tp_linear_desc* qd, int64_t seq, int64
   TP_TRY(attn_carve(P, c, &w));
   const int64_t ld = P.e.cols, d = P.d;
   for (int comp = 0; comp < 3; ++comp) TP_TRY(pack(P, qkv, w.buf[comp], ld, comp * d, 3 * d, 0, s));
-  TP_TRY(rsa_fwd(local_grid(), &P.rd, w.buf[0], w.buf[1], w.buf[2], w.buf[3], w.rsa, w.rsa_bytes, s));
+  static const int use_flash = [] {
+    const char* e = std::getenv("TP_FLASH");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (use_flash && flash_supported(d, qd->dtype) && P.problems <= 65535) {
+    // fused forward: the scores stay on chip (flash.cu)
+    const float sc = scale != 0.f ? scale : 1.f / std::sqrt(static_cast<float>(d));
+    TP_TRY(flash_attn_fwd(P.problems, P.seq, d, w.buf[0], w.buf[1], w.buf[2], w.buf[3], sc, s));
+  } else {
+    TP_TRY(rsa_fwd(local_grid(), &P.rd, w.buf[0], w.buf[1], w.buf[2], w.buf[3], w.rsa, w.rsa_bytes, s));
+  }
   return pack(P, w.buf[3], out, P.heads_local * d, 0, d, 1, s);
 }
 

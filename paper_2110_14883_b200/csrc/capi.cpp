@@ -837,3 +837,10 @@ extern "C" tp_status tp_add(const void* a, const void* b, void* out, size_t n, t
   if (dt != TP_BF16 && dt != TP_FP32) return tp::fail(TP_ERR_ARG, "tp_add: dtype");
   return tp::launch_add(a, b, out, n, dt, static_cast<cudaStream_t>(stream));
 }
+
+namespace tp { extern volatile unsigned* g_flash_dbg; }
+// tools only: progress markers of the fused attention kernel's first CTA (mapped host memory)
+extern "C" tp_status tp_flash_debug(unsigned* host_mapped) {
+  tp::g_flash_dbg = host_mapped;
+  return TP_OK;
+}

@@ -1,0 +1,347 @@
+// Fused attention forward for sm_100a: O = softmax(Q K^T scale) V per problem (batch x head),
+// the scores never leaving the SM (online softmax over key tiles; the two-pass form of rsa.cu
+// writes every score to HBM and reads it back). Used by the attention core (attn.cu) for the
+// local problems of every TP layout. bf16 in, fp32 accumulation and statistics, bf16 out.
+//
+// One CTA per (problem, 128-query tile); 192 threads:
+//   warp 0    TMA: Q once, then K / V tiles of 128 keys through a 2-stage ring;
+//   warp 1    tcgen05 MMA issuer (cta_group::1): S_j = Q K_j^T into one of two TMEM score
+//             buffers (128 columns each), O += P_j V_j into the TMEM output accumulator;
+//   warps 2-5 softmax (one query row per thread, TMEM lane quadrant = warp % 4): row max of
+//             S_j, p = exp2(s * scale log2 e - m), running sum, bf16 P_j to shared memory in
+//             the 128-byte-swizzled K-major layout the PV MMA reads, and the rescale of the O row
+//             by exp2(m_old - m_new) (tcgen05.ld / st) before P_j V_j is accumulated.
+// Keys past the sequence end are masked to -inf (their K / V rows are read but weigh 0).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+
+#include <cmath>
+#include <mutex>
+
+#include "sm100_ptx.cuh"
+#include "tp_internal.h"
+
+namespace tp {
+volatile unsigned* g_flash_dbg = nullptr;  // tools only (tp_flash_debug)
+namespace {
+
+using namespace ptx;
+
+constexpr int kFThreads = 192;
+constexpr int kQT = 128;   // query rows per CTA
+constexpr int kKT = 128;   // keys per tile
+constexpr int kKvStages = 2;
+
+template <int D>
+struct FC {
+  static constexpr int QBytes = kQT * D * 2;           // D/64 boxes of [128 rows][128 B]
+  static constexpr int KBytes = kKT * D * 2;
+  static constexpr int VBytes = kKT * D * 2;           // 2 key blocks x D/64 chunks of [64][128 B]
+  static constexpr int PBytes = kQT * kKT * 2;         // 2 key blocks of [128 rows][128 B]
+  static constexpr int StageBytes = KBytes + VBytes;
+  static constexpr int Smem = QBytes + kKvStages * StageBytes + PBytes + 1024 + 256;
+  static constexpr int TmemCols = 2 * kKT + (D < 32 ? 32 : D);  // S[2] + O
+};
+
+struct FParams {
+  CUtensorMap tmQ, tmK, tmV;
+  __nv_bfloat16* out;
+  int64_t s, problems;
+  float scale_log2;  // scale * log2(e)
+  volatile unsigned* dbg;  // tools only: progress markers (mapped host memory) or null
+};
+
+template <int D>
+__global__ void __launch_bounds__(kFThreads, 1) flash_fwd_kernel(const __grid_constant__ FParams F) {
+  using C = FC<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sKV = sQ + C::QBytes;
+  uint8_t* sP = sKV + kKvStages * C::StageBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + C::PBytes);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = bars + 1;
+  uint64_t* kv_empty = kv_full + kKvStages;
+  uint64_t* s_full = kv_empty + kKvStages;
+  uint64_t* s_empty = s_full + 2;
+  uint64_t* p_full = s_empty + 2;
+  uint64_t* o_done = p_full + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(o_done + 1);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int64_t prob = blockIdx.y;
+  const int64_t q0 = int64_t(blockIdx.x) * kQT;
+  const int64_t row_base = prob * F.s;          // first row of this problem in [problems*s, D]
+  const int ntiles = static_cast<int>((F.s + kKT - 1) / kKT);
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&F.tmQ);
+    tma_prefetch(&F.tmK);
+    tma_prefetch(&F.tmV);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < kKvStages; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], 4);
+    }
+    mbar_init(p_full, 4);
+    mbar_init(o_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_cg1(tslot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t tS[2] = {tmem, tmem + kKT};
+  const uint32_t tO = tmem + 2 * kKT;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      // ---- TMA producer
+      mbar_expect_tx(q_full, C::QBytes);
+      for (int c = 0; c < D / 64; ++c)
+        tma_load_2d(&F.tmQ, q_full, sQ + c * kQT * 128, c * 64, static_cast<int>(row_base + q0));
+      for (int j = 0; j < ntiles; ++j) {
+        const int st = j % kKvStages;
+        mbar_wait(&kv_empty[st], ((j / kKvStages) & 1) ^ 1);
+        if (F.dbg && blockIdx.x == 0 && blockIdx.y == 0) F.dbg[0] = 100 + j;
+        mbar_expect_tx(&kv_full[st], C::StageBytes);
+        uint8_t* kd = sKV + st * C::StageBytes;
+        uint8_t* vd = kd + C::KBytes;
+        const int key0 = static_cast<int>(row_base + int64_t(j) * kKT);
+        for (int c = 0; c < D / 64; ++c) tma_load_2d(&F.tmK, &kv_full[st], kd + c * kKT * 128, c * 64, key0);
+        // V: MN-major B operand, per 64-key block the D/64 chunks of [64 keys][64 d]
+        for (int kb = 0; kb < 2; ++kb)
+          for (int c = 0; c < D / 64; ++c)
+            tma_load_2d(&F.tmV, &kv_full[st], vd + (kb * (D / 64) + c) * 64 * 128, c * 64, key0 + kb * 64);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (elect_one()) {
+      // ---- MMA issuer
+      constexpr uint32_t idS = idesc_bf16_f32(128, kKT, false, false);
+      constexpr uint32_t idO = idesc_bf16_f32(128, D, false, true);
+      const uint64_t qd = sdesc_sw128(smem_u32(sQ), 16, 1024);
+      auto issue_s = [&](int j) {
+        const int st = j % kKvStages;
+        mbar_wait(&kv_full[st], (j / kKvStages) & 1);
+        if (F.dbg && blockIdx.x == 0 && blockIdx.y == 0) F.dbg[1] = 200 + j;
+        const int b = j & 1;
+        mbar_wait(&s_empty[b], ((j >> 1) & 1) ^ 1);  // softmax done with S_{j-2}
+        if (F.dbg && blockIdx.x == 0 && blockIdx.y == 0) F.dbg[2] = 300 + j;
+        tc_fence_after();
+        const uint64_t kdsc = sdesc_sw128(smem_u32(sKV + st * C::StageBytes), 16, 1024);
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          // K step of 16 inside a 64-wide box: +32 B; next box: +128 rows x 128 B
+          const uint32_t off = (k / 4) * (kQT * 128 / 16) + (k % 4) * 2;
+          const uint32_t offk = (k / 4) * (kKT * 128 / 16) + (k % 4) * 2;
+          umma_bf16_cg1(tS[b], qd + off, kdsc + offk, idS, k > 0 ? 1u : 0u);
+        }
+        umma_commit_cg1(&s_full[b]);
+      };
+      mbar_wait(q_full, 0);
+      issue_s(0);
+      for (int j = 0; j < ntiles; ++j) {
+        if (j + 1 < ntiles) issue_s(j + 1);
+        if (F.dbg && blockIdx.x == 0 && blockIdx.y == 0) F.dbg[3] = 400 + j;
+        mbar_wait(p_full, j & 1);  // P_j in smem, O rescaled
+        if (F.dbg && blockIdx.x == 0 && blockIdx.y == 0) F.dbg[4] = 500 + j;
+        tc_fence_after();
+        const int st = j % kKvStages;
+        const uint64_t pd = sdesc_sw128(smem_u32(sP), 16, 1024);
+        const uint64_t vdsc = sdesc_sw128(smem_u32(sKV + st * C::StageBytes + C::KBytes), 64 * 128, 1024);
+#pragma unroll
+        for (int k = 0; k < kKT / 16; ++k) {
+          const int kb = k / 4, kk = k % 4;
+          const uint32_t offp = kb * (kQT * 128 / 16) + kk * 2;                 // K-major P
+          const uint32_t offv = kb * ((D / 64) * 64 * 128 / 16) + kk * (2048 / 16);  // MN-major V
+          umma_bf16_cg1(tO, pd + offp, vdsc + offv, idO, (j > 0 || k > 0) ? 1u : 0u);
+        }
+        umma_commit_cg1(&kv_empty[st]);
+        umma_commit_cg1(o_done);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---- softmax warps: row = (warp % 4) * 32 + lane
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < ntiles; ++j) {
+      const int b = j & 1;
+      if (F.dbg && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0) F.dbg[5 + quad] = 600 + j;
+      mbar_wait(&s_full[b], (j >> 1) & 1);
+      if (F.dbg && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0) F.dbg[9 + quad] = 700 + j;
+      tc_fence_after();
+      const int64_t valid = F.s - int64_t(j) * kKT;  // keys of this tile inside the sequence
+      // pass 1: row max
+      float mx = -INFINITY;
+#pragma unroll 1
+      for (int c = 0; c < kKT / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tS[b] + lane_off + c * 32, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (c * 32 + i < valid) mx = fmaxf(mx, __uint_as_float(v[i]));
+      }
+      const float m_new = fmaxf(m, mx * F.scale_log2);
+      const float alpha = exp2f(m - m_new);  // 0 on the first tile (m = -inf)
+      // the previous PV MMA must be complete before P is overwritten and O rescaled
+      if (j > 0) mbar_wait(o_done, (j - 1) & 1);
+      if (F.dbg && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0) F.dbg[13 + quad] = 800 + j;
+      tc_fence_after();
+      // pass 2: p = exp2(s scale log2e - m_new) -> bf16 P row (swizzled K-major), row sum
+      float rs = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < kKT / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tS[b] + lane_off + c * 32, v);
+        tmem_wait_ld();
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float p0 = (c * 32 + 2 * i < valid) ? exp2f(__uint_as_float(v[2 * i]) * F.scale_log2 - m_new) : 0.f;
+          const float p1 = (c * 32 + 2 * i + 1 < valid) ? exp2f(__uint_as_float(v[2 * i + 1]) * F.scale_log2 - m_new) : 0.f;
+          rs += p0 + p1;
+          __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
+          pk[i] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        // 32 keys = 64 B = 4 swizzled 16-byte chunks of the row in key block c / 2
+        uint8_t* rowp = sP + (c / 2) * (kQT * 128) + r * 128;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int chunk = (c % 2) * 4 + q;
+          *reinterpret_cast<uint4*>(rowp + ((chunk ^ (r & 7)) << 4)) =
+              make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_empty[b]);  // S buffer b may be overwritten
+      l = l * alpha + rs;
+      // rescale the O row (warp-uniform: tcgen05.ld / st are .sync.aligned; alpha = 1 is exact)
+      if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll 1
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld32(tO + lane_off + c * 32, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
+          tmem_st32(tO + lane_off + c * 32, v);
+        }
+        tmem_wait_st();
+      }
+      m = m_new;
+      fence_proxy_async_smem();  // P visible to the MMA (async proxy)
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+      if (F.dbg && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0) F.dbg[17 + quad] = 900 + j;
+    }
+    // epilogue: O / l -> bf16 row
+    mbar_wait(o_done, (ntiles - 1) & 1);
+    tc_fence_after();
+    const int64_t q = q0 + r;
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll 1
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t v[32];
+      tmem_ld32(tO + lane_off + c * 32, v);
+      tmem_wait_ld();
+      if (q < F.s) {
+        __nv_bfloat16* dst = F.out + (row_base + q) * D + c * 32;
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          uint4 u;
+          __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            h[k] = __floats2bfloat162_rn(__uint_as_float(v[i + 2 * k]) * inv, __uint_as_float(v[i + 2 * k + 1]) * inv);
+          *reinterpret_cast<uint4*>(dst + i) = u;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_cg1(tmem, 512);
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+tp_status map(CUtensorMap* m, const void* base, uint64_t rows, int D, uint32_t box_rows) {
+  auto fn = encode();
+  if (!fn) return fail(TP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(D), rows};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(D) * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  if (fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return fail(TP_ERR_SHAPE, "flash: tensor map encode failed");
+  return TP_OK;
+}
+
+template <int D>
+tp_status launch(const FParams& F, cudaStream_t s) {
+  using C = FC<D>;
+  auto k = flash_fwd_kernel<D>;
+  static std::once_flag once;
+  std::call_once(once, [&] { cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::Smem); });
+  dim3 grid(static_cast<unsigned>((F.s + kQT - 1) / kQT), static_cast<unsigned>(F.problems));
+  k<<<grid, kFThreads, C::Smem, s>>>(F);
+  count_launch();
+  TP_CUDA(cudaGetLastError());
+  return TP_OK;
+}
+
+}  // namespace
+
+bool flash_supported(int64_t d, tp_dtype dt) { return dt == TP_BF16 && (d == 64 || d == 128); }
+
+// q, k, v, out: [problems, s, d] bf16 contiguous.
+tp_status flash_attn_fwd(int64_t problems, int64_t s, int64_t d, const void* q, const void* k,
+                         const void* v, void* out, float scale, cudaStream_t st) {
+  if (!problems || !s) return TP_OK;
+  if (d != 64 && d != 128) return fail(TP_ERR_UNSUPPORTED, "flash: d must be 64 or 128");
+  if (problems > 65535) return fail(TP_ERR_UNSUPPORTED, "flash: too many problems for one grid");
+  FParams F{};
+  const uint64_t rows = uint64_t(problems) * uint64_t(s);
+  TP_TRY(map(&F.tmQ, q, rows, static_cast<int>(d), kQT));
+  TP_TRY(map(&F.tmK, k, rows, static_cast<int>(d), kKT));
+  TP_TRY(map(&F.tmV, v, rows, static_cast<int>(d), 64));
+  F.out = static_cast<__nv_bfloat16*>(out);
+  F.s = s;
+  F.problems = problems;
+  F.scale_log2 = scale * 1.4426950408889634f;
+  F.dbg = g_flash_dbg;
+  return d == 64 ? launch<64>(F, st) : launch<128>(F, st);
+}
+
+}  // namespace tp

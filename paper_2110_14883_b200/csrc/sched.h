@@ -51,6 +51,11 @@ tp_status rsa_bwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k
                   const void* dout, void* dq, void* dk, void* dv, void* ws, size_t ws_bytes,
                   cudaStream_t s);
 
+// Fused attention forward (flash.cu): [problems, s, d] bf16, d in {64, 128}.
+bool flash_supported(int64_t d, tp_dtype dt);
+tp_status flash_attn_fwd(int64_t problems, int64_t s, int64_t d, const void* q, const void* k,
+                         const void* v, void* out, float scale, cudaStream_t st);
+
 // Multi-head attention core in the TP layouts (attn.cu).
 tp_status attention_ws_bytes(const tp_grid* g, const tp_linear_desc* qd, int64_t seq, int64_t heads,
                              size_t* bytes);
