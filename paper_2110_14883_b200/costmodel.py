@@ -50,9 +50,9 @@ def peaks():
         return 1590.0, "fallback"
 
 
-def model(workload, p, link_gbs=900.0):
+def model(workload, p, link_gbs=900.0, peak_tflops=None):
     M, layers, dtype = WORKLOADS[workload]
-    peak, _ = peaks()
+    peak = peak_tflops if peak_tflops is not None else peaks()[0]
     rows = []
     for label, mode, q, d in grids(p):
         tot = {k: 0.0 for k in ("paper_elems", "counted_elems", "link_bytes", "flops",

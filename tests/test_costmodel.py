@@ -63,9 +63,11 @@ def test_depth_sharded_weight_memory():
 
 def test_roofline_times_and_survey_table():
     """SURVEY 8(d) roofline rows for C2 (two square layers, M=512, h=4096, F = 1663.3 TF/s,
-    900 GB/s): per-GPU NVLink MB and the bound / max % of peak."""
+    900 GB/s): per-GPU NVLink MB and the bound / max % of peak. F is pinned to SURVEY's value,
+    not read from MEASURED_PEAKS.json (driver-written, changes between rounds)."""
     from paper_2110_14883_b200 import costmodel
-    rows = {(r["grid"], r["gpus"]): r for p in (4, 8) for r in costmodel.model("c2", p)}
+    rows = {(r["grid"], r["gpus"]): r for p in (4, 8)
+            for r in costmodel.model("c2", p, peak_tflops=1663.3)}
     assert rows[("1d", 4)]["link_mb_per_gpu"] == 12.6
     assert rows[("2d", 4)]["link_mb_per_gpu"] == 56.6 and rows[("2d", 4)]["bound"] == "link"
     assert rows[("2.5d(d=2)", 8)]["link_mb_per_gpu"] == 70.3
