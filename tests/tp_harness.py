@@ -98,6 +98,7 @@ def tp_layer(api, mode, p, d, M, K, N, X, W, dY, b=None, dtype="bf16", split_1d=
                 api.tp_linear_fwd(g, ds, x, w, bias, y, sv, ws)
                 bar.wait(120)
                 n_fwd = api.tp_launch_count() - n0
+                bar.wait(120)  # no rank enqueues its backward before every rank has read the count
                 dw = torch.empty_like(w)
                 db = torch.empty(ext["B"][3], device="cuda", dtype=TORCH_DT[dtype])
                 api.tp_linear_bwd(g, ds, dy, x, w, sv, dx, dw, db, ws)
