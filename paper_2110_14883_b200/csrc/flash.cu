@@ -50,6 +50,13 @@ struct FParams {
   int64_t s, problems;
   float scale_log2;  // scale * log2(e)
   volatile unsigned* dbg;  // tools only: progress markers (mapped host memory) or null
+  // Carried online softmax (ring attention: one call per K / V block of the ring). acc
+  // [problems*s, D] fp32 holds the unnormalised O of the blocks seen so far and ml
+  // [problems*s, 2] fp32 their row max (scaled log2 units) and row sum. carry_in: start
+  // from (acc, ml) instead of empty; last: write O / l to `out` (bf16), else (acc, ml).
+  float* acc;
+  float* ml;
+  int carry_in, last;
 };
 
 template <int D>
@@ -163,7 +170,7 @@ __global__ void __launch_bounds__(kFThreads, 1) flash_fwd_kernel(const __grid_co
           const int kb = k / 4, kk = k % 4;
           const uint32_t offp = kb * (kQT * 128 / 16) + kk * 2;                 // K-major P
           const uint32_t offv = kb * ((D / 64) * 64 * 128 / 16) + kk * (2048 / 16);  // MN-major V
-          umma_bf16_cg1(tO, pd + offp, vdsc + offv, idO, (j > 0 || k > 0) ? 1u : 0u);
+          umma_bf16_cg1(tO, pd + offp, vdsc + offv, idO, (j > 0 || k > 0 || F.carry_in) ? 1u : 0u);
         }
         umma_commit_cg1(&kv_empty[st]);
         umma_commit_cg1(o_done);
@@ -176,6 +183,12 @@ __global__ void __launch_bounds__(kFThreads, 1) flash_fwd_kernel(const __grid_co
     const int r = quad * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
     float m = -INFINITY, l = 0.f;
+    const int64_t qrow = q0 + r;  // this thread's query row within the problem
+    if (F.carry_in && qrow < F.s) {
+      const float2 c = *reinterpret_cast<const float2*>(F.ml + 2 * (row_base + qrow));
+      m = c.x;
+      l = c.y;
+    }
     for (int j = 0; j < ntiles; ++j) {
       const int b = j & 1;
       if (F.dbg && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0) F.dbg[5 + quad] = 600 + j;
@@ -229,6 +242,25 @@ __global__ void __launch_bounds__(kFThreads, 1) flash_fwd_kernel(const __grid_co
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_empty[b]);  // S buffer b may be overwritten
       l = l * alpha + rs;
+      if (j == 0 && F.carry_in) {
+        // carried O of the earlier ring blocks, rescaled to this block's running max, into
+        // TMEM before the first P V MMA accumulates onto it
+        const float4* src = reinterpret_cast<const float4*>(F.acc + (row_base + qrow) * D);
+#pragma unroll 1
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t v[32];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float4 x = qrow < F.s ? src[c * 8 + i] : make_float4(0.f, 0.f, 0.f, 0.f);
+            v[4 * i] = __float_as_uint(x.x * alpha);
+            v[4 * i + 1] = __float_as_uint(x.y * alpha);
+            v[4 * i + 2] = __float_as_uint(x.z * alpha);
+            v[4 * i + 3] = __float_as_uint(x.w * alpha);
+          }
+          tmem_st32(tO + lane_off + c * 32, v);
+        }
+        tmem_wait_st();
+      }
       // rescale the O row (warp-uniform: tcgen05.ld / st are .sync.aligned; alpha = 1 is exact)
       if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll 1
@@ -254,8 +286,24 @@ __global__ void __launch_bounds__(kFThreads, 1) flash_fwd_kernel(const __grid_co
     tc_fence_after();
     const int64_t q = q0 + r;
     const float inv = l > 0.f ? 1.f / l : 0.f;
+    if (!F.last) {  // carry out: unnormalised O (fp32) and (m, l) for the next ring block
 #pragma unroll 1
-    for (int c = 0; c < D / 32; ++c) {
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tO + lane_off + c * 32, v);
+        tmem_wait_ld();
+        if (q < F.s) {
+          float4* dst = reinterpret_cast<float4*>(F.acc + (row_base + q) * D + c * 32);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            dst[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                                 __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+        }
+      }
+      if (q < F.s) *reinterpret_cast<float2*>(F.ml + 2 * (row_base + q)) = make_float2(m, l);
+    }
+#pragma unroll 1
+    for (int c = 0; c < (F.last ? D / 32 : 0); ++c) {
       uint32_t v[32];
       tmem_ld32(tO + lane_off + c * 32, v);
       tmem_wait_ld();
@@ -341,6 +389,33 @@ tp_status flash_attn_fwd(int64_t problems, int64_t s, int64_t d, const void* q, 
   F.problems = problems;
   F.scale_log2 = scale * 1.4426950408889634f;
   F.dbg = g_flash_dbg;
+  F.last = 1;
+  return d == 64 ? launch<64>(F, st) : launch<128>(F, st);
+}
+
+// One block of a ring: q [problems, s, d]; k, v [problems, s, d] (this ring step's block);
+// acc [problems*s, d] fp32 and ml [problems*s, 2] fp32 carry the online softmax between calls.
+tp_status flash_attn_fwd_carry(int64_t problems, int64_t s, int64_t d, const void* q, const void* k,
+                               const void* v, void* out, float* acc, float* ml, bool carry_in,
+                               bool last, float scale, cudaStream_t st) {
+  if (!problems || !s) return TP_OK;
+  if (d != 64 && d != 128) return fail(TP_ERR_UNSUPPORTED, "flash: d must be 64 or 128");
+  if (problems > 65535) return fail(TP_ERR_UNSUPPORTED, "flash: too many problems for one grid");
+  if (!acc || !ml) return fail(TP_ERR_ARG, "flash: carry buffers are null");
+  FParams F{};
+  const uint64_t rows = uint64_t(problems) * uint64_t(s);
+  TP_TRY(map(&F.tmQ, q, rows, static_cast<int>(d), kQT));
+  TP_TRY(map(&F.tmK, k, rows, static_cast<int>(d), kKT));
+  TP_TRY(map(&F.tmV, v, rows, static_cast<int>(d), 64));
+  F.out = static_cast<__nv_bfloat16*>(out);
+  F.s = s;
+  F.problems = problems;
+  F.scale_log2 = scale * 1.4426950408889634f;
+  F.dbg = g_flash_dbg;
+  F.acc = acc;
+  F.ml = ml;
+  F.carry_in = carry_in ? 1 : 0;
+  F.last = last ? 1 : 0;
   return d == 64 ? launch<64>(F, st) : launch<128>(F, st);
 }
 

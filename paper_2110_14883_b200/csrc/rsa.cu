@@ -18,6 +18,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 
 #include "sched.h"
@@ -225,6 +226,8 @@ struct RsaWs {
   void* Pm = nullptr;       // [chunk, b, s] probabilities (dtype)
   void* kv[2] = {};         // ring buffers [chunk, b, d] (dtype)
   float* acc = nullptr;     // [chunk, b, d] fp32 output accumulator
+  void* vv[2] = {};         // fused path: V ring buffers [chunk, b, d] (dtype)
+  float* ml = nullptr;      // fused path: [chunk, b, 2] fp32 running row max / sum
   void* gemm_ws = nullptr;  // split-K scratch
   size_t gemm_ws_bytes = 0;
   float *parts_k = nullptr, *parts_v = nullptr;  // backward: [p][chunk][b][d] fp32
@@ -238,6 +241,9 @@ void rsa_carve(Carver& c, const RsaPlan& P, RsaWs* w) {
   w->kv[0] = c.take(ch * P.b * P.d * P.esz);
   w->kv[1] = c.take(ch * P.b * P.d * P.esz);
   w->acc = static_cast<float*>(c.take(ch * P.b * P.d * 4));
+  w->vv[0] = c.take(ch * P.b * P.d * P.esz);
+  w->vv[1] = c.take(ch * P.b * P.d * P.esz);
+  w->ml = static_cast<float*>(c.take(ch * P.b * 2 * 4));
   w->gemm_ws_bytes = gemm_tc2_ws_bytes();
   w->gemm_ws = c.take(w->gemm_ws_bytes);
   // backward: per-destination-block dK / dV contributions and their reduce-scattered sums
@@ -312,9 +318,35 @@ tp_status rsa_fwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k
   const float scale = d->scale != 0.f ? d->scale : 1.f / std::sqrt(static_cast<float>(P.d));
   const int64_t bd = P.b * P.d;
   std::vector<GemmArgs> gs;
+  static const int env_fused = [] {
+    const char* e = std::getenv("TP_RSA_FUSED");
+    return e ? std::atoi(e) : 1;
+  }();
+  const bool fused = env_fused && flash_supported(P.d, dt);
   for (int64_t h0 = 0; h0 < P.heads; h0 += P.chunk) {
     const int64_t nh = std::min<int64_t>(P.chunk, P.heads - h0);
     const char* qc = static_cast<const char*>(q) + h0 * bd * P.esz;
+    if (fused) {
+      // ---- online-softmax ring: K and V blocks travel the ring together;
+      // at every step one fused attention launch (flash.cu: scores in TMEM, never in HBM)
+      // continues each row's softmax from the carried (O, max, sum) of the blocks seen so far
+      const void* ck = static_cast<const char*>(k) + h0 * bd * P.esz;
+      const void* cv = static_cast<const char*>(v) + h0 * bd * P.esz;
+      char* oc = static_cast<char*>(out) + h0 * bd * P.esz;
+      int nb = 0;
+      for (int t = 0; t < P.p; ++t) {
+        const bool last = t + 1 == P.p;
+        TP_TRY(flash_attn_fwd_carry(nh, P.b, P.d, qc, ck, cv, oc, w.acc, w.ml, t > 0, last, scale, s));
+        if (!last) {
+          TP_TRY(ring->shift(ck, w.kv[nb], size_t(nh) * bd, dt, -1, s));
+          TP_TRY(ring->shift(cv, w.vv[nb], size_t(nh) * bd, dt, -1, s));
+          ck = w.kv[nb];
+          cv = w.vv[nb];
+          nb ^= 1;
+        }
+      }
+      continue;
+    }
     // ---- pass 1: K ring -> scores
     const void* cur = static_cast<const char*>(k) + h0 * bd * P.esz;
     int nb = 0;

@@ -55,6 +55,9 @@ tp_status rsa_bwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k
 bool flash_supported(int64_t d, tp_dtype dt);
 tp_status flash_attn_fwd(int64_t problems, int64_t s, int64_t d, const void* q, const void* k,
                          const void* v, void* out, float scale, cudaStream_t st);
+tp_status flash_attn_fwd_carry(int64_t problems, int64_t s, int64_t d, const void* q, const void* k,
+                               const void* v, void* out, float* acc, float* ml, bool carry_in,
+                               bool last, float scale, cudaStream_t st);
 
 // Multi-head attention core in the TP layouts (attn.cu).
 tp_status attention_ws_bytes(const tp_grid* g, const tp_linear_desc* qd, int64_t seq, int64_t heads,

@@ -141,3 +141,14 @@ def test_rsa_backward_vs_oracle(api, p, dtype):
     for i, got in enumerate((dq, dk, dv)):
         want = np.stack([ref[h][i] for h in range(heads)])
         assert rel_fro(got, want) <= tol, ("dq", "dk", "dv")[i]
+
+
+@pytest.mark.parametrize("p,s,d", [(3, 600, 64), (8, 768, 128), (5, 5 * 130, 64)])
+def test_rsa_online_softmax_ring_ragged(api, p, s, d):
+    """bf16, d in {64, 128}: the online-softmax ring (one fused attention launch per ring block,
+    carried row max / sum / unnormalised O). Blocks of b = 200, 96 and 130 rows are not
+    multiples of the kernel's 128-row tiles (masked keys, query rows past the block)."""
+    heads = 3
+    Q, K, V = inputs(31 + p, heads, s, d, "bf16")
+    got = run_rsa(api, p, heads, s, d, "bf16", Q, K, V)
+    assert rel_fro(got, oracle_out(Q, K, V)) <= 1e-2
