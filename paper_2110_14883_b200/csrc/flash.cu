@@ -59,6 +59,12 @@ struct FParams {
   int carry_in, last;
 };
 
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 template <int D>
 __global__ void __launch_bounds__(kFThreads, 1) flash_fwd_kernel(const __grid_constant__ FParams F) {
   using C = FC<D>;
@@ -196,36 +202,52 @@ __global__ void __launch_bounds__(kFThreads, 1) flash_fwd_kernel(const __grid_co
       if (F.dbg && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0) F.dbg[9 + quad] = 700 + j;
       tc_fence_after();
       const int64_t valid = F.s - int64_t(j) * kKT;  // keys of this tile inside the sequence
-      // pass 1: row max
-      float mx = -INFINITY;
-#pragma unroll 1
-      for (int c = 0; c < kKT / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld32(tS[b] + lane_off + c * 32, v);
-        tmem_wait_ld();
+      // the S row (128 fp32) into registers once: four loads in flight, one wait
+      uint32_t sv[kKT / 32][32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (c * 32 + i < valid) mx = fmaxf(mx, __uint_as_float(v[i]));
+      for (int c = 0; c < kKT / 32; ++c) tmem_ld32(tS[b] + lane_off + c * 32, sv[c]);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_empty[b]);  // S buffer b may be overwritten
+      if (valid < kKT) {  // last tile of a ragged sequence: masked keys weigh exp2(-inf) = 0
+#pragma unroll
+        for (int c = 0; c < kKT / 32; ++c)
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (c * 32 + i >= valid) sv[c][i] = 0xff800000u;  // -inf
       }
+      auto sval = [&](int c, int i) { return __uint_as_float(sv[c][i]); };
+      // row max: 8 independent chains, then a tree (a single 128-long fmax chain is latency)
+      float mxs[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mxs[i] = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < kKT / 32; ++c)
+#pragma unroll
+        for (int i = 0; i < 32; ++i) mxs[i & 7] = fmaxf(mxs[i & 7], sval(c, i));
+      const float mx = fmaxf(fmaxf(fmaxf(mxs[0], mxs[1]), fmaxf(mxs[2], mxs[3])),
+                             fmaxf(fmaxf(mxs[4], mxs[5]), fmaxf(mxs[6], mxs[7])));
       const float m_new = fmaxf(m, mx * F.scale_log2);
       const float alpha = exp2f(m - m_new);  // 0 on the first tile (m = -inf)
       // the previous PV MMA must be complete before P is overwritten and O rescaled
       if (j > 0) mbar_wait(o_done, (j - 1) & 1);
       if (F.dbg && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0) F.dbg[13 + quad] = 800 + j;
       tc_fence_after();
-      // pass 2: p = exp2(s scale log2e - m_new) -> bf16 P row (swizzled K-major), row sum
-      float rs = 0.f;
-#pragma unroll 1
+      // p = exp2(s scale log2e - m_new) (one FFMA + MUFU.EX2 each) -> bf16 P row (swizzled
+      // K-major), row sum in 8 independent partial sums
+      float rsp[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) rsp[i] = 0.f;
+      const float neg_m = -m_new;
+#pragma unroll
       for (int c = 0; c < kKT / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld32(tS[b] + lane_off + c * 32, v);
-        tmem_wait_ld();
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const float p0 = (c * 32 + 2 * i < valid) ? exp2f(__uint_as_float(v[2 * i]) * F.scale_log2 - m_new) : 0.f;
-          const float p1 = (c * 32 + 2 * i + 1 < valid) ? exp2f(__uint_as_float(v[2 * i + 1]) * F.scale_log2 - m_new) : 0.f;
-          rs += p0 + p1;
+          const float p0 = ex2_approx(fmaf(sval(c, 2 * i), F.scale_log2, neg_m));
+          const float p1 = ex2_approx(fmaf(sval(c, 2 * i + 1), F.scale_log2, neg_m));
+          rsp[i & 7] += p0 + p1;
           __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
           pk[i] = *reinterpret_cast<uint32_t*>(&h);
         }
@@ -238,9 +260,8 @@ __global__ void __launch_bounds__(kFThreads, 1) flash_fwd_kernel(const __grid_co
               make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_empty[b]);  // S buffer b may be overwritten
+  // S buffer b may be overwritten
+      const float rs = ((rsp[0] + rsp[1]) + (rsp[2] + rsp[3])) + ((rsp[4] + rsp[5]) + (rsp[6] + rsp[7]));
       l = l * alpha + rs;
       if (j == 0 && F.carry_in) {
         // carried O of the earlier ring blocks, rescaled to this block's running max, into
@@ -263,14 +284,18 @@ __global__ void __launch_bounds__(kFThreads, 1) flash_fwd_kernel(const __grid_co
       }
       // rescale the O row (warp-uniform: tcgen05.ld / st are .sync.aligned; alpha = 1 is exact)
       if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
-#pragma unroll 1
-        for (int c = 0; c < D / 32; ++c) {
-          uint32_t v[32];
-          tmem_ld32(tO + lane_off + c * 32, v);
+#pragma unroll
+        for (int c0 = 0; c0 < D / 32; c0 += 2) {  // two 32-column loads in flight
+          uint32_t v[2][32];
+          tmem_ld32(tO + lane_off + c0 * 32, v[0]);
+          tmem_ld32(tO + lane_off + (c0 + 1) * 32, v[1]);
           tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
-          tmem_st32(tO + lane_off + c * 32, v);
+          for (int h = 0; h < 2; ++h) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[h][i] = __float_as_uint(__uint_as_float(v[h][i]) * alpha);
+            tmem_st32(tO + lane_off + (c0 + h) * 32, v[h]);
+          }
         }
         tmem_wait_st();
       }

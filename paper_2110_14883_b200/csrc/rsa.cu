@@ -197,6 +197,7 @@ __global__ void rsa_cast(const float* __restrict__ src, int64_t n, T* __restrict
 struct RsaPlan {
   int p = 1, r = 0;
   int64_t s = 0, b = 0, d = 0, heads = 0, chunk = 1;
+  int64_t fchunk = 0;  // heads per online-softmax ring launch (0: two-pass only)
   size_t esz = 2;
 };
 
@@ -218,6 +219,8 @@ tp_status rsa_plan(const tp_grid* g, const tp_rsa_desc* d, RsaPlan* P) {
   const size_t per_head = size_t(P->b) * size_t(P->s) * 4;
   P->chunk = per_head ? std::max<int64_t>(1, std::min<int64_t>(d->heads, kScoreBudget / per_head)) : 1;
   if (P->chunk < 1) P->chunk = 1;
+  // the online-softmax ring keeps no score rows: all heads in one launch per ring step
+  P->fchunk = flash_supported(P->d, d->dtype) ? std::max<int64_t>(1, std::min<int64_t>(d->heads, 65535)) : 0;
   return TP_OK;
 }
 
@@ -226,8 +229,10 @@ struct RsaWs {
   void* Pm = nullptr;       // [chunk, b, s] probabilities (dtype)
   void* kv[2] = {};         // ring buffers [chunk, b, d] (dtype)
   float* acc = nullptr;     // [chunk, b, d] fp32 output accumulator
-  void* vv[2] = {};         // fused path: V ring buffers [chunk, b, d] (dtype)
-  float* ml = nullptr;      // fused path: [chunk, b, 2] fp32 running row max / sum
+  float* facc = nullptr;    // online-softmax ring: [fchunk, b, d] fp32 unnormalised O
+  void* fk[2] = {};         //   K ring buffers [fchunk, b, d] (dtype)
+  void* vv[2] = {};         //   V ring buffers [fchunk, b, d] (dtype)
+  float* ml = nullptr;      //   [fchunk, b, 2] fp32 running row max / sum
   void* gemm_ws = nullptr;  // split-K scratch
   size_t gemm_ws_bytes = 0;
   float *parts_k = nullptr, *parts_v = nullptr;  // backward: [p][chunk][b][d] fp32
@@ -241,9 +246,13 @@ void rsa_carve(Carver& c, const RsaPlan& P, RsaWs* w) {
   w->kv[0] = c.take(ch * P.b * P.d * P.esz);
   w->kv[1] = c.take(ch * P.b * P.d * P.esz);
   w->acc = static_cast<float*>(c.take(ch * P.b * P.d * 4));
-  w->vv[0] = c.take(ch * P.b * P.d * P.esz);
-  w->vv[1] = c.take(ch * P.b * P.d * P.esz);
-  w->ml = static_cast<float*>(c.take(ch * P.b * 2 * 4));
+  const size_t fc = size_t(P.fchunk);
+  w->facc = static_cast<float*>(c.take(fc * P.b * P.d * 4));
+  w->fk[0] = c.take(fc * P.b * P.d * P.esz);
+  w->fk[1] = c.take(fc * P.b * P.d * P.esz);
+  w->vv[0] = c.take(fc * P.b * P.d * P.esz);
+  w->vv[1] = c.take(fc * P.b * P.d * P.esz);
+  w->ml = static_cast<float*>(c.take(fc * P.b * 2 * 4));
   w->gemm_ws_bytes = gemm_tc2_ws_bytes();
   w->gemm_ws = c.take(w->gemm_ws_bytes);
   // backward: per-destination-block dK / dV contributions and their reduce-scattered sums
@@ -322,9 +331,10 @@ tp_status rsa_fwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k
     const char* e = std::getenv("TP_RSA_FUSED");
     return e ? std::atoi(e) : 1;
   }();
-  const bool fused = env_fused && flash_supported(P.d, dt);
-  for (int64_t h0 = 0; h0 < P.heads; h0 += P.chunk) {
-    const int64_t nh = std::min<int64_t>(P.chunk, P.heads - h0);
+  const bool fused = env_fused && P.fchunk > 0;
+  const int64_t step_heads = fused ? P.fchunk : P.chunk;
+  for (int64_t h0 = 0; h0 < P.heads; h0 += step_heads) {
+    const int64_t nh = std::min<int64_t>(step_heads, P.heads - h0);
     const char* qc = static_cast<const char*>(q) + h0 * bd * P.esz;
     if (fused) {
       // ---- online-softmax ring: K and V blocks travel the ring together;
@@ -336,11 +346,11 @@ tp_status rsa_fwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k
       int nb = 0;
       for (int t = 0; t < P.p; ++t) {
         const bool last = t + 1 == P.p;
-        TP_TRY(flash_attn_fwd_carry(nh, P.b, P.d, qc, ck, cv, oc, w.acc, w.ml, t > 0, last, scale, s));
+        TP_TRY(flash_attn_fwd_carry(nh, P.b, P.d, qc, ck, cv, oc, w.facc, w.ml, t > 0, last, scale, s));
         if (!last) {
-          TP_TRY(ring->shift(ck, w.kv[nb], size_t(nh) * bd, dt, -1, s));
+          TP_TRY(ring->shift(ck, w.fk[nb], size_t(nh) * bd, dt, -1, s));
           TP_TRY(ring->shift(cv, w.vv[nb], size_t(nh) * bd, dt, -1, s));
-          ck = w.kv[nb];
+          ck = w.fk[nb];
           cv = w.vv[nb];
           nb ^= 1;
         }
