@@ -40,7 +40,7 @@ struct FC {
   static constexpr int VBytes = kKT * D * 2;           // 2 key blocks x D/64 chunks of [64][128 B]
   static constexpr int PBytes = kQT * kKT * 2;         // 2 key blocks of [128 rows][128 B]
   static constexpr int StageBytes = KBytes + VBytes;
-  static constexpr int Smem = QBytes + kKvStages * StageBytes + PBytes + 1024 + 256;
+  static constexpr int Smem = QBytes + kKvStages * StageBytes + 2 * PBytes + 1024 + 256;
   static constexpr int TmemCols = 2 * kKT + (D < 32 ? 32 : D);  // S[2] + O
 };
 
@@ -73,15 +73,19 @@ __global__ void __launch_bounds__(kFThreads, 1) flash_fwd_kernel(const __grid_co
   uint8_t* sQ = smem;
   uint8_t* sKV = sQ + C::QBytes;
   uint8_t* sP = sKV + kKvStages * C::StageBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + C::PBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * C::PBytes);  // P double-buffered
   uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;
-  uint64_t* kv_empty = kv_full + kKvStages;
-  uint64_t* s_full = kv_empty + kKvStages;
+  // K and V have their own barriers: K_j's slot frees when S_j retires (early), V_j's when
+  // P_j V_j retires, so K_{j+2}'s load is in flight long before S_{j+2} is issued
+  uint64_t* k_full = bars + 1;
+  uint64_t* k_empty = k_full + kKvStages;
+  uint64_t* v_full = k_empty + kKvStages;
+  uint64_t* v_empty = v_full + kKvStages;
+  uint64_t* s_full = v_empty + kKvStages;
   uint64_t* s_empty = s_full + 2;
-  uint64_t* p_full = s_empty + 2;
-  uint64_t* o_done = p_full + 1;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(o_done + 1);
+  uint64_t* p_full = s_empty + 2;   // [2] P_j in buffer j % 2 written (and O rescaled)
+  uint64_t* p_empty = p_full + 2;   // [2] P_j V_j retired: P buffer j % 2 free, O up to date
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(p_empty + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int64_t prob = blockIdx.y;
@@ -95,15 +99,19 @@ __global__ void __launch_bounds__(kFThreads, 1) flash_fwd_kernel(const __grid_co
     tma_prefetch(&F.tmV);
     mbar_init(q_full, 1);
     for (int i = 0; i < kKvStages; ++i) {
-      mbar_init(&kv_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&s_empty[i], 4);
     }
-    mbar_init(p_full, 4);
-    mbar_init(o_done, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&p_full[i], 4);
+      mbar_init(&p_empty[i], 1);
+    }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc_cg1(tslot, 512);
@@ -120,19 +128,31 @@ __global__ void __launch_bounds__(kFThreads, 1) flash_fwd_kernel(const __grid_co
       mbar_expect_tx(q_full, C::QBytes);
       for (int c = 0; c < D / 64; ++c)
         tma_load_2d(&F.tmQ, q_full, sQ + c * kQT * 128, c * 64, static_cast<int>(row_base + q0));
-      for (int j = 0; j < ntiles; ++j) {
+      auto load_k = [&](int j) {
         const int st = j % kKvStages;
-        mbar_wait(&kv_empty[st], ((j / kKvStages) & 1) ^ 1);
-        if (F.dbg && blockIdx.x == 0 && blockIdx.y == 0) F.dbg[0] = 100 + j;
-        mbar_expect_tx(&kv_full[st], C::StageBytes);
+        mbar_wait(&k_empty[st], ((j / kKvStages) & 1) ^ 1);
+        mbar_expect_tx(&k_full[st], C::KBytes);
         uint8_t* kd = sKV + st * C::StageBytes;
-        uint8_t* vd = kd + C::KBytes;
         const int key0 = static_cast<int>(row_base + int64_t(j) * kKT);
-        for (int c = 0; c < D / 64; ++c) tma_load_2d(&F.tmK, &kv_full[st], kd + c * kKT * 128, c * 64, key0);
+        for (int c = 0; c < D / 64; ++c) tma_load_2d(&F.tmK, &k_full[st], kd + c * kKT * 128, c * 64, key0);
+      };
+      auto load_v = [&](int j) {
+        const int st = j % kKvStages;
+        mbar_wait(&v_empty[st], ((j / kKvStages) & 1) ^ 1);
+        mbar_expect_tx(&v_full[st], C::VBytes);
+        uint8_t* vd = sKV + st * C::StageBytes + C::KBytes;
+        const int key0 = static_cast<int>(row_base + int64_t(j) * kKT);
         // V: MN-major B operand, per 64-key block the D/64 chunks of [64 keys][64 d]
         for (int kb = 0; kb < 2; ++kb)
           for (int c = 0; c < D / 64; ++c)
-            tma_load_2d(&F.tmV, &kv_full[st], vd + (kb * (D / 64) + c) * 64 * 128, c * 64, key0 + kb * 64);
+            tma_load_2d(&F.tmV, &v_full[st], vd + (kb * (D / 64) + c) * 64 * 128, c * 64, key0 + kb * 64);
+      };
+      // K runs one tile ahead of V (S_{j+1} is issued before P_j V_j)
+      load_k(0);
+      for (int j = 0; j < ntiles; ++j) {
+        if (F.dbg && blockIdx.x == 0 && blockIdx.y == 0) F.dbg[0] = 100 + j;
+        if (j + 1 < ntiles) load_k(j + 1);
+        load_v(j);
       }
     }
     __syncwarp();
@@ -144,7 +164,7 @@ __global__ void __launch_bounds__(kFThreads, 1) flash_fwd_kernel(const __grid_co
       const uint64_t qd = sdesc_sw128(smem_u32(sQ), 16, 1024);
       auto issue_s = [&](int j) {
         const int st = j % kKvStages;
-        mbar_wait(&kv_full[st], (j / kKvStages) & 1);
+        mbar_wait(&k_full[st], (j / kKvStages) & 1);
         if (F.dbg && blockIdx.x == 0 && blockIdx.y == 0) F.dbg[1] = 200 + j;
         const int b = j & 1;
         mbar_wait(&s_empty[b], ((j >> 1) & 1) ^ 1);  // softmax done with S_{j-2}
@@ -159,17 +179,21 @@ __global__ void __launch_bounds__(kFThreads, 1) flash_fwd_kernel(const __grid_co
           umma_bf16_cg1(tS[b], qd + off, kdsc + offk, idS, k > 0 ? 1u : 0u);
         }
         umma_commit_cg1(&s_full[b]);
+        umma_commit_cg1(&k_empty[st]);  // K_j read
       };
       mbar_wait(q_full, 0);
       issue_s(0);
       for (int j = 0; j < ntiles; ++j) {
         if (j + 1 < ntiles) issue_s(j + 1);
         if (F.dbg && blockIdx.x == 0 && blockIdx.y == 0) F.dbg[3] = 400 + j;
-        mbar_wait(p_full, j & 1);  // P_j in smem, O rescaled
+        const int pb = j & 1;
+        mbar_wait(&p_full[pb], (j >> 1) & 1);  // P_j in smem, O rescaled
         if (F.dbg && blockIdx.x == 0 && blockIdx.y == 0) F.dbg[4] = 500 + j;
         tc_fence_after();
         const int st = j % kKvStages;
-        const uint64_t pd = sdesc_sw128(smem_u32(sP), 16, 1024);
+        mbar_wait(&v_full[st], (j / kKvStages) & 1);
+        tc_fence_after();
+        const uint64_t pd = sdesc_sw128(smem_u32(sP + pb * C::PBytes), 16, 1024);
         const uint64_t vdsc = sdesc_sw128(smem_u32(sKV + st * C::StageBytes + C::KBytes), 64 * 128, 1024);
 #pragma unroll
         for (int k = 0; k < kKT / 16; ++k) {
@@ -178,8 +202,8 @@ __global__ void __launch_bounds__(kFThreads, 1) flash_fwd_kernel(const __grid_co
           const uint32_t offv = kb * ((D / 64) * 64 * 128 / 16) + kk * (2048 / 16);  // MN-major V
           umma_bf16_cg1(tO, pd + offp, vdsc + offv, idO, (j > 0 || k > 0 || F.carry_in) ? 1u : 0u);
         }
-        umma_commit_cg1(&kv_empty[st]);
-        umma_commit_cg1(o_done);
+        umma_commit_cg1(&v_empty[st]);
+        umma_commit_cg1(&p_empty[pb]);
       }
     }
     __syncwarp();
@@ -228,10 +252,16 @@ __global__ void __launch_bounds__(kFThreads, 1) flash_fwd_kernel(const __grid_co
         for (int i = 0; i < 32; ++i) mxs[i & 7] = fmaxf(mxs[i & 7], sval(c, i));
       const float mx = fmaxf(fmaxf(fmaxf(mxs[0], mxs[1]), fmaxf(mxs[2], mxs[3])),
                              fmaxf(fmaxf(mxs[4], mxs[5]), fmaxf(mxs[6], mxs[7])));
-      const float m_new = fmaxf(m, mx * F.scale_log2);
-      const float alpha = exp2f(m - m_new);  // 0 on the first tile (m = -inf)
-      // the previous PV MMA must be complete before P is overwritten and O rescaled
-      if (j > 0) mbar_wait(o_done, (j - 1) & 1);
+      // Lazy rescale: the reference max m moves only when some row of the warp would exceed it
+      // by more than 2^8 (p <= 256 is exact enough in bf16 / fp32), so most tiles leave O alone
+      // and the softmax runs a tile ahead of the P V MMA. O, l and the carried (m, l) all use
+      // the same reference, so O / l is unchanged.
+      const float m_cand = fmaxf(m, mx * F.scale_log2);
+      const bool move = (j == 0 && !F.carry_in) || __any_sync(0xffffffffu, m_cand > m + 8.f);
+      const float m_new = move ? m_cand : m;
+      const float alpha = exp2f(m - m_new);  // 1 when m stays; 0 on the first tile (m = -inf)
+      // P buffer j % 2 was last read by P_{j-2} V_{j-2}
+      if (j >= 2) mbar_wait(&p_empty[j & 1], ((j - 2) >> 1) & 1);
       if (F.dbg && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0) F.dbg[13 + quad] = 800 + j;
       tc_fence_after();
       // p = exp2(s scale log2e - m_new) (one FFMA + MUFU.EX2 each) -> bf16 P row (swizzled
@@ -252,7 +282,7 @@ __global__ void __launch_bounds__(kFThreads, 1) flash_fwd_kernel(const __grid_co
           pk[i] = *reinterpret_cast<uint32_t*>(&h);
         }
         // 32 keys = 64 B = 4 swizzled 16-byte chunks of the row in key block c / 2
-        uint8_t* rowp = sP + (c / 2) * (kQT * 128) + r * 128;
+        uint8_t* rowp = sP + (j & 1) * C::PBytes + (c / 2) * (kQT * 128) + r * 128;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int chunk = (c % 2) * 4 + q;
@@ -283,7 +313,9 @@ __global__ void __launch_bounds__(kFThreads, 1) flash_fwd_kernel(const __grid_co
         tmem_wait_st();
       }
       // rescale the O row (warp-uniform: tcgen05.ld / st are .sync.aligned; alpha = 1 is exact)
-      if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+      if (j > 0 && move) {
+        mbar_wait(&p_empty[(j - 1) & 1], ((j - 1) >> 1) & 1);  // P_{j-1} V_{j-1} retired
+        tc_fence_after();
 #pragma unroll
         for (int c0 = 0; c0 < D / 32; c0 += 2) {  // two 32-column loads in flight
           uint32_t v[2][32];
@@ -303,11 +335,11 @@ __global__ void __launch_bounds__(kFThreads, 1) flash_fwd_kernel(const __grid_co
       fence_proxy_async_smem();  // P visible to the MMA (async proxy)
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
+      if (lane == 0) mbar_arrive(&p_full[j & 1]);
       if (F.dbg && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0) F.dbg[17 + quad] = 900 + j;
     }
     // epilogue: O / l -> bf16 row
-    mbar_wait(o_done, (ntiles - 1) & 1);
+    mbar_wait(&p_empty[(ntiles - 1) & 1], ((ntiles - 1) >> 1) & 1);
     tc_fence_after();
     const int64_t q = q0 + r;
     const float inv = l > 0.f ? 1.f / l : 0.f;
