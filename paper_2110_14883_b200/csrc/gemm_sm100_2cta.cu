@@ -807,7 +807,9 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
         acc_phase ^= 1;
       }
     }
-    if (lane == 0) bulk_wait0();
+    // staging buffers must outlive the bulk stores' smem reads; the global writes complete with
+    // the grid (as CUTLASS's store tail: wait_group.read, not a full-completion wait)
+    if (lane == 0) bulk_wait_read0();
     if (G.trace && warp == 2 && lane == 0) {
       G.trace[blockIdx.x * 16 + 5] = t_tf;
       G.trace[blockIdx.x * 16 + 6] = clock64() - t_begin;
