@@ -343,16 +343,33 @@ tp_status rsa_fwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k
       const void* ck = static_cast<const char*>(k) + h0 * bd * P.esz;
       const void* cv = static_cast<const char*>(v) + h0 * bd * P.esz;
       char* oc = static_cast<char*>(out) + h0 * bd * P.esz;
-      int nb = 0;
+      // block t+1 travels on the grid's comm stream while block t is attended on `s`
+      // (double-buffered: the shift into buffer t % 2 waits for the launch that last read it)
+      cudaStream_t cs = g->comm_stream ? g->comm_stream : s;
+      cudaEvent_t ev_flash = nullptr, ev_shift = nullptr;
+      if (P.p > 1 && cs != s) {
+        cudaEvent_t e = g->ev();
+        TP_CUDA(cudaEventRecord(e, s));  // inputs (and earlier users of the buffers) are done
+        TP_CUDA(cudaStreamWaitEvent(cs, e, 0));
+      }
       for (int t = 0; t < P.p; ++t) {
         const bool last = t + 1 == P.p;
+        if (!last) {
+          if (ev_flash && cs != s) TP_CUDA(cudaStreamWaitEvent(cs, ev_flash, 0));
+          TP_TRY(ring->shift(ck, w.fk[t & 1], size_t(nh) * bd, dt, -1, cs));
+          TP_TRY(ring->shift(cv, w.vv[t & 1], size_t(nh) * bd, dt, -1, cs));
+        }
         TP_TRY(flash_attn_fwd_carry(nh, P.b, P.d, qc, ck, cv, oc, w.facc, w.ml, t > 0, last, scale, s));
         if (!last) {
-          TP_TRY(ring->shift(ck, w.fk[nb], size_t(nh) * bd, dt, -1, s));
-          TP_TRY(ring->shift(cv, w.vv[nb], size_t(nh) * bd, dt, -1, s));
-          ck = w.fk[nb];
-          cv = w.vv[nb];
-          nb ^= 1;
+          if (cs != s) {
+            ev_flash = g->ev();
+            TP_CUDA(cudaEventRecord(ev_flash, s));
+            ev_shift = g->ev();
+            TP_CUDA(cudaEventRecord(ev_shift, cs));
+            TP_CUDA(cudaStreamWaitEvent(s, ev_shift, 0));  // block t+1 has arrived
+          }
+          ck = w.fk[t & 1];
+          cv = w.vv[t & 1];
         }
       }
       continue;
