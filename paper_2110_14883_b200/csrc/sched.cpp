@@ -584,9 +584,108 @@ tp_status fused_abt_atb(Ctx& C, const Plane& P, const void* dy, const void* x, c
   return fused_barrier(C);
 }
 
+// ---- fused depth-sharded 2.5D (TP_FLAG_W25_DEPTH_SHARDED + TP_FLAG_PEER_FUSED; the north
+// star's 1/p weight layout). W[t,j] is split by rows over the d planes: rank (e,t,j) holds rows
+// e hq .. e hq + hq - 1 of it (hq = K/(q d)), so each K-panel of the 2D product splits into d
+// sub-panels read from d planes:
+//   Y[dep,i,j]            = sum_t sum_e X[dep,i,t][:, e hq : +hq] . W_e[t,j]      (q d panels)
+//   dX[dep,i,j][:, e hq:] = sum_n dY[dep,i,n] . W_e[j,n]^T                        (d GEMMs, q panels)
+//   dW_dep[i,j]           = sum_e sum_m X[e,m,i][:, dep hq : +hq]^T . dY[e,m,j]  (q d panels)
+// The depth all-gather of W (forward) and reduce-scatter of dW (backward) disappear: the peer
+// panels cover them. Needs q d <= 4 (the kernel's K-panels), hq % 8 == 0 (16-byte sub-panel
+// offsets) and > 128 output rows per product (CTA-pair kernel).
+bool fused25_ok(Ctx& C, const Plane& P, std::initializer_list<const void*> shards,
+                std::initializer_list<int64_t> rows) {
+  if (!(C.d->flags & TP_FLAG_PEER_FUSED) || C.dt != TP_BF16 || !C.g->all) return false;
+  if (C.g->mode != TP_2P5D || !(C.d->flags & TP_FLAG_W25_DEPTH_SHARDED) || P.d < 2) return false;
+  if (P.q * P.d > 4) return false;
+  const int64_t hq = P.kq / P.d;
+  if (hq % 8 || P.kq % 8 || P.nq % 8) return false;
+  for (int64_t r : rows)
+    if (r <= 128) return false;
+  for (const void* sh : shards)
+    if (!sh || !C.g->peer_ptr(C.g->rank, sh)) return false;
+  return true;
+}
+
+int rank25(const Plane& P, int e, int i, int j) { return e * P.q * P.q + i * P.q + j; }
+
+GemmArgs panel_base(Ctx& C, int64_t M, int64_t N, int64_t K, bool ta, bool tb, void* D,
+                    const void* bias, int64_t lda, int64_t ldb, int64_t ldd) {
+  GemmArgs a = C.args(M, N, K, nullptr, ta, nullptr, tb, D, C.dt, C.d->alpha, nullptr, bias);
+  a.reserve_sms = 0;
+  a.ws = nullptr;
+  a.ws_bytes = 0;
+  a.lda = lda;
+  a.ldb = ldb;
+  a.ldd = ldd;
+  return a;
+}
+
+tp_status fused25_fwd(Ctx& C, const Plane& P, const void* x, const void* w, const void* bias, void* y) {
+  if (C.R.plan) return TP_OK;
+  const tp_grid* g = C.g;
+  const int dep = g->coords[0];
+  const int64_t hq = P.kq / P.d;
+  GemmArgs a = panel_base(C, P.mb, P.nq, hq, false, false, y, bias, P.kq, P.nq, P.nq);
+  a.npanels = P.q * P.d;
+  int k = 0;
+  for (int t = 0; t < P.q; ++t)
+    for (int e = 0; e < P.d; ++e, ++k) {
+      a.Ap[k] = static_cast<const char*>(g->peer_ptr(rank25(P, dep, P.i, t), x)) + e * hq * C.esz;
+      a.Bp[k] = g->peer_ptr(rank25(P, e, t, P.j), w);
+    }
+  a.A = a.Ap[0];
+  a.B = a.Bp[0];
+  TP_TRY(fused_barrier(C));  // every owner's shards are written
+  TP_TRY(gemm(a, C.R.s));
+  return fused_barrier(C);   // every reader is done before anyone overwrites its shards
+}
+
+tp_status fused25_bwd(Ctx& C, const Plane& P, const void* dy, const void* x, const void* w,
+                      void* dx, void* dw) {
+  if (C.R.plan) return TP_OK;
+  const tp_grid* g = C.g;
+  const int dep = g->coords[0];
+  const int64_t hq = P.kq / P.d;
+  GemmArgs gs[1 + 4];  // dW + up to d = 4 dX column blocks (q d <= 4)
+  int n = 0;
+  // dW_dep[i,j] [hq, nq]: contraction over every plane's batch rows
+  GemmArgs gw = panel_base(C, hq, P.nq, P.mb, true, false, dw, nullptr, P.kq, P.nq, P.nq);
+  gw.npanels = P.q * P.d;
+  int k = 0;
+  for (int e = 0; e < P.d; ++e)
+    for (int m = 0; m < P.q; ++m, ++k) {
+      gw.Ap[k] = static_cast<const char*>(g->peer_ptr(rank25(P, e, m, P.i), x)) + dep * hq * C.esz;
+      gw.Bp[k] = g->peer_ptr(rank25(P, e, m, P.j), dy);
+    }
+  gw.A = gw.Ap[0];
+  gw.B = gw.Bp[0];
+  gs[n++] = gw;
+  if (dx) {
+    for (int e = 0; e < P.d; ++e) {  // dX column block e: [mb, hq] at column e hq
+      GemmArgs gx = panel_base(C, P.mb, hq, P.nq, false, true,
+                               static_cast<char*>(dx) + e * hq * C.esz, nullptr, P.nq, P.nq, P.kq);
+      gx.npanels = P.q;
+      for (int t = 0; t < P.q; ++t) {
+        gx.Ap[t] = g->peer_ptr(rank25(P, dep, P.i, t), dy);
+        gx.Bp[t] = g->peer_ptr(rank25(P, e, P.j, t), w);
+      }
+      gx.A = gx.Ap[0];
+      gx.B = gx.Bp[0];
+      gs[n++] = gx;
+    }
+  }
+  TP_TRY(fused_barrier(C));
+  for (int i0 = 0; i0 < n; i0 += 4)  // grouped launches of up to four problems
+    TP_TRY(gemm_group(gs + i0, std::min(4, n - i0), C.R.s));
+  return fused_barrier(C);
+}
+
 tp_status fwd_2d(Ctx& C, const void* x, const void* w, const void* bias, void* y) {
   Plane P = plane_of(C);
   if (fused_ok(C, P, {x, w}, {P.mb})) return fused_ab(C, P, x, w, bias, y);
+  if (fused25_ok(C, P, {x, w}, {P.mb, P.kq / P.d})) return fused25_fwd(C, P, x, w, bias, y);
   const void* W = w;
   if (C.g->mode == TP_2P5D && (C.d->flags & TP_FLAG_W25_DEPTH_SHARDED) && P.d > 1) {
     // depth-sharded W: all-gather the depth pieces of W[i,j] (row-contiguous) into `saved`
@@ -611,7 +710,17 @@ tp_status bwd_2d(Ctx& C, const void* dy, const void* x, const void* w, const voi
   float* scratch = dbias ? C.colsum_scratch(P.nq) : nullptr;
   void* db_t[2] = {dbias ? C.ws(P.nq) : nullptr, dbias ? C.ws(P.nq) : nullptr};
   // the two SUMMA chains carve separate buffers so both pipelines can stay in flight
-  if (!sharded && fused_ok(C, P, {x, w, dy}, {P.mb, P.kq})) {
+  const bool fused_sh = sharded && fused25_ok(C, P, {x, w, dy}, {P.mb, P.kq / P.d});
+  if (sharded && !fused_sh && !C.R.plan && fused25_ok(C, P, {x, w}, {P.mb, P.kq / P.d})) {
+    // the forward ran fused (no depth-gathered W in `saved`) but dY is not a registered
+    // buffer: gather W here for the collective backward
+    TP_TRY(C.order(C.R.s, C.R.cs));
+    TP_TRY(P.depth->allgather(w, const_cast<void*>(saved), (P.kq / P.d) * P.nq, C.dt, C.R.cs));
+    TP_TRY(C.order(C.R.cs, C.R.s));
+  }
+  if (fused_sh) {
+    TP_TRY(fused25_bwd(C, P, dy, x, w, dx, dw));  // dW comes out as this plane's depth shard
+  } else if (!sharded && fused_ok(C, P, {x, w, dy}, {P.mb, P.kq})) {
     TP_TRY(fused_abt_atb(C, P, dy, x, w, dx, dwt));
   } else if (P.q == 1 && dx) {  // one-rank plane: both products local and independent
     if (!C.R.plan)
@@ -622,7 +731,7 @@ tp_status bwd_2d(Ctx& C, const void* dy, const void* x, const void* w, const voi
     TP_TRY(summa_atb(C, P, x, dy, dwt));
   }
   if (C.R.plan) return TP_OK;
-  if (depth) {  // 2.5D: sum the planes' dW partials over depth (a-8)
+  if (depth && !fused_sh) {  // 2.5D: sum the planes' dW partials over depth (a-8)
     TP_TRY(C.order(C.R.s, C.R.cs));
     if (sharded)
       TP_TRY(P.depth->reducescatter(dwt, dw, (P.kq / P.d) * P.nq, C.dt, C.R.cs));

@@ -172,3 +172,42 @@ def test_fused_1d_exact_integer(api):
         assert np.array_equal(gather("1d", 4, 1, spec, per, "Y", "Y"), Yr)
         assert np.array_equal(gather("1d", 4, 1, spec, per, "dX", "X"), dXr)
         assert np.array_equal(gather("1d", 4, 1, spec, per, "dW", "W"), dWr)
+
+
+DEPTH_SHARDED = 0x1  # TP_FLAG_W25_DEPTH_SHARDED
+
+
+@pytest.mark.parametrize("p,d,M,K,N", [
+    (8, 2, 800, 544, 528),   # q=2, d=2: blocks 200 x 272 (W shard 136 x 264), four panels
+    (4, 4, 600, 544, 520),   # q=1, d=4: blocks 150 x 544 (W shard 136 x 520), four panels
+    (8, 2, 528, 1056, 400),  # hq = 264: K-panels not a multiple of the 64-wide k-block
+], ids=["q2d2", "q1d4", "q2d2-ragged"])
+@pytest.mark.parametrize("with_bias", [False, True])
+def test_fused_depth_sharded_25d(api, p, d, M, K, N, with_bias):
+    """2.5D with the weight depth-sharded (1/p per rank): every product is one multi-panel GEMM
+    whose q*d K-panels are the depth pieces of the SUMMA panels, read from their owners; no depth
+    all-gather of W, no depth reduce-scatter of dW."""
+    X, W, dY, b = synth.layer_inputs(17, M, K, N, with_bias=True)
+    b = b if with_bias else None
+    fl = FUSED | DEPTH_SHARDED
+    per = tp_layer(api, "2.5d", p, d, M, K, N, X, W, dY, b, "bf16", flags=fl, alpha=0.5)
+    spec = spec_of(M, K, N, flags=fl)
+    Yr, dXr, dWr, dbr = oracle_layer("2.5d", p, d, spec, X, W, dY, b, alpha=0.5)
+    assert rel_fro(gather("2.5d", p, d, spec, per, "Y", "Y"), Yr) <= 1e-2
+    assert rel_fro(gather("2.5d", p, d, spec, per, "dX", "X"), dXr) <= 1e-2
+    assert rel_fro(gather("2.5d", p, d, spec, per, "dW", "W"), dWr) <= 1e-2
+    if with_bias:
+        assert rel_fro(gather("2.5d", p, d, spec, per, "dB", "B"), dbr) <= 1e-2
+    assert per[0]["n_fwd"] == p  # one GEMM per rank: the fused path ran
+
+
+def test_fused_depth_sharded_25d_exact_integer(api):
+    M, K, N = 544, 544, 272
+    X, W, dY, _ = synth.layer_inputs(6, M, K, N, kind="ternary")
+    fl = FUSED | DEPTH_SHARDED
+    per = tp_layer(api, "2.5d", 8, 2, M, K, N, X, W, dY, None, "bf16", flags=fl)
+    spec = spec_of(M, K, N, flags=fl)
+    Yr, dXr, dWr, _ = oracle_layer("2.5d", 8, 2, spec, X, W, dY)
+    assert np.array_equal(gather("2.5d", 8, 2, spec, per, "Y", "Y"), Yr)
+    assert np.array_equal(gather("2.5d", 8, 2, spec, per, "dX", "X"), dXr)
+    assert np.array_equal(gather("2.5d", 8, 2, spec, per, "dW", "W"), dWr)
