@@ -79,6 +79,14 @@ typedef enum { TP_TENSOR_X = 0, TP_TENSOR_W = 1, TP_TENSOR_Y = 2, TP_TENSOR_BIAS
  * shifts along the grid rows / columns) instead of SUMMA's broadcasts; same layouts and
  * results. The backward keeps the SUMMA ABT / ATB schedule. */
 #define TP_FLAG_CANNON 0x10u
+/* 2.5D as Solomonik & Demmel's 2.5D matrix multiplication (P:L526 cites it; SURVEY 8(f)
+ * NEXT-4; oracle/solomonik.py, reading N5) instead of the paper's batch-split 2.5D: every
+ * layer holds the full q x q block layout (X [M/q, K/q], W [K/q, N/q], Y [M/q, N/q] at
+ * (dep, i, j), replicated over depth), layer dep runs the SUMMA steps [dep q/d, (dep+1) q/d),
+ * Y is all-reduced over depth, dX / dW are depth-broadcast from the layer that reduced them.
+ * Needs q % d == 0 and M, K, N divisible by q; excludes TP_FLAG_W25_DEPTH_SHARDED, CANNON
+ * and PEER_FUSED (TP_ERR_ARG). */
+#define TP_FLAG_SOLOMONIK 0x20u
 
 typedef struct tp_grid tp_grid; /* opaque; library-owned (communicators, streams, events) */
 

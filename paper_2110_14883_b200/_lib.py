@@ -30,6 +30,7 @@ TP_FLAG_SERIAL = 0x2
 TP_FLAG_PEER_FUSED = 0x4
 TP_FLAG_GELU = 0x8
 TP_FLAG_CANNON = 0x10
+TP_FLAG_SOLOMONIK = 0x20
 
 EXPORTED = [
     "tp_status_string", "tp_last_error", "tp_version", "tp_get_unique_id", "tp_grid_init",

@@ -10,7 +10,7 @@ import ctypes as C
 
 from . import _lib as L
 from ._lib import (TP_1D, TP_2D, TP_2P5D, TP_3D, TP_BF16, TP_FP32, TP_FLAG_SERIAL,  # noqa: F401
-                   TP_FLAG_PEER_FUSED, TP_FLAG_GELU, TP_FLAG_CANNON,
+                   TP_FLAG_PEER_FUSED, TP_FLAG_GELU, TP_FLAG_CANNON, TP_FLAG_SOLOMONIK,
                    TP_FLAG_W25_DEPTH_SHARDED, TP_TENSOR_BIAS, TP_TENSOR_W, TP_TENSOR_X,
                    TP_TENSOR_Y, TP_TRANSPORT_LOCAL, TP_TRANSPORT_NCCL, TP_TRANSPORT_NONE,
                    tp_cost, tp_linear_desc, tp_rsa_desc)

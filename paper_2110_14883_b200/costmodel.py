@@ -36,6 +36,8 @@ def grids(p):
         for d in range(1, p + 1):
             if d * q * q == p and q > 1:
                 out.append((f"2.5d(d={d})", "2.5d", q, d))
+                if d > 1 and q % d == 0:  # Solomonik's 2.5D (TP_FLAG_SOLOMONIK, reading N5)
+                    out.append((f"2.5d-solomonik(d={d})", "2.5d", q, d))
         if q ** 3 == p:
             out.append(("3d", "3d", q, 1))
     return out
@@ -59,7 +61,8 @@ def model(workload, p, link_gbs=900.0, peak_tflops=None):
                                 "t_tensor_us", "t_link_us")}
         ok = True
         for i, (K, N) in enumerate(layers):
-            ds = api.desc(M, K, N, dtype, split_1d=i % 2, parity_3d=i % 2)
+            fl = api.TP_FLAG_SOLOMONIK if "solomonik" in label else 0
+            ds = api.desc(M, K, N, dtype, split_1d=i % 2, parity_3d=i % 2, flags=fl)
             try:
                 c = api.tp_cost_model(mode, p, ds, q=q, depth=d, peak_tflops=peak,
                                       link_gbs=link_gbs)

@@ -731,6 +731,17 @@ extern "C" tp_status tp_cost_model(tp_mode mode, int world, int q, int d, const 
       c.mem_y = Sy / p;
       break;
     case TP_2P5D:  // d planes of SUMMA on S_x/d rows + depth AR(dW) or AG(W)+RS(dW) (A6, A11)
+      if (desc->flags & TP_FLAG_SOLOMONIK) {
+        // N5 (oracle/solomonik.py closed_form_volume): the q/d steps of every layer move
+        // (q-1)(S_x+S_w)/d per product; depth AR of Y, depth bcasts of dX and dW. The Table has
+        // no row for this scheme: paper_elems = the paper's 2.5D row, for comparison.
+        c.paper_elems = 3.0 * (j - 1) * (Sx / dd + Sw);
+        c.counted_elems = 3.0 * (j - 1) * (Sx + Sw) + 2.0 * (dd - 1) * Sy + (dd - 1) * (Sx + Sw);
+        c.mem_x = Sx / (double(j) * j);
+        c.mem_w = Sw / (double(j) * j);
+        c.mem_y = Sy / (double(j) * j);
+        break;
+      }
       c.paper_elems = 3.0 * (j - 1) * (Sx / dd + Sw);
       c.counted_elems = dd * 3.0 * (j - 1) * (Sx / dd + Sw) + 2.0 * (dd - 1) * Sw;
       if (desc->flags & TP_FLAG_CANNON) c.counted_elems += dd * (j - 1) * (Sx / dd + Sw) / j;

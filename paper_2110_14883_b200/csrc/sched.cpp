@@ -117,6 +117,17 @@ tp_status check_divisible(const tp_grid* g, const tp_linear_desc* d) {
       break;
     case TP_2P5D: {
       const bool sh = d->flags & TP_FLAG_W25_DEPTH_SHARDED;
+      if (d->flags & TP_FLAG_SOLOMONIK) {  // replicated layers, depth-split SUMMA steps (N5)
+        if (d->flags & (TP_FLAG_W25_DEPTH_SHARDED | TP_FLAG_CANNON | TP_FLAG_PEER_FUSED))
+          return fail(TP_ERR_ARG, "TP_FLAG_SOLOMONIK excludes W25_DEPTH_SHARDED, CANNON, PEER_FUSED");
+        if (q % dd)
+          return fail(TP_ERR_CONSTRAINT, "Solomonik 2.5D: q = " + std::to_string(q) +
+                                             " not divisible by d = " + std::to_string(dd));
+        if (!divides(M, q)) return bad("M", M, q);
+        if (!divides(K, q)) return bad("K", K, q);
+        if (!divides(N, q)) return bad("N", N, q);
+        break;
+      }
       if (!divides(M, int64_t(dd) * q)) return bad("M", M, int64_t(dd) * q);
       if (!divides(N, q)) return bad("N", N, q);
       if (!divides(K, sh ? int64_t(q) * dd : q)) return bad("K", K, sh ? int64_t(q) * dd : q);
@@ -167,6 +178,12 @@ tp_status extent(const tp_grid* g, const tp_linear_desc* d, int tensor, Ext* e) 
     }
     case TP_2P5D: {
       const int64_t dep = c[0], i = c[1], j = c[2], q = g->q, dd = g->d;
+      if (d->flags & TP_FLAG_SOLOMONIK) {  // the 2D block layout on every layer
+        if (tensor == TP_TENSOR_X) return set(i * M / q, M / q, j * K / q, K / q);
+        if (tensor == TP_TENSOR_W) return set(i * K / q, K / q, j * N / q, N / q);
+        if (tensor == TP_TENSOR_Y) return set(i * M / q, M / q, j * N / q, N / q);
+        return set(0, 1, j * N / q, N / q);
+      }
       const int64_t mb = M / (dd * q);
       if (tensor == TP_TENSOR_X) return set((dep * q + i) * mb, mb, j * K / q, K / q);
       if (tensor == TP_TENSOR_W) {
@@ -320,6 +337,7 @@ struct Plane {
   Comm* depth;  // 2.5D depth line (nullptr for 2D or d == 1)
   int i, j, q, d;
   int64_t mb, kq, nq;
+  int t0, t1;  // SUMMA steps this rank's layer runs: all (q), or Solomonik's [dep q/d, +q/d)
 };
 
 Plane plane_of(Ctx& C) {
@@ -342,6 +360,14 @@ Plane plane_of(Ctx& C) {
     P.d = g->d;
   }
   P.mb = C.d->M / (int64_t(P.d) * P.q);
+  if (C.g->mode == TP_2P5D && (C.d->flags & TP_FLAG_SOLOMONIK)) {  // layers replicate, steps split
+    P.mb = C.d->M / P.q;
+    P.t0 = g->coords[0] * (P.q / P.d);
+    P.t1 = P.t0 + P.q / P.d;
+  } else {
+    P.t0 = 0;
+    P.t1 = P.q;
+  }
   P.kq = C.d->K / P.q;
   P.nq = C.d->N / P.q;
   return P;
@@ -350,7 +376,7 @@ Plane plane_of(Ctx& C) {
 // SUMMA "AB" (a-5): for t: bcast X[i,t] along row i, W[t,j] along column j; Y += X_t W_t.
 tp_status summa_ab(Ctx& C, const Plane& P, const void* x, const void* W, const void* bias, void* y) {
   const float alpha = C.d->alpha;
-  if (P.q == 1) {
+  if (P.q == 1 && P.t1 - P.t0 == 1) {
     if (C.R.plan) return TP_OK;
     return C.mm(P.mb, P.nq, P.kq, x, false, W, false, y, C.dt, alpha, nullptr, bias);
   }
@@ -369,15 +395,15 @@ tp_status summa_ab(Ctx& C, const Plane& P, const void* x, const void* W, const v
     ready[t & 1] = C.record(C.R.cs);
     return TP_OK;
   };
-  TP_TRY(issue(0));
-  TP_TRY(issue(1));
-  for (int t = 0; t < P.q; ++t) {
+  TP_TRY(issue(P.t0));
+  if (P.t0 + 1 < P.t1) TP_TRY(issue(P.t0 + 1));
+  for (int t = P.t0; t < P.t1; ++t) {
     TP_CUDA(cudaStreamWaitEvent(C.R.s, ready[t & 1], 0));
-    const bool last = t == P.q - 1;
+    const bool last = t == P.t1 - 1;
     TP_TRY(C.mm(P.mb, P.nq, P.kq, xpan(t), false, wpan(t), false, last ? y : acc,
-                last ? C.dt : TP_FP32, last ? alpha : 1.f, t > 0 ? acc : nullptr,
+                last ? C.dt : TP_FP32, last ? alpha : 1.f, t > P.t0 ? acc : nullptr,
                 last ? bias : nullptr));
-    if (t + 2 < P.q) {
+    if (t + 2 < P.t1) {
       TP_TRY(C.order(C.R.s, C.R.cs));  // panel buffers of step t are free again
       TP_TRY(issue(t + 2));
     }
@@ -456,15 +482,15 @@ tp_status summa_abt(Ctx& C, const Plane& P, const void* dy, const void* W, void*
     ready[k & 1] = C.record(C.R.cs);
     return TP_OK;
   };
-  TP_TRY(issue(0));
-  TP_TRY(issue(1));
-  for (int k = 0; k < P.q; ++k) {
+  TP_TRY(issue(P.t0));
+  if (P.t0 + 1 < P.t1) TP_TRY(issue(P.t0 + 1));
+  for (int k = P.t0; k < P.t1; ++k) {
     TP_CUDA(cudaStreamWaitEvent(C.R.s, ready[k & 1], 0));
     void* part = P.j == k ? dx : bp[k & 1];  // the root reduces in place into dX
     TP_TRY(C.mm(P.mb, P.kq, P.nq, dy, false, wpan(k), true, part, C.dt, alpha, nullptr, nullptr));
     TP_TRY(C.order(C.R.s, C.R.cs));
     TP_TRY(P.row->reduce(part, dx, P.mb * P.kq, C.dt, k, C.R.cs));
-    if (k + 2 < P.q) TP_TRY(issue(k + 2));
+    if (k + 2 < P.t1) TP_TRY(issue(k + 2));
   }
   return TP_OK;
 }
@@ -486,15 +512,15 @@ tp_status summa_atb(Ctx& C, const Plane& P, const void* x, const void* dy, void*
     ready[k & 1] = C.record(C.R.cs);
     return TP_OK;
   };
-  TP_TRY(issue(0));
-  TP_TRY(issue(1));
-  for (int k = 0; k < P.q; ++k) {
+  TP_TRY(issue(P.t0));
+  if (P.t0 + 1 < P.t1) TP_TRY(issue(P.t0 + 1));
+  for (int k = P.t0; k < P.t1; ++k) {
     TP_CUDA(cudaStreamWaitEvent(C.R.s, ready[k & 1], 0));
     void* part = P.i == k ? dwt : bp[k & 1];
     TP_TRY(C.mm(P.kq, P.nq, P.mb, xpan(k), true, dy, false, part, C.dt, alpha, nullptr, nullptr));
     TP_TRY(C.order(C.R.s, C.R.cs));
     TP_TRY(P.col->reduce(part, dwt, P.kq * P.nq, C.dt, k, C.R.cs));
-    if (k + 2 < P.q) TP_TRY(issue(k + 2));
+    if (k + 2 < P.t1) TP_TRY(issue(k + 2));
   }
   return TP_OK;
 }
@@ -682,8 +708,47 @@ tp_status fused25_bwd(Ctx& C, const Plane& P, const void* dy, const void* x, con
   return fused_barrier(C);
 }
 
+// ---- Solomonik-style 2.5D (TP_FLAG_SOLOMONIK, reading N5; oracle/
+// solomonik.py): every layer holds the 2D block layout, layer dep runs SUMMA steps [t0, t1).
+// Forward: the layer's partial Y (bias on layer 0 only) all-reduced over depth. Backward: the
+// layer reduces dX[i,k] / dW[k,j] for its k's; every rank then receives its own block by a
+// depth broadcast from the layer that owns its column (dX) / row (dW) index.
+bool solomonik(const Ctx& C) { return C.g->mode == TP_2P5D && (C.d->flags & TP_FLAG_SOLOMONIK); }
+
+tp_status fwd_solomonik(Ctx& C, const Plane& P, const void* x, const void* w, const void* bias, void* y) {
+  void* yp = P.d > 1 ? C.ws(P.mb * P.nq) : y;
+  TP_TRY(summa_ab(C, P, x, w, C.g->coords[0] == 0 ? bias : nullptr, yp));
+  if (C.R.plan || P.d == 1) return TP_OK;
+  TP_TRY(C.order(C.R.s, C.R.cs));
+  return P.depth->allreduce(yp, y, P.mb * P.nq, C.dt, C.R.cs);
+}
+
+tp_status bwd_solomonik(Ctx& C, const Plane& P, const void* dy, const void* x, const void* w,
+                        void* dx, void* dw, void* dbias) {
+  float* scratch = dbias ? C.colsum_scratch(P.nq) : nullptr;
+  void* dbt = (dbias && P.q > 1) ? C.ws(P.nq) : nullptr;
+  if (dx) TP_TRY(summa_abt(C, P, dy, w, dx));
+  TP_TRY(summa_atb(C, P, x, dy, dw));
+  if (C.R.plan) return TP_OK;
+  if (P.d > 1) {
+    const int span = P.q / P.d;  // steps per layer: block index k is reduced on layer k / span
+    TP_TRY(C.order(C.R.s, C.R.cs));
+    if (dx) TP_TRY(P.depth->bcast(dx, P.mb * P.kq, C.dt, P.j / span, C.R.cs));
+    TP_TRY(P.depth->bcast(dw, P.kq * P.nq, C.dt, P.i / span, C.R.cs));
+  }
+  if (dbias) {  // dY is replicated over depth: column sums reduced along the column only
+    TP_TRY(C.colsum(dy, P.mb, P.nq, dbt ? dbt : dbias, scratch));
+    if (dbt) {
+      TP_TRY(C.order(C.R.s, C.R.cs));
+      TP_TRY(P.col->allreduce(dbt, dbias, P.nq, C.dt, C.R.cs));
+    }
+  }
+  return TP_OK;
+}
+
 tp_status fwd_2d(Ctx& C, const void* x, const void* w, const void* bias, void* y) {
   Plane P = plane_of(C);
+  if (solomonik(C)) return fwd_solomonik(C, P, x, w, bias, y);
   if (fused_ok(C, P, {x, w}, {P.mb})) return fused_ab(C, P, x, w, bias, y);
   if (fused25_ok(C, P, {x, w}, {P.mb, P.kq / P.d})) return fused25_fwd(C, P, x, w, bias, y);
   const void* W = w;
@@ -703,6 +768,7 @@ tp_status fwd_2d(Ctx& C, const void* x, const void* w, const void* bias, void* y
 tp_status bwd_2d(Ctx& C, const void* dy, const void* x, const void* w, const void* saved, void* dx,
                  void* dw, void* dbias) {
   Plane P = plane_of(C);
+  if (solomonik(C)) return bwd_solomonik(C, P, dy, x, w, dx, dw, dbias);
   const bool sharded = C.g->mode == TP_2P5D && (C.d->flags & TP_FLAG_W25_DEPTH_SHARDED) && P.d > 1;
   const void* W = sharded ? saved : w;
   const bool depth = P.d > 1;

@@ -103,3 +103,40 @@ def test_cannon_volume_matches_oracle_ledger(q):
     c1 = api.tp_cost_model("2d", q * q, api.desc(M, K, N, flags=0x10), q=q)
     summa_fwd = cf.counted_volume("2d", M, K, N, q=q, part="fwd")
     assert c1["counted_elems"] - c0["counted_elems"] == pytest.approx(fwd - summa_fwd)
+
+
+def test_solomonik_volume_equals_oracle():
+    """TP_FLAG_SOLOMONIK (reading N5): the cost model's counted volume and shard sizes equal
+    oracle/solomonik.py's closed form and its layout."""
+    from oracle import solomonik as so
+    from oracle.grid import build_grid
+    from oracle.shards import LayerSpec
+    for (q, d) in [(2, 2), (4, 2), (2, 1)]:
+        M, K, N = 64 * q, 32 * q, 48 * q
+        c = api.tp_cost_model("2.5d", d * q * q, api.desc(M, K, N, "bf16", flags=api.TP_FLAG_SOLOMONIK),
+                              q=q, depth=d)
+        grid, spec = build_grid("2.5d", d * q * q, d), LayerSpec(M, K, N)
+        cf = so.closed_form_volume(grid, spec)
+        assert c["counted_elems"] == cf["fwd"] + cf["bwd"]
+        e = so.extent(grid, spec, 0, "W")
+        assert c["mem_w"] == e.rows * e.cols
+
+
+def test_solomonik_extents_match_oracle():
+    from oracle import solomonik as so
+    from oracle.grid import build_grid
+    from oracle.shards import LayerSpec
+    q, d = 2, 2
+    M, K, N = 96, 64, 80
+    grid, spec = build_grid("2.5d", 8, 2), LayerSpec(M, K, N)
+    ds = api.desc(M, K, N, "bf16", flags=api.TP_FLAG_SOLOMONIK)
+    for r in range(8):
+        g = api.tp_grid_init("2.5d", 8, r, 0, 2, 0, api.TP_TRANSPORT_NONE)
+        try:
+            for t in ("X", "W", "Y", "B"):
+                e = so.extent(grid, spec, r, t)
+                assert api.tp_shard_extent(g, ds, t) == (e.row0, e.rows, e.col0, e.cols)
+        finally:
+            api.tp_grid_destroy(g)
+    with pytest.raises(api.TPError):   # q = 2 is not divisible by d = 4 ... (p = 16, q = 2, d = 4)
+        api.tp_cost_model("2.5d", 16, ds, q=2, depth=4)
