@@ -28,7 +28,15 @@ namespace {
 
 using namespace ptx;
 
-constexpr int kFThreads = 192;
+// Softmax warps: 4 (one per TMEM lane quadrant, all 128 keys of a row) or 8 (two per
+// quadrant, each 64 keys of the row and half of O's columns; the row max is exchanged through
+// shared memory, the row sums are combined at the end). 8 for d = 64, whose tiles are bound
+// by the exp2 stream (the XU pipe) rather than the tensor core; d = 128 has no smem left for
+// the exchange and is balanced.
+template <int D>
+constexpr int soft_warps() { return D == 64 ? 8 : 4; }
+template <int D>
+constexpr int f_threads() { return 64 + 32 * soft_warps<D>(); }
 constexpr int kQT = 128;   // query rows per CTA
 constexpr int kKT = 128;   // keys per tile
 constexpr int kKvStages = 2;
@@ -40,7 +48,8 @@ struct FC {
   static constexpr int VBytes = kKT * D * 2;           // 2 key blocks x D/64 chunks of [64][128 B]
   static constexpr int PBytes = kQT * kKT * 2;         // 2 key blocks of [128 rows][128 B]
   static constexpr int StageBytes = KBytes + VBytes;
-  static constexpr int Smem = QBytes + kKvStages * StageBytes + 2 * PBytes + 1024 + 256;
+  static constexpr int XBytes = soft_warps<D>() == 8 ? 2 * 2 * kQT * 4 : 0;  // [tile parity][half][row]
+  static constexpr int Smem = QBytes + kKvStages * StageBytes + 2 * PBytes + XBytes + 1024 + 256;
   static constexpr int TmemCols = 2 * kKT + (D < 32 ? 32 : D);  // S[2] + O
 };
 
@@ -66,14 +75,15 @@ __device__ __forceinline__ float ex2_approx(float x) {
 }
 
 template <int D>
-__global__ void __launch_bounds__(kFThreads, 1) flash_fwd_kernel(const __grid_constant__ FParams F) {
+__global__ void __launch_bounds__(f_threads<D>(), 1) flash_fwd_kernel(const __grid_constant__ FParams F) {
   using C = FC<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
   uint8_t* sKV = sQ + C::QBytes;
   uint8_t* sP = sKV + kKvStages * C::StageBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * C::PBytes);  // P double-buffered
+  float* sX = reinterpret_cast<float*>(sP + 2 * C::PBytes);  // P double-buffered; max exchange
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * C::PBytes + C::XBytes);
   uint64_t* q_full = bars;
   // K and V have their own barriers: K_j's slot frees when S_j retires (early), V_j's when
   // P_j V_j retires, so K_{j+2}'s load is in flight long before S_{j+2} is issued
@@ -106,10 +116,10 @@ __global__ void __launch_bounds__(kFThreads, 1) flash_fwd_kernel(const __grid_co
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 4);
+      mbar_init(&s_empty[i], soft_warps<D>());
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&p_full[i], 4);
+      mbar_init(&p_full[i], soft_warps<D>());
       mbar_init(&p_empty[i], 1);
     }
     fence_barrier_init();
@@ -208,61 +218,72 @@ __global__ void __launch_bounds__(kFThreads, 1) flash_fwd_kernel(const __grid_co
     }
     __syncwarp();
   } else {
-    // ---- softmax warps: row = (warp % 4) * 32 + lane
+    // ---- softmax warps: row = (warp % 4) * 32 + lane; with 8 warps the two warps of a lane
+    // quadrant take keys [half * 64, +64) of every tile and O columns [half * D/2, +D/2)
+    constexpr int kH = soft_warps<D>() / 4;  // warps per quadrant
+    constexpr int KW = kKT / kH;             // keys per warp per tile
+    constexpr int OC = D / kH;               // O columns per warp
     const int quad = warp & 3;
+    const int half = (warp - 2) / 4;
     const int r = quad * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
-    float m = -INFINITY, l = 0.f;
+    const uint32_t s_off = static_cast<uint32_t>(half * KW);
+    const uint32_t o_off = static_cast<uint32_t>(half * OC);
+    float m = -INFINITY, l = 0.f;  // l: this warp's keys only (the halves are added at the end)
     const int64_t qrow = q0 + r;  // this thread's query row within the problem
     if (F.carry_in && qrow < F.s) {
       const float2 c = *reinterpret_cast<const float2*>(F.ml + 2 * (row_base + qrow));
       m = c.x;
-      l = c.y;
+      l = half == 0 ? c.y : 0.f;
     }
     for (int j = 0; j < ntiles; ++j) {
       const int b = j & 1;
-      if (F.dbg && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0) F.dbg[5 + quad] = 600 + j;
       mbar_wait(&s_full[b], (j >> 1) & 1);
-      if (F.dbg && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0) F.dbg[9 + quad] = 700 + j;
       tc_fence_after();
-      const int64_t valid = F.s - int64_t(j) * kKT;  // keys of this tile inside the sequence
-      // the S row (128 fp32) into registers once: four loads in flight, one wait
-      uint32_t sv[kKT / 32][32];
+      const int64_t valid = F.s - int64_t(j) * kKT - half * KW;  // this warp's keys in range
+      // this warp's part of the S row into registers once: all loads in flight, one wait
+      uint32_t sv[KW / 32][32];
 #pragma unroll
-      for (int c = 0; c < kKT / 32; ++c) tmem_ld32(tS[b] + lane_off + c * 32, sv[c]);
+      for (int c = 0; c < KW / 32; ++c) tmem_ld32(tS[b] + lane_off + s_off + c * 32, sv[c]);
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_empty[b]);  // S buffer b may be overwritten
-      if (valid < kKT) {  // last tile of a ragged sequence: masked keys weigh exp2(-inf) = 0
+      if (valid < KW) {  // last tile of a ragged sequence: masked keys weigh exp2(-inf) = 0
 #pragma unroll
-        for (int c = 0; c < kKT / 32; ++c)
+        for (int c = 0; c < KW / 32; ++c)
 #pragma unroll
           for (int i = 0; i < 32; ++i)
             if (c * 32 + i >= valid) sv[c][i] = 0xff800000u;  // -inf
       }
       auto sval = [&](int c, int i) { return __uint_as_float(sv[c][i]); };
-      // row max: 8 independent chains, then a tree (a single 128-long fmax chain is latency)
+      // row max: 8 independent chains, then a tree (a single long fmax chain is latency)
       float mxs[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) mxs[i] = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < kKT / 32; ++c)
+      for (int c = 0; c < KW / 32; ++c)
 #pragma unroll
         for (int i = 0; i < 32; ++i) mxs[i & 7] = fmaxf(mxs[i & 7], sval(c, i));
-      const float mx = fmaxf(fmaxf(fmaxf(mxs[0], mxs[1]), fmaxf(mxs[2], mxs[3])),
-                             fmaxf(fmaxf(mxs[4], mxs[5]), fmaxf(mxs[6], mxs[7])));
+      float mx = fmaxf(fmaxf(fmaxf(mxs[0], mxs[1]), fmaxf(mxs[2], mxs[3])),
+                       fmaxf(fmaxf(mxs[4], mxs[5]), fmaxf(mxs[6], mxs[7])));
+      if (kH == 2) {  // the other half's max of the same row (double-buffered by tile parity)
+        float* xc = sX + (j & 1) * (2 * kQT);
+        xc[half * kQT + r] = mx;
+        named_barrier_sync(1 + quad, 64);
+        mx = fmaxf(mx, xc[(half ^ 1) * kQT + r]);
+      }
       // Lazy rescale: the reference max m moves only when some row of the warp would exceed it
       // by more than 2^8 (p <= 256 is exact enough in bf16 / fp32), so most tiles leave O alone
       // and the softmax runs a tile ahead of the P V MMA. O, l and the carried (m, l) all use
-      // the same reference, so O / l is unchanged.
+      // the same reference, so O / l is unchanged. Both warps of a quadrant see the same rows
+      // and the same row max, so they take the same decision.
       const float m_cand = fmaxf(m, mx * F.scale_log2);
       const bool move = (j == 0 && !F.carry_in) || __any_sync(0xffffffffu, m_cand > m + 8.f);
       const float m_new = move ? m_cand : m;
       const float alpha = exp2f(m - m_new);  // 1 when m stays; 0 on the first tile (m = -inf)
       // P buffer j % 2 was last read by P_{j-2} V_{j-2}
       if (j >= 2) mbar_wait(&p_empty[j & 1], ((j - 2) >> 1) & 1);
-      if (F.dbg && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0) F.dbg[13 + quad] = 800 + j;
       tc_fence_after();
       // p = exp2(s scale log2e - m_new) (one FFMA + MUFU.EX2 each) -> bf16 P row (swizzled
       // K-major), row sum in 8 independent partial sums
@@ -271,7 +292,7 @@ __global__ void __launch_bounds__(kFThreads, 1) flash_fwd_kernel(const __grid_co
       for (int i = 0; i < 8; ++i) rsp[i] = 0.f;
       const float neg_m = -m_new;
 #pragma unroll
-      for (int c = 0; c < kKT / 32; ++c) {
+      for (int c = 0; c < KW / 32; ++c) {
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
@@ -281,24 +302,24 @@ __global__ void __launch_bounds__(kFThreads, 1) flash_fwd_kernel(const __grid_co
           __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
           pk[i] = *reinterpret_cast<uint32_t*>(&h);
         }
-        // 32 keys = 64 B = 4 swizzled 16-byte chunks of the row in key block c / 2
-        uint8_t* rowp = sP + (j & 1) * C::PBytes + (c / 2) * (kQT * 128) + r * 128;
+        // 32 keys = 64 B = 4 swizzled 16-byte chunks of the row in key block (key / 64)
+        const int key0 = half * KW + c * 32;
+        uint8_t* rowp = sP + (j & 1) * C::PBytes + (key0 / 64) * (kQT * 128) + r * 128;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const int chunk = (c % 2) * 4 + q;
+          const int chunk = ((key0 % 64) / 32) * 4 + q;
           *reinterpret_cast<uint4*>(rowp + ((chunk ^ (r & 7)) << 4)) =
               make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
         }
       }
-  // S buffer b may be overwritten
       const float rs = ((rsp[0] + rsp[1]) + (rsp[2] + rsp[3])) + ((rsp[4] + rsp[5]) + (rsp[6] + rsp[7]));
       l = l * alpha + rs;
       if (j == 0 && F.carry_in) {
         // carried O of the earlier ring blocks, rescaled to this block's running max, into
         // TMEM before the first P V MMA accumulates onto it
-        const float4* src = reinterpret_cast<const float4*>(F.acc + (row_base + qrow) * D);
+        const float4* src = reinterpret_cast<const float4*>(F.acc + (row_base + qrow) * D + o_off);
 #pragma unroll 1
-        for (int c = 0; c < D / 32; ++c) {
+        for (int c = 0; c < OC / 32; ++c) {
           uint32_t v[32];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
@@ -308,26 +329,23 @@ __global__ void __launch_bounds__(kFThreads, 1) flash_fwd_kernel(const __grid_co
             v[4 * i + 2] = __float_as_uint(x.z * alpha);
             v[4 * i + 3] = __float_as_uint(x.w * alpha);
           }
-          tmem_st32(tO + lane_off + c * 32, v);
+          tmem_st32(tO + lane_off + o_off + c * 32, v);
         }
         tmem_wait_st();
       }
-      // rescale the O row (warp-uniform: tcgen05.ld / st are .sync.aligned; alpha = 1 is exact)
+      // rescale this warp's O columns (warp-uniform: tcgen05.ld / st are .sync.aligned)
       if (j > 0 && move) {
         mbar_wait(&p_empty[(j - 1) & 1], ((j - 1) >> 1) & 1);  // P_{j-1} V_{j-1} retired
         tc_fence_after();
+        uint32_t v[OC / 32][32];
 #pragma unroll
-        for (int c0 = 0; c0 < D / 32; c0 += 2) {  // two 32-column loads in flight
-          uint32_t v[2][32];
-          tmem_ld32(tO + lane_off + c0 * 32, v[0]);
-          tmem_ld32(tO + lane_off + (c0 + 1) * 32, v[1]);
-          tmem_wait_ld();
+        for (int c = 0; c < OC / 32; ++c) tmem_ld32(tO + lane_off + o_off + c * 32, v[c]);
+        tmem_wait_ld();
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
+        for (int c = 0; c < OC / 32; ++c) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[h][i] = __float_as_uint(__uint_as_float(v[h][i]) * alpha);
-            tmem_st32(tO + lane_off + (c0 + h) * 32, v[h]);
-          }
+          for (int i = 0; i < 32; ++i) v[c][i] = __float_as_uint(__uint_as_float(v[c][i]) * alpha);
+          tmem_st32(tO + lane_off + o_off + c * 32, v[c]);
         }
         tmem_wait_st();
       }
@@ -336,36 +354,41 @@ __global__ void __launch_bounds__(kFThreads, 1) flash_fwd_kernel(const __grid_co
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[j & 1]);
-      if (F.dbg && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0) F.dbg[17 + quad] = 900 + j;
     }
-    // epilogue: O / l -> bf16 row
+    // epilogue: O / l -> bf16 row (this warp's columns)
     mbar_wait(&p_empty[(ntiles - 1) & 1], ((ntiles - 1) >> 1) & 1);
     tc_fence_after();
+    if (kH == 2) {  // full row sum = the two halves' sums
+      float* xc = sX + (ntiles & 1) * (2 * kQT);  // the parity the last tile did not use
+      xc[half * kQT + r] = l;
+      named_barrier_sync(1 + quad, 64);
+      l += xc[(half ^ 1) * kQT + r];
+    }
     const int64_t q = q0 + r;
     const float inv = l > 0.f ? 1.f / l : 0.f;
     if (!F.last) {  // carry out: unnormalised O (fp32) and (m, l) for the next ring block
 #pragma unroll 1
-      for (int c = 0; c < D / 32; ++c) {
+      for (int c = 0; c < OC / 32; ++c) {
         uint32_t v[32];
-        tmem_ld32(tO + lane_off + c * 32, v);
+        tmem_ld32(tO + lane_off + o_off + c * 32, v);
         tmem_wait_ld();
         if (q < F.s) {
-          float4* dst = reinterpret_cast<float4*>(F.acc + (row_base + q) * D + c * 32);
+          float4* dst = reinterpret_cast<float4*>(F.acc + (row_base + q) * D + o_off + c * 32);
 #pragma unroll
           for (int i = 0; i < 8; ++i)
             dst[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
                                  __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
         }
       }
-      if (q < F.s) *reinterpret_cast<float2*>(F.ml + 2 * (row_base + q)) = make_float2(m, l);
+      if (q < F.s && half == 0) *reinterpret_cast<float2*>(F.ml + 2 * (row_base + q)) = make_float2(m, l);
     }
 #pragma unroll 1
-    for (int c = 0; c < (F.last ? D / 32 : 0); ++c) {
+    for (int c = 0; c < (F.last ? OC / 32 : 0); ++c) {
       uint32_t v[32];
-      tmem_ld32(tO + lane_off + c * 32, v);
+      tmem_ld32(tO + lane_off + o_off + c * 32, v);
       tmem_wait_ld();
       if (q < F.s) {
-        __nv_bfloat16* dst = F.out + (row_base + q) * D + c * 32;
+        __nv_bfloat16* dst = F.out + (row_base + q) * D + o_off + c * 32;
 #pragma unroll
         for (int i = 0; i < 32; i += 8) {
           uint4 u;
@@ -420,7 +443,7 @@ tp_status launch(const FParams& F, cudaStream_t s) {
   static std::once_flag once;
   std::call_once(once, [&] { cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::Smem); });
   dim3 grid(static_cast<unsigned>((F.s + kQT - 1) / kQT), static_cast<unsigned>(F.problems));
-  k<<<grid, kFThreads, C::Smem, s>>>(F);
+  k<<<grid, f_threads<D>(), C::Smem, s>>>(F);
   count_launch();
   TP_CUDA(cudaGetLastError());
   return TP_OK;
