@@ -364,11 +364,29 @@ def run_ours(a):
                 "peak_source": src + (" bf16_tflops_sustained (long step)" if long_step
                                       else " bf16_tflops (burst)"),
                 "traffic": traffic_of(a.workload, world), "traffic_unit": "bytes/launch (ncu)",
-                "alg_bytes_per_launch": alg_bytes_per_gemm(M, layers, world, mode),
+                "alg_bytes_per_gemm": alg_bytes_per_gemm(M, layers, world, mode),
+                "alg_bytes_per_step": (sum(2 * (M * K + K * N + M * N) * 3 for K, N in layers)
+                                       if world == 1 else None),
                 "launches_timed": gemm_n,
                 "gemm_share_of_step": round(gemm_ms / a.steps / ms, 3) if ms > 0 else None,
                 "timing": "per-GEMM CUDA events on the launching stream, recorded inside the "
                           "step graph (external event nodes), K instrumented replays"}
+        # which roof binds the GEMM family: algorithmic flops at the tensor peak vs algorithmic
+        # operand + output bytes at the measured HBM bandwidth (p = 1; e.g. C3's 64-row GEMMs
+        # stream a 512 MB weight per launch and are HBM-bound)
+        step_b = roof["alg_bytes_per_step"]
+        hbm = pk.get("hbm_gbs")
+        if ach and step_b and hbm and gemm_n:
+            t_tensor = gemm_flops / (peak * 1e12)
+            t_hbm = step_b * a.steps / (hbm * 1e9)
+            if t_hbm > t_tensor:
+                gbs = step_b * a.steps / (gemm_ms * 1e-3) / 1e9
+                roof.update({"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s",
+                             "frac": round(gbs / hbm, 4), "peak_source": src + " hbm_gbs",
+                             "tensor_achieved_tflops": round(ach, 2),
+                             "tensor_frac": round(ach / peak, 4)})
+            roof["roof_times_us_per_step"] = {"tensor": round(t_tensor / a.steps * 1e6, 1),
+                                              "hbm": round(t_hbm / a.steps * 1e6, 1)}
     else:
         peak = 148 * 128 * 2 * 1.965  # fp32 FFMA: SMs x lanes x 2 flop x GHz (GFLOP/s->TFLOP/s /1e3)
         peak = peak / 1e3
