@@ -522,7 +522,7 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
         const uint64_t b_desc0 = sdesc_sw128(smem_u32(sB), pr.b_mn ? kBK * 128 : 16, 1024);
         {
           const unsigned long long t0 = clock64();
-          mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
+          mbar_wait(&tempty[acc], acc_phase ^ 1);
           t_temp += clock64() - t0;
         }
         __syncwarp();
@@ -682,7 +682,7 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(&tempty[acc], lead);
+        if (lane == 0) mbar_arrive_remote(&tempty[acc], lead);
       } else if (pr.splits == 1) {
         if (pr.out_bf16) {
 #pragma unroll 1
@@ -701,7 +701,7 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(&tempty[acc], lead);
+        if (lane == 0) mbar_arrive_remote(&tempty[acc], lead);
       } else if (pr.owner_wait && t.split == 0) {
         // ---- split-K, owner: every split is co-resident (one unit per cluster), so split 0
         // keeps its accumulator in TMEM, waits for the other splits' partials and adds them
@@ -738,7 +738,7 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(&tempty[acc], lead);
+        if (lane == 0) mbar_arrive_remote(&tempty[acc], lead);
       } else {
         // ---- split-K: publish this split's fp32 partial; with owner_wait split 0 adds it,
         // otherwise the last split to arrive reduces all partials ----
@@ -763,7 +763,7 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(&tempty[acc], lead);  // TMEM free for the next unit
+        if (lane == 0) mbar_arrive_remote(&tempty[acc], lead);  // TMEM free for the next unit
         __threadfence();
         named_barrier_sync(1, kEpiThreads);
         if (pr.owner_wait) {

@@ -82,6 +82,14 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t rank
                    mapa(smem_u32(bar), rank))
                : "memory");
 }
+// arrive on the barrier at the same offset in CTA `rank`, default semantics (release at CTA
+// scope), as CUTLASS's ClusterBarrier::arrive(cta_id): enough to hand TMEM back between the
+// epilogue warps and the MMA issuer (tcgen05 fences around the sync), without the GPU-scope
+// MEMBAR + ERRBAR the .release.cluster form compiles to
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t rank) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(mapa(smem_u32(bar), rank))
+               : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
