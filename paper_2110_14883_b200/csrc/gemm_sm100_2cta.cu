@@ -46,11 +46,12 @@ constexpr int kBM = 128;  // A rows per CTA (pair tile: 256 rows)
 constexpr int kBK = 64;
 constexpr int kABytes = kBM * kBK * 2;
 constexpr int kOutBytes = 32 * 128;  // per epilogue warp and buffer: 32 rows x 128 B staging
-// Epilogue warps: 4 (one per TMEM lane quadrant) or 8 (two per quadrant, each half of the
-// columns). 8 measured no faster on short-K tiles and costs a ring stage (r01_gemm_v3_summary).
-constexpr int kEpiWarps = 4;
-constexpr int kEpiThreads = kEpiWarps * 32;
-constexpr int kThreads = 64 + kEpiThreads;  // warp 0 TMA, warp 1 MMA, warps 2.. epilogue
+// Epilogue warps EW: 4 (one per TMEM lane quadrant) or 8 (two per quadrant, each half of the
+// columns; one ring stage less). 8 wins only where the epilogue is everything (1-2 k-blocks per
+// tile: C3's 16384^2 x 64 dW 132 -> 113 us) and loses elsewhere (C2 891 -> 860 TFLOP/s;
+// profiles/r01_attention_summary.md), so the dispatcher picks it per problem.
+template <int EW>
+constexpr int threads_of() { return 64 + 32 * EW; }  // warp 0 TMA, warp 1 MMA, warps 2.. epilogue
 constexpr int kMaxProbs = 4;
 constexpr int kMaxPanels = 4;  // K-panels per problem (peer shards of a fused SUMMA)
 constexpr int kMaxDPanels = 8;  // D row-panels per problem (fused 1D reduce-scatter slots)
@@ -58,16 +59,16 @@ constexpr int kMaxDPanels = 8;  // D row-panels per problem (fused 1D reduce-sca
 // Pair-tile width BNP (256 or 128): B columns per CTA, ring depth, TMEM, smem. MC 5 (K-split
 // pair cluster) gives one ring stage to the 32 KB DSMEM receive buffer of the split reduction.
 constexpr int kRxBytes = 2 * 32 * kBM * 4;  // MC 5: two [32 cols][128 rows] fp32 chunks
-template <int BNP, int MC = 1>
+template <int BNP, int MC = 1, int EW = 4>
 struct PC {
   static constexpr int BNC = BNP / 2;
-  static constexpr int Stages = kEpiWarps == 8 ? (BNP == 256 ? (MC == 5 ? 4 : 5) : (MC == 5 ? 5 : 6))
+  static constexpr int Stages = EW == 8 ? (BNP == 256 ? (MC == 5 ? 4 : 5) : (MC == 5 ? 5 : 6))
                                                : (BNP == 256 ? (MC == 5 ? 5 : 6) : (MC == 5 ? 6 : 8));
   static constexpr int BBytes = BNC * kBK * 2;
   static constexpr int StageBytes = kABytes + BBytes;
   static constexpr int TmemCols = 2 * BNP;
   static constexpr int Rx = MC == 5 ? kRxBytes : 0;
-  static constexpr int Smem = Stages * StageBytes + 2 * kEpiWarps * kOutBytes + Rx + 1024 + 256;
+  static constexpr int Smem = Stages * StageBytes + 2 * EW * kOutBytes + Rx + 1024 + 256;
   static constexpr int TileElems = 256 * BNP;
 };
 
@@ -321,10 +322,10 @@ __device__ __forceinline__ void add_partials(const float4* base, int splits, int
   }
 }
 
-template <int BNP, int MC>
-__global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThreads, 1)
+template <int BNP, int MC, int EW>
+__global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threads_of<EW>(), 1)
     gemm_tc2_kernel(const __grid_constant__ Group G) {
-  using P = PC<BNP, MC>;
+  using P = PC<BNP, MC, EW>;
   constexpr int NP = pairs_of(MC);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -332,8 +333,8 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
   uint8_t* sA = smem;
   uint8_t* sB = sA + P::Stages * kABytes;
   uint8_t* sOut = sB + P::Stages * P::BBytes;
-  float* rx = reinterpret_cast<float*>(sOut + 2 * kEpiWarps * kOutBytes);  // MC 5: [2][32][128]
-  uint64_t* full = reinterpret_cast<uint64_t*>(sOut + 2 * kEpiWarps * kOutBytes + P::Rx);
+  float* rx = reinterpret_cast<float*>(sOut + 2 * EW * kOutBytes);  // MC 5: [2][32][128]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sOut + 2 * EW * kOutBytes + P::Rx);
   uint64_t* empty = full + P::Stages;
   uint64_t* tfull = empty + P::Stages;
   uint64_t* tempty = tfull + 2;
@@ -381,7 +382,7 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 2 * kEpiWarps);  // epilogue warps x 2 CTAs (the leader's copy is used)
+      mbar_init(&tempty[a], 2 * EW);  // epilogue warps x 2 CTAs (the leader's copy is used)
       mbar_init(&rxf[a], 1);  // MC 5 owner: its own expect_tx arrive + the sender's bulk bytes
       mbar_init(&rxe[a], 4);  // MC 5 sender: the owner's 4 epilogue warps
     }
@@ -586,7 +587,7 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
     // quadrant take the two halves of the tile's columns (`half`) =====
     const int quad = warp & 3;
     const int half = (warp - 2) / 4;
-    constexpr int kHalves = kEpiWarps / 4;
+    constexpr int kHalves = EW / 4;
     constexpr int kSub64 = BNP / 64, kSub32 = BNP / 32;  // column sub-chunks per tile
     const int s64_0 = half * (kSub64 / kHalves), s64_1 = s64_0 + kSub64 / kHalves;
     const int s32_0 = half * (kSub32 / kHalves), s32_1 = s32_0 + kSub32 / kHalves;
@@ -718,7 +719,7 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
           __threadfence();
           *cnt = 0;  // ready for the next launch
         }
-        named_barrier_sync(1, kEpiThreads);
+        named_barrier_sync(1, (EW * 32));
         if (pr.out_bf16) {
 #pragma unroll 1
           for (int sub = s64_0; sub < s64_1; ++sub) {
@@ -765,7 +766,7 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
         __syncwarp();
         if (lane == 0) mbar_arrive_remote(&tempty[acc], lead);  // TMEM free for the next unit
         __threadfence();
-        named_barrier_sync(1, kEpiThreads);
+        named_barrier_sync(1, (EW * 32));
         if (pr.owner_wait) {
           if (threadIdx.x == 64) atomicAdd(pr.counters + tile * 2 + rank, 1);
         } else if (threadIdx.x == 64) {
@@ -775,9 +776,9 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(kThre
           if (last) *cnt = 0;  // ready for the next launch
           *sflag = last;
         }
-        named_barrier_sync(1, kEpiThreads);
+        named_barrier_sync(1, (EW * 32));
         const int last = pr.owner_wait ? 0 : *sflag;
-        named_barrier_sync(1, kEpiThreads);
+        named_barrier_sync(1, (EW * 32));
         if (last) {
           __threadfence();
           const float4* base =
@@ -874,10 +875,10 @@ int sm_count() {
 
 // Max co-resident clusters of a kernel (clusters of 4 may strand SMs on some GPCs).
 template <typename Kern>
-int max_clusters(Kern kern, int csize, int smem) {
+int max_clusters(Kern kern, int csize, int smem, int threads) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(csize * 64);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = smem;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -996,17 +997,17 @@ tp_status setup_prob(const GemmArgs& g, Prob& pr, int clusters, int split_mode, 
   return TP_OK;
 }
 
-template <int BNP, int MC>
+template <int BNP, int MC, int EW = 4>
 tp_status launch2(const GemmArgs* gs, int n, cudaStream_t s) {
-  using P = PC<BNP, MC>;
-  auto kern = gemm_tc2_kernel<BNP, MC>;
+  using P = PC<BNP, MC, EW>;
+  auto kern = gemm_tc2_kernel<BNP, MC, EW>;
   static int clusters = 0;
   {
     static std::mutex mu;
     std::lock_guard<std::mutex> lk(mu);
     if (!clusters) {
       TP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, P::Smem));
-      clusters = max_clusters(kern, 2 * pairs_of(MC), P::Smem);
+      clusters = max_clusters(kern, 2 * pairs_of(MC), P::Smem, threads_of<EW>());
     }
   }
   Group G;
@@ -1057,7 +1058,7 @@ tp_status launch2(const GemmArgs* gs, int n, cudaStream_t s) {
   for (int i = 0; i < n; ++i)
     G.p[i].owner_wait = (env_owner && G.p[i].splits > 1 && units <= grid / (2 * pairs_of(MC))) ? 1 : 0;
   const int tok = prof_begin(0, s, flops);
-  TP_CUDA(launch_pdl(kern, dim3(grid), dim3(kThreads), P::Smem, s, G));
+  TP_CUDA(launch_pdl(kern, dim3(grid), dim3(threads_of<EW>()), P::Smem, s, G));
   count_launch();
   prof_end(tok, s);
   TP_CUDA(cudaGetLastError());
@@ -1106,6 +1107,13 @@ tp_status gemm_tc2_bf16(const GemmArgs& g, cudaStream_t s) {
     if (mc == 4 && ncols >= 2 && nrows >= 2) return launch2<256, 4>(&g, 1, s);
     if (mc == 2 && ncols >= 2) return launch2<256, 2>(&g, 1, s);
     if (mc == 3 && nrows >= 2) return launch2<256, 3>(&g, 1, s);
+    // epilogue-bound (1-2 k-blocks per tile, e.g. a dW over 64 tokens): 8 epilogue warps
+    static const int env_ew = [] {
+      const char* e = std::getenv("TP_GEMM_EPI_WARPS");
+      return e ? std::atoi(e) : 0;
+    }();
+    const bool ew8 = env_ew ? env_ew == 8 : kblocks <= 2;
+    if (ew8) return launch2<256, 1, 8>(&g, 1, s);
     return launch2<256, 1>(&g, 1, s);
   }
   if (mc == 4 && ncols >= 2 && nrows >= 2) return launch2<128, 4>(&g, 1, s);

@@ -162,6 +162,7 @@ def test_gemm_split_k_is_deterministic(api):
     {"TP_GEMM_KERNEL": "2", "TP_GEMM_MC": "5", "TP_GEMM_BN": "128"},
     {"TP_GEMM_KERNEL": "2", "TP_GEMM_BN": "128"},              # 256x128 pair tiles
     {"TP_GEMM_KERNEL": "2", "TP_GEMM_BN": "256", "TP_GEMM_SPLITK": "0"},
+    {"TP_GEMM_KERNEL": "2", "TP_GEMM_BN": "256", "TP_GEMM_EPI_WARPS": "8"},  # 8 epilogue warps
 ], ids=lambda e: "-".join(f"{k[8:]}{v}" for k, v in e.items()))
 def test_gemm_kernel_variants_forced(api, env):
     """Every kernel variant the dispatcher can pick, forced for every shape of the GEMM parity
@@ -172,10 +173,22 @@ def test_gemm_kernel_variants_forced(api, env):
     env = dict(os.environ, **env)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "tests/test_gpu_kernels.py",
-                        "-k", "bf16_vs_oracle or exact_integer or wide_tile or epilogue or pair_kernel"
+                        "-k", "bf16_vs_oracle or exact_integer or wide_tile or epilogue or pair_kernel or short_k"
                               " or deterministic"],
                        cwd=root, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("ta,tb", [(0, 0), (1, 0), (0, 1)])
+@pytest.mark.parametrize("M,N,K", [(2560, 2048, 64), (2600, 2056, 120)])
+def test_gemm_short_k_eight_epilogue_warps(api, ta, tb, M, N, K):
+    """<= 2 k-blocks per 256x256 tile and enough tiles: the dispatcher's 8-epilogue-warp pair
+    kernel (ragged tails included)."""
+    got, ref = _gemm_case(api, ta, tb, M, N, K, "bf16", "fp32", seed=17)
+    assert rel_fro(got, ref) <= 2e-5
+    got, ref = _gemm_case(api, ta, tb, M, N, K, "bf16", "bf16", seed=17, alpha=0.5, with_c=True,
+                          with_bias=True)
+    assert rel_fro(got, ref) <= 1e-2
 
 
 def test_gemm_bf16_wide_tile_path(api):
