@@ -74,6 +74,23 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
+// 2^x on the FMA pipe (Cody-Waite split x = n + f, |f| <= 1/2, degree-4 Taylor of 2^f, relative
+// error < 5e-5, below bf16's 4e-3): takes part of the exponentials off the XU pipe (16 / clk / SM)
+// that bounds the softmax. x >= -126 (masked keys give 2^-126 ~ 1e-38, not 0: negligible).
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -126.f);
+  const float t = x + 12582912.f;  // 1.5 * 2^23: the integer part lands in the low mantissa bits
+  const float f = x - (t - 12582912.f);
+  float p = fmaf(f, 0.0096181291f, 0.0555041087f);
+  p = fmaf(p, f, 0.2402265070f);
+  p = fmaf(p, f, 0.6931471806f);
+  p = fmaf(p, f, 1.0f);
+  return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
+}
+#ifndef TP_FLASH_POLY_EVERY
+#define TP_FLASH_POLY_EVERY 0  // one exp pair in every N on the FMA pipe; 0 = none (measured: no gain, the softmax is latency-bound, profiles/r01_exp49_poly_exp.log)
+#endif
+
 template <int D>
 __global__ void __launch_bounds__(f_threads<D>(), 1) flash_fwd_kernel(const __grid_constant__ FParams F) {
   using C = FC<D>;
@@ -296,8 +313,12 @@ __global__ void __launch_bounds__(f_threads<D>(), 1) flash_fwd_kernel(const __gr
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const float p0 = ex2_approx(fmaf(sval(c, 2 * i), F.scale_log2, neg_m));
-          const float p1 = ex2_approx(fmaf(sval(c, 2 * i + 1), F.scale_log2, neg_m));
+          const bool poly = TP_FLASH_POLY_EVERY > 0 && (i % (TP_FLASH_POLY_EVERY > 0 ? TP_FLASH_POLY_EVERY : 1)) ==
+                                                          (TP_FLASH_POLY_EVERY > 0 ? TP_FLASH_POLY_EVERY - 1 : 0);
+          const float x0 = fmaf(sval(c, 2 * i), F.scale_log2, neg_m);
+          const float x1 = fmaf(sval(c, 2 * i + 1), F.scale_log2, neg_m);
+          const float p0 = poly ? ex2_poly(x0) : ex2_approx(x0);
+          const float p1 = poly ? ex2_poly(x1) : ex2_approx(x1);
           rsp[i & 7] += p0 + p1;
           __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
           pk[i] = *reinterpret_cast<uint32_t*>(&h);
