@@ -40,6 +40,13 @@ constexpr int f_threads() { return 64 + 32 * soft_warps<D>(); }
 constexpr int kQT = 128;   // query rows per CTA
 constexpr int kKT = 128;   // keys per tile
 constexpr int kKvStages = 2;
+// S_j = Q K_j^T buffers in TMEM (2; 3 measured equal: profiles/r01_exp50_sbuf.log). Three let S run two tiles ahead of P V (S_{j+2}
+// is queued right after P_{j-1} V_{j-1}), so the softmax never waits for its scores; with O
+// that is 3 x 128 + D <= 512 columns for D <= 128.
+#ifndef TP_FLASH_SBUF
+#define TP_FLASH_SBUF 2
+#endif
+constexpr int kSBuf = TP_FLASH_SBUF;
 
 template <int D>
 struct FC {
@@ -109,8 +116,8 @@ __global__ void __launch_bounds__(f_threads<D>(), 1) flash_fwd_kernel(const __gr
   uint64_t* v_full = k_empty + kKvStages;
   uint64_t* v_empty = v_full + kKvStages;
   uint64_t* s_full = v_empty + kKvStages;
-  uint64_t* s_empty = s_full + 2;
-  uint64_t* p_full = s_empty + 2;   // [2] P_j in buffer j % 2 written (and O rescaled)
+  uint64_t* s_empty = s_full + kSBuf;
+  uint64_t* p_full = s_empty + kSBuf;   // [2] P_j in buffer j % 2 written (and O rescaled)
   uint64_t* p_empty = p_full + 2;   // [2] P_j V_j retired: P buffer j % 2 free, O up to date
   uint32_t* tslot = reinterpret_cast<uint32_t*>(p_empty + 2);
 
@@ -131,7 +138,7 @@ __global__ void __launch_bounds__(f_threads<D>(), 1) flash_fwd_kernel(const __gr
       mbar_init(&v_full[i], 1);
       mbar_init(&v_empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kSBuf; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&s_empty[i], soft_warps<D>());
     }
@@ -146,8 +153,8 @@ __global__ void __launch_bounds__(f_threads<D>(), 1) flash_fwd_kernel(const __gr
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
-  const uint32_t tS[2] = {tmem, tmem + kKT};
-  const uint32_t tO = tmem + 2 * kKT;
+  auto tS = [&](int b) { return tmem + static_cast<uint32_t>(b * kKT); };
+  const uint32_t tO = tmem + kSBuf * kKT;
 
   if (warp == 0) {
     if (elect_one()) {
@@ -175,10 +182,10 @@ __global__ void __launch_bounds__(f_threads<D>(), 1) flash_fwd_kernel(const __gr
             tma_load_2d(&F.tmV, &v_full[st], vd + (kb * (D / 64) + c) * 64 * 128, c * 64, key0 + kb * 64);
       };
       // K runs one tile ahead of V (S_{j+1} is issued before P_j V_j)
-      load_k(0);
+      for (int j = 0; j < kSBuf - 1 && j < ntiles; ++j) load_k(j);
       for (int j = 0; j < ntiles; ++j) {
         if (F.dbg && blockIdx.x == 0 && blockIdx.y == 0) F.dbg[0] = 100 + j;
-        if (j + 1 < ntiles) load_k(j + 1);
+        if (j + kSBuf - 1 < ntiles) load_k(j + kSBuf - 1);
         load_v(j);
       }
     }
@@ -193,8 +200,8 @@ __global__ void __launch_bounds__(f_threads<D>(), 1) flash_fwd_kernel(const __gr
         const int st = j % kKvStages;
         mbar_wait(&k_full[st], (j / kKvStages) & 1);
         if (F.dbg && blockIdx.x == 0 && blockIdx.y == 0) F.dbg[1] = 200 + j;
-        const int b = j & 1;
-        mbar_wait(&s_empty[b], ((j >> 1) & 1) ^ 1);  // softmax done with S_{j-2}
+        const int b = j % kSBuf;
+        mbar_wait(&s_empty[b], ((j / kSBuf) & 1) ^ 1);  // softmax done with S_{j-kSBuf}
         if (F.dbg && blockIdx.x == 0 && blockIdx.y == 0) F.dbg[2] = 300 + j;
         tc_fence_after();
         const uint64_t kdsc = sdesc_sw128(smem_u32(sKV + st * C::StageBytes), 16, 1024);
@@ -203,15 +210,15 @@ __global__ void __launch_bounds__(f_threads<D>(), 1) flash_fwd_kernel(const __gr
           // K step of 16 inside a 64-wide box: +32 B; next box: +128 rows x 128 B
           const uint32_t off = (k / 4) * (kQT * 128 / 16) + (k % 4) * 2;
           const uint32_t offk = (k / 4) * (kKT * 128 / 16) + (k % 4) * 2;
-          umma_bf16_cg1(tS[b], qd + off, kdsc + offk, idS, k > 0 ? 1u : 0u);
+          umma_bf16_cg1(tS(b), qd + off, kdsc + offk, idS, k > 0 ? 1u : 0u);
         }
         umma_commit_cg1(&s_full[b]);
         umma_commit_cg1(&k_empty[st]);  // K_j read
       };
       mbar_wait(q_full, 0);
-      issue_s(0);
+      for (int j = 0; j < kSBuf - 1 && j < ntiles; ++j) issue_s(j);
       for (int j = 0; j < ntiles; ++j) {
-        if (j + 1 < ntiles) issue_s(j + 1);
+        if (j + kSBuf - 1 < ntiles) issue_s(j + kSBuf - 1);
         if (F.dbg && blockIdx.x == 0 && blockIdx.y == 0) F.dbg[3] = 400 + j;
         const int pb = j & 1;
         mbar_wait(&p_full[pb], (j >> 1) & 1);  // P_j in smem, O rescaled
@@ -254,14 +261,14 @@ __global__ void __launch_bounds__(f_threads<D>(), 1) flash_fwd_kernel(const __gr
       l = half == 0 ? c.y : 0.f;
     }
     for (int j = 0; j < ntiles; ++j) {
-      const int b = j & 1;
-      mbar_wait(&s_full[b], (j >> 1) & 1);
+      const int b = j % kSBuf;
+      mbar_wait(&s_full[b], (j / kSBuf) & 1);
       tc_fence_after();
       const int64_t valid = F.s - int64_t(j) * kKT - half * KW;  // this warp's keys in range
       // this warp's part of the S row into registers once: all loads in flight, one wait
       uint32_t sv[KW / 32][32];
 #pragma unroll
-      for (int c = 0; c < KW / 32; ++c) tmem_ld32(tS[b] + lane_off + s_off + c * 32, sv[c]);
+      for (int c = 0; c < KW / 32; ++c) tmem_ld32(tS(b) + lane_off + s_off + c * 32, sv[c]);
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
