@@ -49,7 +49,7 @@ def oracle_chain(X, Ws, dY):
     return acts[-1], d, dWs
 
 
-def run_chain(api, mode, p, d, M, layers, seed=42):
+def run_chain(api, mode, p, d, M, layers, seed=42, flags=0):
     from paper_2110_14883_b200.mlp import TPMLP
     transport = api.TP_TRANSPORT_LOCAL if p > 1 else api.TP_TRANSPORT_NONE
     uid = api.tp_get_unique_id(transport)
@@ -59,7 +59,7 @@ def run_chain(api, mode, p, d, M, layers, seed=42):
         s = torch.cuda.Stream()
         try:
             with torch.cuda.stream(s):
-                m = TPMLP(g, M, layers, seed=seed)
+                m = TPMLP(g, M, layers, seed=seed, flags=flags)
                 m.step()
             s.synchronize()
             return {"Y": to_np(m.Y[-1]), "dX": to_np(m.dX[0]), "dW": [to_np(w) for w in m.dW]}
@@ -122,3 +122,30 @@ def test_c3_literal_3d_8ranks_full(api):
     assert rel_fro(gather_full(g, spec, {r: per[r]["Y"] for r in range(8)}, "Y"), Yr) <= 1e-2
     assert rel_fro(gather_full(g, spec, {r: per[r]["dX"] for r in range(8)}, "X"), dXr) <= 1e-2
     assert rel_fro(gather_full(g, spec, {r: per[r]["dW"][0] for r in range(8)}, "W"), dWr[0]) <= 1e-2
+
+
+@pytest.mark.parametrize("variant", ["fused-2d", "depth-sharded-2.5d", "fused-depth-sharded-2.5d",
+                                     "solomonik-2.5d"])
+def test_c2_chain_full_variants(api, variant):
+    """configs[1] at full size through the variant schedules: the fused peer-panel 2D (q=2 on 4
+    ranks), the 2.5D with depth-sharded weights (collective and fused requested; C2's 128-row
+    plane blocks take the collective path), and Solomonik's 2.5D (q=2, d=2 on 8 ranks)."""
+    from oracle import solomonik as so
+    M, layers = 512, [(4096, 4096), (4096, 4096)]
+    mode, p, d, flags = {"fused-2d": ("2d", 4, 1, api.TP_FLAG_PEER_FUSED),
+                         "depth-sharded-2.5d": ("2.5d", 8, 2, api.TP_FLAG_W25_DEPTH_SHARDED),
+                         "fused-depth-sharded-2.5d": ("2.5d", 8, 2, api.TP_FLAG_W25_DEPTH_SHARDED
+                                                      | api.TP_FLAG_PEER_FUSED),
+                         "solomonik-2.5d": ("2.5d", 8, 2, api.TP_FLAG_SOLOMONIK)}[variant]
+    per = run_chain(api, mode, p, d, M, layers, flags=flags)
+    X, Ws, dY = chain_inputs(42, M, layers)
+    Yr, dXr, dWr = oracle_chain(X, Ws, dY)
+    g = build_grid(mode, p, d)
+    sharded = bool(flags & api.TP_FLAG_W25_DEPTH_SHARDED)
+    specs = [LayerSpec(M, K, N, w_depth_sharded=sharded) for K, N in layers]
+    gf = (lambda sp, sh, t: so.gather_full(g, sp, sh, t)) if flags & api.TP_FLAG_SOLOMONIK else \
+        (lambda sp, sh, t: gather_full(g, sp, sh, t))
+    assert rel_fro(gf(specs[-1], {r: per[r]["Y"] for r in range(p)}, "Y"), Yr) <= 1e-2
+    assert rel_fro(gf(specs[0], {r: per[r]["dX"] for r in range(p)}, "X"), dXr) <= 1e-2
+    for i in range(len(layers)):
+        assert rel_fro(gf(specs[i], {r: per[r]["dW"][i] for r in range(p)}, "W"), dWr[i]) <= 1e-2
