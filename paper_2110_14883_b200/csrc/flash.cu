@@ -33,8 +33,15 @@ using namespace ptx;
 // shared memory, the row sums are combined at the end). 8 for d = 64, whose tiles are bound
 // by the exp2 stream (the XU pipe) rather than the tensor core; d = 128 has no smem left for
 // the exchange and is balanced.
+#ifndef TP_FLASH_W128
+#define TP_FLASH_W128 0  // d = 128 with eight softmax warps + one P buffer: measured slower (profiles/r01_exp51_w128.log)
+#endif
 template <int D>
-constexpr int soft_warps() { return D == 64 ? 8 : 4; }
+constexpr int soft_warps() { return TP_FLASH_W128 && D == 128 ? 8 : (D == 64 ? 8 : 4); }
+// P buffers in shared memory: two (the softmax runs a tile ahead of P V), one for d = 128 with
+// eight softmax warps (no shared memory left for a second buffer and the max exchange)
+template <int D>
+constexpr int p_bufs() { return D == 128 && soft_warps<D>() == 8 ? 1 : 2; }
 template <int D>
 constexpr int f_threads() { return 64 + 32 * soft_warps<D>(); }
 constexpr int kQT = 128;   // query rows per CTA
@@ -56,7 +63,7 @@ struct FC {
   static constexpr int PBytes = kQT * kKT * 2;         // 2 key blocks of [128 rows][128 B]
   static constexpr int StageBytes = KBytes + VBytes;
   static constexpr int XBytes = soft_warps<D>() == 8 ? 2 * 2 * kQT * 4 : 0;  // [tile parity][half][row]
-  static constexpr int Smem = QBytes + kKvStages * StageBytes + 2 * PBytes + XBytes + 1024 + 256;
+  static constexpr int Smem = QBytes + kKvStages * StageBytes + p_bufs<D>() * PBytes + XBytes + 1024 + 256;
   static constexpr int TmemCols = 2 * kKT + (D < 32 ? 32 : D);  // S[2] + O
 };
 
@@ -106,8 +113,9 @@ __global__ void __launch_bounds__(f_threads<D>(), 1) flash_fwd_kernel(const __gr
   uint8_t* sQ = smem;
   uint8_t* sKV = sQ + C::QBytes;
   uint8_t* sP = sKV + kKvStages * C::StageBytes;
-  float* sX = reinterpret_cast<float*>(sP + 2 * C::PBytes);  // P double-buffered; max exchange
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * C::PBytes + C::XBytes);
+  constexpr int NP = p_bufs<D>();
+  float* sX = reinterpret_cast<float*>(sP + NP * C::PBytes);  // P buffers; max exchange
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + NP * C::PBytes + C::XBytes);
   uint64_t* q_full = bars;
   // K and V have their own barriers: K_j's slot frees when S_j retires (early), V_j's when
   // P_j V_j retires, so K_{j+2}'s load is in flight long before S_{j+2} is issued
@@ -220,8 +228,8 @@ __global__ void __launch_bounds__(f_threads<D>(), 1) flash_fwd_kernel(const __gr
       for (int j = 0; j < ntiles; ++j) {
         if (j + kSBuf - 1 < ntiles) issue_s(j + kSBuf - 1);
         if (F.dbg && blockIdx.x == 0 && blockIdx.y == 0) F.dbg[3] = 400 + j;
-        const int pb = j & 1;
-        mbar_wait(&p_full[pb], (j >> 1) & 1);  // P_j in smem, O rescaled
+        const int pb = j % NP;
+        mbar_wait(&p_full[pb], (j / NP) & 1);  // P_j in smem, O rescaled
         if (F.dbg && blockIdx.x == 0 && blockIdx.y == 0) F.dbg[4] = 500 + j;
         tc_fence_after();
         const int st = j % kKvStages;
@@ -306,8 +314,8 @@ __global__ void __launch_bounds__(f_threads<D>(), 1) flash_fwd_kernel(const __gr
       const bool move = (j == 0 && !F.carry_in) || __any_sync(0xffffffffu, m_cand > m + 8.f);
       const float m_new = move ? m_cand : m;
       const float alpha = exp2f(m - m_new);  // 1 when m stays; 0 on the first tile (m = -inf)
-      // P buffer j % 2 was last read by P_{j-2} V_{j-2}
-      if (j >= 2) mbar_wait(&p_empty[j & 1], ((j - 2) >> 1) & 1);
+      // P buffer j % NP was last read by P_{j-NP} V_{j-NP}
+      if (j >= NP) mbar_wait(&p_empty[j % NP], ((j - NP) / NP) & 1);
       tc_fence_after();
       // p = exp2(s scale log2e - m_new) (one FFMA + MUFU.EX2 each) -> bf16 P row (swizzled
       // K-major), row sum in 8 independent partial sums
@@ -332,7 +340,7 @@ __global__ void __launch_bounds__(f_threads<D>(), 1) flash_fwd_kernel(const __gr
         }
         // 32 keys = 64 B = 4 swizzled 16-byte chunks of the row in key block (key / 64)
         const int key0 = half * KW + c * 32;
-        uint8_t* rowp = sP + (j & 1) * C::PBytes + (key0 / 64) * (kQT * 128) + r * 128;
+        uint8_t* rowp = sP + (j % NP) * C::PBytes + (key0 / 64) * (kQT * 128) + r * 128;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int chunk = ((key0 % 64) / 32) * 4 + q;
@@ -363,7 +371,7 @@ __global__ void __launch_bounds__(f_threads<D>(), 1) flash_fwd_kernel(const __gr
       }
       // rescale this warp's O columns (warp-uniform: tcgen05.ld / st are .sync.aligned)
       if (j > 0 && move) {
-        mbar_wait(&p_empty[(j - 1) & 1], ((j - 1) >> 1) & 1);  // P_{j-1} V_{j-1} retired
+        mbar_wait(&p_empty[(j - 1) % NP], ((j - 1) / NP) & 1);  // P_{j-1} V_{j-1} retired
         tc_fence_after();
         uint32_t v[OC / 32][32];
 #pragma unroll
@@ -381,10 +389,10 @@ __global__ void __launch_bounds__(f_threads<D>(), 1) flash_fwd_kernel(const __gr
       fence_proxy_async_smem();  // P visible to the MMA (async proxy)
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[j & 1]);
+      if (lane == 0) mbar_arrive(&p_full[j % NP]);
     }
     // epilogue: O / l -> bf16 row (this warp's columns)
-    mbar_wait(&p_empty[(ntiles - 1) & 1], ((ntiles - 1) >> 1) & 1);
+    mbar_wait(&p_empty[(ntiles - 1) % NP], ((ntiles - 1) / NP) & 1);
     tc_fence_after();
     if (kH == 2) {  // full row sum = the two halves' sums
       float* xc = sX + (ntiles & 1) * (2 * kQT);  // the parity the last tile did not use
