@@ -300,10 +300,10 @@ __global__ void __launch_bounds__(f_threads<D>(), 1) flash_fwd_kernel(const __gr
       float mx = fmaxf(fmaxf(fmaxf(mxs[0], mxs[1]), fmaxf(mxs[2], mxs[3])),
                        fmaxf(fmaxf(mxs[4], mxs[5]), fmaxf(mxs[6], mxs[7])));
       if (kH == 2) {  // the other half's max of the same row (double-buffered by tile parity)
-        float* xc = sX + (j & 1) * (2 * kQT);
-        xc[half * kQT + r] = mx;
+        const uint32_t xc = smem_u32(sX) + (j & 1) * (2 * kQT * 4);
+        sts32(xc + (half * kQT + r) * 4, mx);
         named_barrier_sync(1 + quad, 64);
-        mx = fmaxf(mx, xc[(half ^ 1) * kQT + r]);
+        mx = fmaxf(mx, lds32(xc + ((half ^ 1) * kQT + r) * 4));
       }
       // Lazy rescale: the reference max m moves only when some row of the warp would exceed it
       // by more than 2^8 (p <= 256 is exact enough in bf16 / fp32), so most tiles leave O alone
@@ -340,12 +340,11 @@ __global__ void __launch_bounds__(f_threads<D>(), 1) flash_fwd_kernel(const __gr
         }
         // 32 keys = 64 B = 4 swizzled 16-byte chunks of the row in key block (key / 64)
         const int key0 = half * KW + c * 32;
-        uint8_t* rowp = sP + (j % NP) * C::PBytes + (key0 / 64) * (kQT * 128) + r * 128;
+        const uint32_t rowp = smem_u32(sP) + (j % NP) * C::PBytes + (key0 / 64) * (kQT * 128) + r * 128;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int chunk = ((key0 % 64) / 32) * 4 + q;
-          *reinterpret_cast<uint4*>(rowp + ((chunk ^ (r & 7)) << 4)) =
-              make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+          sts128(rowp + ((chunk ^ (r & 7)) << 4), pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
         }
       }
       const float rs = ((rsp[0] + rsp[1]) + (rsp[2] + rsp[3])) + ((rsp[4] + rsp[5]) + (rsp[6] + rsp[7]));
@@ -395,10 +394,10 @@ __global__ void __launch_bounds__(f_threads<D>(), 1) flash_fwd_kernel(const __gr
     mbar_wait(&p_empty[(ntiles - 1) % NP], ((ntiles - 1) / NP) & 1);
     tc_fence_after();
     if (kH == 2) {  // full row sum = the two halves' sums
-      float* xc = sX + (ntiles & 1) * (2 * kQT);  // the parity the last tile did not use
-      xc[half * kQT + r] = l;
+      const uint32_t xc = smem_u32(sX) + (ntiles & 1) * (2 * kQT * 4);  // parity the last tile did not use
+      sts32(xc + (half * kQT + r) * 4, l);
       named_barrier_sync(1 + quad, 64);
-      l += xc[(half ^ 1) * kQT + r];
+      l += lds32(xc + ((half ^ 1) * kQT + r) * 4);
     }
     const int64_t q = q0 + r;
     const float inv = l > 0.f ? 1.f / l : 0.f;

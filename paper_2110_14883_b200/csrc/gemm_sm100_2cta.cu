@@ -201,21 +201,23 @@ __device__ __forceinline__ void finish_vals(const Prob& ep, float (&v)[CW], int6
 // Stage one 32-row x 128-byte box (row = lane) with the 128-byte swizzle the TMA store expects.
 template <int CW>
 __device__ __forceinline__ void stage_row(uint8_t* stg, int lane, const float (&v)[CW]) {
-  uint8_t* rowp = stg + lane * 128;
+  const uint32_t rowp = smem_u32(stg) + lane * 128;
   if (CW == 64) {  // bf16
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      uint4 u;
-      __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+      uint32_t u[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) h[k] = __floats2bfloat162_rn(v[8 * j + 2 * k], v[8 * j + 2 * k + 1]);
-      *reinterpret_cast<uint4*>(rowp + ((j ^ (lane & 7)) << 4)) = u;
+      for (int k = 0; k < 4; ++k) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(v[8 * j + 2 * k], v[8 * j + 2 * k + 1]);
+        u[k] = *reinterpret_cast<uint32_t*>(&h);
+      }
+      sts128(rowp + ((j ^ (lane & 7)) << 4), u[0], u[1], u[2], u[3]);
     }
   } else {  // fp32, CW == 32
 #pragma unroll
     for (int j = 0; j < 8; ++j)
-      *reinterpret_cast<float4*>(rowp + ((j ^ (lane & 7)) << 4)) =
-          make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+      sts128(rowp + ((j ^ (lane & 7)) << 4), __float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]),
+             __float_as_uint(v[4 * j + 2]), __float_as_uint(v[4 * j + 3]));
   }
 }
 
