@@ -22,6 +22,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "sm100_ptx.cuh"
@@ -42,7 +43,8 @@ struct Cfg {
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTmemCols = 2 * BN;
   static constexpr int kBarBytes = 256;
-  static constexpr int kSmem = kStages * kStageBytes + 1024 + kBarBytes;
+  static constexpr int kOutBytes = 4 * 2 * 4096;  // epilogue staging: 4 warps x 2 x [32 rows][128 B]
+  static constexpr int kSmem = kStages * kStageBytes + kOutBytes + 1024 + kBarBytes;
 };
 
 struct EpiParams {
@@ -53,6 +55,7 @@ struct EpiParams {
   float alpha;
   int out_bf16;
   int vec_ok;  // D, C rows 16-byte aligned
+  int tma;     // D written through smem staging + TMA bulk tensor stores (tmD)
 };
 
 // ------------------------------------------------------------------------------ PTX helpers
@@ -247,18 +250,51 @@ __device__ __forceinline__ void epilogue_row32(const EpiParams& ep, const uint32
   }
 }
 
+// alpha * (acc + C) + bias for 32 consecutive columns of one row (TMA-store epilogue).
+__device__ __forceinline__ void finish32(const EpiParams& ep, float (&v)[32], int64_t row, int64_t col0,
+                                         int M, int N) {
+  const bool in_row = row < M;
+  const bool full = (col0 + 32 <= N) && ep.vec_ok;
+  if (ep.C && in_row) {
+    if (full) {
+      const float4* c4 = reinterpret_cast<const float4*>(ep.C + row * ep.ldc + col0);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float4 c = c4[i];
+        v[4 * i] += c.x;
+        v[4 * i + 1] += c.y;
+        v[4 * i + 2] += c.z;
+        v[4 * i + 3] += c.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (col0 + i < N) v[i] += ep.C[row * ep.ldc + col0 + i];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] *= ep.alpha;
+  if (ep.bias) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (col0 + i < N) v[i] += bias_at(ep.bias, 0, col0 + i);
+  }
+}
+
 // ------------------------------------------------------------------------------ the kernel
 template <int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const EpiParams ep, int M, int N, int K, int num_m, int num_n) {
+                   const __grid_constant__ CUtensorMap tmD, const EpiParams ep, int M, int N, int K,
+                   int num_m, int num_n) {
   using C = Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::kStages * C::kABytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::kStages * C::kBBytes);
+  uint8_t* sOut = sB + C::kStages * C::kBBytes;  // epilogue staging
+  uint64_t* full = reinterpret_cast<uint64_t*>(sOut + C::kOutBytes);
   uint64_t* empty = full + C::kStages;
   uint64_t* tfull = empty + C::kStages;
   uint64_t* tempty = tfull + 2;
@@ -272,6 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
+    if (ep.tma) tma_prefetch(&tmD);
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -384,6 +421,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     // ===== epilogue warps 2..5: TMEM lane quadrant = warp % 4 =====
     const int quad = warp & 3;
+    int nbox = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
@@ -392,15 +430,71 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mbar_wait(&tfull[acc], acc_phase);  // one poller per warp
       __syncwarp();
       tc_fence_after();
-      const int64_t row = static_cast<int64_t>(mb) * BM + quad * 32 + lane;
+      const int64_t row0 = static_cast<int64_t>(mb) * BM + quad * 32;  // warp's first row
+      const int64_t row = row0 + lane;
+      const uint32_t tq = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
+                          static_cast<uint32_t>(acc * BN);
+      if (ep.tma) {
+        // TMEM -> registers -> alpha / C / bias / cast -> 128-byte-swizzled smem box [32 rows]
+        // [128 B] (explicit st.shared) -> TMA bulk tensor store; two boxes per warp in flight
+        constexpr int kCols = 64;  // bf16: 64 columns per box; fp32: 32 (two boxes per step)
 #pragma unroll 1
-      for (int ch = 0; ch < BN / 32; ++ch) {
-        uint32_t r[32];
-        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
-                               static_cast<uint32_t>(acc * BN + ch * 32);
-        tmem_ld32(taddr, r);
-        const int64_t col0 = static_cast<int64_t>(nb) * BN + ch * 32;
-        if (row < M && col0 < N) epilogue_row32(ep, r, row, col0, N);
+        for (int c64 = 0; c64 < BN / kCols; ++c64) {
+          uint32_t r0[32], r1[32];
+          tmem_ld32(tq + c64 * 64, r0);
+          tmem_ld32(tq + c64 * 64 + 32, r1);
+          float v0[32], v1[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            v0[i] = __uint_as_float(r0[i]);
+            v1[i] = __uint_as_float(r1[i]);
+          }
+          const int64_t col0 = static_cast<int64_t>(nb) * BN + c64 * 64;
+          finish32(ep, v0, row, col0, M, N);
+          finish32(ep, v1, row, col0 + 32, M, N);
+#pragma unroll 1
+          for (int h = 0; h < (ep.out_bf16 ? 1 : 2); ++h) {
+            uint8_t* buf = sOut + (warp - 2) * 2 * 4096 + (nbox & 1) * 4096;
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            __syncwarp();
+            const uint32_t rowp = smem_u32(buf) + lane * 128;
+            if (ep.out_bf16) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const float* src = j < 4 ? v0 + 8 * j : v1 + 8 * (j - 4);
+                uint32_t u[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                  __nv_bfloat162 b2 = __floats2bfloat162_rn(src[2 * k], src[2 * k + 1]);
+                  u[k] = *reinterpret_cast<uint32_t*>(&b2);
+                }
+                ptx::sts128(rowp + ((j ^ (lane & 7)) << 4), u[0], u[1], u[2], u[3]);
+              }
+            } else {
+              const float* src = h == 0 ? v0 : v1;
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                ptx::sts128(rowp + ((j ^ (lane & 7)) << 4), __float_as_uint(src[4 * j]),
+                            __float_as_uint(src[4 * j + 1]), __float_as_uint(src[4 * j + 2]),
+                            __float_as_uint(src[4 * j + 3]));
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+              ptx::tma_store_2d(&tmD, buf, static_cast<int>(col0 + h * 32), static_cast<int>(row0));
+              asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+            ++nbox;
+          }
+        }
+      } else {
+#pragma unroll 1
+        for (int ch = 0; ch < BN / 32; ++ch) {
+          uint32_t r[32];
+          tmem_ld32(tq + ch * 32, r);
+          const int64_t col0 = static_cast<int64_t>(nb) * BN + ch * 32;
+          if (row < M && col0 < N) epilogue_row32(ep, r, row, col0, N);
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -410,6 +504,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         acc_phase ^= 1;
       }
     }
+    // the staging boxes must outlive the bulk stores' shared-memory reads
+    if (ep.tma && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
   }
 
   tc_fence_before();
@@ -439,14 +535,15 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // 2-D bf16 tensor map: `inner` contiguous elements per row, `outer` rows, row stride ld.
 tp_status make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
-                   uint32_t box_inner, uint32_t box_outer) {
+                   uint32_t box_inner, uint32_t box_outer, bool fp32 = false) {
   auto fn = encode_fn();
   if (!fn) return fail(TP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {ld * 2};
+  cuuint64_t strides[1] = {ld * (fp32 ? 4 : 2)};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+  CUresult r = fn(m, fp32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                  const_cast<void*>(base), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
@@ -513,8 +610,18 @@ tp_status launch(const GemmArgs& g, cudaStream_t s) {
   ep.vec_ok = ((reinterpret_cast<uintptr_t>(g.D) % 16) == 0) && ((g.ldd * osz) % 16 == 0) &&
               (!g.C || (((reinterpret_cast<uintptr_t>(g.C) % 16) == 0) && ((g.ldc * 4) % 16 == 0))) &&
               (!g.bias || (reinterpret_cast<uintptr_t>(g.bias) % 16) == 0);
+  // D through TMA stores when its rows are 16-byte aligned (bf16 box 64 x 32, fp32 32 x 32)
+  CUtensorMap td;
+  std::memset(&td, 0, sizeof(td));
+  static const int env_tma = [] {
+    const char* e = std::getenv("TP_GEMM_V1_TMA_STORE");
+    return e ? std::atoi(e) : 1;
+  }();
+  ep.tma = env_tma && (reinterpret_cast<uintptr_t>(g.D) % 16) == 0 && (g.ldd * osz) % 16 == 0;
+  if (ep.tma)
+    TP_TRY(make_map(&td, g.D, g.N, g.M, g.ldd, ep.out_bf16 ? 64 : 32, 32, !ep.out_bf16));
   const int tok = prof_begin(0, s, 2.0 * double(g.M) * double(g.N) * double(g.K));
-  TP_CUDA(launch_pdl(kern, dim3(grid), dim3(kThreads), C::kSmem, s, ta, tb, ep,
+  TP_CUDA(launch_pdl(kern, dim3(grid), dim3(kThreads), C::kSmem, s, ta, tb, td, ep,
                      static_cast<int>(g.M), static_cast<int>(g.N), static_cast<int>(g.K), num_m,
                      num_n));
   count_launch();
