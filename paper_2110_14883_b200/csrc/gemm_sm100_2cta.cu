@@ -50,6 +50,11 @@ constexpr int kOutBytes = 32 * 128;  // per epilogue warp and buffer: 32 rows x 
 // columns; one ring stage less). 8 wins only where the epilogue is everything (1-2 k-blocks per
 // tile: C3's 16384^2 x 64 dW 132 -> 113 us) and loses elsewhere (C2 891 -> 860 TFLOP/s;
 // profiles/r01_attention_summary.md), so the dispatcher picks it per problem.
+// release / acquire at GPU scope for the split-K partial hand-off (each writer fences before the
+// CTA barrier that precedes the counter atomic; the reader fences after observing the count).
+// __threadfence() is fence.sc.gpu, a heavier sequentially consistent fence than this needs.
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
 template <int EW>
 constexpr int threads_of() { return 64 + 32 * EW; }  // warp 0 TMA, warp 1 MMA, warps 2.. epilogue
 constexpr int kMaxProbs = 4;
@@ -718,7 +723,7 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
         if (threadIdx.x == 64) {
           volatile int* cnt = pr.counters + tile * 2 + rank;
           while (*cnt < pr.splits - 1) __nanosleep(64);
-          __threadfence();
+          fence_acq_rel_gpu();
           *cnt = 0;  // ready for the next launch
         }
         named_barrier_sync(1, (EW * 32));
@@ -767,7 +772,7 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_remote(&tempty[acc], lead);  // TMEM free for the next unit
-        __threadfence();
+        fence_acq_rel_gpu();
         named_barrier_sync(1, (EW * 32));
         if (pr.owner_wait) {
           if (threadIdx.x == 64) atomicAdd(pr.counters + tile * 2 + rank, 1);
@@ -782,7 +787,7 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
         const int last = pr.owner_wait ? 0 : *sflag;
         named_barrier_sync(1, (EW * 32));
         if (last) {
-          __threadfence();
+          fence_acq_rel_gpu();
           const float4* base =
               reinterpret_cast<const float4*>(pr.part + static_cast<int64_t>(tile) * pr.splits * P::TileElems +
                                               rank * (kBM * BNP)) +
