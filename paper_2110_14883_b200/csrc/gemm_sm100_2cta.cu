@@ -94,6 +94,7 @@ struct Prob {
   int splits, kb_per_split;
   int c_vec;
   int owner_wait;  // split-K: split 0 keeps its tile in TMEM and waits for the other splits
+  int ptiles;      // pair tiles of this problem (split-K flag layout)
   int npanels, kb_panel, num_kb;  // K = npanels panels of kb_panel 64-wide k-blocks
   int unit0;  // first unit of this problem in the launch's unit space
 };
@@ -710,6 +711,79 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_remote(&tempty[acc], lead);
+      } else if (EW == 4 && pr.owner_wait && pr.splits == 2) {
+        // ---- split-K of two, co-resident, reduce-scatter style: split s keeps the columns
+        // [s BNP/2, (s+1) BNP/2) of the tile. Each split publishes its fp32 partial of the OTHER
+        // half, then adds its sibling's partial of its own half and stores it: both CTAs of the
+        // tile move half the bytes at the same time instead of one writing all and the other
+        // reading all. acc + partial is the same sum as split 0 + split 1 (fp add commutes).
+        const int tile = t.ptile;
+        const int me = t.split, other = 1 - t.split;
+        float4* part_me = reinterpret_cast<float4*>(pr.part + (int64_t(tile) * 2 + me) * P::TileElems +
+                                                    rank * (kBM * BNP)) + quad * 32 + lane;
+        const float4* part_ot = reinterpret_cast<const float4*>(pr.part + (int64_t(tile) * 2 + other) * P::TileElems +
+                                                                rank * (kBM * BNP)) + quad * 32 + lane;
+        int* flags = pr.counters + 2 * pr.ptiles + (tile * 2 + rank) * 2;
+        constexpr int kHalfChunks = BNP / 64;  // 32-column chunks per half tile
+#pragma unroll 1
+        for (int ch = other * kHalfChunks; ch < (other + 1) * kHalfChunks; ++ch) {
+          uint32_t r0[32];
+          tmem_ld32(t_row + ch * 32, r0);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            part_me[(ch * 8 + i) * kBM] =
+                make_float4(__uint_as_float(r0[4 * i]), __uint_as_float(r0[4 * i + 1]),
+                            __uint_as_float(r0[4 * i + 2]), __uint_as_float(r0[4 * i + 3]));
+        }
+        fence_acq_rel_gpu();
+        named_barrier_sync(1, (EW * 32));
+        if (threadIdx.x == 64) {
+          atomicAdd(&flags[me], 1);
+          volatile int* f = &flags[other];
+          while (*f < 1) __nanosleep(32);
+          *f = 0;  // ready for the next launch
+          fence_acq_rel_gpu();
+        }
+        named_barrier_sync(1, (EW * 32));
+        if (pr.out_bf16) {
+#pragma unroll 1
+          for (int sub = me * (BNP / 128); sub < (me + 1) * (BNP / 128); ++sub) {
+            float v[64];
+            tmem_cols<64>(t_row, sub, v);
+            const float4* q = part_ot + (sub * 16) * kBM;
+            float4 x[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) x[i] = __ldcg(q + i * kBM);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              v[4 * i] += x[i].x;
+              v[4 * i + 1] += x[i].y;
+              v[4 * i + 2] += x[i].z;
+              v[4 * i + 3] += x[i].w;
+            }
+            store_box<64>(pr, stg, nbox, lane, v, row, n0 + sub * 64, row0);
+          }
+        } else {
+#pragma unroll 1
+          for (int ch = me * kHalfChunks; ch < (me + 1) * kHalfChunks; ++ch) {
+            float v[32];
+            tmem_cols<32>(t_row, ch, v);
+            const float4* q = part_ot + (ch * 8) * kBM;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float4 x = __ldcg(q + i * kBM);
+              v[4 * i] += x.x;
+              v[4 * i + 1] += x.y;
+              v[4 * i + 2] += x.z;
+              v[4 * i + 3] += x.w;
+            }
+            store_box<32>(pr, stg, nbox, lane, v, row, n0 + ch * 32, row0);
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(&tempty[acc], lead);
       } else if (pr.owner_wait && t.split == 0) {
         // ---- split-K, owner: every split is co-resident (one unit per cluster), so split 0
         // keeps its accumulator in TMEM, waits for the other splits' partials and adds them
@@ -965,9 +1039,9 @@ tp_status setup_prob(const GemmArgs& g, Prob& pr, int clusters, int split_mode, 
   // of the clusters idle (up to 16 ways, every split >= 4 k-blocks). split_mode < 0: a problem
   // of a group whose tiles are far longer than the group's per-cluster share of work
   // (-split_mode = that share in k-blocks): split so no unit exceeds ~ the share.
-  const auto need_of = [&](int sp) {
-    return size_t(ptiles) * sp * P::TileElems * 4 + 256 * ((ptiles * 8 + 255) / 256);
-  };
+  // counters: per pair tile 2 ints (per CTA of the pair) + 4 flags (CTA x split, exchange path)
+  const size_t cbytes = 256 * ((size_t(ptiles) * 24 + 255) / 256);
+  const auto need_of = [&](int sp) { return size_t(ptiles) * sp * P::TileElems * 4 + cbytes; };
   if (split_mode > 0 && env_split) {
     for (int sp = 2; sp <= 16; ++sp)
       if (2 * supers <= clusters && supers * sp <= clusters && num_k >= 4 * sp && need_of(sp) <= ws_left)
@@ -993,13 +1067,13 @@ tp_status setup_prob(const GemmArgs& g, Prob& pr, int clusters, int split_mode, 
   pr.splits = S;
   pr.kb_per_split = S > 1 ? kbps : num_k;
   if (S > 1) {
-    const size_t cbytes = 256 * ((ptiles * 8 + 255) / 256);
     pr.counters = reinterpret_cast<int*>(ws);
+    pr.ptiles = ptiles;
     pr.part = reinterpret_cast<float*>(ws + cbytes);
     const size_t used = cbytes + size_t(ptiles) * S * P::TileElems * 4;
     ws += used;
     ws_left -= used;
-    TP_CUDA(cudaMemsetAsync(pr.counters, 0, ptiles * 2 * sizeof(int), s));
+    TP_CUDA(cudaMemsetAsync(pr.counters, 0, cbytes, s));
   }
   return TP_OK;
 }
