@@ -605,6 +605,7 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
     uint32_t acc_phase = 0;
     uint32_t rx_round = 0;  // MC 5: DSMEM chunk rounds so far (both pairs count alike)
     unsigned long long t_tf = 0, t_begin = clock64();
+    unsigned long long t_pub = 0, t_xwait = 0;  // split exchange: publish / sibling-wait cycles
     for (int u = cid; u < G.total_units; u += ncl) {
       const Unit t = unit_of<MC>(G, u, pair);
       const Prob& pr = G.p[t.prob];
@@ -725,6 +726,7 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
                                                                 rank * (kBM * BNP)) + quad * 32 + lane;
         int* flags = pr.counters + 2 * pr.ptiles + (tile * 2 + rank) * 2;
         constexpr int kHalfChunks = BNP / 64;  // 32-column chunks per half tile
+        const unsigned long long tx0 = clock64();
 #pragma unroll 1
         for (int ch = other * kHalfChunks; ch < (other + 1) * kHalfChunks; ++ch) {
           uint32_t r0[32];
@@ -738,6 +740,8 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
         }
         fence_acq_rel_gpu();
         named_barrier_sync(1, (EW * 32));
+        const unsigned long long tx1 = clock64();
+        t_pub += tx1 - tx0;
         if (threadIdx.x == 64) {
           atomicAdd(&flags[me], 1);
           volatile int* f = &flags[other];
@@ -746,6 +750,7 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
           fence_acq_rel_gpu();
         }
         named_barrier_sync(1, (EW * 32));
+        t_xwait += clock64() - tx1;
         if (pr.out_bf16) {
 #pragma unroll 1
           for (int sub = me * (BNP / 128); sub < (me + 1) * (BNP / 128); ++sub) {
@@ -894,6 +899,7 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
     if (lane == 0) bulk_wait_read0();
     if (G.trace && warp == 2 && lane == 0) {
       G.trace[blockIdx.x * 16 + 5] = t_tf;
+      G.trace[blockIdx.x * 16 + 15] = (t_xwait << 32) | (t_pub & 0xffffffffull);
       G.trace[blockIdx.x * 16 + 6] = clock64() - t_begin;
     }
   }

@@ -67,6 +67,9 @@ def main():
     out["mma_wait_first_kb"] = round(float(first.mean()), 0) if len(first) else 0
     st, ns = t[:, 13], t[:, 14]
     out["steady_cyc_per_kb"] = round(float(st.sum() / max(ns.sum(), 1)), 1)
+    xw = t[:, 15].long()
+    out["epi_split_publish"] = round(float((xw & 0xffffffff).double().mean()), 0)
+    out["epi_split_wait"] = round(float((xw >> 32).double().mean()), 0)
     out["mma_full_wait_frac"] = round(out["mma_wait_full"] / max(out["mma_total"], 1), 3)
     out["prod_wait_frac"] = round(out["prod_wait_empty"] / max(out["prod_total"], 1), 3)
     print(json.dumps(out))
