@@ -46,7 +46,11 @@ template <int D>
 constexpr int f_threads() { return 64 + 32 * soft_warps<D>(); }
 constexpr int kQT = 128;   // query rows per CTA
 constexpr int kKT = 128;   // keys per tile
-constexpr int kKvStages = 2;
+#ifndef TP_FLASH_KV64
+#define TP_FLASH_KV64 2  // K / V ring depth for d = 64 (3 measured equal: profiles/r01_exp58_kv64.log)
+#endif
+template <int D>
+constexpr int kv_stages() { return D == 64 ? TP_FLASH_KV64 : 2; }
 // S_j = Q K_j^T buffers in TMEM (2; 3 measured equal: profiles/r01_exp50_sbuf.log). Three let S run two tiles ahead of P V (S_{j+2}
 // is queued right after P_{j-1} V_{j-1}), so the softmax never waits for its scores; with O
 // that is 3 x 128 + D <= 512 columns for D <= 128.
@@ -63,7 +67,7 @@ struct FC {
   static constexpr int PBytes = kQT * kKT * 2;         // 2 key blocks of [128 rows][128 B]
   static constexpr int StageBytes = KBytes + VBytes;
   static constexpr int XBytes = soft_warps<D>() == 8 ? 2 * 2 * kQT * 4 : 0;  // [tile parity][half][row]
-  static constexpr int Smem = QBytes + kKvStages * StageBytes + p_bufs<D>() * PBytes + XBytes + 1024 + 256;
+  static constexpr int Smem = QBytes + kv_stages<D>() * StageBytes + p_bufs<D>() * PBytes + XBytes + 1024 + 256;
   static constexpr int TmemCols = 2 * kKT + (D < 32 ? 32 : D);  // S[2] + O
 };
 
@@ -112,7 +116,7 @@ __global__ void __launch_bounds__(f_threads<D>(), 1) flash_fwd_kernel(const __gr
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
   uint8_t* sKV = sQ + C::QBytes;
-  uint8_t* sP = sKV + kKvStages * C::StageBytes;
+  uint8_t* sP = sKV + kv_stages<D>() * C::StageBytes;
   constexpr int NP = p_bufs<D>();
   float* sX = reinterpret_cast<float*>(sP + NP * C::PBytes);  // P buffers; max exchange
   uint64_t* bars = reinterpret_cast<uint64_t*>(sP + NP * C::PBytes + C::XBytes);
@@ -120,10 +124,10 @@ __global__ void __launch_bounds__(f_threads<D>(), 1) flash_fwd_kernel(const __gr
   // K and V have their own barriers: K_j's slot frees when S_j retires (early), V_j's when
   // P_j V_j retires, so K_{j+2}'s load is in flight long before S_{j+2} is issued
   uint64_t* k_full = bars + 1;
-  uint64_t* k_empty = k_full + kKvStages;
-  uint64_t* v_full = k_empty + kKvStages;
-  uint64_t* v_empty = v_full + kKvStages;
-  uint64_t* s_full = v_empty + kKvStages;
+  uint64_t* k_empty = k_full + kv_stages<D>();
+  uint64_t* v_full = k_empty + kv_stages<D>();
+  uint64_t* v_empty = v_full + kv_stages<D>();
+  uint64_t* s_full = v_empty + kv_stages<D>();
   uint64_t* s_empty = s_full + kSBuf;
   uint64_t* p_full = s_empty + kSBuf;   // [2] P_j in buffer j % 2 written (and O rescaled)
   uint64_t* p_empty = p_full + 2;   // [2] P_j V_j retired: P buffer j % 2 free, O up to date
@@ -140,7 +144,7 @@ __global__ void __launch_bounds__(f_threads<D>(), 1) flash_fwd_kernel(const __gr
     tma_prefetch(&F.tmK);
     tma_prefetch(&F.tmV);
     mbar_init(q_full, 1);
-    for (int i = 0; i < kKvStages; ++i) {
+    for (int i = 0; i < kv_stages<D>(); ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&k_empty[i], 1);
       mbar_init(&v_full[i], 1);
@@ -171,16 +175,16 @@ __global__ void __launch_bounds__(f_threads<D>(), 1) flash_fwd_kernel(const __gr
       for (int c = 0; c < D / 64; ++c)
         tma_load_2d(&F.tmQ, q_full, sQ + c * kQT * 128, c * 64, static_cast<int>(row_base + q0));
       auto load_k = [&](int j) {
-        const int st = j % kKvStages;
-        mbar_wait(&k_empty[st], ((j / kKvStages) & 1) ^ 1);
+        const int st = j % kv_stages<D>();
+        mbar_wait(&k_empty[st], ((j / kv_stages<D>()) & 1) ^ 1);
         mbar_expect_tx(&k_full[st], C::KBytes);
         uint8_t* kd = sKV + st * C::StageBytes;
         const int key0 = static_cast<int>(row_base + int64_t(j) * kKT);
         for (int c = 0; c < D / 64; ++c) tma_load_2d(&F.tmK, &k_full[st], kd + c * kKT * 128, c * 64, key0);
       };
       auto load_v = [&](int j) {
-        const int st = j % kKvStages;
-        mbar_wait(&v_empty[st], ((j / kKvStages) & 1) ^ 1);
+        const int st = j % kv_stages<D>();
+        mbar_wait(&v_empty[st], ((j / kv_stages<D>()) & 1) ^ 1);
         mbar_expect_tx(&v_full[st], C::VBytes);
         uint8_t* vd = sKV + st * C::StageBytes + C::KBytes;
         const int key0 = static_cast<int>(row_base + int64_t(j) * kKT);
@@ -205,8 +209,8 @@ __global__ void __launch_bounds__(f_threads<D>(), 1) flash_fwd_kernel(const __gr
       constexpr uint32_t idO = idesc_bf16_f32(128, D, false, true);
       const uint64_t qd = sdesc_sw128(smem_u32(sQ), 16, 1024);
       auto issue_s = [&](int j) {
-        const int st = j % kKvStages;
-        mbar_wait(&k_full[st], (j / kKvStages) & 1);
+        const int st = j % kv_stages<D>();
+        mbar_wait(&k_full[st], (j / kv_stages<D>()) & 1);
         if (F.dbg && blockIdx.x == 0 && blockIdx.y == 0) F.dbg[1] = 200 + j;
         const int b = j % kSBuf;
         mbar_wait(&s_empty[b], ((j / kSBuf) & 1) ^ 1);  // softmax done with S_{j-kSBuf}
@@ -232,8 +236,8 @@ __global__ void __launch_bounds__(f_threads<D>(), 1) flash_fwd_kernel(const __gr
         mbar_wait(&p_full[pb], (j / NP) & 1);  // P_j in smem, O rescaled
         if (F.dbg && blockIdx.x == 0 && blockIdx.y == 0) F.dbg[4] = 500 + j;
         tc_fence_after();
-        const int st = j % kKvStages;
-        mbar_wait(&v_full[st], (j / kKvStages) & 1);
+        const int st = j % kv_stages<D>();
+        mbar_wait(&v_full[st], (j / kv_stages<D>()) & 1);
         tc_fence_after();
         const uint64_t pd = sdesc_sw128(smem_u32(sP + pb * C::PBytes), 16, 1024);
         const uint64_t vdsc = sdesc_sw128(smem_u32(sKV + st * C::StageBytes + C::KBytes), 64 * 128, 1024);
