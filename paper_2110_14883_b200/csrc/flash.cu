@@ -37,20 +37,32 @@ using namespace ptx;
 #define TP_FLASH_W128 0  // d = 128 with eight softmax warps + one P buffer: measured slower (profiles/r01_exp51_w128.log)
 #endif
 template <int D>
-constexpr int soft_warps() { return TP_FLASH_W128 && D == 128 ? 8 : (D == 64 ? 8 : 4); }
+constexpr int soft_warps();
+// d = 64 as two CTAs per SM (TP_FLASH_2CTA64): 4 softmax warps, one S and one P buffer, 256 TMEM
+// columns and ~111 KB of shared memory each, so two query tiles share an SM and one CTA's
+// softmax overlaps the other's MMAs
+#ifndef TP_FLASH_KV64
+#define TP_FLASH_KV64 2  // K / V ring depth for d = 64 (3 measured equal: profiles/r01_exp58_kv64.log)
+#endif
+#ifndef TP_FLASH_2CTA64
+#define TP_FLASH_2CTA64 1
+#endif
+template <int D>
+constexpr bool two_cta() { return D == 64 && TP_FLASH_2CTA64; }
+template <int D>
+constexpr int kv_stages() { return two_cta<D>() ? 1 : (D == 64 ? TP_FLASH_KV64 : 2); }
+template <int D>
+constexpr int soft_warps() { return TP_FLASH_W128 && D == 128 ? 8 : (D == 64 ? (two_cta<D>() ? 4 : 8) : 4); }
 // P buffers in shared memory: two (the softmax runs a tile ahead of P V), one for d = 128 with
 // eight softmax warps (no shared memory left for a second buffer and the max exchange)
 template <int D>
-constexpr int p_bufs() { return D == 128 && soft_warps<D>() == 8 ? 1 : 2; }
+constexpr int p_bufs() { return (D == 128 && soft_warps<D>() == 8) || two_cta<D>() ? 1 : 2; }
 template <int D>
 constexpr int f_threads() { return 64 + 32 * soft_warps<D>(); }
 constexpr int kQT = 128;   // query rows per CTA
 constexpr int kKT = 128;   // keys per tile
-#ifndef TP_FLASH_KV64
-#define TP_FLASH_KV64 2  // K / V ring depth for d = 64 (3 measured equal: profiles/r01_exp58_kv64.log)
-#endif
 template <int D>
-constexpr int kv_stages() { return D == 64 ? TP_FLASH_KV64 : 2; }
+constexpr int kv_stages();
 // S_j = Q K_j^T buffers in TMEM (2; 3 measured equal: profiles/r01_exp50_sbuf.log). Three let S run two tiles ahead of P V (S_{j+2}
 // is queued right after P_{j-1} V_{j-1}), so the softmax never waits for its scores; with O
 // that is 3 x 128 + D <= 512 columns for D <= 128.
@@ -58,6 +70,10 @@ constexpr int kv_stages() { return D == 64 ? TP_FLASH_KV64 : 2; }
 #define TP_FLASH_SBUF 2
 #endif
 constexpr int kSBuf = TP_FLASH_SBUF;
+template <int D>
+constexpr int s_bufs() { return two_cta<D>() ? 1 : kSBuf; }
+template <int D>
+constexpr int tmem_cols_of() { return two_cta<D>() ? 256 : 512; }
 
 template <int D>
 struct FC {
@@ -110,7 +126,8 @@ __device__ __forceinline__ float ex2_poly(float x) {
 #endif
 
 template <int D>
-__global__ void __launch_bounds__(f_threads<D>(), 1) flash_fwd_kernel(const __grid_constant__ FParams F) {
+__global__ void __launch_bounds__(f_threads<D>(), two_cta<D>() ? 2 : 1) flash_fwd_kernel(const __grid_constant__ FParams F) {
+  constexpr int SB = s_bufs<D>();
   using C = FC<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -128,8 +145,8 @@ __global__ void __launch_bounds__(f_threads<D>(), 1) flash_fwd_kernel(const __gr
   uint64_t* v_full = k_empty + kv_stages<D>();
   uint64_t* v_empty = v_full + kv_stages<D>();
   uint64_t* s_full = v_empty + kv_stages<D>();
-  uint64_t* s_empty = s_full + kSBuf;
-  uint64_t* p_full = s_empty + kSBuf;   // [2] P_j in buffer j % 2 written (and O rescaled)
+  uint64_t* s_empty = s_full + SB;
+  uint64_t* p_full = s_empty + SB;   // [2] P_j in buffer j % 2 written (and O rescaled)
   uint64_t* p_empty = p_full + 2;   // [2] P_j V_j retired: P buffer j % 2 free, O up to date
   uint32_t* tslot = reinterpret_cast<uint32_t*>(p_empty + 2);
 
@@ -150,7 +167,7 @@ __global__ void __launch_bounds__(f_threads<D>(), 1) flash_fwd_kernel(const __gr
       mbar_init(&v_full[i], 1);
       mbar_init(&v_empty[i], 1);
     }
-    for (int i = 0; i < kSBuf; ++i) {
+    for (int i = 0; i < SB; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&s_empty[i], soft_warps<D>());
     }
@@ -160,13 +177,13 @@ __global__ void __launch_bounds__(f_threads<D>(), 1) flash_fwd_kernel(const __gr
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc_cg1(tslot, 512);
+  if (warp == 1) tmem_alloc_cg1(tslot, tmem_cols_of<D>());
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
   auto tS = [&](int b) { return tmem + static_cast<uint32_t>(b * kKT); };
-  const uint32_t tO = tmem + kSBuf * kKT;
+  const uint32_t tO = tmem + SB * kKT;
 
   if (warp == 0) {
     if (elect_one()) {
@@ -194,10 +211,10 @@ __global__ void __launch_bounds__(f_threads<D>(), 1) flash_fwd_kernel(const __gr
             tma_load_2d(&F.tmV, &v_full[st], vd + (kb * (D / 64) + c) * 64 * 128, c * 64, key0 + kb * 64);
       };
       // K runs one tile ahead of V (S_{j+1} is issued before P_j V_j)
-      for (int j = 0; j < kSBuf - 1 && j < ntiles; ++j) load_k(j);
+      for (int j = 0; j < SB - 1 && j < ntiles; ++j) load_k(j);
       for (int j = 0; j < ntiles; ++j) {
         if (F.dbg && blockIdx.x == 0 && blockIdx.y == 0) F.dbg[0] = 100 + j;
-        if (j + kSBuf - 1 < ntiles) load_k(j + kSBuf - 1);
+        if (j + SB - 1 < ntiles) load_k(j + SB - 1);
         load_v(j);
       }
     }
@@ -212,8 +229,8 @@ __global__ void __launch_bounds__(f_threads<D>(), 1) flash_fwd_kernel(const __gr
         const int st = j % kv_stages<D>();
         mbar_wait(&k_full[st], (j / kv_stages<D>()) & 1);
         if (F.dbg && blockIdx.x == 0 && blockIdx.y == 0) F.dbg[1] = 200 + j;
-        const int b = j % kSBuf;
-        mbar_wait(&s_empty[b], ((j / kSBuf) & 1) ^ 1);  // softmax done with S_{j-kSBuf}
+        const int b = j % SB;
+        mbar_wait(&s_empty[b], ((j / SB) & 1) ^ 1);  // softmax done with S_{j-SB}
         if (F.dbg && blockIdx.x == 0 && blockIdx.y == 0) F.dbg[2] = 300 + j;
         tc_fence_after();
         const uint64_t kdsc = sdesc_sw128(smem_u32(sKV + st * C::StageBytes), 16, 1024);
@@ -228,9 +245,9 @@ __global__ void __launch_bounds__(f_threads<D>(), 1) flash_fwd_kernel(const __gr
         umma_commit_cg1(&k_empty[st]);  // K_j read
       };
       mbar_wait(q_full, 0);
-      for (int j = 0; j < kSBuf - 1 && j < ntiles; ++j) issue_s(j);
+      for (int j = 0; j < SB - 1 && j < ntiles; ++j) issue_s(j);
       for (int j = 0; j < ntiles; ++j) {
-        if (j + kSBuf - 1 < ntiles) issue_s(j + kSBuf - 1);
+        if (j + SB - 1 < ntiles) issue_s(j + SB - 1);
         if (F.dbg && blockIdx.x == 0 && blockIdx.y == 0) F.dbg[3] = 400 + j;
         const int pb = j % NP;
         mbar_wait(&p_full[pb], (j / NP) & 1);  // P_j in smem, O rescaled
@@ -273,8 +290,8 @@ __global__ void __launch_bounds__(f_threads<D>(), 1) flash_fwd_kernel(const __gr
       l = half == 0 ? c.y : 0.f;
     }
     for (int j = 0; j < ntiles; ++j) {
-      const int b = j % kSBuf;
-      mbar_wait(&s_full[b], (j / kSBuf) & 1);
+      const int b = j % SB;
+      mbar_wait(&s_full[b], (j / SB) & 1);
       tc_fence_after();
       const int64_t valid = F.s - int64_t(j) * kKT - half * KW;  // this warp's keys in range
       // this warp's part of the S row into registers once: all loads in flight, one wait
@@ -444,7 +461,7 @@ __global__ void __launch_bounds__(f_threads<D>(), 1) flash_fwd_kernel(const __gr
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc_cg1(tmem, 512);
+    tmem_dealloc_cg1(tmem, tmem_cols_of<D>());
   }
 }
 
