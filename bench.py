@@ -78,7 +78,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="c3head", choices=sorted(WORKLOADS))
     ap.add_argument("--mode", default="auto")
     ap.add_argument("--depth", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -200,6 +200,9 @@ def run_ours(a):
     # ---- this rank's shards, generated in place by the library's seeded generator ----
     from paper_2110_14883_b200.mlp import TPMLP
     fused = a.fused and world > 1
+    torch.cuda.synchronize()
+    mem0 = torch.cuda.memory_allocated()
+    torch.cuda.reset_peak_memory_stats()
     model = TPMLP(g, M, layers, dtype=dtype, seed=a.seed,
                   flags=api.TP_FLAG_PEER_FUSED if fused else 0)
     x, ws_, dy_last, dacts, grads_w = model.x, model.W, model.dY, model.dX, model.dW
@@ -215,6 +218,7 @@ def run_ours(a):
     for _ in range(a.warmup):
         step()
     barrier()
+    mem_peak = torch.cuda.max_memory_allocated() - mem0
     stream = torch.cuda.current_stream()
 
     # ---- pass 1 (instrumented): CUDA events around every GEMM launch on its launching stream
@@ -231,16 +235,22 @@ def run_ours(a):
             step()
         api.tp_prof_enable(False)
         launches_per_step = api.tp_launch_count() - n0
+        prof_step_ms = 0.0
         for k in range(a.steps):
             api.tp_l2_flush(flush)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
             gprof.replay()
+            e1.record(stream)
             torch.cuda.synchronize()
+            prof_step_ms += e0.elapsed_time(e1)
             m_, n_, f_ = api.tp_prof_read(0)
             gemm_ms, gemm_n, gemm_flops = gemm_ms + m_, gemm_n + n_, gemm_flops + f_
             m_, n_, f_ = api.tp_prof_read(1)
             simt_ms, simt_n, simt_flops = simt_ms + m_, simt_n + n_, simt_flops + f_
         del gprof
     else:
+        prof_step_ms = 0.0
         for k in range(a.steps):
             api.tp_l2_flush(flush)
             torch.cuda._sleep(2_000_000)   # host runs ahead: events bracket device time only
@@ -345,55 +355,96 @@ def run_ours(a):
                "ms_per_step": round(ems, 4), "h2d_bytes_per_step": nbytes([hx, hdy]),
                "d2h_bytes_per_step": nbytes([hdx]),
                "what": "per step: X and dY host->device (dY on a side stream under the forward), "
-                       "fwd+bwd through TPMLP / tp_linear_*, dX device->host; weights resident",
+                       "fwd+bwd through TPMLP / tp_linear_*, dX device->host; weights resident "
+                       "(W1, W2 stay in HBM; dW1, dW2 stay in HBM for an on-device optimizer)",
                "weights_streamed": {"value": round(flops / (sms * 1e-3) / 1e12, 3),
                                     "ms_per_step": round(sms, 4),
                                     "h2d_bytes_per_step": nbytes([hx, hdy] + hws),
                                     "d2h_bytes_per_step": nbytes(houts)}}
 
     pk, src = peaks()
+    flops_gpu = flops / world                      # TP avoids no work: 6MKN/p per GPU per layer
+    costs = [api.tp_cost_model(mode, world, d_, depth=depth) for d_ in model.descs]
+    link_bytes = sum(c["link_bytes"] for c in costs)   # algorithmic NVLink bytes per GPU per step
+    nvlink_gbs = 900.0                                 # NVLink 5 per direction per GPU
     if dtype == "bf16":
         # a short step times each GEMM alone (burst peak); a step of several ms keeps the GPU at
         # its power cap, where the sustained figure is the denominator (B200_PROFILING.md)
         long_step = ms > 5.0
         peak = pk.get("bf16_tflops_sustained" if long_step else "bf16_tflops")
-        ach = gemm_flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
-        roof = {"bound": "tensor", "kernel": "gemm_tc_kernel / gemm_tc2_kernel (tcgen05, bf16->fp32)",
-                "achieved": round(ach, 2) if ach else None, "peak": peak, "unit": "TFLOP/s",
-                "frac": round(ach / peak, 4) if ach else None,
+        # achieved = the step's algorithmic GEMM flops per GPU / the uninstrumented timed step
+        # (at p = 1 every flop of the step is a GEMM flop; collectives count as step time)
+        ach = flops_gpu / (ms * 1e-3) / 1e12
+        kern = gemm_flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
+        roof = {"bound": "tensor", "kernel": "gemm_tc2_kernel / gemm_tc_kernel (tcgen05, bf16->fp32)",
+                "achieved": round(ach, 2), "peak": peak, "unit": "TFLOP/s",
+                "frac": round(ach / peak, 4),
+                "achieved_from": "step GEMM flops per GPU / ms_per_step (uninstrumented timed step)",
                 "peak_source": src + (" bf16_tflops_sustained (long step)" if long_step
                                       else " bf16_tflops (burst)"),
                 "traffic": traffic_of(a.workload, world), "traffic_unit": "bytes/launch (ncu)",
                 "alg_bytes_per_gemm": alg_bytes_per_gemm(M, layers, world, mode),
                 "alg_bytes_per_step": (sum(2 * (M * K + K * N + M * N) * 3 for K, N in layers)
                                        if world == 1 else None),
-                "launches_timed": gemm_n,
-                "gemm_share_of_step": round(gemm_ms / a.steps / ms, 3) if ms > 0 else None,
-                "timing": "per-GEMM CUDA events on the launching stream, recorded inside the "
-                          "step graph (external event nodes), K instrumented replays"}
-        # which roof binds the GEMM family: algorithmic flops at the tensor peak vs algorithmic
-        # operand + output bytes at the measured HBM bandwidth (p = 1; e.g. C3's 64-row GEMMs
-        # stream a 512 MB weight per launch and are HBM-bound)
+                "breakdown": {
+                    "gemm_launches_per_step": gemm_n // max(a.steps, 1),
+                    "gemm_kernel_tflops": round(kern, 2) if kern else None,
+                    "gemm_share_of_step": (round(min(1.0, gemm_ms / prof_step_ms), 3)
+                                           if prof_step_ms > 0 else None),
+                    "how": "per-GEMM CUDA events on the launching stream (external event nodes "
+                           "in a separately captured graph), share = their sum / the same "
+                           "instrumented replays' step time"}}
+        # which roof binds: flops at the tensor peak vs algorithmic operand + output bytes at the
+        # measured HBM bandwidth (p = 1; e.g. C3's 64-row GEMMs stream a 512 MB weight each)
         step_b = roof["alg_bytes_per_step"]
         hbm = pk.get("hbm_gbs")
-        if ach and step_b and hbm and gemm_n:
-            t_tensor = gemm_flops / (peak * 1e12)
-            t_hbm = step_b * a.steps / (hbm * 1e9)
+        t_tensor = flops_gpu / (peak * 1e12)
+        if step_b and hbm:
+            t_hbm = step_b / (hbm * 1e9)
             if t_hbm > t_tensor:
-                gbs = step_b * a.steps / (gemm_ms * 1e-3) / 1e9
+                gbs = step_b / (ms * 1e-3) / 1e9
                 roof.update({"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s",
                              "frac": round(gbs / hbm, 4), "peak_source": src + " hbm_gbs",
                              "tensor_achieved_tflops": round(ach, 2),
                              "tensor_frac": round(ach / peak, 4)})
-            roof["roof_times_us_per_step"] = {"tensor": round(t_tensor / a.steps * 1e6, 1),
-                                              "hbm": round(t_hbm / a.steps * 1e6, 1)}
+            roof["roof_times_us_per_step"] = {"tensor": round(t_tensor * 1e6, 1),
+                                              "hbm": round(t_hbm * 1e6, 1)}
+        if world > 1:
+            # the second roof of a sharded step: the schedule's algorithmic NVLink bytes per GPU
+            # (tp_cost_model) at 900 GB/s per direction
+            t_link = link_bytes / (nvlink_gbs * 1e9)
+            roof["nvlink"] = {"bytes_per_gpu_per_step": link_bytes,
+                              "achieved_gbs": round(link_bytes / (ms * 1e-3) / 1e9, 1),
+                              "peak_gbs": nvlink_gbs, "frac": round(link_bytes / (ms * 1e-3) / 1e9
+                                                                    / nvlink_gbs, 4)}
+            roof["roof_times_us_per_step"] = {"tensor": round(t_tensor * 1e6, 1),
+                                              "nvlink": round(t_link * 1e6, 1)}
+            if t_link > t_tensor:
+                roof["bound"] = "nvlink"
+            roof["frac_of_roofline"] = round(max(t_tensor, t_link) / (ms * 1e-3), 4)
     else:
         peak = 148 * 128 * 2 * 1.965  # fp32 FFMA: SMs x lanes x 2 flop x GHz (GFLOP/s->TFLOP/s /1e3)
         peak = peak / 1e3
-        ach = simt_flops / (simt_ms * 1e-3) / 1e12 if simt_ms > 0 else None
-        roof = {"bound": "alu", "kernel": "gemm_simt_kernel (fp32 FFMA)", "achieved": ach,
-                "peak": round(peak, 2), "unit": "TFLOP/s", "frac": (ach / peak) if ach else None,
+        ach = flops_gpu / (ms * 1e-3) / 1e12
+        roof = {"bound": "alu", "kernel": "gemm_simt_kernel (fp32 FFMA)", "achieved": round(ach, 4),
+                "peak": round(peak, 2), "unit": "TFLOP/s", "frac": round(ach / peak, 5),
                 "traffic": None}
+
+    # per-rank device memory: the paper's measurement ("max allocated CUDA memory")
+    # next to its closed form (at-rest shards of X, Y1, Y2, W1, W2 from tp_cost_model) and the
+    # closed form of everything the step allocates (+ dY, dX_i, dW_i, workspace, saved)
+    esz = 2 if dtype == "bf16" else 4
+    at_rest = (costs[0]["mem_x"] + sum(c["mem_w"] + c["mem_y"] for c in costs)) * esz
+    nb = lambda t: t.numel() * t.element_size() if t is not None else 0
+    allocated = (nb(model.x) + sum(map(nb, model.W)) + sum(map(nb, model.Y)) + nb(model.dY)
+                 + sum(map(nb, model.dX)) + sum(map(nb, model.dW)) + nb(model.ws)
+                 + sum(map(nb, model.saved)))
+    mem = {"peak_allocated_bytes": int(mem_peak),
+           "closed_form_at_rest_bytes": int(at_rest),
+           "closed_form_step_bytes": int(allocated),
+           "peak_over_step_closed_form": round(mem_peak / allocated, 4) if allocated else None,
+           "how": "torch.cuda.max_memory_allocated over model build + warm-up steps, minus the "
+                  "allocation before the model; closed forms: tp_cost_model shard sizes"}
 
     cpu = None
     if rank == 0 and not a.no_cpu_baseline:
@@ -411,6 +462,7 @@ def run_ours(a):
         "launch": "cuda-graph replay" if graph is not None else "eager",
         "gpu_launches": launches,
         "roofline": roof,
+        "memory_per_rank": mem,
         "clocks": clk.summary(),
         "e2e": e2e,
         "cpu_baseline": cpu,
@@ -424,69 +476,106 @@ def run_ours(a):
 
 # ------------------------------------------------------------------------------- oracle arm
 
-def oracle_step(wl, mode, world, depth, seed, M_sample=None):
-    """One fwd+bwd of the two-layer model through the oracle's rank-by-rank programs.
-    Returns flops of the sample."""
+def oracle_setup(wl, mode, world, depth, seed, max_rows):
+    """The oracle's inputs, generated ONCE outside every timed region: the first `max_rows` rows
+    of the global X and dY (a row sample of the batch) and the full weights, in fp64. Returns a
+    closure building the rank-by-rank shards for a sample of M rows (also untimed)."""
     import numpy as np
     import synth
-    from oracle import programs
-    from oracle.fabric import Fabric
     from oracle.grid import build_grid
     from oracle.shards import LayerSpec, shard
-    M = wl["M"] if M_sample is None else M_sample
-    layers = wl["layers"]
+    layers, dt = wl["layers"], wl["dtype"]
     g = build_grid(mode, world, depth)
-    specs = [LayerSpec(M, K, N, split_1d="row" if i % 2 else "col", parity=i % 2)
-             for i, (K, N) in enumerate(layers)]
-    fab = Fabric()
-    X = synth.tensor(seed, 0, M, layers[0][0], dtype=wl["dtype"]).astype(np.float64)
-    acts = [shard(g, specs[0], X, "X")]
-    Ws, saves = [], []
-    for i, (K, N) in enumerate(layers):
-        W = synth.tensor(seed, 16 * i + 1, K, N, scale=synth.xavier_scale(K, N), dtype=wl["dtype"])
-        Ws.append(shard(g, specs[i], W.astype(np.float64), "W"))
-        Y, sv = programs.layer_fwd(g, specs[i], acts[-1], Ws[-1], fab=fab)
+    X = synth.tensor(seed, 0, wl["M"], layers[0][0], dtype=dt, nrows=max_rows).astype(np.float64)
+    Ws = [synth.tensor(seed, 16 * i + 1, K, N, scale=synth.xavier_scale(K, N), dtype=dt)
+          .astype(np.float64) for i, (K, N) in enumerate(layers)]
+    dY = synth.tensor(seed, 16 * (len(layers) - 1) + 2, wl["M"], layers[-1][1], dtype=dt,
+                      nrows=max_rows).astype(np.float64)
+
+    def for_rows(M):
+        specs = [LayerSpec(M, K, N, split_1d="row" if i % 2 else "col", parity=i % 2)
+                 for i, (K, N) in enumerate(layers)]
+        return {"g": g, "specs": specs, "X": shard(g, specs[0], X[:M], "X"),
+                "W": [shard(g, sp, W, "W") for sp, W in zip(specs, Ws)],
+                "dY": shard(g, specs[-1], dY[:M], "Y"),
+                "flops": sum(6.0 * M * K * N for K, N in layers)}
+    return for_rows
+
+
+def oracle_step(st):
+    """One fwd+bwd of the layer chain through the oracle's rank-by-rank programs (the timed
+    work: the per-rank GEMMs and simulated collectives only). Returns the sample's flops."""
+    from oracle import programs
+    from oracle.fabric import Fabric
+    g, specs, fab = st["g"], st["specs"], Fabric()
+    acts, saves = [st["X"]], []
+    for i, sp in enumerate(specs):
+        Y, sv = programs.layer_fwd(g, sp, acts[-1], st["W"][i], fab=fab)
         acts.append(Y)
         saves.append(sv)
-    dY = synth.tensor(seed, 16 * (len(layers) - 1) + 2, M, layers[-1][1], dtype=wl["dtype"])
-    dy = shard(g, specs[-1], dY.astype(np.float64), "Y")
-    for i in reversed(range(len(layers))):
-        dy, _, _ = programs.layer_bwd(g, specs[i], dy, acts[i], Ws[i], fab=fab, saved=saves[i])
-    return sum(6.0 * M * K * N for K, N in layers)
+    dy = st["dY"]
+    for i in reversed(range(len(specs))):
+        dy, _, _ = programs.layer_bwd(g, specs[i], dy, acts[i], st["W"][i], fab=fab, saved=saves[i])
+    return st["flops"]
 
 
-def oracle_threads():
+def host_info():
+    model = None
     try:
-        from threadpoolctl import threadpool_info
-        n = [i.get("num_threads") for i in threadpool_info() if i.get("user_api") == "blas"]
-        return max(n) if n else 1
-    except Exception:  # noqa: BLE001
-        return os.cpu_count()
+        with open("/proc/cpuinfo") as f:
+            model = next((l.split(":", 1)[1].strip() for l in f if l.startswith("model name")), None)
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu": model}
 
 
-def cpu_baseline(a, mode, world, depth, budget_s=12.0):
+def one_blas_thread():
+    """The oracle is timed single-threaded: BLAS pinned to one thread."""
+    from threadpoolctl import threadpool_limits
+    return threadpool_limits(limits=1, user_api="blas")
+
+
+def oracle_sample(a, mode, world, depth, step_s):
+    """Inputs generated once; the row sample sized (by a calibration step) so that one oracle
+    step takes about step_s seconds on one core. Returns (state, M_run, M_full)."""
     wl = WORKLOADS[a.workload]
-    M_s = wl["M"]
-    # bounded sample: shrink the batch (rows) until one oracle step fits the budget
-    t0 = time.perf_counter()
-    fl = oracle_step(wl, mode, world, depth, a.seed, min(M_s, 64 * world * world))
-    dt = time.perf_counter() - t0
-    rate = fl / dt
-    full = sum(6.0 * M_s * K * N for K, N in wl["layers"])
-    M_run = M_s if full / rate <= budget_s else max(world * world, int(M_s * budget_s * rate / full))
-    M_run = max(world * world * depth, (M_run // (world * world * depth)) * world * world * depth)
-    t0 = time.perf_counter()
-    n, fl_tot = 0, 0.0
-    while True:
-        fl_tot += oracle_step(wl, mode, world, depth, a.seed, M_run)
-        n += 1
-        if time.perf_counter() - t0 > 0.5 * budget_s or n >= 3:
-            break
-    dt = time.perf_counter() - t0
-    return {"value": round(fl_tot / dt / 1e12, 6), "unit": "TFLOP/s", "cores": oracle_threads(),
+    M_full = wl["M"]
+    unit, gd = 1, grid_dims(mode, world, depth)
+    if mode == "2d":
+        unit = gd[0]
+    elif mode == "2.5d":
+        unit = gd[0] * gd[1]
+    elif mode == "3d":
+        unit = gd[0] * gd[0]
+    unit = max(unit, 8)
+    cap = min(M_full, 64 * unit)
+    build = oracle_setup(wl, mode, world, depth, a.seed, cap)
+    M_cal = min(M_full, unit)
+    with one_blas_thread():
+        st = build(M_cal)
+        t0 = time.perf_counter()
+        oracle_step(st)
+        rate = st["flops"] / (time.perf_counter() - t0)
+    per_row = st["flops"] / M_cal
+    M_run = int(step_s * rate / per_row) // unit * unit
+    M_run = max(unit, min(cap, M_run))
+    return build(M_run), M_run, M_full
+
+
+def cpu_baseline(a, mode, world, depth, budget_s=15.0):
+    st, M_run, M_full = oracle_sample(a, mode, world, depth, budget_s / 3)
+    n, fl = 0, 0.0
+    with one_blas_thread():
+        t0 = time.perf_counter()
+        while n < 3 and (n == 0 or time.perf_counter() - t0 < budget_s):
+            fl += oracle_step(st)
+            n += 1
+        dt = time.perf_counter() - t0
+    return {"value": round(fl / dt / 1e12, 6), "unit": "TFLOP/s", "cores": 1, **host_info(),
             "kind": "oracle",
-            "sample": f"{n} oracle step(s) of {a.workload} {mode} p={world} with M={M_run} rows "
-                      f"(of {M_s}); fp64 numpy rank-by-rank program, {dt:.1f} s"}
+            "sample": f"{n} oracle step(s) of {a.workload} {mode} p={world}, rows 0..{M_run} of "
+                      f"{M_full} (full weights); fp64 numpy rank-by-rank program, BLAS on 1 thread, "
+                      f"inputs generated before timing; {dt:.1f} s"}
 
 
 def run_reference(a):
@@ -497,26 +586,27 @@ def run_reference(a):
     wl = WORKLOADS[a.workload]
     mode = DEFAULT_MODE.get(world, "1d") if a.mode == "auto" else a.mode
     depth = a.depth if mode == "2.5d" else 1
-    M = wl["M"]
-    unit = world * world * depth
-    # each step: a bounded sample of the workload (rows) sized so the run stays ~minutes
-    M_run = max(unit, min(M, 128 * unit) // unit * unit)
-    for _ in range(a.warmup):
-        oracle_step(wl, mode, world, depth, a.seed, M_run)
-    t0 = time.perf_counter()
-    fl = 0.0
-    for _ in range(a.steps):
-        fl += oracle_step(wl, mode, world, depth, a.seed, M_run)
-    dt = time.perf_counter() - t0
+    # each step: a bounded row sample of the workload (~1 s of one core), inputs generated once
+    st, M_run, M = oracle_sample(a, mode, world, depth, 1.0)
+    with one_blas_thread():
+        for _ in range(a.warmup):
+            oracle_step(st)
+        t0 = time.perf_counter()
+        fl = 0.0
+        for _ in range(a.steps):
+            fl += oracle_step(st)
+        dt = time.perf_counter() - t0
     v = fl / dt / 1e12
     line = {"impl": "reference", "metric": METRIC,
             "value": round(v, 6), "unit": "TFLOP/s", "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": round(dt / a.steps * 1e3, 3), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_of(a.workload, mode, depth, world),
-            "cpu_baseline": {"value": round(v, 6), "unit": "TFLOP/s", "kind": "oracle",
-                             "cores": oracle_threads(),
-                             "sample": f"M={M_run} of {M} rows per step, fp64 numpy oracle"},
+            "cpu_baseline": {"value": round(v, 6), "unit": "TFLOP/s", "kind": "oracle", "cores": 1,
+                             **host_info(),
+                             "sample": f"rows 0..{M_run} of {M} per step (full weights), fp64 "
+                                       f"numpy rank-by-rank oracle, BLAS on 1 thread, inputs "
+                                       f"generated before timing"},
             "e2e": {"value": round(v, 6), "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)

@@ -71,3 +71,77 @@ def db_entries(spec, cols):
 def sample_indices(seed, n, *bounds):
     rng = np.random.default_rng(seed)
     return [rng.integers(0, b, size=n) for b in bounds]
+
+
+def stratified_indices(seed, extent, block=128):
+    """One index inside every `block`-wide slab of [0, extent) (random offset per slab, the last
+    slab may be ragged). Crossing a row sample with a column sample from this puts one checked
+    entry in every block x block output tile, so a single wrong GEMM tile cannot go unseen."""
+    rng = np.random.default_rng(seed)
+    lo = np.arange(0, extent, block, dtype=np.int64)
+    width = np.minimum(block, extent - lo)
+    return lo + rng.integers(0, width)
+
+
+# ---------------------------------------------------------------- row x column grids, one layer
+
+def y_grid(spec, rows, cols, alpha=1.0):
+    """Y[rows][:, cols] = alpha * X[rows, :] . W[:, cols] (every (row, col) pair)."""
+    M, K, N = spec["M"], spec["K"], spec["N"]
+    return alpha * (_rows(spec, spec["tx"], M, K, rows) @ _cols(spec, spec["tw"], K, N, cols))
+
+
+def dx_grid(spec, rows, ks, alpha=1.0):
+    """dX[rows][:, ks] = alpha * dY[rows, :] . W[ks, :]^T."""
+    M, K, N = spec["M"], spec["K"], spec["N"]
+    return alpha * (_rows(spec, spec["tdy"], M, N, rows) @ _rows(spec, spec["tw"], K, N, ks).T)
+
+
+def dw_grid(spec, ks, cols, alpha=1.0):
+    """dW[ks][:, cols] = alpha * X[:, ks]^T . dY[:, cols]."""
+    M, K, N = spec["M"], spec["K"], spec["N"]
+    return alpha * (_cols(spec, spec["tx"], M, K, ks).T @ _cols(spec, spec["tdy"], M, N, cols))
+
+
+# ---------------------------------------------------------------- the two-layer chain
+
+def _mm(A, B, chunk=2048):
+    """fp64 A . B with A converted to fp64 one block of rows at a time (memory only: each output
+    entry is still one full-length dot product)."""
+    B = np.asarray(B, np.float64)
+    out = np.empty((A.shape[0], B.shape[1]), dtype=np.float64)
+    for r in range(0, A.shape[0], chunk):
+        out[r:r + chunk] = np.asarray(A[r:r + chunk], np.float64) @ B
+    return out
+
+
+def chain2_grids(X, W1, W2, dY, idx):
+    """Sampled outputs of the paper's range-test model, two linear layers ("a model
+    which consists of two linear layers"; reading A14; activations ignored), from the
+    global inputs X [M,K], W1 [K,H], W2 [H,N], dY (= dY2) [M,N]:
+
+        Y1 = X.W1,  Y2 = Y1.W2;   dY1 = dY.W2^T,  dW2 = Y1^T.dY,  dX = dY1.W1^T,  dW1 = X^T.dY1
+
+    idx maps each output to its (row sample, column sample):
+        "Y": rows of M, cols of N;  "dX": rows of M, cols of K;
+        "dW1": rows of K, cols of H;  "dW2": rows of H, cols of N.
+    Returns {name: fp64 [len(rows), len(cols)]}. Only the rows / columns of Y1 and dY1 the
+    samples touch are formed (a row of Y1 needs all of W1, a column of Y1 all of X)."""
+    out = {}
+    if "Y" in idx:
+        r, c = idx["Y"]
+        Y1r = _mm(X[r], W1)                                  # Y1[r, :]
+        out["Y"] = Y1r @ np.asarray(W2[:, c], np.float64)
+    if "dX" in idx:
+        r, c = idx["dX"]
+        dY1r = _mm(dY[r], np.asarray(W2, np.float64).T)      # dY1[r, :]
+        out["dX"] = dY1r @ np.asarray(W1[c, :], np.float64).T
+    if "dW1" in idx:
+        r, c = idx["dW1"]
+        dY1c = _mm(dY, np.asarray(W2[c, :], np.float64).T)   # dY1[:, c]
+        out["dW1"] = np.asarray(X[:, r], np.float64).T @ dY1c
+    if "dW2" in idx:
+        r, c = idx["dW2"]
+        Y1c = _mm(X, np.asarray(W1[:, r], np.float64))       # Y1[:, r]
+        out["dW2"] = Y1c.T @ np.asarray(dY[:, c], np.float64)
+    return out

@@ -26,6 +26,8 @@ only GPU-vs-oracle differences are accumulation order and output rounding.
 from __future__ import annotations
 
 import math
+import os
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 
@@ -98,16 +100,44 @@ def values_at(seed: int, tensor_id: int, counters: np.ndarray, kind: str,
     return quantise(v, dtype)
 
 
+_PAR_MIN = 1 << 22      # elements above which tensor() splits its rows over threads
+
+
+def _threads() -> int:
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except (AttributeError, OSError):
+        return os.cpu_count() or 1
+
+
 def tensor(seed: int, tensor_id: int, rows: int, cols: int, kind: str = "uniform",
            scale: float = 1.0, dtype: str = "bf16", row0: int = 0, nrows: int | None = None,
            col0: int = 0, ncols: int | None = None) -> np.ndarray:
-    """Block [row0:row0+nrows, col0:col0+ncols] of the global [rows, cols] tensor, fp32."""
+    """Block [row0:row0+nrows, col0:col0+ncols] of the global [rows, cols] tensor, fp32.
+
+    Large blocks are generated as row chunks on a thread pool (numpy releases the GIL in its
+    ufuncs); every element depends only on its own counter, so the values are identical."""
     nrows = rows - row0 if nrows is None else nrows
     ncols = cols - col0 if ncols is None else ncols
-    r = np.arange(row0, row0 + nrows, dtype=np.uint64)[:, None]
     c = np.arange(col0, col0 + ncols, dtype=np.uint64)[None, :]
-    ctr = r * np.uint64(cols) + c
-    return values_at(seed, tensor_id, ctr, kind, scale, dtype).reshape(nrows, ncols)
+
+    def block(r_lo, r_hi):
+        r = np.arange(r_lo, r_hi, dtype=np.uint64)[:, None]
+        return values_at(seed, tensor_id, r * np.uint64(cols) + c, kind, scale, dtype)
+
+    nt = _threads()
+    if nrows * ncols < _PAR_MIN or nt == 1 or nrows < 2:
+        return block(row0, row0 + nrows).reshape(nrows, ncols)
+    out = np.empty((nrows, ncols), dtype=np.float32)
+    step = max(1, min(nrows, (1 << 20) // max(ncols, 1)))
+
+    def fill(lo):
+        hi = min(nrows, lo + step)
+        out[lo:hi] = block(row0 + lo, row0 + hi)
+
+    with ThreadPoolExecutor(nt) as ex:
+        list(ex.map(fill, range(0, nrows, step)))
+    return out
 
 
 def rows_of(seed, tensor_id, rows, cols, row_idx, kind="uniform", scale=1.0, dtype="bf16"):

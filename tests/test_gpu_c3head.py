@@ -1,0 +1,142 @@
+"""Parity at the north star's target configuration: configs[2] HEAD reading (M = b*s = 64*256 =
+16384 tokens, hidden 16384, two square linear layers, bf16; "With hidden size of 16384",
+reading A14), on the grids the north star names for 1 / 4 / 8 GPUs:
+
+  1D p=1 (bench N=1), 2D q=2 on 4 ranks (collective and fused peer-panel schedules),
+  2.5D q=2 d=2 on 8 ranks (replicated W, reading A6, and depth-sharded W), 3D l=2 on 8 ranks
+  (collective and fused), 1D p=8.
+
+Multi-rank grids run in one process on one GPU through the in-process transport.
+Inputs are generated on the device by tp_fill (bit-exact with synth, test_gpu_kernels) and on
+the host by synth. Expected values: oracle/sampled.chain2_grids, computed ONCE for the module
+(the dense result does not depend on the grid), fp64 from the quantised inputs.
+
+Sampling is tile-stratified: one row in every 128-row block crossed with one column in every
+128-column block of each output (Y2, dX, dW1, dW2), i.e. one checked entry in every 128x128
+output tile (16384 entries per output). Bars: relative Frobenius error over the sample <= 1e-2
+(the north star's bf16 bar) AND every entry within 5e-2 * rms(expected) of the oracle - the
+per-entry guard that a single wrong tile cannot slip under (DESIGN §2 reading A18). Entries
+held by several ranks (replicas) must agree bit for bit.
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import sampled
+from oracle.grid import build_grid
+from oracle.shards import LayerSpec, extent
+
+from tp_harness import run_ranks
+
+pytestmark = pytest.mark.gpu
+
+M = H = 16384
+LAYERS = [(H, H), (H, H)]
+SEED = 42
+# output name -> (layer, tensor layout, row extent, col extent)
+OUTPUTS = {"Y": (1, "Y", M, H), "dX": (0, "X", M, H), "dW1": (0, "W", H, H), "dW2": (1, "W", H, H)}
+
+
+@pytest.fixture(scope="module")
+def api():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2110_14883_b200 import api
+    return api
+
+
+@pytest.fixture(scope="module")
+def expected():
+    X = synth.tensor(SEED, synth.layer_tid(0, synth.TID_X), M, H)
+    W1 = synth.tensor(SEED, synth.layer_tid(0, synth.TID_W), H, H, scale=synth.xavier_scale(H, H))
+    W2 = synth.tensor(SEED, synth.layer_tid(1, synth.TID_W), H, H, scale=synth.xavier_scale(H, H))
+    dY = synth.tensor(SEED, synth.layer_tid(1, synth.TID_DY), M, H)
+    idx = {name: (sampled.stratified_indices(100 + 2 * n, rows),
+                  sampled.stratified_indices(101 + 2 * n, cols))
+           for n, (name, (_, _, rows, cols)) in enumerate(OUTPUTS.items())}
+    ref = sampled.chain2_grids(X, W1, W2, dY, idx)
+    del X, W1, W2, dY
+    return idx, ref
+
+
+def sampled_outputs(api, mode, p, d, flags, idx):
+    """Run the two-layer step on p in-process ranks; every rank reads the sampled entries that
+    fall inside its shards. Returns {name: [rows, cols] float64}, replicas checked bit-equal."""
+    from paper_2110_14883_b200.mlp import TPMLP
+    transport = api.TP_TRANSPORT_LOCAL if p > 1 else api.TP_TRANSPORT_NONE
+    uid = api.tp_get_unique_id(transport)
+    grid = build_grid(mode, p, d)
+    sharded = bool(flags & api.TP_FLAG_W25_DEPTH_SHARDED)
+    specs = [LayerSpec(M, K, N, split_1d="row" if i % 2 else "col", parity=i % 2,
+                       w_depth_sharded=sharded) for i, (K, N) in enumerate(LAYERS)]
+
+    def rank_fn(r):
+        g = api.tp_grid_init(mode, p, r, 0, d, 0, transport, uid)
+        s = torch.cuda.Stream()
+        try:
+            with torch.cuda.stream(s):
+                m = TPMLP(g, M, LAYERS, seed=SEED, flags=flags)
+                m.step()
+                bufs = {"Y": m.Y[-1], "dX": m.dX[0], "dW1": m.dW[0], "dW2": m.dW[1]}
+                got = {}
+                for name, (layer, t, _, _) in OUTPUTS.items():
+                    e = extent(grid, specs[layer], r, t)
+                    ri, ci = idx[name]
+                    rs = np.nonzero((ri >= e.row0) & (ri < e.row0 + e.rows))[0]
+                    cs = np.nonzero((ci >= e.col0) & (ci < e.col0 + e.cols))[0]
+                    assert tuple(bufs[name].shape) == (e.rows, e.cols), (name, bufs[name].shape, e)
+                    lr = torch.from_numpy(ri[rs] - e.row0).cuda()
+                    lc = torch.from_numpy(ci[cs] - e.col0).cuda()
+                    vals = bufs[name].index_select(0, lr).index_select(1, lc).float()
+                    got[name] = (rs, cs, vals)
+                got = {k: (rs, cs, v.cpu().numpy().astype(np.float64)) for k, (rs, cs, v) in got.items()}
+            s.synchronize()
+            del m
+            return got
+        finally:
+            s.synchronize()
+            api.tp_grid_destroy(g)
+
+    per = run_ranks(p, rank_fn, timeout=900)
+    out = {}
+    for name in OUTPUTS:
+        ri, ci = idx[name]
+        G = np.full((len(ri), len(ci)), np.nan)
+        for r in range(p):
+            rs, cs, v = per[r][name]
+            view = G[np.ix_(rs, cs)]
+            have = ~np.isnan(view)
+            assert np.array_equal(view[have], v[have]), f"{name}: replicas disagree at rank {r}"
+            G[np.ix_(rs, cs)] = v
+        assert not np.isnan(G).any(), f"{name}: sample not covered by the ranks' shards"
+        out[name] = G
+    torch.cuda.empty_cache()
+    return out
+
+
+def check(got, ref):
+    for name, exp in ref.items():
+        err = got[name] - exp
+        rel = np.linalg.norm(err) / np.linalg.norm(exp)
+        rms = np.sqrt(np.mean(exp ** 2))
+        worst = np.abs(err).max() / rms
+        assert rel <= 1e-2, f"{name}: relative Frobenius error {rel:.3e}"
+        assert worst <= 5e-2, f"{name}: worst entry off by {worst:.3e} x rms (a wrong tile?)"
+
+
+GRIDS = [("1d", 1, 1, ""), ("2d", 4, 1, ""), ("2d", 4, 1, "fused"), ("2.5d", 8, 2, ""),
+         ("2.5d", 8, 2, "depth"), ("2.5d", 8, 2, "depth+fused"), ("3d", 8, 1, ""),
+         ("3d", 8, 1, "fused"), ("1d", 8, 1, "")]
+
+
+@pytest.mark.parametrize("mode,p,d,variant", GRIDS,
+                         ids=[f"{m}-p{p}" + (f"-{v}" if v else "") for m, p, _, v in GRIDS])
+def test_c3head_two_layers_target_grids(api, expected, mode, p, d, variant):
+    flags = 0
+    if "fused" in variant:
+        flags |= api.TP_FLAG_PEER_FUSED
+    if "depth" in variant:
+        flags |= api.TP_FLAG_W25_DEPTH_SHARDED
+    idx, ref = expected
+    got = sampled_outputs(api, mode, p, d, flags, idx)
+    check(got, ref)

@@ -481,3 +481,47 @@ def test_sampled_entries_equal_dense_definition():
     assert np.allclose(sampled.dx_entries(spec, r, k, 0.5), dX[r, k], rtol=1e-13, atol=1e-13)
     assert np.allclose(sampled.dw_entries(spec, k, c, 0.5), dW[k, c], rtol=1e-13, atol=1e-13)
     assert np.allclose(sampled.db_entries(spec, c), db[c], rtol=1e-13, atol=1e-13)
+    rs, cs, ks = (sampled.stratified_indices(s, n, 16) for s, n in ((2, M), (3, N), (4, K)))
+    assert np.allclose(sampled.y_grid(spec, rs, cs, 0.5), (Y - b[None, :])[np.ix_(rs, cs)],
+                       rtol=1e-13, atol=1e-13)
+    assert np.allclose(sampled.dx_grid(spec, rs, ks, 0.5), dX[np.ix_(rs, ks)], rtol=1e-13, atol=1e-13)
+    assert np.allclose(sampled.dw_grid(spec, ks, cs, 0.5), dW[np.ix_(ks, cs)], rtol=1e-13, atol=1e-13)
+
+
+def test_stratified_indices_hit_every_tile():
+    from oracle import sampled
+    for extent, block in ((16384, 128), (200, 64), (128, 128), (5, 128)):
+        idx = sampled.stratified_indices(7, extent, block)
+        assert len(idx) == -(-extent // block)
+        assert np.all(idx // block == np.arange(len(idx)))
+        assert idx.min() >= 0 and idx.max() < extent
+
+
+def test_chain2_grids_equal_brute_force():
+    """The sampled two-layer chain == pure-Python loops of the chain rule (tiny, non-square
+    widths so a transposed operand or swapped layer fails) and == the dense oracle's mlp2."""
+    from oracle import sampled
+    M, K, H, N = 6, 5, 4, 3
+    X = synth.tensor(1, 0, M, K)
+    W1 = synth.tensor(1, 1, K, H, scale=0.5)
+    W2 = synth.tensor(1, 17, H, N, scale=0.5)
+    dY = synth.tensor(1, 18, M, N)
+    x, w1, w2, dy = (a.astype(float).tolist() for a in (X, W1, W2, dY))
+    y1 = [[sum(x[m][k] * w1[k][h] for k in range(K)) for h in range(H)] for m in range(M)]
+    y2 = [[sum(y1[m][h] * w2[h][n] for h in range(H)) for n in range(N)] for m in range(M)]
+    dy1 = [[sum(dy[m][n] * w2[h][n] for n in range(N)) for h in range(H)] for m in range(M)]
+    dx = [[sum(dy1[m][h] * w1[k][h] for h in range(H)) for k in range(K)] for m in range(M)]
+    dw1 = [[sum(x[m][k] * dy1[m][h] for m in range(M)) for h in range(H)] for k in range(K)]
+    dw2 = [[sum(y1[m][h] * dy[m][n] for m in range(M)) for n in range(N)] for h in range(H)]
+    idx = {"Y": ([0, 3, 5], [0, 2]), "dX": ([1, 4], [0, 1, 4]), "dW1": ([2, 4], [0, 3]),
+           "dW2": ([0, 1, 3], [1, 2])}
+    got = sampled.chain2_grids(X, W1, W2, dY, idx)
+    brute = {"Y": y2, "dX": dx, "dW1": dw1, "dW2": dw2}
+    for name, (r, c) in idx.items():
+        exp = np.array(brute[name])[np.ix_(r, c)]
+        assert np.allclose(got[name], exp, rtol=1e-13, atol=1e-14), name
+    Y1, Y2 = dense.mlp2_fwd(X, W1, W2)
+    dXd, dW1d, dW2d, _ = dense.mlp2_bwd(dY, X, Y1, W1, W2)
+    for name, full in (("Y", Y2), ("dX", dXd), ("dW1", dW1d), ("dW2", dW2d)):
+        r, c = idx[name]
+        assert np.allclose(got[name], full[np.ix_(r, c)], rtol=1e-13, atol=1e-14), name
