@@ -135,6 +135,38 @@ tp_status tp_grid_dims(const tp_grid* grid, int dims[3], int* ndims);
 tp_status tp_grid_group(const tp_grid* grid, int axis, int* members);
 tp_status tp_grid_destroy(tp_grid* grid);
 
+/* Collective-contract check (debug; SURVEY 8(b) "Every rank of the grid must call fwd/bwd with
+ * an identical desc, in the same order ... A debug flag verifies this"). When enabled, every
+ * collective entry point (tp_linear_fwd/bwd, tp_layernorm_fwd/bwd, tp_rsa_fwd/bwd,
+ * tp_attention_fwd/bwd) first exchanges a 64-bit hash of (entry point, per-grid call number,
+ * desc fields, the entry point's scalar arguments) with every rank of the grid on the host and
+ * returns TP_ERR_ARG - with nothing enqueued, on every rank - if any rank's hash differs, so a
+ * mismatched call fails instead of deadlocking inside a collective. The exchange is a host
+ * rendezvous (LOCAL) or a blocking 8-byte NCCL all-gather (NCCL): not stream-capturable, debug
+ * only. A rank that skips the call entirely still hangs its peers. No effect at world == 1.
+ * Collective when the grid is shared: every rank must set the same value. */
+tp_status tp_grid_set_contract_check(tp_grid* grid, int enable);
+
+/* ---- the grid's line communicators ("only incur communication on a sub-group") ---- */
+/* One collective over this rank's line along `axis` (members by ascending coordinate, as
+ * tp_grid_group), the primitive the schedules are built from:
+ *   TP_COLL_BCAST          recv (in place) := recv of member `arg` (root position on the line)
+ *   TP_COLL_REDUCE         recv := sum over members of send, significant at member `arg`
+ *   TP_COLL_ALLREDUCE      recv := sum over members of send
+ *   TP_COLL_ALLGATHER      recv [size*count] := concat over members of send [count]
+ *   TP_COLL_REDUCESCATTER  recv [count] := slice `pos` of sum over members of send [size*count]
+ *   TP_COLL_SHIFT          recv := send of member (pos + arg) mod size
+ * count in elements of dt (TP_BF16 / TP_FP32), device buffers, stream-ordered on `stream`.
+ * Collective: every member of the line calls it with the same op, count, dt and arg. A
+ * size-1 line is the identity (NCCL: a 1-rank communicator, so the NCCL calls still run).
+ * Errors: TP_ERR_ARG (axis, op, null buffers), TP_ERR_NCCL / TP_ERR_CUDA. */
+typedef enum {
+  TP_COLL_BCAST = 0, TP_COLL_REDUCE = 1, TP_COLL_ALLREDUCE = 2, TP_COLL_ALLGATHER = 3,
+  TP_COLL_REDUCESCATTER = 4, TP_COLL_SHIFT = 5
+} tp_collective;
+tp_status tp_axis_collective(tp_grid* grid, int axis, tp_collective op, const void* send,
+                             void* recv, size_t count, tp_dtype dt, int arg, void* stream);
+
 /* ---- layout (P:L524 2D, P:L526 2.5D, P:L528 3D, P:L486-488 1D) ----------------------- */
 /* Global block of `tensor` held by this rank: rows [row0, row0+rows), cols [col0, col0+cols).
  * BIAS is a [1, N] row. Gradients share their tensor's extent (dX~X, dW~W, dY~Y, db~BIAS).

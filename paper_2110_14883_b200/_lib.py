@@ -35,6 +35,7 @@ TP_FLAG_SOLOMONIK = 0x20
 EXPORTED = [
     "tp_status_string", "tp_last_error", "tp_version", "tp_get_unique_id", "tp_grid_init",
     "tp_grid_coords", "tp_grid_dims", "tp_grid_group", "tp_grid_destroy", "tp_shard_extent",
+    "tp_grid_set_contract_check", "tp_axis_collective",
     "tp_workspace_size", "tp_linear_fwd", "tp_linear_bwd", "tp_pack", "tp_unpack", "tp_gemm",
     "tp_gemm_ws_bytes",
     "tp_colsum", "tp_fill", "tp_l2_flush", "tp_prof_enable", "tp_prof_reset", "tp_prof_read",
@@ -75,6 +76,8 @@ _sigs = {
     "tp_grid_dims": (_i, [_vp, C.POINTER(_i), C.POINTER(_i)]),
     "tp_grid_group": (_i, [_vp, _i, C.POINTER(_i)]),
     "tp_grid_destroy": (_i, [_vp]),
+    "tp_grid_set_contract_check": (_i, [_vp, _i]),
+    "tp_axis_collective": (_i, [_vp, _i, _i, _vp, _vp, _sz, _i, _i, _vp]),
     "tp_shard_extent": (_i, [_vp, C.POINTER(tp_linear_desc), _i, _P64, _P64, _P64, _P64]),
     "tp_workspace_size": (_i, [_vp, C.POINTER(tp_linear_desc), C.POINTER(_sz), C.POINTER(_sz)]),
     "tp_linear_fwd": (_i, [_vp, C.POINTER(tp_linear_desc), _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),

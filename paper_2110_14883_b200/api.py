@@ -115,6 +115,29 @@ def tp_grid_destroy(g):
     _check(lib.tp_grid_destroy(g), "tp_grid_destroy")
 
 
+COLLECTIVES = {"bcast": 0, "reduce": 1, "allreduce": 2, "allgather": 3, "reducescatter": 4,
+               "shift": 5}
+
+
+def tp_axis_collective(g, axis, op, send, recv, arg=0, stream=None):
+    """One collective over this rank's grid line along `axis` (torch tensors; count = elements
+    of send, or of recv for bcast / allgather's per-member slice)."""
+    import torch
+    o = COLLECTIVES[op] if isinstance(op, str) else int(op)
+    dt = DTYPES["bf16"] if recv.dtype == torch.bfloat16 else DTYPES["fp32"]
+    src = recv if send is None else send
+    count = src.numel() if o != COLLECTIVES["reducescatter"] else recv.numel()
+    _check(lib.tp_axis_collective(g, int(axis), o, _ptr(send), _ptr(recv), count, dt, int(arg),
+                                  _stream(stream)),
+           "tp_axis_collective")
+
+
+def tp_grid_set_contract_check(g, enable=True):
+    """Debug: verify on every collective call that all ranks passed the same desc (TP_ERR_ARG
+    instead of a deadlock on a mismatch)."""
+    _check(lib.tp_grid_set_contract_check(g, int(bool(enable))), "tp_grid_set_contract_check")
+
+
 def tp_shard_extent(g, d: tp_linear_desc, tensor):
     t = TENSORS[tensor] if isinstance(tensor, str) else int(tensor)
     v = [C.c_int64() for _ in range(4)]

@@ -25,6 +25,48 @@ tp_status fail(tp_status s, const std::string& msg) {
 
 std::atomic<int64_t> g_launches{0};
 
+// ---- collective-contract check (tp_grid_set_contract_check) -----------------
+namespace {
+uint64_t fnv1a(uint64_t h, uint64_t w) {
+  for (int b = 0; b < 8; ++b) {
+    h ^= (w >> (8 * b)) & 0xffu;
+    h *= 0x100000001b3ull;
+  }
+  return h;
+}
+}  // namespace
+
+uint64_t f32_word(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  return u;
+}
+
+tp_status contract_check(tp_grid* g, ContractKind kind, const tp_linear_desc* d,
+                         std::initializer_list<uint64_t> words) {
+  if (!g || !g->contract_check || !g->all || g->world <= 1) return TP_OK;
+  const uint64_t call = g->contract_calls++;
+  uint64_t h = 0xcbf29ce484222325ull;
+  h = fnv1a(h, kind);
+  h = fnv1a(h, call);
+  if (d) {
+    for (uint64_t w : {uint64_t(d->M), uint64_t(d->K), uint64_t(d->N), uint64_t(d->dtype),
+                       uint64_t(d->split_1d), uint64_t(d->parity_3d), uint64_t(d->flags),
+                       f32_word(d->alpha)})
+      h = fnv1a(h, w);
+  }
+  for (uint64_t w : words) h = fnv1a(h, w);
+  std::vector<uint64_t> all(g->world);
+  TP_TRY(g->all->host_allgather(&h, sizeof(h), all.data()));
+  for (int r = 0; r < g->world; ++r)
+    if (all[r] != all[0])
+      return fail(TP_ERR_ARG, "collective contract violated at checked call #" +
+                                  std::to_string(call) + ": rank " + std::to_string(r) +
+                                  " passed a different entry point / desc than rank 0 (this rank " +
+                                  std::to_string(g->rank) + "); nothing was enqueued");
+  return TP_OK;
+}
+
 // ---- instrumentation: events around GEMM launches --------------------------------------
 namespace {
 struct ProfRec {
@@ -340,6 +382,52 @@ tp_status tp_grid_group(const tp_grid* g, int axis, int* members) {
   return TP_OK;
 }
 
+tp_status tp_axis_collective(tp_grid* g, int axis, tp_collective op, const void* send, void* recv,
+                             size_t count, tp_dtype dt, int arg, void* stream) {
+  if (!g) return fail(TP_ERR_ARG, "tp_axis_collective: null grid");
+  if (axis < 0 || axis >= g->ndims) return fail(TP_ERR_ARG, "tp_axis_collective: axis out of range");
+  if (dt != TP_BF16 && dt != TP_FP32) return fail(TP_ERR_ARG, "tp_axis_collective: dtype");
+  if (op < TP_COLL_BCAST || op > TP_COLL_SHIFT) return fail(TP_ERR_ARG, "tp_axis_collective: op");
+  if (count && (!recv || (op != TP_COLL_BCAST && !send)))
+    return fail(TP_ERR_ARG, "tp_axis_collective: null buffer");
+  const int n = g->dims[axis];
+  if ((op == TP_COLL_BCAST || op == TP_COLL_REDUCE) && (arg < 0 || arg >= n))
+    return fail(TP_ERR_ARG, "tp_axis_collective: root out of range");
+  TP_CUDA(cudaSetDevice(g->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Comm* c = g->axis[axis].get();
+  if (!c && n == 1 && g->transport == TP_TRANSPORT_NCCL) {
+    if (!g->unit_axis[axis]) {
+      tp_status st = TP_OK;
+      g->unit_axis[axis] = make_nccl_self_comm(&st);
+      if (st != TP_OK) return st;
+    }
+    c = g->unit_axis[axis].get();
+  }
+  if (!c) {  // a size-1 line without a communicator: the identity
+    if (n != 1) return fail(TP_ERR_ARG, "tp_axis_collective: grid has no transport");
+    if (op != TP_COLL_BCAST && count && send != recv)
+      TP_CUDA(cudaMemcpyAsync(recv, send, count * dtype_size(dt), cudaMemcpyDeviceToDevice, s));
+    return TP_OK;
+  }
+  switch (op) {
+    case TP_COLL_BCAST: return c->bcast(recv, count, dt, arg, s);
+    case TP_COLL_REDUCE: return c->reduce(send, recv, count, dt, arg, s);
+    case TP_COLL_ALLREDUCE: return c->allreduce(send, recv, count, dt, s);
+    case TP_COLL_ALLGATHER: return c->allgather(send, recv, count, dt, s);
+    case TP_COLL_REDUCESCATTER: return c->reducescatter(send, recv, count, dt, s);
+    case TP_COLL_SHIFT: return c->shift(send, recv, count, dt, arg, s);
+  }
+  return fail(TP_ERR_ARG, "tp_axis_collective: op");
+}
+
+tp_status tp_grid_set_contract_check(tp_grid* g, int enable) {
+  if (!g) return fail(TP_ERR_ARG, "null grid");
+  g->contract_check = enable != 0;
+  g->contract_calls = 0;
+  return TP_OK;
+}
+
 tp_status tp_grid_destroy(tp_grid* g) {
   if (!g) return TP_OK;
   if (g->comm_stream) cudaStreamSynchronize(g->comm_stream);
@@ -347,6 +435,7 @@ tp_status tp_grid_destroy(tp_grid* g) {
   g->ipc_cache.clear();
   g->regs.clear();
   for (auto& a : g->axis) a.reset();
+  for (auto& a : g->unit_axis) a.reset();
   g->all.reset();
   if (g->nccl) nccl_world_destroy(g->nccl);
   for (auto& e : g->events)
@@ -404,6 +493,8 @@ static void begin_run(Run& R, tp_grid* g, const tp_linear_desc* d, void* ws, voi
 tp_status tp_linear_fwd(tp_grid* g, const tp_linear_desc* d, const void* x, const void* w,
                         const void* bias, void* y, void* saved, void* ws, size_t ws_bytes,
                         void* stream) {
+  if (!g || !d) return fail(TP_ERR_ARG, "tp_linear_fwd: null grid or desc");
+  TP_TRY(contract_check(g, kCallLinearFwd, d, {uint64_t(bias != nullptr)}));
   size_t need_saved = 0;
   TP_TRY(ready_to_run(g, d, ws_bytes, ws, saved, &need_saved));
   if ((d->M && d->K && !x) || (d->K && d->N && !w) || (d->M && d->N && !y))
@@ -434,6 +525,9 @@ tp_status tp_linear_fwd(tp_grid* g, const tp_linear_desc* d, const void* x, cons
 tp_status tp_linear_bwd(tp_grid* g, const tp_linear_desc* d, const void* dy, const void* x,
                         const void* w, const void* saved, void* dx, void* dw, void* dbias, void* ws,
                         size_t ws_bytes, void* stream) {
+  if (!g || !d) return fail(TP_ERR_ARG, "tp_linear_bwd: null grid or desc");
+  TP_TRY(contract_check(g, kCallLinearBwd, d,
+                        {uint64_t(dx != nullptr), uint64_t(dbias != nullptr)}));
   size_t need_saved = 0;
   TP_TRY(ready_to_run(g, d, ws_bytes, ws, saved, &need_saved));
   if ((d->M && d->N && !dy) || (d->K && d->N && !dw) || (d->M && d->K && !x) ||
@@ -779,6 +873,8 @@ extern "C" tp_status tp_layernorm_fwd(tp_grid* g, const tp_linear_desc* d, tp_te
                                       const void* x, const void* gamma, const void* beta, void* y,
                                       float* stats, void* ws, size_t ws_bytes, void* stream) {
   if (!g || !d) return tp::fail(TP_ERR_ARG, "tp_layernorm_fwd: null grid or desc");
+  TP_TRY(tp::contract_check(g, tp::kCallLnFwd, d, {uint64_t(t), tp::f32_word(eps),
+                                                   uint64_t(stats != nullptr)}));
   if (d->dtype != TP_BF16 && d->dtype != TP_FP32) return tp::fail(TP_ERR_ARG, "unknown dtype");
   TP_CUDA(cudaSetDevice(g->device));
   return tp::layernorm_fwd(g, d, t, eps, x, gamma, beta, y, stats, ws, ws_bytes,
@@ -790,6 +886,8 @@ extern "C" tp_status tp_layernorm_bwd(tp_grid* g, const tp_linear_desc* d, tp_te
                                       const float* stats, void* dx, void* dgamma, void* dbeta,
                                       void* ws, size_t ws_bytes, void* stream) {
   if (!g || !d) return tp::fail(TP_ERR_ARG, "tp_layernorm_bwd: null grid or desc");
+  TP_TRY(tp::contract_check(g, tp::kCallLnBwd, d, {uint64_t(t), uint64_t(dgamma != nullptr),
+                                                   uint64_t(dbeta != nullptr)}));
   if (d->dtype != TP_BF16 && d->dtype != TP_FP32) return tp::fail(TP_ERR_ARG, "unknown dtype");
   TP_CUDA(cudaSetDevice(g->device));
   return tp::layernorm_bwd(g, d, t, dy, x, gamma, stats, dx, dgamma, dbeta, ws, ws_bytes,
@@ -805,6 +903,9 @@ extern "C" tp_status tp_rsa_ws_size(const tp_grid* g, const tp_rsa_desc* d, size
 extern "C" tp_status tp_rsa_fwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k,
                                 const void* v, void* out, void* ws, size_t ws_bytes, void* stream) {
   if (!g || !d) return tp::fail(TP_ERR_ARG, "tp_rsa_fwd: null grid or desc");
+  TP_TRY(tp::contract_check(g, tp::kCallRsaFwd, nullptr,
+                            {uint64_t(d->seq), uint64_t(d->d_k), uint64_t(d->heads),
+                             uint64_t(d->dtype), tp::f32_word(d->scale)}));
   TP_CUDA(cudaSetDevice(g->device));
   return tp::rsa_fwd(g, d, q, k, v, out, ws, ws_bytes, static_cast<cudaStream_t>(stream));
 }
@@ -813,6 +914,9 @@ extern "C" tp_status tp_rsa_bwd(tp_grid* g, const tp_rsa_desc* d, const void* q,
                                 const void* v, const void* dout, void* dq, void* dk, void* dv,
                                 void* ws, size_t ws_bytes, void* stream) {
   if (!g || !d) return tp::fail(TP_ERR_ARG, "tp_rsa_bwd: null grid or desc");
+  TP_TRY(tp::contract_check(g, tp::kCallRsaBwd, nullptr,
+                            {uint64_t(d->seq), uint64_t(d->d_k), uint64_t(d->heads),
+                             uint64_t(d->dtype), tp::f32_word(d->scale)}));
   TP_CUDA(cudaSetDevice(g->device));
   return tp::rsa_bwd(g, d, q, k, v, dout, dq, dk, dv, ws, ws_bytes, static_cast<cudaStream_t>(stream));
 }
@@ -828,6 +932,8 @@ extern "C" tp_status tp_attention_fwd(tp_grid* g, const tp_linear_desc* d, int64
                                       int64_t heads, float scale, const void* qkv, void* out,
                                       void* ws, size_t ws_bytes, void* stream) {
   if (!g) return tp::fail(TP_ERR_ARG, "tp_attention_fwd: null grid");
+  TP_TRY(tp::contract_check(g, tp::kCallAttnFwd, d,
+                            {uint64_t(seq), uint64_t(heads), tp::f32_word(scale)}));
   TP_CUDA(cudaSetDevice(g->device));
   return tp::attention_fwd(g, d, seq, heads, scale, qkv, out, ws, ws_bytes,
                            static_cast<cudaStream_t>(stream));
@@ -837,6 +943,8 @@ extern "C" tp_status tp_attention_bwd(tp_grid* g, const tp_linear_desc* d, int64
                                       int64_t heads, float scale, const void* qkv, const void* dout,
                                       void* dqkv, void* ws, size_t ws_bytes, void* stream) {
   if (!g) return tp::fail(TP_ERR_ARG, "tp_attention_bwd: null grid");
+  TP_TRY(tp::contract_check(g, tp::kCallAttnBwd, d,
+                            {uint64_t(seq), uint64_t(heads), tp::f32_word(scale)}));
   TP_CUDA(cudaSetDevice(g->device));
   return tp::attention_bwd(g, d, seq, heads, scale, qkv, dout, dqkv, ws, ws_bytes,
                            static_cast<cudaStream_t>(stream));

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <initializer_list>
 #include <cstdint>
 #include <memory>
 #include <string>
@@ -169,10 +170,23 @@ NcclWorld* nccl_world_create(int world, int rank, const void* id128, tp_status* 
 std::unique_ptr<Comm> make_nccl_world_comm(NcclWorld* w);
 void nccl_world_destroy(NcclWorld* w);
 tp_status nccl_unique_id(void* id128);
+// A 1-rank NCCL communicator of this process alone (size-1 grid lines in tp_axis_collective).
+std::unique_ptr<Comm> make_nccl_self_comm(tp_status* st);
 
 std::unique_ptr<Comm> make_local_comm(const void* id128, int world, const std::vector<int>& members,
                                       int pos, int device, tp_status* st);
 tp_status local_unique_id(void* id128);
+
+// Collective-contract check (capi.cpp): `kind` names the entry point; `words` its scalar
+// arguments. TP_OK when disabled, at world == 1, or when every rank passed the same values.
+enum ContractKind : uint64_t {
+  kCallLinearFwd = 1, kCallLinearBwd, kCallLnFwd, kCallLnBwd, kCallRsaFwd, kCallRsaBwd,
+  kCallAttnFwd, kCallAttnBwd
+};
+// d may be null (entry points without a linear desc). f32_word: a float's bit pattern.
+uint64_t f32_word(float f);
+tp_status contract_check(tp_grid* g, ContractKind kind, const tp_linear_desc* d,
+                         std::initializer_list<uint64_t> words);
 
 }  // namespace tp
 
@@ -188,6 +202,7 @@ struct tp_grid {
   tp::NcclWorld* nccl = nullptr;
   std::unique_ptr<tp::Comm> axis[3];  // line along each axis (nullptr if size 1 or NONE)
   std::unique_ptr<tp::Comm> all;      // every rank (barriers, registration); nullptr if p == 1
+  std::unique_ptr<tp::Comm> unit_axis[3];  // NCCL 1-rank comms for size-1 lines (lazy)
   // Symmetric registered buffers (tp_register_buffer): this rank's range and every rank's
   // pointer to its own copy, directly dereferenceable here (same process or CUDA IPC).
   struct RegBuf {
@@ -206,6 +221,9 @@ struct tp_grid {
       if (p >= r.base && p < r.base + r.bytes) return r.peer[peer_rank] + (p - r.base);
     return nullptr;
   }
+  // Collective-contract check (tp_grid_set_contract_check): per-grid count of checked calls.
+  bool contract_check = false;
+  uint64_t contract_calls = 0;
   cudaStream_t comm_stream = nullptr;
   static constexpr int kEvents = 64;
   cudaEvent_t events[kEvents] = {};

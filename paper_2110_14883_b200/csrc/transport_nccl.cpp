@@ -172,6 +172,19 @@ std::unique_ptr<Comm> make_nccl_comm(NcclWorld* w, int color, int key, int size,
   return std::make_unique<NcclComm>(c, size, pos);
 }
 
+std::unique_ptr<Comm> make_nccl_self_comm(tp_status* st) {
+  ncclUniqueId id;
+  ncclComm_t c = nullptr;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r == ncclSuccess) r = ncclCommInitRank(&c, 1, id, 0);
+  if (r != ncclSuccess) {
+    *st = nccl_fail(r, "ncclCommInitRank (1-rank line)");
+    return nullptr;
+  }
+  *st = TP_OK;
+  return std::make_unique<NcclComm>(c, 1, 0);
+}
+
 // Non-owning view of the world communicator (destroyed with the NcclWorld).
 std::unique_ptr<Comm> make_nccl_world_comm(NcclWorld* w) {
   return std::make_unique<NcclComm>(w->world, w->size, w->rank, /*owns=*/false);

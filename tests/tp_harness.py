@@ -135,3 +135,20 @@ def rel_fro(a, b):
     a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
     n = np.linalg.norm(b)
     return float(np.linalg.norm(a - b) / (n if n > 0 else 1.0))
+
+
+def chain_reference(seed, M, layers):
+    """Dense fp64 (Y_last, dX, dW_0, dW_1, ...) of a TPMLP chain with the synth recipe of
+    paper_2110_14883_b200/mlp.py (X of layer 0, Xavier W_i, dY of the last layer)."""
+    X = synth.tensor(seed, synth.layer_tid(0, synth.TID_X), M, layers[0][0]).astype(np.float64)
+    Ws = [synth.tensor(seed, synth.layer_tid(i, synth.TID_W), K, N, scale=synth.xavier_scale(K, N))
+          .astype(np.float64) for i, (K, N) in enumerate(layers)]
+    dY = synth.tensor(seed, synth.layer_tid(len(layers) - 1, synth.TID_DY), M,
+                      layers[-1][1]).astype(np.float64)
+    acts = [X]
+    for W in Ws:
+        acts.append(dense.linear_fwd(acts[-1], W))
+    d, dWs = dY, [None] * len(Ws)
+    for i in reversed(range(len(Ws))):
+        d, dWs[i], _ = dense.linear_bwd(d, acts[i], Ws[i])
+    return (acts[-1], d, *dWs)
