@@ -617,7 +617,12 @@ tp_status launch(const GemmArgs& g, cudaStream_t s) {
     const char* e = std::getenv("TP_GEMM_V1_TMA_STORE");
     return e ? std::atoi(e) : 1;
   }();
-  ep.tma = env_tma && (reinterpret_cast<uintptr_t>(g.D) % 16) == 0 && (g.ldd * osz) % 16 == 0;
+  // A TMA store writes whole 16-byte granules of the inner dimension: when a row of D does not
+  // end on a granule (N * osz % 16 != 0) it would also write zeros to the columns between N and
+  // the next granule - elements outside D (measured: tools/gemm_probe_ragged.py). Those
+  // problems take the guarded per-element epilogue instead.
+  ep.tma = env_tma && (reinterpret_cast<uintptr_t>(g.D) % 16) == 0 && (g.ldd * osz) % 16 == 0 &&
+           (g.N * osz) % 16 == 0;
   if (ep.tma)
     TP_TRY(make_map(&td, g.D, g.N, g.M, g.ldd, ep.out_bf16 ? 64 : 32, 32, !ep.out_bf16));
   const int tok = prof_begin(0, s, 2.0 * double(g.M) * double(g.N) * double(g.K));

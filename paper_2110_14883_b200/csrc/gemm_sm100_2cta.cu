@@ -1161,8 +1161,11 @@ bool gemm_tc2_supported(const GemmArgs& g) {
     for (int i = 0; i < g.dpanels; ++i)
       if (!g.Dp[i] || reinterpret_cast<uintptr_t>(g.Dp[i]) % 16) return false;
   }
+  // TMA-store epilogue only: rows of D must end on a 16-byte granule (a store of the last
+  // granule of a ragged row would zero the columns past N, see gemm_sm100.cu)
   return g.M > 128 && (g.dpanels > 1 || reinterpret_cast<uintptr_t>(g.D) % 16 == 0) &&
-         ((g.ldd * osz) % 16 == 0) && (!g.bias || reinterpret_cast<uintptr_t>(g.bias) % 2 == 0);
+         ((g.ldd * osz) % 16 == 0) && ((g.N * osz) % 16 == 0) &&
+         (!g.bias || reinterpret_cast<uintptr_t>(g.bias) % 2 == 0);
 }
 
 size_t gemm_tc2_ws_bytes() {

@@ -172,19 +172,31 @@ __global__ void rsa_dscore(T* __restrict__ P, const float* __restrict__ dP, int6
   if (r >= rows) return;
   T* pr = P + r * s;
   const float* dr = dP + r * s;
+  // a zero probability contributes nothing (and marks the padding columns, whose dP is -inf)
   float dsum = 0.f;
   for (int64_t c = lane; c < s; c += 32) {
     float pv;
     if constexpr (sizeof(T) == 2) pv = __bfloat162float(pr[c]);
     else pv = pr[c];
-    dsum += pv * dr[c];
+    if (pv != 0.f) dsum += pv * dr[c];
   }
   dsum = wsum(dsum);
   for (int64_t c = lane; c < s; c += 32) {
     float pv;
     if constexpr (sizeof(T) == 2) pv = __bfloat162float(pr[c]);
     else pv = pr[c];
-    st_out(pr + c, scale * pv * (dr[c] - dsum));
+    st_out(pr + c, pv != 0.f ? scale * pv * (dr[c] - dsum) : 0.f);
+  }
+}
+
+// Padding columns of the score rows (block offset >= b of each bp-wide block) := -inf.
+__global__ void rsa_fill_pad(float* __restrict__ S, int64_t rows, int64_t ls, int64_t b, int64_t bp) {
+  const int64_t pad = bp - b, nblk = ls / bp;
+  const int64_t n = rows * nblk * pad;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t o = i % pad, j = (i / pad) % nblk, r = i / (pad * nblk);
+    S[r * ls + j * bp + b + o] = -INFINITY;
   }
 }
 
@@ -197,6 +209,11 @@ __global__ void rsa_cast(const float* __restrict__ src, int64_t n, T* __restrict
 struct RsaPlan {
   int p = 1, r = 0;
   int64_t s = 0, b = 0, d = 0, heads = 0, chunk = 1;
+  // score rows are stored as p blocks of bp >= b columns (bp = b rounded up to 8) so that every
+  // block starts 16-byte aligned and every row stride is a TMA-legal multiple of 8 elements
+  // (ragged sequences, e.g. ViT's 197 tokens); the bp - b padding columns hold -inf scores and
+  // zero probabilities. ls = p bp is the row stride of S and P.
+  int64_t bp = 0, ls = 0;
   int64_t fchunk = 0;  // heads per online-softmax ring launch (0: two-pass only)
   size_t esz = 2;
 };
@@ -216,11 +233,23 @@ tp_status rsa_plan(const tp_grid* g, const tp_rsa_desc* d, RsaPlan* P) {
   P->d = d->d_k;
   P->heads = d->heads;
   P->esz = dtype_size(d->dtype);
-  const size_t per_head = size_t(P->b) * size_t(P->s) * 4;
+  P->bp = (P->b + 7) / 8 * 8;
+  P->ls = P->bp * P->p;
+  const size_t per_head = size_t(P->b) * size_t(P->ls) * 4;
   P->chunk = per_head ? std::max<int64_t>(1, std::min<int64_t>(d->heads, kScoreBudget / per_head)) : 1;
   if (P->chunk < 1) P->chunk = 1;
   // the online-softmax ring keeps no score rows: all heads in one launch per ring step
   P->fchunk = flash_supported(P->d, d->dtype) ? std::max<int64_t>(1, std::min<int64_t>(d->heads, 65535)) : 0;
+  return TP_OK;
+}
+
+tp_status fill_pad(const RsaPlan& P, float* S, int64_t rows, cudaStream_t s) {
+  if (P.bp == P.b || !rows) return TP_OK;
+  const int64_t n = rows * P.p * (P.bp - P.b);
+  const unsigned G = static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 148 * 8));
+  rsa_fill_pad<<<G, 256, 0, s>>>(S, rows, P.ls, P.b, P.bp);
+  count_launch();
+  TP_CUDA(cudaGetLastError());
   return TP_OK;
 }
 
@@ -241,8 +270,8 @@ struct RsaWs {
 
 void rsa_carve(Carver& c, const RsaPlan& P, RsaWs* w) {
   const size_t ch = size_t(P.chunk);
-  w->S = static_cast<float*>(c.take(ch * P.b * P.s * 4));
-  w->Pm = c.take(ch * P.b * P.s * P.esz);
+  w->S = static_cast<float*>(c.take(ch * P.b * P.ls * 4));
+  w->Pm = c.take(ch * P.b * P.ls * P.esz);
   w->kv[0] = c.take(ch * P.b * P.d * P.esz);
   w->kv[1] = c.take(ch * P.b * P.d * P.esz);
   w->acc = static_cast<float*>(c.take(ch * P.b * P.d * 4));
@@ -375,6 +404,7 @@ tp_status rsa_fwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k
       continue;
     }
     // ---- pass 1: K ring -> scores
+    TP_TRY(fill_pad(P, w.S, nh * P.b, s));
     const void* cur = static_cast<const char*>(k) + h0 * bd * P.esz;
     int nb = 0;
     for (int t = 0; t < P.p; ++t) {
@@ -383,7 +413,7 @@ tp_status rsa_fwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k
       for (int64_t h = 0; h < nh; ++h)
         gs.push_back(rsa_gemm(P.b, P.b, P.d, qc + h * bd * P.esz, P.d,
                               static_cast<const char*>(cur) + h * bd * P.esz, P.d, true,
-                              w.S + h * P.b * P.s + j * P.b, P.s, dt, TP_FP32, scale, nullptr, w));
+                              w.S + h * P.b * P.ls + j * P.bp, P.ls, dt, TP_FP32, scale, nullptr, w));
       TP_TRY(run_heads(gs, s));
       if (t + 1 < P.p) {
         TP_TRY(ring->shift(cur, w.kv[nb], size_t(nh) * bd, dt, -1, s));
@@ -392,7 +422,7 @@ tp_status rsa_fwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k
       }
     }
     // ---- softmax of the assembled rows
-    TP_TRY(launch_softmax(w.S, nh * P.b, P.s, dt, w.Pm, s));
+    TP_TRY(launch_softmax(w.S, nh * P.b, P.ls, dt, w.Pm, s));
     // ---- pass 2: V ring -> output
     cur = static_cast<const char*>(v) + h0 * bd * P.esz;
     nb = 0;
@@ -402,10 +432,10 @@ tp_status rsa_fwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k
       const bool last = t + 1 == P.p;
       gs.clear();
       for (int64_t h = 0; h < nh; ++h) {
-        const void* A = static_cast<const char*>(w.Pm) + (h * P.b * P.s + j * P.b) * P.esz;
+        const void* A = static_cast<const char*>(w.Pm) + (h * P.b * P.ls + j * P.bp) * P.esz;
         const void* B = static_cast<const char*>(cur) + h * bd * P.esz;
         void* D = last ? static_cast<void*>(oc + h * bd * P.esz) : static_cast<void*>(w.acc + h * bd);
-        gs.push_back(rsa_gemm(P.b, P.d, P.b, A, P.s, B, P.d, false, D, P.d, dt, last ? dt : TP_FP32,
+        gs.push_back(rsa_gemm(P.b, P.d, P.b, A, P.ls, B, P.d, false, D, P.d, dt, last ? dt : TP_FP32,
                               1.f, t > 0 ? w.acc + h * bd : nullptr, w));
       }
       TP_TRY(run_heads(gs, s));
@@ -449,6 +479,7 @@ tp_status rsa_bwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k
     const char* qc = static_cast<const char*>(q) + h0 * bd * P.esz;
     const char* doc = static_cast<const char*>(dout) + h0 * bd * P.esz;
     // ---- K ring: recompute the score rows, softmax
+    TP_TRY(fill_pad(P, w.S, nh * P.b, s));
     const void* cur = static_cast<const char*>(k) + h0 * bd * P.esz;
     int nb = 0;
     for (int t = 0; t < P.p; ++t) {
@@ -457,7 +488,7 @@ tp_status rsa_bwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k
       for (int64_t h = 0; h < nh; ++h)
         gs.push_back(rsa_gemm(P.b, P.b, P.d, qc + h * bd * P.esz, P.d,
                               static_cast<const char*>(cur) + h * bd * P.esz, P.d, true,
-                              w.S + h * P.b * P.s + j * P.b, P.s, dt, TP_FP32, scale, nullptr, w));
+                              w.S + h * P.b * P.ls + j * P.bp, P.ls, dt, TP_FP32, scale, nullptr, w));
       TP_TRY(run_heads(gs, s));
       if (t + 1 < P.p) {
         TP_TRY(ring->shift(cur, w.kv[nb], size_t(nh) * bd, dt, -1, s));
@@ -465,13 +496,13 @@ tp_status rsa_bwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k
         nb ^= 1;
       }
     }
-    TP_TRY(launch_softmax(w.S, nh * P.b, P.s, dt, w.Pm, s));
+    TP_TRY(launch_softmax(w.S, nh * P.b, P.ls, dt, w.Pm, s));
     // ---- dV parts: block j <- P[:, j]^T dO (fp32, laid out [j][h][b][d] for the reduce-scatter)
     gs.clear();
     for (int j = 0; j < P.p; ++j)
       for (int64_t h = 0; h < nh; ++h)
         gs.push_back(rsa_gemm(P.b, P.d, P.b,
-                              static_cast<const char*>(w.Pm) + (h * P.b * P.s + j * P.b) * P.esz, P.s,
+                              static_cast<const char*>(w.Pm) + (h * P.b * P.ls + j * P.bp) * P.esz, P.ls,
                               doc + h * bd * P.esz, P.d, false,
                               w.parts_v + (int64_t(j) * nh + h) * bd, P.d, dt, TP_FP32, 1.f, nullptr, w,
                               true));
@@ -485,7 +516,7 @@ tp_status rsa_bwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k
       for (int64_t h = 0; h < nh; ++h)
         gs.push_back(rsa_gemm(P.b, P.b, P.d, doc + h * bd * P.esz, P.d,
                               static_cast<const char*>(cur) + h * bd * P.esz, P.d, true,
-                              w.S + h * P.b * P.s + j * P.b, P.s, dt, TP_FP32, 1.f, nullptr, w));
+                              w.S + h * P.b * P.ls + j * P.bp, P.ls, dt, TP_FP32, 1.f, nullptr, w));
       TP_TRY(run_heads(gs, s));
       if (t + 1 < P.p) {
         TP_TRY(ring->shift(cur, w.kv[nb], size_t(nh) * bd, dt, -1, s));
@@ -498,9 +529,9 @@ tp_status rsa_bwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k
       const int64_t rows = nh * P.b;
       const unsigned G = static_cast<unsigned>((rows * 32 + 255) / 256);
       if (dt == TP_BF16)
-        rsa_dscore<__nv_bfloat16><<<G, 256, 0, s>>>(static_cast<__nv_bfloat16*>(w.Pm), w.S, rows, P.s, scale);
+        rsa_dscore<__nv_bfloat16><<<G, 256, 0, s>>>(static_cast<__nv_bfloat16*>(w.Pm), w.S, rows, P.ls, scale);
       else
-        rsa_dscore<float><<<G, 256, 0, s>>>(static_cast<float*>(w.Pm), w.S, rows, P.s, scale);
+        rsa_dscore<float><<<G, 256, 0, s>>>(static_cast<float*>(w.Pm), w.S, rows, P.ls, scale);
       count_launch();
       TP_CUDA(cudaGetLastError());
     }
@@ -509,7 +540,7 @@ tp_status rsa_bwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k
     for (int j = 0; j < P.p; ++j)
       for (int64_t h = 0; h < nh; ++h)
         gs.push_back(rsa_gemm(P.b, P.d, P.b,
-                              static_cast<const char*>(w.Pm) + (h * P.b * P.s + j * P.b) * P.esz, P.s,
+                              static_cast<const char*>(w.Pm) + (h * P.b * P.ls + j * P.bp) * P.esz, P.ls,
                               qc + h * bd * P.esz, P.d, false,
                               w.parts_k + (int64_t(j) * nh + h) * bd, P.d, dt, TP_FP32, 1.f, nullptr, w,
                               true));
@@ -525,7 +556,7 @@ tp_status rsa_bwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k
       for (int64_t h = 0; h < nh; ++h) {
         void* D = last ? static_cast<void*>(dqc + h * bd * P.esz) : static_cast<void*>(w.acc + h * bd);
         gs.push_back(rsa_gemm(P.b, P.d, P.b,
-                              static_cast<const char*>(w.Pm) + (h * P.b * P.s + j * P.b) * P.esz, P.s,
+                              static_cast<const char*>(w.Pm) + (h * P.b * P.ls + j * P.bp) * P.esz, P.ls,
                               static_cast<const char*>(cur) + h * bd * P.esz, P.d, false, D, P.d, dt,
                               last ? dt : TP_FP32, 1.f, t > 0 ? w.acc + h * bd : nullptr, w));
       }

@@ -15,7 +15,8 @@ from tp_harness import rel_fro, run_ranks, spec_of, to_np
 
 pytestmark = pytest.mark.gpu
 
-GRIDS = [("1d", 1, 1), ("1d", 2, 1), ("2d", 4, 1), ("3d", 8, 1)]
+GRIDS = [("1d", 1, 1, 0), ("1d", 2, 1, 0), ("2d", 4, 1, 0), ("2.5d", 4, 1, 0), ("2.5d", 8, 2, 0),
+         ("2.5d", 8, 2, 1), ("3d", 8, 1, 0)]
 
 
 @pytest.fixture(scope="module")
@@ -38,11 +39,11 @@ def params(seed, h, F, dtype):
     return P
 
 
-@pytest.mark.parametrize("grid", GRIDS, ids=lambda g: f"{g[0]}-p{g[1]}")
+@pytest.mark.parametrize("grid", GRIDS, ids=lambda g: f"{g[0]}-p{g[1]}" + ("-wsharded" if g[3] else ""))
 @pytest.mark.parametrize("dtype", ["fp32", "bf16"])
 def test_block_vs_oracle(api, grid, dtype):
     from paper_2110_14883_b200.block import TPBlock
-    mode, p, d = grid
+    mode, p, d, wflags = grid
     seq, heads, dh, B = 64, 4, 32, 8
     h, F, M = heads * dh, 256, B * seq
     P = params(7, h, F, dtype)
@@ -61,7 +62,7 @@ def test_block_vs_oracle(api, grid, dtype):
         st = torch.cuda.Stream()
         try:
             with torch.cuda.stream(st):
-                blk = TPBlock(g, M, h, heads, seq, F=F, dtype=dtype)
+                blk = TPBlock(g, M, h, heads, seq, F=F, dtype=dtype, flags=wflags)
                 blk.load(P)
                 api.tp_pack(g, blk.dq, "X", gx, blk.x)
                 api.tp_pack(g, blk.dq, "X", gd, blk.dout)
@@ -82,17 +83,19 @@ def test_block_vs_oracle(api, grid, dtype):
     out_ref, S = oblock.block_fwd(x, P, seq, heads)
     G = oblock.block_bwd(dout, P, S, seq, heads)
     gr = build_grid(mode, p, d)
-    sx = spec_of(M, h, 3 * h, 0, 0)
-    tol = 1e-4 if dtype == "fp32" else 3e-2
+    sx = spec_of(M, h, 3 * h, 0, 0, wflags)
+    tol = 1e-5 if dtype == "fp32" else 1e-2          # the north star's bars
     gat = lambda key, spec, t: gather_full(gr, spec, {r: per[r][key] for r in range(p)}, t)
-    assert rel_fro(gat("out", sx, "X"), out_ref) <= tol
-    assert rel_fro(gat("dx", sx, "X"), G["x"]) <= tol
-    specs = {"qkv": spec_of(M, h, 3 * h, 0, 0), "o": spec_of(M, h, h, 1, 1),
-             "1": spec_of(M, h, F, 0, 0), "2": spec_of(M, F, h, 1, 1)}
+    errs = {"out": rel_fro(gat("out", sx, "X"), out_ref), "dx": rel_fro(gat("dx", sx, "X"), G["x"])}
+    specs = {"qkv": spec_of(M, h, 3 * h, 0, 0, wflags), "o": spec_of(M, h, h, 1, 1, wflags),
+             "1": spec_of(M, h, F, 0, 0, wflags), "2": spec_of(M, F, h, 1, 1, wflags)}
     for k, sp in specs.items():
-        assert rel_fro(gat("dW_" + k, sp, "W"), G["W_" + k]) <= tol, k
-        assert rel_fro(np.ravel(gat("db_" + k, sp, "B")), G["b_" + k]) <= tol, k
+        errs["dW_" + k] = rel_fro(gat("dW_" + k, sp, "W"), G["W_" + k])
+        errs["db_" + k] = rel_fro(np.ravel(gat("db_" + k, sp, "B")), G["b_" + k])
     for k in ("g1", "be1", "g2", "be2"):
-        for r in range(p):
-            c0, n = per[r]["ln_cols"]
-            assert rel_fro(per[r]["d" + k], G[k][c0:c0 + n]) <= tol, k
+        errs["d" + k] = max(rel_fro(per[r]["d" + k], G[k][per[r]["ln_cols"][0]:
+                                                           per[r]["ln_cols"][0] + per[r]["ln_cols"][1]])
+                            for r in range(p))
+    print(dtype, grid, {k: f"{v:.2e}" for k, v in errs.items()})
+    bad = {k: v for k, v in errs.items() if v > tol}
+    assert not bad, bad

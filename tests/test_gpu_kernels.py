@@ -250,3 +250,25 @@ def test_instrumentation_counts_launches_and_times_gemms(api):
     assert n == 1 and ms > 0 and fl == 2.0 * 256 ** 3
     assert api.tp_launch_count() - n0 >= 1
     api.tp_prof_reset()
+
+
+@pytest.mark.parametrize("M,N,K,ldd", [(197, 197, 64, 200), (130, 130, 64, 136), (300, 197, 128, 256),
+                                       (64, 20, 64, 24), (512, 516, 64, 520)])
+@pytest.mark.parametrize("out", ["fp32", "bf16"])
+def test_gemm_writes_only_inside_d(api, M, N, K, ldd, out):
+    """D rows padded to ldd > N: the columns [N, ldd) of every row stay untouched (a TMA store of
+    a ragged row's last 16-byte granule would zero them - the score padding of the ragged
+    attention backward depended on it), and the M x N block is right."""
+    A = torch.from_numpy(synth.tensor(5, 0, M, K)).cuda().to(torch.bfloat16)
+    B = torch.from_numpy(synth.tensor(5, 1, K, N)).cuda().to(torch.bfloat16)
+    dt = torch.float32 if out == "fp32" else torch.bfloat16
+    D = torch.full((M, ldd), float("-inf"), device="cuda", dtype=dt)
+    ws = torch.empty(api.tp_gemm_ws_bytes(), device="cuda", dtype=torch.uint8)
+    ldb = (N + 7) // 8 * 8          # B's row stride must be a multiple of 8 elements (TMA)
+    Bp = torch.zeros(K, ldb, device="cuda", dtype=torch.bfloat16)
+    Bp[:, :N] = B
+    api.tp_gemm(0, 0, M, N, K, "bf16", A, K, Bp, ldb, None, 0, D, ldd, out, 1.0, None, None, ws)
+    torch.cuda.synchronize()
+    assert bool(torch.isinf(D[:, N:]).all()), "GEMM wrote outside D[:, :N]"
+    ref = dense.matmul(to_np(A), to_np(B))
+    assert rel_fro(to_np(D[:, :N]), ref) <= (2e-5 if out == "fp32" else 1e-2)

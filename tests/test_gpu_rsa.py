@@ -128,10 +128,12 @@ def run_rsa_bwd(api, p, heads, s, d, dtype, Q, K, V, dO, scale=0.0):
     return tuple(np.concatenate([x[i] for x in per], axis=1) for i in range(3))
 
 
-@pytest.mark.parametrize("p", [1, 2, 4])
+@pytest.mark.parametrize("p,s", [(1, 512), (2, 512), (4, 512), (1, 197), (2, 2 * 130), (3, 3 * 197)],
+                         ids=lambda v: str(v))
 @pytest.mark.parametrize("dtype", ["bf16", "fp32"])
-def test_rsa_backward_vs_oracle(api, p, dtype):
-    heads, s, d = 2, 512, 64
+def test_rsa_backward_vs_oracle(api, p, s, dtype):
+    """Aligned and ragged ring blocks (b = 197, 130: score blocks padded to 8 columns)."""
+    heads, d = 2, 64
     Q, K, V = inputs(23, heads, s, d, dtype)
     q = "bf16" if dtype == "bf16" else "fp32"
     dO = np.stack([synth.tensor(23, 8 * h + 3, s, d, dtype=q) for h in range(heads)]).astype(np.float64)
