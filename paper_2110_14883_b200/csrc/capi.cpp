@@ -24,6 +24,21 @@ tp_status fail(tp_status s, const std::string& msg) {
 }
 
 std::atomic<int64_t> g_launches{0};
+std::atomic<int> g_shared_device_grids{0};
+
+cudaError_t set_smem_attr(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  for (const auto& kv : done)
+    if (kv.first == kernel && kv.second == dev) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.emplace_back(kernel, dev);
+  return e;
+}
 
 // ---- collective-contract check (tp_grid_set_contract_check) -----------------
 namespace {
@@ -357,6 +372,7 @@ tp_status tp_grid_init(tp_grid** out, tp_mode mode, int world, int rank, int q, 
       }
     }
   }
+  if (transport == TP_TRANSPORT_LOCAL && world > 1) g_shared_device_grids.fetch_add(1);
   *out = g.release();
   return TP_OK;
 }
@@ -430,6 +446,7 @@ tp_status tp_grid_set_contract_check(tp_grid* g, int enable) {
 
 tp_status tp_grid_destroy(tp_grid* g) {
   if (!g) return TP_OK;
+  if (g->transport == TP_TRANSPORT_LOCAL && g->world > 1 && g->all) g_shared_device_grids.fetch_sub(1);
   if (g->comm_stream) cudaStreamSynchronize(g->comm_stream);
   for (auto& kv : g->ipc_cache) cudaIpcCloseMemHandle(kv.second);
   g->ipc_cache.clear();

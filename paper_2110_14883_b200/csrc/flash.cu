@@ -38,9 +38,10 @@ using namespace ptx;
 #endif
 template <int D>
 constexpr int soft_warps();
-// d = 64 as two CTAs per SM (TP_FLASH_2CTA64): 4 softmax warps, one S and one P buffer, 256 TMEM
-// columns and ~111 KB of shared memory each, so two query tiles share an SM and one CTA's
-// softmax overlaps the other's MMAs
+// d = 64 as two CTAs per SM (TP_FLASH_2CTA64): 4 softmax warps, one S and one P buffer, one K/V
+// stage, 256 TMEM columns and FC<64>::Smem = 83,200 B of shared memory each (Q 16 KB + K/V
+// 32 KB + P 32 KB + barriers), so two query tiles share an SM and one CTA's softmax overlaps the
+// other's MMAs
 #ifndef TP_FLASH_KV64
 #define TP_FLASH_KV64 2  // K / V ring depth for d = 64 (3 measured equal: profiles/r01_exp58_kv64.log)
 #endif
@@ -84,7 +85,6 @@ struct FC {
   static constexpr int StageBytes = KBytes + VBytes;
   static constexpr int XBytes = soft_warps<D>() == 8 ? 2 * 2 * kQT * 4 : 0;  // [tile parity][half][row]
   static constexpr int Smem = QBytes + kv_stages<D>() * StageBytes + p_bufs<D>() * PBytes + XBytes + 1024 + 256;
-  static constexpr int TmemCols = 2 * kKT + (D < 32 ? 32 : D);  // S[2] + O
 };
 
 struct FParams {
@@ -496,8 +496,7 @@ template <int D>
 tp_status launch(const FParams& F, cudaStream_t s) {
   using C = FC<D>;
   auto k = flash_fwd_kernel<D>;
-  static std::once_flag once;
-  std::call_once(once, [&] { cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::Smem); });
+  TP_CUDA(set_smem_attr(reinterpret_cast<const void*>(k), C::Smem));
   dim3 grid(static_cast<unsigned>((F.s + kQT - 1) / kQT), static_cast<unsigned>(F.problems));
   k<<<grid, f_threads<D>(), C::Smem, s>>>(F);
   count_launch();

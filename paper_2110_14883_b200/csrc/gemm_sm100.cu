@@ -578,20 +578,10 @@ tp_status launch(const GemmArgs& g, cudaStream_t s) {
   else
     TP_TRY(make_map(&tb, g.B, g.N, g.K, g.ldb, 64, BK));
 
-  static bool attr_set[2] = {false, false};
   int dev = 0;
   TP_CUDA(cudaGetDevice(&dev));
   auto kern = gemm_tc_kernel<BN, A_MN, B_MN>;
-  {
-    static std::mutex mu;
-    std::lock_guard<std::mutex> lk(mu);
-    static int done_mask = 0;  // per-device bit would be nicer; attribute is per function
-    (void)attr_set;
-    if (!(done_mask & 1)) {
-      TP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
-      done_mask |= 1;
-    }
-  }
+  TP_CUDA(set_smem_attr(reinterpret_cast<const void*>(kern), C::kSmem));
   const int num_m = static_cast<int>((g.M + BM - 1) / BM);
   const int num_n = static_cast<int>((g.N + BN - 1) / BN);
   const int tiles = num_m * num_n;

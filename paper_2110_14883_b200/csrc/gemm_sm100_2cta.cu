@@ -1088,14 +1088,19 @@ template <int BNP, int MC, int EW = 4>
 tp_status launch2(const GemmArgs* gs, int n, cudaStream_t s) {
   using P = PC<BNP, MC, EW>;
   auto kern = gemm_tc2_kernel<BNP, MC, EW>;
-  static int clusters = 0;
+  static int clusters_of[64] = {};  // co-resident clusters, per device
+  int dev = 0;
+  TP_CUDA(cudaGetDevice(&dev));
+  int clusters = 0;
   {
     static std::mutex mu;
     std::lock_guard<std::mutex> lk(mu);
-    if (!clusters) {
+    int& c = clusters_of[dev & 63];
+    if (!c) {
       TP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, P::Smem));
-      clusters = max_clusters(kern, 2 * pairs_of(MC), P::Smem, threads_of<EW>());
+      c = max_clusters(kern, 2 * pairs_of(MC), P::Smem, threads_of<EW>());
     }
+    clusters = c;
   }
   Group G;
   G.nprob = n;
@@ -1143,7 +1148,8 @@ tp_status launch2(const GemmArgs* gs, int n, cudaStream_t s) {
     return e ? std::atoi(e) : 1;
   }();
   for (int i = 0; i < n; ++i)
-    G.p[i].owner_wait = (env_owner && G.p[i].splits > 1 && units <= grid / (2 * pairs_of(MC))) ? 1 : 0;
+    G.p[i].owner_wait = (env_owner && g_shared_device_grids.load() == 0 && G.p[i].splits > 1 &&
+                         units <= grid / (2 * pairs_of(MC))) ? 1 : 0;
   const int tok = prof_begin(0, s, flops);
   TP_CUDA(launch_pdl(kern, dim3(grid), dim3(threads_of<EW>()), P::Smem, s, G));
   count_launch();

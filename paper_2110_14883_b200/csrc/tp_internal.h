@@ -33,6 +33,18 @@ tp_status fail(tp_status s, const std::string& msg);
 
 inline size_t dtype_size(tp_dtype t) { return t == TP_BF16 ? 2 : 4; }
 
+// ---- per-device one-time setup ---------------------------------------------------------
+// Kernel attributes (cudaFuncSetAttribute) belong to a device context: set_smem_attr runs
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, current device); callers
+// on other threads block until it has been applied (a launch must never race ahead of it).
+cudaError_t set_smem_attr(const void* kernel, int bytes);
+
+// Number of live in-process multi-rank grids (TP_TRANSPORT_LOCAL, world > 1). While any exists,
+// other ranks' kernels may share the device, so no GEMM may assume its whole persistent grid is
+// co-resident (the split-K owner-wait / exchange spins on sibling clusters): it falls back to
+// the last-arriver reduction.
+extern std::atomic<int> g_shared_device_grids;
+
 // ---- instrumentation ------------------------------------------------------------------
 extern std::atomic<int64_t> g_launches;
 extern unsigned long long* g_gemm_trace;
