@@ -356,12 +356,16 @@ tp_status tp_attention_bwd(tp_grid* grid, const tp_linear_desc* qkv_desc, int64_
  *   flops            per-GPU flops = 6 M K N / world
  *   mem_x/w/y        per-rank at-rest elements of the X, W and Y shards
  *   t_tensor_us, t_link_us, t_roof_us   flops / peak_tflops, link_bytes / link_gbs, their max
+ *   t_exposed_us     communication the library's schedule leaves exposed (not under a GEMM)
+ *                    at those rates: per collective, received bytes / link_gbs minus the GEMM
+ *                    it overlaps (0 at world == 1 or when either rate is <= 0)
  * peak_tflops / link_gbs <= 0 leave the times at 0. Errors: TP_ERR_CONSTRAINT (grid),
  * TP_ERR_INDIVISIBLE, TP_ERR_ARG (null pointers). */
 typedef struct {
   double paper_elems, counted_elems, link_bytes, flops;
   double mem_x, mem_w, mem_y;
   double t_tensor_us, t_link_us, t_roof_us;
+  double t_exposed_us;
 } tp_cost;
 tp_status tp_cost_model(tp_mode mode, int world, int q, int d, const tp_linear_desc* desc,
                         double peak_tflops, double link_gbs, tp_cost* out);

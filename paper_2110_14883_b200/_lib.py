@@ -49,7 +49,7 @@ EXPORTED = [
 class tp_cost(C.Structure):
     _fields_ = [(n, C.c_double) for n in ("paper_elems", "counted_elems", "link_bytes", "flops",
                                           "mem_x", "mem_w", "mem_y", "t_tensor_us", "t_link_us",
-                                          "t_roof_us")]
+                                          "t_roof_us", "t_exposed_us")]
 
 
 class tp_rsa_desc(C.Structure):

@@ -58,7 +58,7 @@ def model(workload, p, link_gbs=900.0, peak_tflops=None):
     rows = []
     for label, mode, q, d in grids(p):
         tot = {k: 0.0 for k in ("paper_elems", "counted_elems", "link_bytes", "flops",
-                                "t_tensor_us", "t_link_us")}
+                                "t_tensor_us", "t_link_us", "t_exposed_us")}
         ok = True
         for i, (K, N) in enumerate(layers):
             fl = api.TP_FLAG_SOLOMONIK if "solomonik" in label else 0
@@ -80,6 +80,8 @@ def model(workload, p, link_gbs=900.0, peak_tflops=None):
                      "link_mb_per_gpu": round(tot["link_bytes"] / 1e6, 1),
                      "t_tensor_us": round(tot["t_tensor_us"], 1),
                      "t_link_us": round(tot["t_link_us"], 1), "bound": bound,
+                     "exposed_comm_us": round(tot["t_exposed_us"], 1),
+                     "step_estimate_us": round(tot["t_tensor_us"] + tot["t_exposed_us"], 1),
                      "max_pct_of_peak": round(100 * tot["t_tensor_us"] / roof, 1) if roof else None,
                      "paper_table_elems": tot["paper_elems"],
                      "schedule_elems": tot["counted_elems"]})
@@ -99,7 +101,7 @@ def main():
             print(json.dumps(r))
         return
     hdr = ["grid", "gpus", "gflop_per_gpu", "link_mb_per_gpu", "t_tensor_us", "t_link_us", "bound",
-           "max_pct_of_peak"]
+           "max_pct_of_peak", "exposed_comm_us", "step_estimate_us"]
     print(" | ".join(hdr))
     for r in rows:
         print(" | ".join(str(r[h]) for h in hdr))

@@ -809,6 +809,77 @@ tp_status tp_gemm_trace(unsigned long long* buf) {
 }  // extern "C"
 
 // ------------------------------------------------------------------------ analytic cost model
+// Communication the schedules leave exposed (not hidden under a GEMM), one layer fwd + bwd, per
+// rank: every collective costs its received bytes / link_gbs, every GEMM its flops / peak, and a
+// collective that runs under a GEMM costs only what exceeds that GEMM (sched.cpp's overlap
+// structure: SUMMA's next-step broadcast / previous-step reduce under each step's GEMM, 1D's
+// AR(dX) under dW, 3D's row-block pipeline with AG(W) / AG(dY)-remainder / the last reduce /
+// RS(dW) exposed; the depth collectives of 2.5D are exposed).
+static double exposed_comm_us(tp_mode mode, const tp_linear_desc* d, int q, int dd, double p,
+                              double peak_tflops, double link_gbs) {
+  const double M = double(d->M), K = double(d->K), N = double(d->N);
+  const double e = d->dtype == TP_BF16 ? 2.0 : 4.0;
+  auto tl = [&](double elems) { return elems * e / (link_gbs * 1e9) * 1e6; };
+  auto tf = [&](double m, double n, double k) { return 2.0 * m * n * k / (peak_tflops * 1e12) * 1e6; };
+  auto over = [](double comm, double gemm) { return comm > gemm ? comm - gemm : 0.0; };
+  double x = 0;
+  switch (mode) {
+    case TP_1D:
+      if (d->split_1d == 0)  // bwd: AR(dX) [M,K] under the dW GEMM (K x N/p x M)
+        x = over(tl(2.0 * (p - 1) / p * M * K), tf(K, N / p, M));
+      else                   // fwd: AR(Y) [M,N] after the only GEMM
+        x = tl(2.0 * (p - 1) / p * M * N);
+      break;
+    case TP_2D:
+    case TP_2P5D: {
+      const bool solo = d->flags & TP_FLAG_SOLOMONIK;
+      const double mb = solo ? M / q : M / (double(dd) * q), kq = K / q, nq = N / q;
+      const int steps = solo ? q / dd : q;
+      // a broadcast panel is received by the q-1 non-roots: (q-1)/q of the steps per rank
+      const double f = double(q - 1) / q;
+      const double sx = mb * kq * f, sw = kq * nq * f, sy = mb * nq;
+      const double rx = mb * kq, rw = kq * nq;  // reduce partials: every rank's time
+      // fwd (AB): first step's X and W panels, then step t+1's under step t's GEMM
+      x += tl(sx + sw);
+      for (int t = 0; t + 1 < steps; ++t) x += over(tl(sx + sw), tf(mb, nq, kq));
+      // ABT: W panel k+1 and reduce k-1 under GEMM k; first W and last reduce exposed
+      x += tl(sw);
+      for (int k = 0; k < steps; ++k)
+        x += over(tl((k + 1 < steps ? sw : 0) + (k > 0 ? rx : 0)), tf(mb, kq, nq));
+      x += tl(rx);
+      // ATB: X panel k+1 and reduce k-1 under GEMM k
+      x += tl(sx);
+      for (int k = 0; k < steps; ++k)
+        x += over(tl((k + 1 < steps ? sx : 0) + (k > 0 ? rw : 0)), tf(kq, nq, mb));
+      x += tl(rw);
+      if (mode == TP_2P5D && dd > 1) {
+        if (solo) x += tl(2.0 * (dd - 1) / dd * sy) + tl(rx) + tl(rw);  // AR(Y), bcast dX, dW
+        else if (d->flags & TP_FLAG_W25_DEPTH_SHARDED)
+          x += 2.0 * tl(double(dd - 1) / dd * rw);                       // AG(W) + RS(dW)
+        else
+          x += tl(2.0 * (dd - 1) / dd * rw);                              // AR(dW)
+      }
+      break;
+    }
+    case TP_3D: {
+      const double l = q, mb = M / (l * l), kl = K / l, kb = K / (l * l), nl = N / l;
+      // fwd: AG(W) exposed; AG(X)'s remote blocks under block 0; reduce j under block j+1; last
+      x += tl((l - 1) * kb * nl);
+      x += over(tl((l - 1) * mb * kl), tf(mb, nl, kl));
+      for (int i = 1; i < q; ++i) x += over(tl(mb * nl), tf(mb, nl, kl));
+      x += tl(mb * nl);
+      // bwd: AG(dY) remote blocks under dX block 0; reduce j under dX block j+1; the last dX
+      // reduce under the dW GEMM; RS(dW) exposed
+      x += over(tl((l - 1) * mb * nl), tf(mb, kl, nl));
+      for (int i = 1; i < q; ++i) x += over(tl(mb * kl), tf(mb, kl, nl));
+      x += over(tl(mb * kl), tf(kl, nl, l * mb));
+      x += tl((l - 1) / l * kl * nl);
+      break;
+    }
+  }
+  return x;
+}
+
 // the paper's Table row next to what the library's schedules move,
 // per-GPU link bytes, flops and at-rest shard sizes, and the roofline times.
 // Written independently of oracle/closed_forms.py (tests compare the two).
@@ -875,6 +946,8 @@ extern "C" tp_status tp_cost_model(tp_mode mode, int world, int q, int d, const 
   if (peak_tflops > 0) c.t_tensor_us = c.flops / (peak_tflops * 1e12) * 1e6;
   if (link_gbs > 0) c.t_link_us = c.link_bytes / (link_gbs * 1e9) * 1e6;
   c.t_roof_us = c.t_tensor_us > c.t_link_us ? c.t_tensor_us : c.t_link_us;
+  if (peak_tflops > 0 && link_gbs > 0 && world > 1)
+    c.t_exposed_us = exposed_comm_us(mode, desc, j, dd, p, peak_tflops, link_gbs);
   *out = c;
   return TP_OK;
 }

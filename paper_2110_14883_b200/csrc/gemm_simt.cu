@@ -186,7 +186,11 @@ tp_status gemm(const GemmArgs& g, cudaStream_t s) {
     if (sms <= 0) sms = 148;
   }
   const int64_t pair_tiles = ((g.M + 255) / 256) * ((g.N + 255) / 256);
-  const bool pair_ok = force == 2 || (force == 0 && pair_tiles >= sms / 2);
+  // Few output tiles and a long K (e.g. C4's dW 192 x 403456 x 576: ten 1-CTA tiles) starve
+  // the 1-CTA kernel, which cannot split K: the pair kernel splits K across the idle SM pairs.
+  const int64_t tiles1 = ((g.M + 127) / 128) * ((g.N + 127) / 128);
+  const bool long_k = tiles1 < sms / 2 && (g.K + 63) / 64 >= 64 && g.ws && g.ws_bytes;
+  const bool pair_ok = force == 2 || (force == 0 && (pair_tiles >= sms / 2 || long_k));
   if (force != 1 && pair_ok && gemm_tc2_supported(g)) return gemm_tc2_bf16(g, s);
   return gemm_tc_bf16(g, s);
 }

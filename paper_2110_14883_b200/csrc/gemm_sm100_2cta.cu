@@ -103,11 +103,12 @@ struct Group {
   Prob p[kMaxProbs];
   int nprob;
   int total_units;
+  int raster;  // pair-tile rows per raster band (8; TP_GEMM_RASTER for measurements)
   unsigned long long* trace;  // optional per-CTA wait-cycle counters (tp_gemm_trace)
 };
 
-__device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb, int& nb) {
-  constexpr int G = 8;  // pair-tile rows per raster band
+__device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb, int& nb, int G) {
+  // G = pair-tile rows per raster band (Group::raster)
   const int band = t / (G * num_n);
   const int m_start = band * G;
   const int band_m = min(G, num_m - m_start);
@@ -149,23 +150,23 @@ __device__ __forceinline__ Unit unit_of(const Group& G, int u, int pair) {
   const int st = lu / P.splits;
   x.split = lu % P.splits;
   if (MC == 5) {  // both pairs on the same tile; `split` = which half of K
-    tile_coords(st, P.num_m, P.num_n, x.mb, x.nb);
+    tile_coords(st, P.num_m, P.num_n, x.mb, x.nb, G.raster);
     x.split = pair;
     x.ptile = st;
     return x;
   } else if (MC == 4) {
     int mbs, nbs;
-    tile_coords(st, (P.num_m + 1) / 2, (P.num_n + 1) / 2, mbs, nbs);
+    tile_coords(st, (P.num_m + 1) / 2, (P.num_n + 1) / 2, mbs, nbs, G.raster);
     x.mb = mbs * 2 + (pair >> 1);
     x.nb = nbs * 2 + (pair & 1);
   } else if (MC == 3) {
     int mbs;
-    tile_coords(st, (P.num_m + 1) / 2, P.num_n, mbs, x.nb);
+    tile_coords(st, (P.num_m + 1) / 2, P.num_n, mbs, x.nb, G.raster);
     x.mb = mbs * 2 + pair;
   } else {
     const int num_ns = (P.num_n + MC - 1) / MC;
     int nbs;
-    tile_coords(st, P.num_m, num_ns, x.mb, nbs);
+    tile_coords(st, P.num_m, num_ns, x.mb, nbs, G.raster);
     x.nb = nbs * MC + pair;
   }
   x.ptile = st * pairs_of(MC) + pair;  // dense pair-tile id (split-K partials / counters)
@@ -1102,8 +1103,13 @@ tp_status launch2(const GemmArgs* gs, int n, cudaStream_t s) {
     }
     clusters = c;
   }
+  static const int env_raster = [] {
+    const char* e = std::getenv("TP_GEMM_RASTER");
+    return e ? std::max(1, std::atoi(e)) : 8;
+  }();
   Group G;
   G.nprob = n;
+  G.raster = env_raster;
   G.trace = g_gemm_trace;
   char* ws = static_cast<char*>(gs[0].ws);
   size_t ws_left = ws ? gs[0].ws_bytes : 0;

@@ -7,6 +7,8 @@
 // finished with, so step t+1's transfer overlaps step t's GEMM; the reduce of step k's
 // partial overlaps step k+1's GEMM. In 3D the reduce-scatter of dX overlaps the dW GEMM.
 // Every collective's root uses its own shard in place (no staging copy).
+#include <algorithm>
+#include <cmath>
 #include <cstdlib>
 
 #include "sched.h"
@@ -67,17 +69,28 @@ struct Ctx {
     a.bias = bias;
     a.ws = gws;
     a.ws_bytes = gws_bytes;
-    a.reserve_sms = comm_sms();
+    a.reserve_sms = comm_sms(2.0 * double(M) * double(N) * double(K));
     return a;
   }
-  // SMs left to the collectives that run on `cs` under the GEMMs (TP_COMM_SMS, default 16)
-  int comm_sms() const {
-    if (g->world == 1 || R.cs == R.s) return 0;
-    static const int n = [] {
+  // Bytes this rank's collectives move on `cs` while the next GEMM runs (set by the schedule
+  // right before the GEMM it overlaps; 0 = nothing in flight under it).
+  double ovb = 0;
+  // SMs the GEMM leaves to the collective running under it, sized to the transfer: none when
+  // nothing overlaps or the transport needs no SMs (LOCAL: copy engines + small sum kernels);
+  // over NCCL, enough channels (one CTA each, ~40 GB/s per channel over NVLink 5) for the
+  // transfer to finish within the GEMM at ~1.4 PFLOP/s, 2..16 (the NCCL communicators are
+  // created with maxCTAs = 16). TP_COMM_SMS=n forces n.
+  int comm_sms(double gemm_flops) const {
+    if (g->world == 1 || R.cs == R.s || ovb <= 0) return 0;
+    static const int forced = [] {
       const char* e = std::getenv("TP_COMM_SMS");
-      return e ? std::atoi(e) : 16;
+      return e ? std::atoi(e) : -1;
     }();
-    return n;
+    if (forced >= 0) return forced;
+    if (g->transport != TP_TRANSPORT_NCCL) return 0;
+    const double t = std::max(gemm_flops / 1.4e15, 1e-6);
+    const int k = static_cast<int>(std::ceil(ovb / (40e9 * t)));
+    return std::min(16, std::max(2, k));
   }
   // split-K scratch shared by this schedule's GEMMs (they run in order on `s`)
   void* gws = nullptr;
@@ -314,7 +327,9 @@ tp_status bwd_1d(Ctx& C, const void* dy, const void* x, const void* w, void* dx,
       }
     }
     // dW_r = X^T . dY_r overlaps the all-reduce
+    C.ovb = (dx && p > 1) ? 2.0 * (p - 1) / p * double(M) * double(K) * C.esz : 0.0;
     TP_TRY(C.mm(K, Nl, M, x, true, dy, false, dw, C.dt, d->alpha, nullptr, nullptr));
+    C.ovb = 0;
     if (dbias) TP_TRY(C.colsum(dy, M, Nl, dbias, scratch));
     return TP_OK;
   }
@@ -397,12 +412,15 @@ tp_status summa_ab(Ctx& C, const Plane& P, const void* x, const void* W, const v
   };
   TP_TRY(issue(P.t0));
   if (P.t0 + 1 < P.t1) TP_TRY(issue(P.t0 + 1));
+  const double panels = double(P.mb * P.kq + P.kq * P.nq) * C.esz;
   for (int t = P.t0; t < P.t1; ++t) {
     TP_CUDA(cudaStreamWaitEvent(C.R.s, ready[t & 1], 0));
     const bool last = t == P.t1 - 1;
+    C.ovb = last ? 0.0 : panels;  // step t+1's broadcasts run under this GEMM
     TP_TRY(C.mm(P.mb, P.nq, P.kq, xpan(t), false, wpan(t), false, last ? y : acc,
                 last ? C.dt : TP_FP32, last ? alpha : 1.f, t > P.t0 ? acc : nullptr,
                 last ? bias : nullptr));
+    C.ovb = 0;
     if (t + 2 < P.t1) {
       TP_TRY(C.order(C.R.s, C.R.cs));  // panel buffers of step t are free again
       TP_TRY(issue(t + 2));
@@ -452,8 +470,10 @@ tp_status cannon_ab(Ctx& C, const Plane& P, const void* x, const void* W, const 
       TP_TRY(P.col->shift(cw, nw, P.kq * P.nq, C.dt, 1, C.R.cs));
       moved = C.record(C.R.cs);
     }
+    C.ovb = last ? 0.0 : double(P.mb * P.kq + P.kq * P.nq) * C.esz;  // next shifts under it
     TP_TRY(C.mm(P.mb, P.nq, P.kq, cx, false, cw, false, last ? y : acc, last ? C.dt : TP_FP32,
                 last ? alpha : 1.f, t > 0 ? acc : nullptr, last ? bias : nullptr));
+    C.ovb = 0;
     if (!last) {
       TP_CUDA(cudaStreamWaitEvent(C.R.s, moved, 0));
       cx = nx;
@@ -487,7 +507,10 @@ tp_status summa_abt(Ctx& C, const Plane& P, const void* dy, const void* W, void*
   for (int k = P.t0; k < P.t1; ++k) {
     TP_CUDA(cudaStreamWaitEvent(C.R.s, ready[k & 1], 0));
     void* part = P.j == k ? dx : bp[k & 1];  // the root reduces in place into dX
+    // under this GEMM: step k+1's W broadcast and step k-1's partial reduce
+    C.ovb = double(k + 1 < P.t1 ? P.kq * P.nq : 0) * C.esz + double(k > P.t0 ? P.mb * P.kq : 0) * C.esz;
     TP_TRY(C.mm(P.mb, P.kq, P.nq, dy, false, wpan(k), true, part, C.dt, alpha, nullptr, nullptr));
+    C.ovb = 0;
     TP_TRY(C.order(C.R.s, C.R.cs));
     TP_TRY(P.row->reduce(part, dx, P.mb * P.kq, C.dt, k, C.R.cs));
     if (k + 2 < P.t1) TP_TRY(issue(k + 2));
@@ -517,7 +540,9 @@ tp_status summa_atb(Ctx& C, const Plane& P, const void* x, const void* dy, void*
   for (int k = P.t0; k < P.t1; ++k) {
     TP_CUDA(cudaStreamWaitEvent(C.R.s, ready[k & 1], 0));
     void* part = P.i == k ? dwt : bp[k & 1];
+    C.ovb = double(k + 1 < P.t1 ? P.mb * P.kq : 0) * C.esz + double(k > P.t0 ? P.kq * P.nq : 0) * C.esz;
     TP_TRY(C.mm(P.kq, P.nq, P.mb, xpan(k), true, dy, false, part, C.dt, alpha, nullptr, nullptr));
+    C.ovb = 0;
     TP_TRY(C.order(C.R.s, C.R.cs));
     TP_TRY(P.col->reduce(part, dwt, P.kq * P.nq, C.dt, k, C.R.cs));
     if (k + 2 < P.t1) TP_TRY(issue(k + 2));
@@ -826,6 +851,7 @@ tp_status bwd_2d(Ctx& C, const void* dy, const void* x, const void* w, const voi
 struct Cube {
   Comm *cx, *cw, *cy;  // X-gather / W-gather / Y-scatter lines
   int ys_coord;         // this rank's coordinate along the Y-scatter axis
+  int xg_coord;         // ... and along the X-gather axis
   int64_t l, mb, ml, kb, kl, nl;
 };
 
@@ -838,6 +864,7 @@ Cube cube_of(Ctx& C) {
   Q.cw = g->axis[0].get();
   Q.cy = g->axis[ax_y].get();
   Q.ys_coord = g->coords[ax_y];
+  Q.xg_coord = g->coords[ax_x];
   Q.l = g->q;
   Q.mb = C.d->M / (Q.l * Q.l);
   Q.ml = C.d->M / Q.l;
@@ -981,15 +1008,32 @@ tp_status fwd_3d(Ctx& C, const void* x, const void* w, const void* bias, void* y
   void* Wg = C.sv(Q.kl * Q.nl);  // W[b,c] [K/l, N/l]
   void* P = C.ws(Q.ml * Q.nl);
   if (C.R.plan) return TP_OK;
-  TP_TRY(Q.cx->group_start());
-  TP_TRY(Q.cx->allgather(x, Xg, Q.mb * Q.kl, C.dt, C.R.cs));
-  TP_TRY(Q.cw->allgather(w, Wg, Q.kb * Q.nl, C.dt, C.R.cs));
-  TP_TRY(Q.cx->group_end());
-  TP_TRY(C.order(C.R.cs, C.R.s));
-  TP_TRY(C.mm(Q.ml, Q.nl, Q.kl, Xg, false, Wg, false, P, C.dt, alpha, nullptr,
-              Q.ys_coord == 0 ? bias : nullptr));
+  // Pipelined by the row blocks of the gathered X (block j = X-gather member j's shard):
+  //   cs: AG(W), then AG(X);   s: block `own` (this rank's own X rows: no wait for AG(X)),
+  //   then the others; every block's partial P_j is reduced to Y-scatter member j (RS(P) over
+  //   the Y line = one reduce per row block) while the next block's GEMM runs.
+  // Exposed: AG(W) and the last block's reduce (vs AG(X) + AG(W) + the whole RS).
+  // Every member of a Y line has the same `own` (the X-gather coordinate), so the lines' reduce
+  // sequences agree.
+  const int l = static_cast<int>(Q.l), own = Q.xg_coord;
   TP_TRY(C.order(C.R.s, C.R.cs));
-  TP_TRY(Q.cy->reducescatter(P, y, Q.mb * Q.nl, C.dt, C.R.cs));
+  TP_TRY(Q.cw->allgather(w, Wg, Q.kb * Q.nl, C.dt, C.R.cs));
+  cudaEvent_t ev_w = C.record(C.R.cs);
+  TP_TRY(Q.cx->allgather(x, Xg, Q.mb * Q.kl, C.dt, C.R.cs));
+  cudaEvent_t ev_x = C.record(C.R.cs);
+  TP_CUDA(cudaStreamWaitEvent(C.R.s, ev_w, 0));
+  for (int i = 0; i < l; ++i) {
+    const int blk = (own + i) % l;
+    if (i == 1) TP_CUDA(cudaStreamWaitEvent(C.R.s, ev_x, 0));
+    const void* A = blk == own ? x : static_cast<const char*>(Xg) + blk * Q.mb * Q.kl * C.esz;
+    void* Pb = static_cast<char*>(P) + blk * Q.mb * Q.nl * C.esz;
+    C.ovb = i == 0 ? double((l - 1) * Q.mb * Q.kl) * C.esz : double(Q.mb * Q.nl) * C.esz;
+    TP_TRY(C.mm(Q.mb, Q.nl, Q.kl, A, false, Wg, false, Pb, C.dt, alpha, nullptr,
+                Q.ys_coord == 0 ? bias : nullptr));
+    C.ovb = 0;
+    TP_TRY(C.order(C.R.s, C.R.cs));
+    TP_TRY(Q.cy->reduce(Pb, y, Q.mb * Q.nl, C.dt, blk, C.R.cs));
+  }
   return TP_OK;
 }
 
@@ -1023,6 +1067,7 @@ tp_status bwd_3d(Ctx& C, const void* dy, const void* x, const void* w, const voi
     TP_TRY(Q.cx->allgather(x, const_cast<void*>(Xg), Q.mb * Q.kl, C.dt, C.R.cs));
     TP_TRY(Q.cw->allgather(w, const_cast<void*>(Wg), Q.kb * Q.nl, C.dt, C.R.cs));
     TP_TRY(Q.cx->group_end());
+    TP_TRY(C.order(C.R.cs, C.R.s));  // the dX blocks below read W[b,c] without further waits
   }
   void* dYg = C.ws(Q.ml * Q.nl);
   void* Px = dx ? C.ws(Q.ml * Q.kl) : nullptr;
@@ -1030,14 +1075,32 @@ tp_status bwd_3d(Ctx& C, const void* dy, const void* x, const void* w, const voi
   float* scratch = dbias ? C.colsum_scratch(Q.nl) : nullptr;
   void* dbt = dbias ? C.ws(Q.nl) : nullptr;
   if (C.R.plan) return TP_OK;
-  TP_TRY(Q.cy->allgather(dy, dYg, Q.mb * Q.nl, C.dt, C.R.cs));  // dY[a,c]
-  TP_TRY(C.order(C.R.cs, C.R.s));
+  // dY[a,c] = AG(dY over the Y line); block j comes from Y-line member j. The dX partial is
+  // pipelined by those row blocks: block `ys` (this rank's own dY rows) first, without waiting
+  // for the gather; each block's partial is reduced to X-line member j (RS(Px) over the X line =
+  // one reduce per row block) under the next GEMM; the dW GEMM needs all of dY[a,c] and its
+  // reduce-scatter over the W line is the one exposed collective.
+  const int l = static_cast<int>(Q.l), ys = Q.ys_coord;
+  TP_TRY(C.order(C.R.s, C.R.cs));
+  TP_TRY(Q.cy->allgather(dy, dYg, Q.mb * Q.nl, C.dt, C.R.cs));
+  cudaEvent_t ev_dy = C.record(C.R.cs);
   if (dx) {
-    TP_TRY(C.mm(Q.ml, Q.kl, Q.nl, dYg, false, Wg, true, Px, C.dt, alpha, nullptr, nullptr));
-    TP_TRY(C.order(C.R.s, C.R.cs));
-    TP_TRY(Q.cx->reducescatter(Px, dx, Q.mb * Q.kl, C.dt, C.R.cs));  // overlaps the dW GEMM
+    for (int i = 0; i < l; ++i) {
+      const int blk = (ys + i) % l;
+      if (i == 1) TP_CUDA(cudaStreamWaitEvent(C.R.s, ev_dy, 0));
+      const void* A = blk == ys ? dy : static_cast<const char*>(dYg) + blk * Q.mb * Q.nl * C.esz;
+      void* Pb = static_cast<char*>(Px) + blk * Q.mb * Q.kl * C.esz;
+      C.ovb = i == 0 ? double((l - 1) * Q.mb * Q.nl) * C.esz : double(Q.mb * Q.kl) * C.esz;
+      TP_TRY(C.mm(Q.mb, Q.kl, Q.nl, A, false, Wg, true, Pb, C.dt, alpha, nullptr, nullptr));
+      C.ovb = 0;
+      TP_TRY(C.order(C.R.s, C.R.cs));
+      TP_TRY(Q.cx->reduce(Pb, dx, Q.mb * Q.kl, C.dt, blk, C.R.cs));
+    }
   }
+  TP_CUDA(cudaStreamWaitEvent(C.R.s, ev_dy, 0));
+  C.ovb = dx ? double(Q.mb * Q.kl) * C.esz : 0.0;  // the last dX block's reduce
   TP_TRY(C.mm(Q.kl, Q.nl, Q.ml, Xg, true, dYg, false, Pw, C.dt, alpha, nullptr, nullptr));
+  C.ovb = 0;
   if (dbias) TP_TRY(C.colsum(dYg, Q.ml, Q.nl, dbt, scratch));
   TP_TRY(C.order(C.R.s, C.R.cs));
   TP_TRY(Q.cw->reducescatter(Pw, dw, Q.kb * Q.nl, C.dt, C.R.cs));

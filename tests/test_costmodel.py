@@ -140,3 +140,25 @@ def test_solomonik_extents_match_oracle():
             api.tp_grid_destroy(g)
     with pytest.raises(api.TPError):   # q = 2 is not divisible by d = 4 ... (p = 16, q = 2, d = 4)
         api.tp_cost_model("2.5d", 16, ds, q=2, depth=4)
+
+
+def test_exposed_comm_term():
+    """The exposed-communication estimate: 0 on one GPU; never more than the whole transfer
+    time; the 3D row-block pipeline leaves less exposed than 2D SUMMA at q=2 for C3-HEAD (what the
+    pipelining is for); more link bandwidth never exposes more."""
+    from paper_2110_14883_b200 import api
+    M = h = 16384
+    for mode, p in (("1d", 1), ("2d", 1), ("3d", 1)):
+        c = api.tp_cost_model(mode, p, api.desc(M, h, h), peak_tflops=1500, link_gbs=900)
+        assert c["t_exposed_us"] == 0
+    for mode, p, flags in (("1d", 8, 0), ("2d", 4, 0), ("2.5d", 8, 0), ("2.5d", 8, 1), ("3d", 8, 0)):
+        d = 2 if mode == "2.5d" else 1
+        for par in (0, 1):
+            ds = api.desc(M, h, h, split_1d=par, parity_3d=par, flags=flags)
+            c = api.tp_cost_model(mode, p, ds, depth=d, peak_tflops=1500, link_gbs=900)
+            assert 0 <= c["t_exposed_us"] <= c["t_link_us"] * 1.0000001 + 1e-9, (mode, par)
+            c2 = api.tp_cost_model(mode, p, ds, depth=d, peak_tflops=1500, link_gbs=1800)
+            assert c2["t_exposed_us"] <= c["t_exposed_us"] + 1e-9
+    e3 = api.tp_cost_model("3d", 8, api.desc(M, h, h), peak_tflops=1500, link_gbs=900)
+    e2 = api.tp_cost_model("2d", 4, api.desc(M, h, h), peak_tflops=1500, link_gbs=900)
+    assert e3["t_exposed_us"] < e2["t_exposed_us"]

@@ -272,3 +272,11 @@ def test_gemm_writes_only_inside_d(api, M, N, K, ldd, out):
     assert bool(torch.isinf(D[:, N:]).all()), "GEMM wrote outside D[:, :N]"
     ref = dense.matmul(to_np(A), to_np(B))
     assert rel_fro(to_np(D[:, :N]), ref) <= (2e-5 if out == "fp32" else 1e-2)
+
+
+@pytest.mark.parametrize("M,K,N,ta", [(192, 65536, 576, 1), (256, 32768, 384, 0), (136, 16384, 200, 1)])
+def test_gemm_few_tiles_long_k(api, M, K, N, ta):
+    """Few output tiles, long K (C4's QKV dW shape class): dispatched to the split-K pair
+    kernel; fp32 out against the oracle."""
+    got, ref = _gemm_case(api, ta, 0, M, N, K, "bf16", "fp32", seed=M + K, split_k=True)
+    assert rel_fro(got, ref) <= 2e-5
