@@ -25,6 +25,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <climits>
 #include <cstdlib>
 #include <mutex>
 
@@ -918,6 +919,210 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
   }
 }
 
+// ------------------------------------------------------------------ wide pair tiles (512 x 256)
+// For the large products (C3-HEAD, C5: the per-rank GEMMs of the north-star configurations),
+// which run at the 1 kW power cap: a CTA pair computes a 512 x 256 tile. Each CTA stages 256 rows
+// of A and 128 columns of B per k-block, and the leader issues TWO M=256 N=256 MMAs per K step
+// (A rows 0-127 and 128-255 of both CTAs) into the two 256-column halves of the 512-column TMEM,
+// so every B k-block serves 512 rows: 25% fewer L2 -> SM bytes per flop than the 256 x 256 pair
+// tile, and bigger tiles mean fewer distinct operand panels per wave (less DRAM traffic), i.e.
+// less energy per flop - the currency at the power cap (profiles/r02_ncu_gemm_shapes.md).
+// Single TMEM accumulator: the epilogue (4 warps per CTA, both row halves) drains it before the
+// next unit's first MMA. No split-K, no K-panels / D row-panels (the caller checks).
+constexpr int kWStages = 4;
+constexpr int kWABytes = 2 * kBM * kBK * 2;  // 256 rows x 64 k
+constexpr int kWBBytes = 128 * kBK * 2;      // 128 columns x 64 k (half of the pair's 256)
+constexpr int kWStageBytes = kWABytes + kWBBytes;
+constexpr int kWSmem = kWStages * kWStageBytes + 2 * 4 * kOutBytes + 1024 + 256;
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(threads_of<4>(), 1)
+    gemm_tc2w_kernel(const __grid_constant__ Group G) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + kWStages * kWABytes;
+  uint8_t* sOut = sB + kWStages * kWBBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sOut + 2 * 4 * kOutBytes);
+  uint64_t* empty = full + kWStages;
+  uint64_t* tfull = empty + kWStages;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 1);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_rank() & 1;
+  const bool leader = rank == 0;
+  const int cid = blockIdx.x / 2, ncl = gridDim.x / 2;
+
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < G.nprob; ++i) {
+      tma_prefetch(&G.p[i].tmA[0]);
+      tma_prefetch(&G.p[i].tmB[0]);
+      tma_prefetch(&G.p[i].tmD[0]);
+    }
+    for (int s = 0; s < kWStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 2 * 4);  // 4 epilogue warps x 2 CTAs
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_cg2(tslot, 512);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tslot;
+  pdl_launch_dependents();
+  pdl_wait();
+
+  auto unit_prob = [&](int u, int& lu) {
+    int pi = 0;
+#pragma unroll
+    for (int i = 1; i < kMaxProbs; ++i)
+      if (i < G.nprob && u >= G.p[i].unit0) pi = i;
+    lu = u - G.p[pi].unit0;
+    return pi;
+  };
+
+  if (warp == 0) {
+    // ===== TMA producer (both CTAs; bytes land on the leader's `full`) =====
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int u = cid; u < G.total_units; u += ncl) {
+      int lu;
+      const Prob& pr = G.p[unit_prob(u, lu)];
+      int mb, nb;
+      tile_coords(lu, pr.num_m, pr.num_n, mb, nb, G.raster);
+      const int m0 = mb * 512 + static_cast<int>(rank) * 256;
+      const int n0 = nb * 256 + static_cast<int>(rank) * 128;
+      const bool a_mn = pr.a_mn != 0, b_mn = pr.b_mn != 0;
+      const CUtensorMap* mA = &pr.tmA[0];
+      const CUtensorMap* mB = &pr.tmB[0];
+      for (int kb = 0; kb < pr.num_kb; ++kb) {
+        const int kc = kb * kBK;
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (elect_one()) {
+          if (leader) mbar_expect_tx(&full[stage], 2 * kWStageBytes);
+          uint8_t* a_dst = sA + stage * kWABytes;
+          uint8_t* b_dst = sB + stage * kWBBytes;
+          if (!a_mn) {
+            tma_load_2d_pair(mA, &full[stage], a_dst, kc, m0);  // one [256 rows][128 B] box
+          } else {
+            for (int c = 0; c < 4; ++c)
+              tma_load_2d_pair(mA, &full[stage], a_dst + c * (kBK * 128), m0 + c * 64, kc);
+          }
+          if (!b_mn) {
+            tma_load_2d_pair(mB, &full[stage], b_dst, kc, n0);
+          } else {
+            for (int c = 0; c < 2; ++c)
+              tma_load_2d_pair(mB, &full[stage], b_dst + c * (kBK * 128), n0 + c * 64, kc);
+          }
+        }
+        __syncwarp();
+        if (++stage == kWStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader) {
+      // ===== MMA issuer: two M=256 N=256 MMAs per K step (row halves 0 / 1 of each CTA) =====
+      int stage = 0;
+      uint32_t phase = 0, acc_phase = 0;
+      for (int u = cid; u < G.total_units; u += ncl) {
+        int lu;
+        const Prob& pr = G.p[unit_prob(u, lu)];
+        const uint32_t idesc = idesc_bf16_f32(256, 256, pr.a_mn != 0, pr.b_mn != 0);
+        const uint32_t a_step4 = pr.a_mn ? 2048u / 16 : 32u / 16;
+        const uint32_t b_step4 = pr.b_mn ? 2048u / 16 : 32u / 16;
+        // second row half: +128 rows x 128 B (K-major) = +2 MN chunks of 64 x 128 B (MN-major)
+        constexpr uint32_t a_half4 = (kBM * 128) / 16;
+        const uint64_t a_desc0 = sdesc_sw128(smem_u32(sA), pr.a_mn ? kBK * 128 : 16, 1024);
+        const uint64_t b_desc0 = sdesc_sw128(smem_u32(sB), pr.b_mn ? kBK * 128 : 16, 1024);
+        mbar_wait(tempty, acc_phase ^ 1);  // the epilogue drained the previous unit
+        __syncwarp();
+        tc_fence_after();
+        for (int kb = 0; kb < pr.num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t ad = a_desc0 + static_cast<uint32_t>(stage * (kWABytes / 16));
+          const uint64_t bd = b_desc0 + static_cast<uint32_t>(stage * (kWBBytes / 16));
+          if (elect_one()) {
+#pragma unroll
+            for (int k = 0; k < kBK / 16; ++k) {
+              const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
+              umma_bf16_cg2(tmem_base, ad + k * a_step4, bd + k * b_step4, idesc, acc);
+              umma_bf16_cg2(tmem_base + 256, ad + a_half4 + k * a_step4, bd + k * b_step4, idesc, acc);
+            }
+            umma_commit_cg2_mc(&empty[stage], 0x3);
+          }
+          __syncwarp();
+          if (++stage == kWStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (elect_one()) umma_commit_cg2_mc(tfull, 0x3);
+        __syncwarp();
+        acc_phase ^= 1;
+      }
+    }
+  } else {
+    // ===== epilogue warps 2..5 (both CTAs): lane quadrant warp % 4, both row halves =====
+    const int quad = warp & 3;
+    uint8_t* stg = sOut + (warp - 2) * 2 * kOutBytes;
+    int nbox = 0;
+    uint32_t acc_phase = 0;
+    for (int u = cid; u < G.total_units; u += ncl) {
+      int lu;
+      const Prob& pr = G.p[unit_prob(u, lu)];
+      int mb, nb;
+      tile_coords(lu, pr.num_m, pr.num_n, mb, nb, G.raster);
+      const int64_t n0 = static_cast<int64_t>(nb) * 256;
+      if (lane == 0) mbar_wait_sleep(tfull, acc_phase, 200);
+      __syncwarp();
+      tc_fence_after();
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {
+        const int64_t row0 = static_cast<int64_t>(mb) * 512 + rank * 256 + h * 128 + quad * 32;
+        const int64_t row = row0 + lane;
+        const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
+                               static_cast<uint32_t>(h * 256);
+        if (pr.out_bf16) {
+#pragma unroll 1
+          for (int sub = 0; sub < 4; ++sub) {
+            float v[64];
+            tmem_cols<64>(t_row, sub, v);
+            store_box<64>(pr, stg, nbox, lane, v, row, n0 + sub * 64, row0);
+          }
+        } else {
+#pragma unroll 1
+          for (int sub = 0; sub < 8; ++sub) {
+            float v[32];
+            tmem_cols<32>(t_row, sub, v);
+            store_box<32>(pr, stg, nbox, lane, v, row, n0 + sub * 32, row0);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(tempty, 0);
+      acc_phase ^= 1;
+    }
+    if (lane == 0) bulk_wait_read0();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_cg2(tmem_base, 512);
+  }
+}
+
 // ------------------------------------------------------------------------------ host side
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -1166,6 +1371,89 @@ tp_status launch2(const GemmArgs* gs, int n, cudaStream_t s) {
 
 }  // namespace
 
+// ---- wide pair tiles (gemm_tc2w_kernel): up to kMaxProbs problems, no split-K / panels
+bool gemm_wide_ok(const GemmArgs& g) {
+  return g.npanels <= 1 && g.dpanels <= 1 && g.K > 0 && gemm_tc2_supported(g);
+}
+
+tp_status launch_wide(const GemmArgs* gs, int n, cudaStream_t s) {
+  if (n < 1 || n > kMaxProbs) return fail(TP_ERR_UNSUPPORTED, "wide gemm: 1..4 problems");
+  auto kern = gemm_tc2w_kernel;
+  static int clusters_of[64] = {};
+  int dev = 0;
+  TP_CUDA(cudaGetDevice(&dev));
+  int clusters = 0;
+  {
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
+    int& c = clusters_of[dev & 63];
+    if (!c) {
+      TP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kWSmem));
+      c = max_clusters(kern, 2, kWSmem, threads_of<4>());
+    }
+    clusters = c;
+  }
+  static const int env_raster = [] {
+    const char* e = std::getenv("TP_GEMM_WIDE_RASTER");
+    return e ? std::max(1, std::atoi(e)) : 8;
+  }();
+  Group G;
+  G.nprob = n;
+  G.raster = env_raster;
+  G.trace = nullptr;
+  const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  int units = 0;
+  double flops = 0;
+  for (int i = 0; i < n; ++i) {
+    const GemmArgs& g = gs[i];
+    Prob& pr = G.p[i];
+    pr.a_mn = g.trans_a ? 1 : 0;
+    pr.b_mn = g.trans_b ? 0 : 1;
+    if (!pr.a_mn) TP_TRY(make_map2(&pr.tmA[0], BF, 2, g.A, g.K, g.M, g.lda, kBK, 2 * kBM));
+    else TP_TRY(make_map2(&pr.tmA[0], BF, 2, g.A, g.M, g.K, g.lda, 64, kBK));
+    if (!pr.b_mn) TP_TRY(make_map2(&pr.tmB[0], BF, 2, g.B, g.K, g.N, g.ldb, kBK, 128));
+    else TP_TRY(make_map2(&pr.tmB[0], BF, 2, g.B, g.N, g.K, g.ldb, 64, kBK));
+    if (g.out_dtype == TP_BF16)
+      TP_TRY(make_map2(&pr.tmD[0], BF, 2, g.D, g.N, g.M, g.ldd, 64, 32));
+    else
+      TP_TRY(make_map2(&pr.tmD[0], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, g.D, g.N, g.M, g.ldd, 32, 32));
+    pr.d_rows = 0;
+    pr.C = g.C;
+    pr.bias = g.bias;
+    pr.ldc = g.ldc;
+    pr.alpha = g.alpha;
+    pr.out_bf16 = g.out_dtype == TP_BF16;
+    pr.M = static_cast<int>(g.M);
+    pr.N = static_cast<int>(g.N);
+    pr.K = static_cast<int>(g.K);
+    pr.num_m = static_cast<int>((g.M + 511) / 512);
+    pr.num_n = static_cast<int>((g.N + 255) / 256);
+    pr.c_vec = !g.C || ((reinterpret_cast<uintptr_t>(g.C) % 16 == 0) && (g.ldc % 4 == 0));
+    pr.part = nullptr;
+    pr.counters = nullptr;
+    pr.owner_wait = 0;
+    pr.splits = 1;
+    pr.npanels = 1;
+    pr.kb_panel = static_cast<int>((g.K + kBK - 1) / kBK);
+    pr.num_kb = pr.kb_panel;
+    pr.kb_per_split = pr.num_kb;
+    pr.ptiles = pr.num_m * pr.num_n;
+    pr.unit0 = units;
+    units += pr.num_m * pr.num_n;
+    flops += 2.0 * double(g.M) * double(g.N) * double(g.K);
+  }
+  G.total_units = units;
+  int cap = clusters;
+  if (gs[0].reserve_sms > 0) cap = std::max(1, std::min(cap, (sm_count() - gs[0].reserve_sms) / 2));
+  const int grid = 2 * (units < cap ? units : cap);
+  const int tok = prof_begin(0, s, flops);
+  TP_CUDA(launch_pdl(kern, dim3(grid), dim3(threads_of<4>()), kWSmem, s, G));
+  count_launch();
+  prof_end(tok, s);
+  TP_CUDA(cudaGetLastError());
+  return TP_OK;
+}
+
 bool gemm_tc2_supported(const GemmArgs& g) {
   const size_t osz = dtype_size(g.out_dtype);
   if (g.dpanels > 1) {
@@ -1186,7 +1474,34 @@ size_t gemm_tc2_ws_bytes() {
   return size_t(76) * PC<256>::TileElems * 4 + 4096;
 }
 
+// Wide 512 x 256 pair tiles for the big products: two waves of tiles or more and a long K
+// (>= 12288: the un-overlapped epilogue of the single TMEM accumulator is then ~1%, and the
+// operand panels overflow L2). TP_GEMM_WIDE=0 turns it off (A/B measurements), =1 forces it.
+static int wide_mode() {
+  static const int m = [] {
+    const char* e = std::getenv("TP_GEMM_WIDE");
+    return e ? std::atoi(e) : -1;
+  }();
+  return m;
+}
+
+static bool want_wide(const GemmArgs* gs, int n) {
+  const int mode = wide_mode();
+  if (mode == 0) return false;
+  int64_t units = 0, kmin = INT64_MAX;
+  for (int i = 0; i < n; ++i) {
+    if (!gemm_wide_ok(gs[i])) return false;
+    units += ((gs[i].M + 511) / 512) * ((gs[i].N + 255) / 256);
+    kmin = std::min<int64_t>(kmin, gs[i].K);
+  }
+  if (mode == 1) return true;
+  // measured (interleaved A/B, profiles/r02_gemm_wide_ab.md): +10% on 16384^3 (NN / NT / TN,
+  // = cuBLAS), neutral to -4% on the 8192-class shapes (operand panels mostly L2-resident)
+  return units >= sm_count() && kmin >= 12288;
+}
+
 tp_status gemm_tc2_bf16(const GemmArgs& g, cudaStream_t s) {
+  if (want_wide(&g, 1)) return launch_wide(&g, 1, s);
   // Pair tile 256x256 when those tiles fill the SM pairs, else 256x128 (twice the tiles).
   // TP_GEMM_BN / TP_GEMM_MC force a width / cluster shape (tests, A/B measurements).
   static const int force_bn = [] {
@@ -1228,6 +1543,7 @@ tp_status gemm_tc2_bf16(const GemmArgs& g, cudaStream_t s) {
 // blocks per tile go first so the round-robin unit assignment front-loads the long units.
 tp_status gemm_tc2_group(const GemmArgs* in, int n, cudaStream_t s) {
   if (n < 1 || n > kMaxProbs) return fail(TP_ERR_UNSUPPORTED, "gemm group: 1..4 problems");
+  if (want_wide(in, n)) return launch_wide(in, n, s);
   GemmArgs gs[kMaxProbs];
   for (int i = 0; i < n; ++i) gs[i] = in[i];
   auto kblocks = [](const GemmArgs& g) { return g.K * (g.npanels > 1 ? g.npanels : 1); };

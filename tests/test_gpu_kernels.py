@@ -163,6 +163,7 @@ def test_gemm_split_k_is_deterministic(api):
     {"TP_GEMM_KERNEL": "2", "TP_GEMM_BN": "128"},              # 256x128 pair tiles
     {"TP_GEMM_KERNEL": "2", "TP_GEMM_BN": "256", "TP_GEMM_SPLITK": "0"},
     {"TP_GEMM_KERNEL": "2", "TP_GEMM_BN": "256", "TP_GEMM_EPI_WARPS": "8"},  # 8 epilogue warps
+    {"TP_GEMM_KERNEL": "2", "TP_GEMM_WIDE": "1"},              # 512x256 pair tiles wherever legal
 ], ids=lambda e: "-".join(f"{k[8:]}{v}" for k, v in e.items()))
 def test_gemm_kernel_variants_forced(api, env):
     """Every kernel variant the dispatcher can pick, forced for every shape of the GEMM parity
@@ -174,7 +175,7 @@ def test_gemm_kernel_variants_forced(api, env):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "tests/test_gpu_kernels.py",
                         "-k", "bf16_vs_oracle or exact_integer or wide_tile or epilogue or pair_kernel or short_k"
-                              " or deterministic"],
+                              " or deterministic or wide_pair"],
                        cwd=root, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
@@ -280,3 +281,15 @@ def test_gemm_few_tiles_long_k(api, M, K, N, ta):
     kernel; fp32 out against the oracle."""
     got, ref = _gemm_case(api, ta, 0, M, N, K, "bf16", "fp32", seed=M + K, split_k=True)
     assert rel_fro(got, ref) <= 2e-5
+
+
+@pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
+def test_gemm_wide_pair_tiles(api, ta, tb):
+    """Shapes the dispatcher sends to the 512 x 256 pair-tile kernel (>= 74 tiles, K >= 4096),
+    incl. ragged M / N tails: fp32 out exact to accumulation order, bf16 with alpha, C and bias."""
+    for (M, N, K) in [(4096, 4608, 4096), (4000, 4616, 4160)]:
+        got, ref = _gemm_case(api, ta, tb, M, N, K, "bf16", "fp32", seed=29)
+        assert rel_fro(got, ref) <= 2e-5
+        got, ref = _gemm_case(api, ta, tb, M, N, K, "bf16", "bf16", seed=29, alpha=0.5, with_c=True,
+                              with_bias=True)
+        assert rel_fro(got, ref) <= 1e-2
