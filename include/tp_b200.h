@@ -215,6 +215,16 @@ tp_status tp_unpack(const tp_grid* grid, const tp_linear_desc* desc, tp_tensor t
 tp_status tp_register_buffer(tp_grid* grid, void* ptr, size_t bytes);
 tp_status tp_deregister_all(tp_grid* grid);
 #define TP_FLAG_PEER_FUSED 0x4u /* tp_linear_desc.flags: fused owner-computes panel GEMMs (2D, 2.5D, 3D l=2) */
+/* With TP_FLAG_PEER_FUSED: every panel a rank reads from a peer is first pulled ONCE into local
+ * workspace by the copy engine (cudaMemcpyAsync on the comm stream, after the grid barrier that
+ * marks the owners' shards ready), and the panel GEMM reads the local copy. A panel GEMM that
+ * reads a peer's shard directly re-reads it once per output tile row / column it feeds (~M/256
+ * or N/256 times over NVLink); staged, each remote byte crosses the link exactly once - the same
+ * bytes SUMMA receives. Staging is automatic for peers on another GPU; this flag forces it for
+ * every peer (in-process ranks on one GPU: tests). */
+#define TP_FLAG_PEER_STAGED 0x40u
+/* Cumulative bytes this rank has pulled from peers by staging copies (host counter). */
+tp_status tp_peer_staged_bytes(const tp_grid* grid, uint64_t* bytes);
 
 /* ---- kernels exposed for parity tests and benchmarks ----------------------------------- */
 /* Local GEMM, the per-step shard product of every mode:
@@ -356,6 +366,12 @@ tp_status tp_attention_bwd(tp_grid* grid, const tp_linear_desc* qkv_desc, int64_
  *   flops            per-GPU flops = 6 M K N / world
  *   mem_x/w/y        per-rank at-rest elements of the X, W and Y shards
  *   t_tensor_us, t_link_us, t_roof_us   flops / peak_tflops, link_bytes / link_gbs, their max
+ *   fused_direct_bytes, fused_staged_bytes   bytes one rank reads from peers per layer fwd+bwd
+ *                    on the fused owner-computes path (TP_FLAG_PEER_FUSED, 2D / 2.5D replicated
+ *                    W / 3D l=2; 0 elsewhere): panels TMA-read straight from the peers (each
+ *                    re-read once per 256-wide output tile row / column it feeds), and staged
+ *                    (TP_FLAG_PEER_STAGED: each distinct remote shard pulled once). Generic rank:
+ *                    every panel remote except the rank's own shards.
  *   t_exposed_us     communication the library's schedule leaves exposed (not under a GEMM)
  *                    at those rates: per collective, received bytes / link_gbs minus the GEMM
  *                    it overlaps (0 at world == 1 or when either rate is <= 0)
@@ -366,6 +382,7 @@ typedef struct {
   double mem_x, mem_w, mem_y;
   double t_tensor_us, t_link_us, t_roof_us;
   double t_exposed_us;
+  double fused_direct_bytes, fused_staged_bytes;
 } tp_cost;
 tp_status tp_cost_model(tp_mode mode, int world, int q, int d, const tp_linear_desc* desc,
                         double peak_tflops, double link_gbs, tp_cost* out);

@@ -31,11 +31,12 @@ TP_FLAG_PEER_FUSED = 0x4
 TP_FLAG_GELU = 0x8
 TP_FLAG_CANNON = 0x10
 TP_FLAG_SOLOMONIK = 0x20
+TP_FLAG_PEER_STAGED = 0x40
 
 EXPORTED = [
     "tp_status_string", "tp_last_error", "tp_version", "tp_get_unique_id", "tp_grid_init",
     "tp_grid_coords", "tp_grid_dims", "tp_grid_group", "tp_grid_destroy", "tp_shard_extent",
-    "tp_grid_set_contract_check", "tp_axis_collective",
+    "tp_grid_set_contract_check", "tp_axis_collective", "tp_peer_staged_bytes",
     "tp_workspace_size", "tp_linear_fwd", "tp_linear_bwd", "tp_pack", "tp_unpack", "tp_gemm",
     "tp_gemm_ws_bytes",
     "tp_colsum", "tp_fill", "tp_l2_flush", "tp_prof_enable", "tp_prof_reset", "tp_prof_read",
@@ -49,7 +50,8 @@ EXPORTED = [
 class tp_cost(C.Structure):
     _fields_ = [(n, C.c_double) for n in ("paper_elems", "counted_elems", "link_bytes", "flops",
                                           "mem_x", "mem_w", "mem_y", "t_tensor_us", "t_link_us",
-                                          "t_roof_us", "t_exposed_us")]
+                                          "t_roof_us", "t_exposed_us", "fused_direct_bytes",
+                                          "fused_staged_bytes")]
 
 
 class tp_rsa_desc(C.Structure):
@@ -78,6 +80,7 @@ _sigs = {
     "tp_grid_destroy": (_i, [_vp]),
     "tp_grid_set_contract_check": (_i, [_vp, _i]),
     "tp_axis_collective": (_i, [_vp, _i, _i, _vp, _vp, _sz, _i, _i, _vp]),
+    "tp_peer_staged_bytes": (_i, [_vp, C.POINTER(C.c_uint64)]),
     "tp_shard_extent": (_i, [_vp, C.POINTER(tp_linear_desc), _i, _P64, _P64, _P64, _P64]),
     "tp_workspace_size": (_i, [_vp, C.POINTER(tp_linear_desc), C.POINTER(_sz), C.POINTER(_sz)]),
     "tp_linear_fwd": (_i, [_vp, C.POINTER(tp_linear_desc), _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),

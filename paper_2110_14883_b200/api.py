@@ -11,6 +11,7 @@ import ctypes as C
 from . import _lib as L
 from ._lib import (TP_1D, TP_2D, TP_2P5D, TP_3D, TP_BF16, TP_FP32, TP_FLAG_SERIAL,  # noqa: F401
                    TP_FLAG_PEER_FUSED, TP_FLAG_GELU, TP_FLAG_CANNON, TP_FLAG_SOLOMONIK,
+                   TP_FLAG_PEER_STAGED,
                    TP_FLAG_W25_DEPTH_SHARDED, TP_TENSOR_BIAS, TP_TENSOR_W, TP_TENSOR_X,
                    TP_TENSOR_Y, TP_TRANSPORT_LOCAL, TP_TRANSPORT_NCCL, TP_TRANSPORT_NONE,
                    tp_cost, tp_linear_desc, tp_rsa_desc)
@@ -130,6 +131,13 @@ def tp_axis_collective(g, axis, op, send, recv, arg=0, stream=None):
     _check(lib.tp_axis_collective(g, int(axis), o, _ptr(send), _ptr(recv), count, dt, int(arg),
                                   _stream(stream)),
            "tp_axis_collective")
+
+
+def tp_peer_staged_bytes(g) -> int:
+    """Bytes this rank has pulled from peers by staging copies (TP_FLAG_PEER_STAGED)."""
+    v = C.c_uint64()
+    _check(lib.tp_peer_staged_bytes(g, C.byref(v)), "tp_peer_staged_bytes")
+    return int(v.value)
 
 
 def tp_grid_set_contract_check(g, enable=True):

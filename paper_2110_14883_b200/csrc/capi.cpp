@@ -4,6 +4,7 @@
 #include <cudaTypedefs.h>
 #include <unistd.h>
 
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -766,6 +767,8 @@ tp_status tp_register_buffer(tp_grid* g, void* ptr, size_t bytes) {
     }
     std::vector<RegRecord> all(g->world);
     TP_TRY(g->all->host_allgather(&mine, sizeof(RegRecord), all.data()));
+    g->peer_device.assign(g->world, g->device);
+    for (int r = 0; r < g->world; ++r) g->peer_device[r] = all[r].device;
     for (int r = 0; r < g->world; ++r) {
       if (r == g->rank) continue;
       if (all[r].pid == mine.pid) {  // same process (LOCAL transport / threads): share directly
@@ -794,6 +797,12 @@ tp_status tp_register_buffer(tp_grid* g, void* ptr, size_t bytes) {
   return TP_OK;
 }
 
+tp_status tp_peer_staged_bytes(const tp_grid* g, uint64_t* bytes) {
+  if (!g || !bytes) return fail(TP_ERR_ARG, "tp_peer_staged_bytes: null argument");
+  *bytes = g->staged_bytes;
+  return TP_OK;
+}
+
 tp_status tp_deregister_all(tp_grid* g) {
   if (!g) return fail(TP_ERR_ARG, "grid is null");
   if (g->comm_stream) cudaStreamSynchronize(g->comm_stream);
@@ -815,6 +824,34 @@ tp_status tp_gemm_trace(unsigned long long* buf) {
 // structure: SUMMA's next-step broadcast / previous-step reduce under each step's GEMM, 1D's
 // AR(dX) under dW, 3D's row-block pipeline with AG(W) / AG(dY)-remainder / the last reduce /
 // RS(dW) exposed; the depth collectives of 2.5D are exposed).
+// Peer bytes of the fused owner-computes path per rank, layer fwd + bwd (sched.cpp fused_ab /
+// fused_abt_atb / fused3_fwd / fused3_bwd): direct TMA panels are re-read once per 256-wide
+// output tile they feed; staged, each distinct remote shard crosses once.
+static void fused_peer_bytes(tp_mode mode, const tp_linear_desc* d, int q, int dd, double* direct,
+                             double* staged) {
+  *direct = *staged = 0;
+  if (q < 2) return;
+  const double M = double(d->M), K = double(d->K), N = double(d->N);
+  const double e = d->dtype == TP_BF16 ? 2.0 : 4.0;
+  auto t = [](double x) { return std::ceil(x / 256.0); };
+  if ((mode == TP_2D || mode == TP_2P5D) && !(d->flags & (TP_FLAG_W25_DEPTH_SHARDED | TP_FLAG_SOLOMONIK))) {
+    const double mb = M / (double(dd) * q), kq = K / q, nq = N / q, r = q - 1;
+    *direct = r * (t(nq) * mb * kq + t(mb) * kq * nq)           // Y = sum_t X[i,t] W[t,j]
+            + r * (t(kq) * mb * nq + t(mb) * kq * nq)           // dX = sum_t dY[i,t] W[j,t]^T
+            + r * (t(nq) * mb * kq + t(kq) * mb * nq);          // dW = sum_t X[t,i]^T dY[t,j]
+    *staged = r * (mb * kq + kq * nq) + r * (2 * mb * nq + kq * nq + mb * kq);
+  } else if (mode == TP_3D && q == 2) {
+    const double l = q, mb = M / (l * l), kl = K / l, kb = K / (l * l), nl = N / l;
+    *direct = l * l * t(nl) * mb * kb + (l * l - 1) * t(mb) * kb * nl                 // forward
+            + l * (l * t(kb) * mb * nl + l * t(mb) * kb * nl)                        // dX blocks
+            + l * l * (t(nl) * mb * kb + t(kb) * mb * nl);                           // dW
+    *staged = l * mb * kl + (l * l - 1) * kb * nl
+            + l * mb * nl + (l * l - 1) * kb * nl + (l * l - 1) * mb * kl + (l * l - 1) * mb * nl;
+  }
+  *direct *= e;
+  *staged *= e;
+}
+
 static double exposed_comm_us(tp_mode mode, const tp_linear_desc* d, int q, int dd, double p,
                               double peak_tflops, double link_gbs) {
   const double M = double(d->M), K = double(d->K), N = double(d->N);
@@ -948,6 +985,7 @@ extern "C" tp_status tp_cost_model(tp_mode mode, int world, int q, int d, const 
   c.t_roof_us = c.t_tensor_us > c.t_link_us ? c.t_tensor_us : c.t_link_us;
   if (peak_tflops > 0 && link_gbs > 0 && world > 1)
     c.t_exposed_us = exposed_comm_us(mode, desc, j, dd, p, peak_tflops, link_gbs);
+  fused_peer_bytes(mode, desc, j, dd, &c.fused_direct_bytes, &c.fused_staged_bytes);
   *out = c;
   return TP_OK;
 }

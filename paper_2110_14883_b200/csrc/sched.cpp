@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <vector>
 
 #include "sched.h"
 
@@ -91,6 +92,56 @@ struct Ctx {
     const double t = std::max(gemm_flops / 1.4e15, 1e-6);
     const int k = static_cast<int>(std::ceil(ovb / (40e9 * t)));
     return std::min(16, std::max(2, k));
+  }
+  // ---- peer-panel staging (TP_FLAG_PEER_STAGED, or peers on another GPU): a fused panel GEMM
+  // reads a local copy of every staged peer shard, pulled once by the copy engine on `cs`
+  char* stage_base = nullptr;
+  size_t stage_cap = 0, stage_used = 0;
+  bool stage_copies = false;
+  std::vector<std::pair<const void*, const void*>> staged;  // peer pointer -> local copy
+  void carve_stage(size_t bytes) {
+    stage_base = static_cast<char*>(R.ws.take(bytes));
+    stage_cap = bytes;
+  }
+  bool must_stage(int owner) const {
+    if (owner == g->rank) return false;
+    if (d->flags & TP_FLAG_PEER_STAGED) return true;
+    return owner < static_cast<int>(g->peer_device.size()) && g->peer_device[owner] != g->device;
+  }
+  // `owner`'s copy of the registered shard `mine` (bytes long) as this rank reads it: the peer
+  // pointer, or (staged) a local copy. Call after the barrier that marks the shards ready.
+  const void* shard(int owner, const void* mine, size_t bytes, tp_status* st) {
+    const void* p = g->peer_ptr(owner, mine);
+    if (!p || !must_stage(owner)) return p;
+    for (const auto& kv : staged)
+      if (kv.first == p) return kv.second;
+    const size_t off = (stage_used + 255) & ~size_t(255);
+    if (off + bytes > stage_cap) {
+      *st = fail(TP_ERR_WORKSPACE, "peer staging: workspace too small");
+      return nullptr;
+    }
+    char* dst = stage_base + off;
+    stage_used = off + bytes;
+    if (!stage_copies) {
+      if (order(R.s, R.cs) != TP_OK) {
+        *st = TP_ERR_CUDA;
+        return nullptr;
+      }
+      stage_copies = true;
+    }
+    if (cudaMemcpyAsync(dst, p, bytes, cudaMemcpyDefault, R.cs) != cudaSuccess) {
+      *st = fail(TP_ERR_CUDA, "peer staging copy failed");
+      return nullptr;
+    }
+    g->staged_bytes += bytes;
+    staged.emplace_back(p, dst);
+    return dst;
+  }
+  // the panel GEMMs on `s` wait for the staging copies issued so far
+  tp_status stage_done() {
+    if (!stage_copies) return TP_OK;
+    stage_copies = false;
+    return order(R.cs, R.s);
   }
   // split-K scratch shared by this schedule's GEMMs (they run in order on `s`)
   void* gws = nullptr;
@@ -579,19 +630,20 @@ bool fused_ok(Ctx& C, const Plane& P, std::initializer_list<const void*> shards,
 
 tp_status fused_barrier(Ctx& C) { return C.g->all->barrier(C.R.s); }
 
+// Panel t of A / B is the whole shard A_shard / B_shard of rank a_owner(t) / b_owner(t), of
+// a_bytes / b_bytes (staged copies when the owner's shard must be pulled).
 GemmArgs panel_args(Ctx& C, const Plane& P, int64_t M, int64_t N, int64_t K, bool ta, bool tb,
                     void* D, float alpha, const void* bias, const void* A_shard,
                     const void* B_shard, int (*a_owner)(const Plane&, int), int (*b_owner)(const Plane&, int),
-                    const Plane& Pp) {
-  (void)Pp;
+                    size_t a_bytes, size_t b_bytes, tp_status* st) {
   GemmArgs a = C.args(M, N, K, nullptr, ta, nullptr, tb, D, C.dt, alpha, nullptr, bias);
   a.reserve_sms = 0;
   a.ws = nullptr;
   a.ws_bytes = 0;
   a.npanels = P.q;
   for (int t = 0; t < P.q; ++t) {
-    a.Ap[t] = C.g->peer_ptr(a_owner(P, t), A_shard);
-    a.Bp[t] = C.g->peer_ptr(b_owner(P, t), B_shard);
+    a.Ap[t] = C.shard(a_owner(P, t), A_shard, a_bytes, st);
+    a.Bp[t] = C.shard(b_owner(P, t), B_shard, b_bytes, st);
   }
   a.A = a.Ap[0];
   a.B = a.Bp[0];
@@ -610,9 +662,12 @@ int own_dy_tj(const Plane& P, int t) { return plane_rank(t_grid, P, t, P.j); }  
 tp_status fused_ab(Ctx& C, const Plane& P, const void* x, const void* w, const void* bias, void* y) {
   if (C.R.plan) return TP_OK;
   t_grid = C.g;
-  GemmArgs a = panel_args(C, P, P.mb, P.nq, P.kq, false, false, y, C.d->alpha, bias, x, w, own_x_it,
-                          own_w_tj, P);
   TP_TRY(fused_barrier(C));  // every owner's shards are written
+  tp_status st = TP_OK;
+  GemmArgs a = panel_args(C, P, P.mb, P.nq, P.kq, false, false, y, C.d->alpha, bias, x, w, own_x_it,
+                          own_w_tj, P.mb * P.kq * C.esz, P.kq * P.nq * C.esz, &st);
+  TP_TRY(st);
+  TP_TRY(C.stage_done());
   TP_TRY(gemm(a, C.R.s));
   return fused_barrier(C);   // every reader is done before anyone overwrites its shards
 }
@@ -622,14 +677,20 @@ tp_status fused_abt_atb(Ctx& C, const Plane& P, const void* dy, const void* x, c
   if (C.R.plan) return TP_OK;
   t_grid = C.g;
   const float alpha = C.d->alpha;
-  GemmArgs gw = panel_args(C, P, P.kq, P.nq, P.mb, true, false, dwt, alpha, nullptr, x, dy,
-                           own_x_ti, own_dy_tj, P);
   TP_TRY(fused_barrier(C));
+  tp_status st = TP_OK;
+  const size_t xb = P.mb * P.kq * C.esz, wb = P.kq * P.nq * C.esz, yb = P.mb * P.nq * C.esz;
+  GemmArgs gw = panel_args(C, P, P.kq, P.nq, P.mb, true, false, dwt, alpha, nullptr, x, dy,
+                           own_x_ti, own_dy_tj, xb, yb, &st);
+  TP_TRY(st);
   if (dx) {
     GemmArgs gx = panel_args(C, P, P.mb, P.kq, P.nq, false, true, dx, alpha, nullptr, dy, w,
-                             own_dy_it, own_w_jt, P);
+                             own_dy_it, own_w_jt, yb, wb, &st);
+    TP_TRY(st);
+    TP_TRY(C.stage_done());
     TP_TRY(gemm_pair(gx, gw, C.R.s));  // both products in one grouped launch
   } else {
+    TP_TRY(C.stage_done());
     TP_TRY(gemm(gw, C.R.s));
   }
   return fused_barrier(C);
@@ -678,17 +739,21 @@ tp_status fused25_fwd(Ctx& C, const Plane& P, const void* x, const void* w, cons
   const tp_grid* g = C.g;
   const int dep = g->coords[0];
   const int64_t hq = P.kq / P.d;
+  TP_TRY(fused_barrier(C));  // every owner's shards are written
+  tp_status st = TP_OK;
+  const size_t xb = P.mb * P.kq * C.esz, wb = hq * P.nq * C.esz;
   GemmArgs a = panel_base(C, P.mb, P.nq, hq, false, false, y, bias, P.kq, P.nq, P.nq);
   a.npanels = P.q * P.d;
   int k = 0;
   for (int t = 0; t < P.q; ++t)
     for (int e = 0; e < P.d; ++e, ++k) {
-      a.Ap[k] = static_cast<const char*>(g->peer_ptr(rank25(P, dep, P.i, t), x)) + e * hq * C.esz;
-      a.Bp[k] = g->peer_ptr(rank25(P, e, t, P.j), w);
+      a.Ap[k] = static_cast<const char*>(C.shard(rank25(P, dep, P.i, t), x, xb, &st)) + e * hq * C.esz;
+      a.Bp[k] = C.shard(rank25(P, e, t, P.j), w, wb, &st);
     }
+  TP_TRY(st);
   a.A = a.Ap[0];
   a.B = a.Bp[0];
-  TP_TRY(fused_barrier(C));  // every owner's shards are written
+  TP_TRY(C.stage_done());
   TP_TRY(gemm(a, C.R.s));
   return fused_barrier(C);   // every reader is done before anyone overwrites its shards
 }
@@ -701,14 +766,17 @@ tp_status fused25_bwd(Ctx& C, const Plane& P, const void* dy, const void* x, con
   const int64_t hq = P.kq / P.d;
   GemmArgs gs[1 + 4];  // dW + up to d = 4 dX column blocks (q d <= 4)
   int n = 0;
+  TP_TRY(fused_barrier(C));
+  tp_status st = TP_OK;
+  const size_t xb = P.mb * P.kq * C.esz, yb = P.mb * P.nq * C.esz, wb = hq * P.nq * C.esz;
   // dW_dep[i,j] [hq, nq]: contraction over every plane's batch rows
   GemmArgs gw = panel_base(C, hq, P.nq, P.mb, true, false, dw, nullptr, P.kq, P.nq, P.nq);
   gw.npanels = P.q * P.d;
   int k = 0;
   for (int e = 0; e < P.d; ++e)
     for (int m = 0; m < P.q; ++m, ++k) {
-      gw.Ap[k] = static_cast<const char*>(g->peer_ptr(rank25(P, e, m, P.i), x)) + dep * hq * C.esz;
-      gw.Bp[k] = g->peer_ptr(rank25(P, e, m, P.j), dy);
+      gw.Ap[k] = static_cast<const char*>(C.shard(rank25(P, e, m, P.i), x, xb, &st)) + dep * hq * C.esz;
+      gw.Bp[k] = C.shard(rank25(P, e, m, P.j), dy, yb, &st);
     }
   gw.A = gw.Ap[0];
   gw.B = gw.Bp[0];
@@ -719,15 +787,16 @@ tp_status fused25_bwd(Ctx& C, const Plane& P, const void* dy, const void* x, con
                                static_cast<char*>(dx) + e * hq * C.esz, nullptr, P.nq, P.nq, P.kq);
       gx.npanels = P.q;
       for (int t = 0; t < P.q; ++t) {
-        gx.Ap[t] = g->peer_ptr(rank25(P, dep, P.i, t), dy);
-        gx.Bp[t] = g->peer_ptr(rank25(P, e, P.j, t), w);
+        gx.Ap[t] = C.shard(rank25(P, dep, P.i, t), dy, yb, &st);
+        gx.Bp[t] = C.shard(rank25(P, e, P.j, t), w, wb, &st);
       }
       gx.A = gx.Ap[0];
       gx.B = gx.Bp[0];
       gs[n++] = gx;
     }
   }
-  TP_TRY(fused_barrier(C));
+  TP_TRY(st);
+  TP_TRY(C.stage_done());
   for (int i0 = 0; i0 < n; i0 += 4)  // grouped launches of up to four problems
     TP_TRY(gemm_group(gs + i0, std::min(4, n - i0), C.R.s));
   return fused_barrier(C);
@@ -935,17 +1004,21 @@ tp_status fused3_fwd(Ctx& C, const Cube& Q, const void* x, const void* w, const 
   const tp_grid* g = C.g;
   const Cube3 r = cube3_of(C);
   const int l = static_cast<int>(Q.l);
+  TP_TRY(fused_barrier(C));  // every owner's shards are written
+  tp_status st = TP_OK;
+  const size_t xb = Q.mb * Q.kl * C.esz, wb = Q.kb * Q.nl * C.esz;
   GemmArgs a = fused_args(C, Q.mb, Q.nl, Q.kb, false, false, y, Q.kl, Q.nl, Q.nl, bias);
   a.npanels = l * l;
   for (int u2 = 0; u2 < l; ++u2)
     for (int a2 = 0; a2 < l; ++a2) {
       const int p = u2 * l + a2;
-      a.Ap[p] = at_col(g->peer_ptr(cube_rank(g, r.par, r.a, u2, r.u), x), a2 * Q.kb, C.esz);
-      a.Bp[p] = g->peer_ptr(cube_rank(g, r.par, a2, u2, r.v), w);
+      a.Ap[p] = at_col(C.shard(cube_rank(g, r.par, r.a, u2, r.u), x, xb, &st), a2 * Q.kb, C.esz);
+      a.Bp[p] = C.shard(cube_rank(g, r.par, a2, u2, r.v), w, wb, &st);
     }
+  TP_TRY(st);
   a.A = a.Ap[0];
   a.B = a.Bp[0];
-  TP_TRY(fused_barrier(C));  // every owner's shards are written
+  TP_TRY(C.stage_done());
   TP_TRY(gemm(a, C.R.s));
   return fused_barrier(C);   // every reader is done before anyone overwrites its shards
 }
@@ -958,6 +1031,9 @@ tp_status fused3_bwd(Ctx& C, const Cube& Q, const void* dy, const void* x, const
   const int l = static_cast<int>(Q.l);
   GemmArgs gs[4];
   int n = 0;
+  TP_TRY(fused_barrier(C));
+  tp_status st = TP_OK;
+  const size_t xb = Q.mb * Q.kl * C.esz, wb = Q.kb * Q.nl * C.esz, yb = Q.mb * Q.nl * C.esz;
   if (dx) {
     for (int a2 = 0; a2 < l; ++a2) {  // dX column sub-block a2 needs W rows owned by (a2,u,*)
       GemmArgs& d = gs[n++];
@@ -965,8 +1041,8 @@ tp_status fused3_bwd(Ctx& C, const Cube& Q, const void* dy, const void* x, const
                      Q.nl, Q.nl, Q.kl, nullptr);
       d.npanels = l;
       for (int v2 = 0; v2 < l; ++v2) {
-        d.Ap[v2] = g->peer_ptr(cube_rank(g, r.par, r.a, r.v, v2), dy);
-        d.Bp[v2] = g->peer_ptr(cube_rank(g, r.par, a2, r.u, v2), w);
+        d.Ap[v2] = C.shard(cube_rank(g, r.par, r.a, r.v, v2), dy, yb, &st);
+        d.Bp[v2] = C.shard(cube_rank(g, r.par, a2, r.u, v2), w, wb, &st);
       }
       d.A = d.Ap[0];
       d.B = d.Bp[0];
@@ -978,12 +1054,13 @@ tp_status fused3_bwd(Ctx& C, const Cube& Q, const void* dy, const void* x, const
   for (int a1 = 0; a1 < l; ++a1)
     for (int v2 = 0; v2 < l; ++v2) {
       const int p = a1 * l + v2;
-      e.Ap[p] = at_col(g->peer_ptr(cube_rank(g, r.par, a1, r.u, v2), x), r.a * Q.kb, C.esz);
-      e.Bp[p] = g->peer_ptr(cube_rank(g, r.par, a1, v2, r.v), dy);
+      e.Ap[p] = at_col(C.shard(cube_rank(g, r.par, a1, r.u, v2), x, xb, &st), r.a * Q.kb, C.esz);
+      e.Bp[p] = C.shard(cube_rank(g, r.par, a1, v2, r.v), dy, yb, &st);
     }
+  TP_TRY(st);
   e.A = e.Ap[0];
   e.B = e.Bp[0];
-  TP_TRY(fused_barrier(C));
+  TP_TRY(C.stage_done());
   TP_TRY(gemm_group(gs, n, C.R.s));  // the dX sub-blocks and dW in one persistent launch
   TP_TRY(fused_barrier(C));
   if (dbias) {  // db[v] = sum over the l^2 ranks holding column block v (axes a and u)
@@ -1110,9 +1187,39 @@ tp_status bwd_3d(Ctx& C, const void* dy, const void* x, const void* w, const voi
 
 }  // namespace
 
+// Upper bound of the peer shards one fused call may stage (every panel's whole shard; 256 B
+// alignment slack each). 0 when the call cannot take a fused panel path.
+size_t stage_bound(Ctx& C, bool fwd) {
+  if (!(C.d->flags & TP_FLAG_PEER_FUSED) || C.g->world == 1 || C.dt != TP_BF16) return 0;
+  double elems = 0, shards = 0;
+  if (C.g->mode == TP_2D || C.g->mode == TP_2P5D) {
+    const Plane P = plane_of(C);
+    const double q = P.q, d = P.d, mb = P.mb, kq = P.kq, nq = P.nq;
+    if (fwd) {
+      elems = q * mb * kq + q * kq * nq;
+      shards = q + q * d;
+    } else {
+      elems = (q + q * d) * mb * nq + q * kq * nq + q * d * mb * kq;
+      shards = 2 * q + 3 * q * d;
+    }
+  } else if (C.g->mode == TP_3D) {
+    const Cube Q = cube_of(C);
+    const double l = Q.l, mb = Q.mb, kl = Q.kl, kb = Q.kb, nl = Q.nl;
+    if (fwd) {
+      elems = l * mb * kl + l * l * kb * nl;
+      shards = l + l * l;
+    } else {
+      elems = l * mb * nl + l * l * kb * nl + l * l * mb * kl + l * l * mb * nl;
+      shards = l + 3 * l * l;
+    }
+  }
+  return static_cast<size_t>(elems) * C.esz + static_cast<size_t>(shards) * 256;
+}
+
 tp_status sched_fwd(Run& R, const void* x, const void* w, const void* bias, void* y) {
   Ctx C(R);
   C.carve_gemm_scratch();
+  if (const size_t sb = stage_bound(C, true)) C.carve_stage(sb);
   switch (R.g->mode) {
     case TP_1D: return fwd_1d(C, x, w, bias, y);
     case TP_2D:
@@ -1126,6 +1233,7 @@ tp_status sched_bwd(Run& R, const void* dy, const void* x, const void* w, void* 
                     void* dbias) {
   Ctx C(R);
   C.carve_gemm_scratch();
+  if (const size_t sb = stage_bound(C, false)) C.carve_stage(sb);
   const void* saved = R.saved.base;
   switch (R.g->mode) {
     case TP_1D: return bwd_1d(C, dy, x, w, dx, dw, dbias);

@@ -224,6 +224,8 @@ struct tp_grid {
     std::vector<void*> ipc_opened;  // IPC mappings to close on deregistration
   };
   std::vector<RegBuf> regs;
+  std::vector<int> peer_device;   // each rank's CUDA device (filled by tp_register_buffer)
+  uint64_t staged_bytes = 0;      // bytes pulled from peers by staging copies (TP_FLAG_PEER_STAGED)
   std::vector<std::pair<std::string, void*>> ipc_cache;  // (peer rank + IPC handle) -> mapping
   // Pointer on `peer_rank` corresponding to `mine` (same offset in the same registered buffer),
   // or nullptr if `mine` is not inside a registered buffer.

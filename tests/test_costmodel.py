@@ -162,3 +162,20 @@ def test_exposed_comm_term():
     e3 = api.tp_cost_model("3d", 8, api.desc(M, h, h), peak_tflops=1500, link_gbs=900)
     e2 = api.tp_cost_model("2d", 4, api.desc(M, h, h), peak_tflops=1500, link_gbs=900)
     assert e3["t_exposed_us"] < e2["t_exposed_us"]
+
+
+def test_fused_peer_bytes():
+    """The fused owner-computes path's NVLink bytes per rank: panels read straight from peers
+    are re-read once per 256-wide output tile (C3-HEAD 2D: ~32x SUMMA's volume); staged
+    (TP_FLAG_PEER_STAGED) each remote shard crosses once - for 2D exactly the collective
+    schedule's received bytes."""
+    from paper_2110_14883_b200 import api
+    M = h = 16384
+    for par in (0, 1):
+        c = api.tp_cost_model("2d", 4, api.desc(M, h, h, split_1d=par, parity_3d=par))
+        assert c["fused_staged_bytes"] == pytest.approx(c["link_bytes"], rel=1e-12)
+        assert c["fused_direct_bytes"] > 20 * c["fused_staged_bytes"]
+        c3 = api.tp_cost_model("3d", 8, api.desc(M, h, h, split_1d=par, parity_3d=par))
+        assert c3["fused_direct_bytes"] > 10 * c3["fused_staged_bytes"] > 0
+    c1 = api.tp_cost_model("1d", 8, api.desc(M, h, h))
+    assert c1["fused_direct_bytes"] == 0 and c1["fused_staged_bytes"] == 0

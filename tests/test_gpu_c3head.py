@@ -124,9 +124,9 @@ def check(got, ref):
         assert worst <= 5e-2, f"{name}: worst entry off by {worst:.3e} x rms (a wrong tile?)"
 
 
-GRIDS = [("1d", 1, 1, ""), ("2d", 4, 1, ""), ("2d", 4, 1, "fused"), ("2.5d", 8, 2, ""),
-         ("2.5d", 8, 2, "depth"), ("2.5d", 8, 2, "depth+fused"), ("3d", 8, 1, ""),
-         ("3d", 8, 1, "fused"), ("1d", 8, 1, "")]
+GRIDS = [("1d", 1, 1, ""), ("2d", 4, 1, ""), ("2d", 4, 1, "fused"), ("2d", 4, 1, "fused+staged"),
+         ("2.5d", 8, 2, ""), ("2.5d", 8, 2, "depth"), ("2.5d", 8, 2, "depth+fused"),
+         ("3d", 8, 1, ""), ("3d", 8, 1, "fused"), ("3d", 8, 1, "fused+staged"), ("1d", 8, 1, "")]
 
 
 @pytest.mark.parametrize("mode,p,d,variant", GRIDS,
@@ -137,6 +137,8 @@ def test_c3head_two_layers_target_grids(api, expected, mode, p, d, variant):
         flags |= api.TP_FLAG_PEER_FUSED
     if "depth" in variant:
         flags |= api.TP_FLAG_W25_DEPTH_SHARDED
+    if "staged" in variant:
+        flags |= api.TP_FLAG_PEER_STAGED
     idx, ref = expected
     got = sampled_outputs(api, mode, p, d, flags, idx)
     check(got, ref)

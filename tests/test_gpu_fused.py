@@ -211,3 +211,44 @@ def test_fused_depth_sharded_25d_exact_integer(api):
     assert np.array_equal(gather("2.5d", 8, 2, spec, per, "Y", "Y"), Yr)
     assert np.array_equal(gather("2.5d", 8, 2, spec, per, "dX", "X"), dXr)
     assert np.array_equal(gather("2.5d", 8, 2, spec, per, "dW", "W"), dWr)
+
+
+STAGED = 0x40  # TP_FLAG_PEER_STAGED
+
+
+@pytest.mark.parametrize("case", CASES, ids=_id)
+def test_fused_staged_exact_integer_bit_equal(api, case):
+    """TP_FLAG_PEER_STAGED: every peer shard a panel GEMM reads is first pulled once by the copy
+    engine into local workspace (the path taken automatically for peers on another GPU). Same
+    products, so bit-equal on exact-integer inputs; the forward is still one GEMM launch."""
+    mode, p, d, M, K, N, par = case
+    X, W, dY, _ = synth.layer_inputs(5, M, K, N, kind="ternary")
+    per = tp_layer(api, mode, p, d, M, K, N, X, W, dY, None, "bf16", parity=par, flags=FUSED | STAGED)
+    spec = spec_of(M, K, N, parity=par)
+    Yr, dXr, dWr, dbr = oracle_layer(mode, p, d, spec, X, W, dY)
+    for key, t, ref in (("Y", "Y", Yr), ("dX", "X", dXr), ("dW", "W", dWr), ("dB", "B", dbr)):
+        assert np.array_equal(gather(mode, p, d, spec, per, key, t), ref), key
+    assert per[0]["n_fwd"] == p
+    assert all(r["staged_fwd"] > 0 and r["staged_bwd"] > 0 for r in per)
+
+
+def test_fused_staged_bytes_equal_summa_volume(api):
+    """2D q=2: staged, each rank pulls exactly the distinct peer shards its panels need, once -
+    in the forward X[i,t] (t != j) and W[t,j] (t != i): the bytes SUMMA's broadcasts deliver; the
+    backward's owner-computes products need dY[i,t], W[j,t], X[t,i], dY[t,j] (deduplicated)."""
+    M, K, N = 520, 400, 656
+    q = 2
+    mb, kq, nq = M // q, K // q, N // q
+    X, W, dY, _ = synth.layer_inputs(5, M, K, N, kind="ternary")
+    per = tp_layer(api, "2d", 4, 1, M, K, N, X, W, dY, None, "bf16", flags=FUSED | STAGED)
+    for r in range(4):
+        i, j = divmod(r, q)
+        fwd = {("x", i, t) for t in range(q)} | {("w", t, j) for t in range(q)}
+        bwd = ({("dy", i, t) for t in range(q)} | {("w", j, t) for t in range(q)}
+               | {("x", t, i) for t in range(q)} | {("dy", t, j) for t in range(q)})
+        size = {"x": mb * kq * 2, "w": kq * nq * 2, "dy": mb * nq * 2}
+        exp = lambda s: sum(size[k] for (k, a, b) in s if (a, b) != (i, j))
+        assert per[r]["staged_fwd"] == exp(fwd), r
+        assert per[r]["staged_bwd"] == exp(bwd), r
+        # forward = SUMMA's received bytes: (q-1) X panels + (q-1) W panels
+        assert per[r]["staged_fwd"] == (q - 1) * (size["x"] + size["w"])

@@ -95,7 +95,9 @@ def tp_layer(api, mode, p, d, M, K, N, X, W, dY, b=None, dtype="bf16", split_1d=
                 bar.wait(120)  # count the launches of all ranks' forward calls (rank 0 reads)
                 n0 = api.tp_launch_count()
                 bar.wait(120)
+                st0 = api.tp_peer_staged_bytes(g)
                 api.tp_linear_fwd(g, ds, x, w, bias, y, sv, ws)
+                staged_fwd = api.tp_peer_staged_bytes(g) - st0
                 bar.wait(120)
                 n_fwd = api.tp_launch_count() - n0
                 bar.wait(120)  # no rank enqueues its backward before every rank has read the count
@@ -103,7 +105,8 @@ def tp_layer(api, mode, p, d, M, K, N, X, W, dY, b=None, dtype="bf16", split_1d=
                 db = torch.empty(ext["B"][3], device="cuda", dtype=TORCH_DT[dtype])
                 api.tp_linear_bwd(g, ds, dy, x, w, sv, dx, dw, db, ws)
             s.synchronize()
-            res = {"Y": to_np(y), "dW": to_np(dw), "dB": to_np(db), "n_fwd": n_fwd}
+            res = {"Y": to_np(y), "dW": to_np(dw), "dB": to_np(db), "n_fwd": n_fwd,
+                   "staged_fwd": staged_fwd, "staged_bwd": api.tp_peer_staged_bytes(g) - st0 - staged_fwd}
             if want_dx:
                 res["dX"] = to_np(dx)
             return res
