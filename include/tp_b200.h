@@ -270,6 +270,18 @@ tp_status tp_prof_reset(void);
 /* kernel_class: 0 = tcgen05 GEMM, 1 = SIMT GEMM. Synchronises the recorded events and
  * returns the summed device time (ms), the launch count and the algorithmic flops. */
 tp_status tp_prof_read(int kernel_class, double* total_ms, int64_t* launches, double* flops);
+/* Span trace of the recorded regions (tracing): with tp_prof_enable(1) the library
+ * also records every collective of the grids' line communicators (class 2, value = elements x
+ * element size) next to the GEMM launches (classes 0 / 1, value = flops), each tagged with the
+ * grid rank whose call issued it. After the work completed, up to `max` spans are written to
+ * out (start / end in ms relative to the earliest recorded start, in recording order); *n gets
+ * the number of records. Synchronises the recorded events. */
+typedef struct {
+  int kernel_class;  /* 0 tcgen05 GEMM, 1 SIMT GEMM, 2 collective */
+  int rank;          /* grid rank of the issuing call (-1: outside a grid call) */
+  double start_ms, end_ms, value;
+} tp_span;
+tp_status tp_prof_spans(int max, tp_span* out, int* n);
 /* Number of kernels this library has launched since load (all classes). */
 int64_t tp_launch_count(void);
 /* Diagnostics: when buf (device, >= 16 x uint64 per CTA of the largest grid) is non-NULL, the

@@ -133,6 +133,15 @@ def tp_axis_collective(g, axis, op, send, recv, arg=0, stream=None):
            "tp_axis_collective")
 
 
+def tp_prof_spans(max_spans=1 << 16):
+    """Recorded spans (tp_prof_enable): list of dicts class / rank / start_ms / end_ms / value."""
+    buf = (L.tp_span * max_spans)()
+    n = C.c_int()
+    _check(lib.tp_prof_spans(max_spans, buf, C.byref(n)), "tp_prof_spans")
+    return [{"cls": b.kernel_class, "rank": b.rank, "start_ms": b.start_ms, "end_ms": b.end_ms,
+             "value": b.value} for b in buf[:min(n.value, max_spans)]]
+
+
 def tp_peer_staged_bytes(g) -> int:
     """Bytes this rank has pulled from peers by staging copies (TP_FLAG_PEER_STAGED)."""
     v = C.c_uint64()

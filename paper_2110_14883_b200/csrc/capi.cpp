@@ -60,6 +60,7 @@ uint64_t f32_word(float f) {
 
 tp_status contract_check(tp_grid* g, ContractKind kind, const tp_linear_desc* d,
                          std::initializer_list<uint64_t> words) {
+  if (g) t_rank = g->rank;  // span tags (tp_prof_spans) of the work this call issues
   if (!g || !g->contract_check || !g->all || g->world <= 1) return TP_OK;
   const uint64_t call = g->contract_calls++;
   uint64_t h = 0xcbf29ce484222325ull;
@@ -89,6 +90,7 @@ struct ProfRec {
   int cls;
   double flops;
   cudaEvent_t a, b;
+  int rank;
 };
 std::mutex g_prof_mu;
 std::vector<ProfRec> g_prof;
@@ -96,6 +98,7 @@ std::atomic<bool> g_prof_on{false};
 }  // namespace
 
 bool prof_on() { return g_prof_on.load(std::memory_order_relaxed); }
+thread_local int t_rank = -1;
 
 bool pdl_enabled() {
   static const bool on = [] {
@@ -117,7 +120,7 @@ static void record_timing_event(cudaEvent_t e, cudaStream_t s) {
 
 int prof_begin(int cls, cudaStream_t s, double flops) {
   if (!prof_on()) return -1;
-  ProfRec r{cls, flops, nullptr, nullptr};
+  ProfRec r{cls, flops, nullptr, nullptr, t_rank};
   cudaEventCreate(&r.a);
   cudaEventCreate(&r.b);
   record_timing_event(r.a, s);
@@ -136,6 +139,55 @@ void prof_end(int token, cudaStream_t s) {
   }
   record_timing_event(b, s);
 }
+
+// Decorator: every collective of a line communicator as a span of class 2 (tp_prof_spans).
+namespace {
+class TracedComm final : public Comm {
+ public:
+  explicit TracedComm(std::unique_ptr<Comm> c) : c_(std::move(c)) {}
+  int size() const override { return c_->size(); }
+  int pos() const override { return c_->pos(); }
+  tp_status bcast(void* buf, size_t n, tp_dtype dt, int root, cudaStream_t s) override {
+    return span(n, dt, s, [&] { return c_->bcast(buf, n, dt, root, s); });
+  }
+  tp_status reduce(const void* a, void* b, size_t n, tp_dtype dt, int root, cudaStream_t s) override {
+    return span(n, dt, s, [&] { return c_->reduce(a, b, n, dt, root, s); });
+  }
+  tp_status allreduce(const void* a, void* b, size_t n, tp_dtype dt, cudaStream_t s) override {
+    return span(n, dt, s, [&] { return c_->allreduce(a, b, n, dt, s); });
+  }
+  tp_status allgather(const void* a, void* b, size_t n, tp_dtype dt, cudaStream_t s) override {
+    return span(n * c_->size(), dt, s, [&] { return c_->allgather(a, b, n, dt, s); });
+  }
+  tp_status reducescatter(const void* a, void* b, size_t n, tp_dtype dt, cudaStream_t s) override {
+    return span(n * c_->size(), dt, s, [&] { return c_->reducescatter(a, b, n, dt, s); });
+  }
+  tp_status shift(const void* a, void* b, size_t n, tp_dtype dt, int off, cudaStream_t s) override {
+    return span(n, dt, s, [&] { return c_->shift(a, b, n, dt, off, s); });
+  }
+  tp_status group_start() override { return c_->group_start(); }
+  tp_status group_end() override { return c_->group_end(); }
+  tp_status barrier(cudaStream_t s) override {
+    return span(0, TP_BF16, s, [&] { return c_->barrier(s); });
+  }
+  tp_status host_allgather(const void* in, size_t bytes, void* out) override {
+    return c_->host_allgather(in, bytes, out);
+  }
+
+ private:
+  template <typename F>
+  tp_status span(size_t n, tp_dtype dt, cudaStream_t s, F f) {
+    const int tok = prof_begin(2, s, double(n) * double(dtype_size(dt)));
+    const tp_status st = f();
+    prof_end(tok, s);
+    return st;
+  }
+  std::unique_ptr<Comm> c_;
+};
+std::unique_ptr<Comm> traced(std::unique_ptr<Comm> c) {
+  return c ? std::unique_ptr<Comm>(new TracedComm(std::move(c))) : nullptr;
+}
+}  // namespace
 
 }  // namespace tp
 
@@ -359,6 +411,7 @@ tp_status tp_grid_init(tp_grid** out, tp_mode mode, int world, int rank, int q, 
       tp_grid_destroy(g.release());
       return st;
     }
+    g->axis[ax] = traced(std::move(g->axis[ax]));
   }
   if (world > 1) {  // all ranks: barriers of the fused peer-memory path, buffer registration
     if (transport == TP_TRANSPORT_NCCL) {
@@ -373,6 +426,7 @@ tp_status tp_grid_init(tp_grid** out, tp_mode mode, int world, int rank, int q, 
       }
     }
   }
+  g->all = traced(std::move(g->all));
   if (transport == TP_TRANSPORT_LOCAL && world > 1) g_shared_device_grids.fetch_add(1);
   *out = g.release();
   return TP_OK;
@@ -709,6 +763,29 @@ tp_status tp_prof_read(int cls, double* total_ms, int64_t* launches, double* flo
   *total_ms = ms;
   *launches = n;
   *flops = fl;
+  return TP_OK;
+}
+
+tp_status tp_prof_spans(int max, tp_span* out, int* n) {
+  if (!n || (max > 0 && !out)) return fail(TP_ERR_ARG, "tp_prof_spans: null output");
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  *n = static_cast<int>(g_prof.size());
+  if (g_prof.empty()) return TP_OK;
+  for (auto& r : g_prof) TP_CUDA(cudaEventSynchronize(r.b));
+  // the earliest start: every other start is measured from it
+  size_t first = 0;
+  for (size_t i = 1; i < g_prof.size(); ++i) {
+    float d = 0;
+    TP_CUDA(cudaEventElapsedTime(&d, g_prof[first].a, g_prof[i].a));
+    if (d < 0) first = i;
+  }
+  for (int i = 0; i < *n && i < max; ++i) {
+    const ProfRec& r = g_prof[i];
+    float a = 0, b = 0;
+    TP_CUDA(cudaEventElapsedTime(&a, g_prof[first].a, r.a));
+    TP_CUDA(cudaEventElapsedTime(&b, g_prof[first].a, r.b));
+    out[i] = tp_span{r.cls, r.rank, a, b, r.flops};
+  }
   return TP_OK;
 }
 

@@ -50,6 +50,7 @@ extern std::atomic<int64_t> g_launches;
 extern unsigned long long* g_gemm_trace;
 inline void count_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 bool prof_on();
+extern thread_local int t_rank;  // grid rank of the calling entry point (span tags)
 // Opens a timed region for kernel class `cls` on `s`; returns a token for prof_end.
 int prof_begin(int cls, cudaStream_t s, double flops);
 void prof_end(int token, cudaStream_t s);
