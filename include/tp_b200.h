@@ -147,6 +147,14 @@ tp_status tp_grid_destroy(tp_grid* grid);
  * Collective when the grid is shared: every rank must set the same value. */
 tp_status tp_grid_set_contract_check(tp_grid* grid, int enable);
 
+/* Failure detection. tp_grid_check: TP_OK, or TP_ERR_NCCL with the detail when a
+ * communicator of the grid reports an asynchronous error (ncclCommGetAsyncError: a peer died,
+ * a network / NVLink fault); non-blocking, callable from a watchdog thread while collectives
+ * run. tp_grid_abort: aborts every communicator (ncclCommAbort), so collectives blocked on a
+ * dead peer return; afterwards the grid only supports tp_grid_destroy. LOCAL / NONE: no-ops. */
+tp_status tp_grid_check(const tp_grid* grid);
+tp_status tp_grid_abort(tp_grid* grid);
+
 /* ---- the grid's line communicators ("only incur communication on a sub-group") ---- */
 /* One collective over this rank's line along `axis` (members by ascending coordinate, as
  * tp_grid_group), the primitive the schedules are built from:

@@ -36,7 +36,7 @@ TP_FLAG_PEER_STAGED = 0x40
 EXPORTED = [
     "tp_status_string", "tp_last_error", "tp_version", "tp_get_unique_id", "tp_grid_init",
     "tp_grid_coords", "tp_grid_dims", "tp_grid_group", "tp_grid_destroy", "tp_shard_extent",
-    "tp_grid_set_contract_check", "tp_axis_collective", "tp_peer_staged_bytes", "tp_prof_spans",
+    "tp_grid_set_contract_check", "tp_grid_check", "tp_grid_abort", "tp_axis_collective", "tp_peer_staged_bytes", "tp_prof_spans",
     "tp_workspace_size", "tp_linear_fwd", "tp_linear_bwd", "tp_pack", "tp_unpack", "tp_gemm",
     "tp_gemm_ws_bytes",
     "tp_colsum", "tp_fill", "tp_l2_flush", "tp_prof_enable", "tp_prof_reset", "tp_prof_read",
@@ -84,6 +84,8 @@ _sigs = {
     "tp_grid_group": (_i, [_vp, _i, C.POINTER(_i)]),
     "tp_grid_destroy": (_i, [_vp]),
     "tp_grid_set_contract_check": (_i, [_vp, _i]),
+    "tp_grid_check": (_i, [_vp]),
+    "tp_grid_abort": (_i, [_vp]),
     "tp_axis_collective": (_i, [_vp, _i, _i, _vp, _vp, _sz, _i, _i, _vp]),
     "tp_peer_staged_bytes": (_i, [_vp, C.POINTER(C.c_uint64)]),
     "tp_prof_spans": (_i, [_i, C.POINTER(tp_span), C.POINTER(_i)]),

@@ -149,6 +149,16 @@ def tp_peer_staged_bytes(g) -> int:
     return int(v.value)
 
 
+def tp_grid_check(g):
+    """Raise TPError if a communicator of the grid reports an asynchronous error."""
+    _check(lib.tp_grid_check(g), "tp_grid_check")
+
+
+def tp_grid_abort(g):
+    """Abort the grid's communicators (blocked collectives return); destroy-only afterwards."""
+    _check(lib.tp_grid_abort(g), "tp_grid_abort")
+
+
 def tp_grid_set_contract_check(g, enable=True):
     """Debug: verify on every collective call that all ranks passed the same desc (TP_ERR_ARG
     instead of a deadlock on a mismatch)."""

@@ -1,6 +1,7 @@
 // The C ABI (include/tp_b200.h): argument validation, the grid / parallel context
 // ("parallel context manager"), and dispatch into the per-mode schedules.
 #include <cuda.h>
+#include <nvtx3/nvToolsExt.h>
 #include <cudaTypedefs.h>
 #include <unistd.h>
 
@@ -25,6 +26,12 @@ tp_status fail(tp_status s, const std::string& msg) {
 }
 
 std::atomic<int64_t> g_launches{0};
+
+// NVTX range over an entry point (host-side; nsys / ncu --nvtx show the library's calls)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 std::atomic<int> g_shared_device_grids{0};
 
 cudaError_t set_smem_attr(const void* kernel, int bytes) {
@@ -173,6 +180,8 @@ class TracedComm final : public Comm {
   tp_status host_allgather(const void* in, size_t bytes, void* out) override {
     return c_->host_allgather(in, bytes, out);
   }
+  tp_status async_error() override { return c_->async_error(); }
+  void abort() override { c_->abort(); }
 
  private:
   template <typename F>
@@ -455,6 +464,7 @@ tp_status tp_grid_group(const tp_grid* g, int axis, int* members) {
 
 tp_status tp_axis_collective(tp_grid* g, int axis, tp_collective op, const void* send, void* recv,
                              size_t count, tp_dtype dt, int arg, void* stream) {
+  tp::NvtxRange nvtx_("tp_axis_collective");
   if (!g) return fail(TP_ERR_ARG, "tp_axis_collective: null grid");
   if (axis < 0 || axis >= g->ndims) return fail(TP_ERR_ARG, "tp_axis_collective: axis out of range");
   if (dt != TP_BF16 && dt != TP_FP32) return fail(TP_ERR_ARG, "tp_axis_collective: dtype");
@@ -490,6 +500,24 @@ tp_status tp_axis_collective(tp_grid* g, int axis, tp_collective op, const void*
     case TP_COLL_SHIFT: return c->shift(send, recv, count, dt, arg, s);
   }
   return fail(TP_ERR_ARG, "tp_axis_collective: op");
+}
+
+tp_status tp_grid_check(const tp_grid* g) {
+  if (!g) return fail(TP_ERR_ARG, "tp_grid_check: null grid");
+  if (g->nccl) TP_TRY(nccl_world_async_error(g->nccl));
+  for (const auto& a : g->axis)
+    if (a) TP_TRY(a->async_error());
+  return TP_OK;
+}
+
+tp_status tp_grid_abort(tp_grid* g) {
+  if (!g) return fail(TP_ERR_ARG, "tp_grid_abort: null grid");
+  for (auto& a : g->axis)
+    if (a) a->abort();
+  for (auto& a : g->unit_axis)
+    if (a) a->abort();
+  if (g->nccl) nccl_world_abort(g->nccl);
+  return TP_OK;
 }
 
 tp_status tp_grid_set_contract_check(tp_grid* g, int enable) {
@@ -565,6 +593,7 @@ static void begin_run(Run& R, tp_grid* g, const tp_linear_desc* d, void* ws, voi
 tp_status tp_linear_fwd(tp_grid* g, const tp_linear_desc* d, const void* x, const void* w,
                         const void* bias, void* y, void* saved, void* ws, size_t ws_bytes,
                         void* stream) {
+  tp::NvtxRange nvtx_("tp_linear_fwd");
   if (!g || !d) return fail(TP_ERR_ARG, "tp_linear_fwd: null grid or desc");
   TP_TRY(contract_check(g, kCallLinearFwd, d, {uint64_t(bias != nullptr)}));
   size_t need_saved = 0;
@@ -597,6 +626,7 @@ tp_status tp_linear_fwd(tp_grid* g, const tp_linear_desc* d, const void* x, cons
 tp_status tp_linear_bwd(tp_grid* g, const tp_linear_desc* d, const void* dy, const void* x,
                         const void* w, const void* saved, void* dx, void* dw, void* dbias, void* ws,
                         size_t ws_bytes, void* stream) {
+  tp::NvtxRange nvtx_("tp_linear_bwd");
   if (!g || !d) return fail(TP_ERR_ARG, "tp_linear_bwd: null grid or desc");
   TP_TRY(contract_check(g, kCallLinearBwd, d,
                         {uint64_t(dx != nullptr), uint64_t(dbias != nullptr)}));
@@ -658,11 +688,13 @@ static tp_status pack_common(const tp_grid* g, const tp_linear_desc* d, tp_tenso
 
 tp_status tp_pack(const tp_grid* g, const tp_linear_desc* d, tp_tensor t, const void* global,
                   void* shard, void* stream) {
+  tp::NvtxRange nvtx_("tp_pack");
   return pack_common(g, d, t, true, global, shard, stream);
 }
 
 tp_status tp_unpack(const tp_grid* g, const tp_linear_desc* d, tp_tensor t, const void* shard,
                     void* global, void* stream) {
+  tp::NvtxRange nvtx_("tp_unpack");
   return pack_common(g, d, t, false, shard, global, stream);
 }
 
@@ -670,6 +702,7 @@ tp_status tp_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, tp_
                   const void* A, int64_t lda, const void* B, int64_t ldb, const float* C,
                   int64_t ldc, void* D, int64_t ldd, tp_dtype out_dtype, float alpha,
                   const void* bias, void* ws, size_t ws_bytes, void* stream) {
+  tp::NvtxRange nvtx_("tp_gemm");
   if (in_dtype != TP_BF16 && in_dtype != TP_FP32) return fail(TP_ERR_ARG, "in_dtype");
   if (out_dtype != TP_BF16 && out_dtype != TP_FP32) return fail(TP_ERR_ARG, "out_dtype");
   GemmArgs a;
@@ -823,6 +856,7 @@ tp_status alloc_range(const void* ptr, void** base) {
 }  // namespace
 
 tp_status tp_register_buffer(tp_grid* g, void* ptr, size_t bytes) {
+  tp::NvtxRange nvtx_("tp_register_buffer");
   if (!g || !ptr || !bytes) return fail(TP_ERR_ARG, "tp_register_buffer: null argument");
   tp_grid::RegBuf rb;
   rb.base = static_cast<char*>(ptr);
@@ -1077,6 +1111,7 @@ extern "C" tp_status tp_layernorm_ws_size(const tp_grid* g, const tp_linear_desc
 extern "C" tp_status tp_layernorm_fwd(tp_grid* g, const tp_linear_desc* d, tp_tensor t, float eps,
                                       const void* x, const void* gamma, const void* beta, void* y,
                                       float* stats, void* ws, size_t ws_bytes, void* stream) {
+  tp::NvtxRange nvtx_("tp_layernorm_fwd");
   if (!g || !d) return tp::fail(TP_ERR_ARG, "tp_layernorm_fwd: null grid or desc");
   TP_TRY(tp::contract_check(g, tp::kCallLnFwd, d, {uint64_t(t), tp::f32_word(eps),
                                                    uint64_t(stats != nullptr)}));
@@ -1090,6 +1125,7 @@ extern "C" tp_status tp_layernorm_bwd(tp_grid* g, const tp_linear_desc* d, tp_te
                                       const void* dy, const void* x, const void* gamma,
                                       const float* stats, void* dx, void* dgamma, void* dbeta,
                                       void* ws, size_t ws_bytes, void* stream) {
+  tp::NvtxRange nvtx_("tp_layernorm_bwd");
   if (!g || !d) return tp::fail(TP_ERR_ARG, "tp_layernorm_bwd: null grid or desc");
   TP_TRY(tp::contract_check(g, tp::kCallLnBwd, d, {uint64_t(t), uint64_t(dgamma != nullptr),
                                                    uint64_t(dbeta != nullptr)}));
@@ -1107,6 +1143,7 @@ extern "C" tp_status tp_rsa_ws_size(const tp_grid* g, const tp_rsa_desc* d, size
 
 extern "C" tp_status tp_rsa_fwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k,
                                 const void* v, void* out, void* ws, size_t ws_bytes, void* stream) {
+  tp::NvtxRange nvtx_("tp_rsa_fwd");
   if (!g || !d) return tp::fail(TP_ERR_ARG, "tp_rsa_fwd: null grid or desc");
   TP_TRY(tp::contract_check(g, tp::kCallRsaFwd, nullptr,
                             {uint64_t(d->seq), uint64_t(d->d_k), uint64_t(d->heads),
@@ -1118,6 +1155,7 @@ extern "C" tp_status tp_rsa_fwd(tp_grid* g, const tp_rsa_desc* d, const void* q,
 extern "C" tp_status tp_rsa_bwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k,
                                 const void* v, const void* dout, void* dq, void* dk, void* dv,
                                 void* ws, size_t ws_bytes, void* stream) {
+  tp::NvtxRange nvtx_("tp_rsa_bwd");
   if (!g || !d) return tp::fail(TP_ERR_ARG, "tp_rsa_bwd: null grid or desc");
   TP_TRY(tp::contract_check(g, tp::kCallRsaBwd, nullptr,
                             {uint64_t(d->seq), uint64_t(d->d_k), uint64_t(d->heads),
@@ -1136,6 +1174,7 @@ extern "C" tp_status tp_attention_ws_size(const tp_grid* g, const tp_linear_desc
 extern "C" tp_status tp_attention_fwd(tp_grid* g, const tp_linear_desc* d, int64_t seq,
                                       int64_t heads, float scale, const void* qkv, void* out,
                                       void* ws, size_t ws_bytes, void* stream) {
+  tp::NvtxRange nvtx_("tp_attention_fwd");
   if (!g) return tp::fail(TP_ERR_ARG, "tp_attention_fwd: null grid");
   TP_TRY(tp::contract_check(g, tp::kCallAttnFwd, d,
                             {uint64_t(seq), uint64_t(heads), tp::f32_word(scale)}));
@@ -1147,6 +1186,7 @@ extern "C" tp_status tp_attention_fwd(tp_grid* g, const tp_linear_desc* d, int64
 extern "C" tp_status tp_attention_bwd(tp_grid* g, const tp_linear_desc* d, int64_t seq,
                                       int64_t heads, float scale, const void* qkv, const void* dout,
                                       void* dqkv, void* ws, size_t ws_bytes, void* stream) {
+  tp::NvtxRange nvtx_("tp_attention_bwd");
   if (!g) return tp::fail(TP_ERR_ARG, "tp_attention_bwd: null grid");
   TP_TRY(tp::contract_check(g, tp::kCallAttnBwd, d,
                             {uint64_t(seq), uint64_t(heads), tp::f32_word(scale)}));

@@ -174,6 +174,10 @@ class Comm {
   virtual tp_status barrier(cudaStream_t s) = 0;
   // Host-side all-gather of `bytes` per member (setup only: buffer registration).
   virtual tp_status host_allgather(const void* in, size_t bytes, void* out) = 0;
+  // Failure detection (safe from another thread): an asynchronous transport error (NCCL:
+  // ncclCommGetAsyncError), and abort, which makes blocked / future collectives return.
+  virtual tp_status async_error() { return TP_OK; }
+  virtual void abort() {}
 };
 
 struct NcclWorld;  // transport_nccl.cpp
@@ -182,6 +186,8 @@ std::unique_ptr<Comm> make_nccl_comm(NcclWorld* w, int color, int key, int size,
 NcclWorld* nccl_world_create(int world, int rank, const void* id128, tp_status* st);
 std::unique_ptr<Comm> make_nccl_world_comm(NcclWorld* w);
 void nccl_world_destroy(NcclWorld* w);
+tp_status nccl_world_async_error(NcclWorld* w);
+void nccl_world_abort(NcclWorld* w);
 tp_status nccl_unique_id(void* id128);
 // A 1-rank NCCL communicator of this process alone (size-1 grid lines in tp_axis_collective).
 std::unique_ptr<Comm> make_nccl_self_comm(tp_status* st);

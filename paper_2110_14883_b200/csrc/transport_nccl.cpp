@@ -88,6 +88,18 @@ class NcclComm final : public Comm {
     TP_NCCL(ncclGroupStart());
     return TP_OK;
   }
+  tp_status async_error() override {
+    ncclResult_t e = ncclSuccess;
+    TP_NCCL(ncclCommGetAsyncError(c_, &e));
+    if (e != ncclSuccess && e != ncclInProgress) return nccl_fail(e, "communicator async error");
+    return TP_OK;
+  }
+  void abort() override {
+    if (c_ && owns_) {
+      ncclCommAbort(c_);
+      c_ = nullptr;
+    }
+  }
   tp_status group_end() override {
     TP_NCCL(ncclGroupEnd());
     return TP_OK;
@@ -151,6 +163,21 @@ NcclWorld* nccl_world_create(int world, int rank, const void* id128, tp_status* 
   }
   *st = TP_OK;
   return w;
+}
+
+tp_status nccl_world_async_error(NcclWorld* w) {
+  if (!w || !w->world) return TP_OK;
+  ncclResult_t e = ncclSuccess;
+  TP_NCCL(ncclCommGetAsyncError(w->world, &e));
+  if (e != ncclSuccess && e != ncclInProgress) return nccl_fail(e, "world communicator async error");
+  return TP_OK;
+}
+
+void nccl_world_abort(NcclWorld* w) {
+  if (w && w->world) {
+    ncclCommAbort(w->world);
+    w->world = nullptr;
+  }
 }
 
 void nccl_world_destroy(NcclWorld* w) {

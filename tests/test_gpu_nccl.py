@@ -302,3 +302,31 @@ def test_nccl_axis_collectives_one_rank_lines(api, dt):
                 assert torch.equal(recv, v), (ax, op)
     finally:
         api.tp_grid_destroy(g)
+
+
+def test_grid_check_and_abort(api):
+    """Failure detection: tp_grid_check is TP_OK on healthy grids (NCCL and LOCAL); after
+    tp_grid_abort the NCCL grid can still be destroyed."""
+    uid = api.tp_get_unique_id(api.TP_TRANSPORT_NCCL)
+    g = api.tp_grid_init("3d", 1, 0, 0, 1, 0, api.TP_TRANSPORT_NCCL, uid)
+    try:
+        api.tp_grid_check(g)
+        x = torch.ones(256, device="cuda")
+        y = torch.empty_like(x)
+        api.tp_axis_collective(g, 0, "allreduce", x, y)  # a 1-rank NCCL line communicator
+        torch.cuda.synchronize()
+        api.tp_grid_check(g)
+        api.tp_grid_abort(g)
+    finally:
+        api.tp_grid_destroy(g)
+    uidl = api.tp_get_unique_id(api.TP_TRANSPORT_LOCAL)
+
+    def rank_fn(r):
+        gl = api.tp_grid_init("2d", 4, r, 0, 1, 0, api.TP_TRANSPORT_LOCAL, uidl)
+        try:
+            api.tp_grid_check(gl)
+            return True
+        finally:
+            api.tp_grid_destroy(gl)
+
+    assert all(run_ranks(4, rank_fn, timeout=60))
