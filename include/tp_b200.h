@@ -367,12 +367,18 @@ tp_status tp_rsa_bwd(tp_grid* grid, const tp_rsa_desc* desc, const void* q, cons
  * block splits a head or a sequence, d % 8), TP_ERR_WORKSPACE. */
 tp_status tp_attention_ws_size(const tp_grid* grid, const tp_linear_desc* qkv_desc, int64_t seq,
                                int64_t heads, size_t* ws_bytes);
+/* lse (nullable): fp32 [heads_local x rows] (problem order: sequence-major, then head, then
+ * position) - the forward's per-row log-sum-exp (base 2, scaled scores). Written by the fused
+ * forward (bf16, d in {64, 128}); passing it and the forward's `out` to the backward selects the
+ * fused backward (scores recomputed on chip from lse, never stored in HBM); with either NULL the
+ * backward recomputes the scores two-pass through workspace. */
 tp_status tp_attention_fwd(tp_grid* grid, const tp_linear_desc* qkv_desc, int64_t seq,
-                           int64_t heads, float scale, const void* qkv, void* out, void* ws,
-                           size_t ws_bytes, void* stream);
+                           int64_t heads, float scale, const void* qkv, void* out, float* lse,
+                           void* ws, size_t ws_bytes, void* stream);
 tp_status tp_attention_bwd(tp_grid* grid, const tp_linear_desc* qkv_desc, int64_t seq,
-                           int64_t heads, float scale, const void* qkv, const void* dout,
-                           void* dqkv, void* ws, size_t ws_bytes, void* stream);
+                           int64_t heads, float scale, const void* qkv, const void* out,
+                           const float* lse, const void* dout, void* dqkv, void* ws,
+                           size_t ws_bytes, void* stream);
 
 /* ---- analytic cost model --------------------- */
 /* One linear layer, fwd+bwd, bias-free, on the grid (mode, world, q, d) with desc's M, K, N,

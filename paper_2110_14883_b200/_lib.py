@@ -119,10 +119,10 @@ _sigs = {
     "tp_rsa_bwd": (_i, [_vp, C.POINTER(tp_rsa_desc), _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz,
                         _vp]),
     "tp_attention_ws_size": (_i, [_vp, C.POINTER(tp_linear_desc), _i64, _i64, C.POINTER(_sz)]),
-    "tp_attention_fwd": (_i, [_vp, C.POINTER(tp_linear_desc), _i64, _i64, _f, _vp, _vp, _vp, _sz,
-                              _vp]),
-    "tp_attention_bwd": (_i, [_vp, C.POINTER(tp_linear_desc), _i64, _i64, _f, _vp, _vp, _vp, _vp,
+    "tp_attention_fwd": (_i, [_vp, C.POINTER(tp_linear_desc), _i64, _i64, _f, _vp, _vp, _vp, _vp,
                               _sz, _vp]),
+    "tp_attention_bwd": (_i, [_vp, C.POINTER(tp_linear_desc), _i64, _i64, _f, _vp, _vp, _vp, _vp,
+                              _vp, _vp, _sz, _vp]),
     "tp_add": (_i, [_vp, _vp, _vp, _sz, _i, _vp]),
     "tp_cost_model": (_i, [_i, _i, _i, _i, C.POINTER(tp_linear_desc), C.c_double, C.c_double,
                            C.POINTER(tp_cost)]),

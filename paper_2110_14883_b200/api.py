@@ -332,17 +332,22 @@ def tp_attention_ws_size(g, d, seq, heads) -> int:
     return n.value
 
 
-def tp_attention_fwd(g, d, seq, heads, qkv, out, ws, scale=0.0, stream=None, ws_bytes=None):
+def tp_attention_fwd(g, d, seq, heads, qkv, out, ws, scale=0.0, stream=None, ws_bytes=None,
+                     lse=None):
+    """lse (optional fp32 tensor, heads_local x rows): the forward's row log-sum-exp, which with
+    `out` selects the fused backward."""
     wb = _nbytes(ws) if ws_bytes is None else ws_bytes
     _check(lib.tp_attention_fwd(g, C.byref(d), int(seq), int(heads), float(scale), _ptr(qkv),
-                                _ptr(out), _ptr(ws), wb, _stream(stream)), "tp_attention_fwd")
+                                _ptr(out), _ptr(lse), _ptr(ws), wb, _stream(stream)),
+           "tp_attention_fwd")
 
 
-def tp_attention_bwd(g, d, seq, heads, qkv, dout, dqkv, ws, scale=0.0, stream=None, ws_bytes=None):
+def tp_attention_bwd(g, d, seq, heads, qkv, dout, dqkv, ws, scale=0.0, stream=None, ws_bytes=None,
+                     out=None, lse=None):
     wb = _nbytes(ws) if ws_bytes is None else ws_bytes
     _check(lib.tp_attention_bwd(g, C.byref(d), int(seq), int(heads), float(scale), _ptr(qkv),
-                                _ptr(dout), _ptr(dqkv), _ptr(ws), wb, _stream(stream)),
-           "tp_attention_bwd")
+                                _ptr(out), _ptr(lse), _ptr(dout), _ptr(dqkv), _ptr(ws), wb,
+                                _stream(stream)), "tp_attention_bwd")
 
 
 def tp_add(a, b, out, dtype=None, stream=None):

@@ -46,6 +46,9 @@ class TPBlock:
         self.qkv, self.o = mk(self.dq, "Y"), mk(self.dp, "X")
         self.y1, self.f, self.y2 = mk(self.dp, "Y"), mk(self.d1, "Y"), mk(self.d2, "Y")
         rows = ex[1]
+        # attention row log-sum-exp (fused forward -> fused backward): heads_local x rows
+        self.lse = torch.empty(self.qkv.shape[1] // (3 * (h // heads)) * rows, device="cuda",
+                               dtype=torch.float32)
         self.st1 = torch.empty(rows, 2, device="cuda", dtype=torch.float32)
         self.st2 = torch.empty_like(self.st1)
         # gradients
@@ -98,7 +101,7 @@ class TPBlock:
         api.tp_layernorm_fwd(g, self.dq, "X", self.eps, self.x, self.ln["g1"], self.ln["be1"], self.a,
                              self.st1, ws)
         api.tp_linear_fwd(g, self.dq, self.a, self.W["qkv"], self.b["qkv"], self.qkv, sv[0], ws)
-        api.tp_attention_fwd(g, self.dq, self.seq, self.heads, self.qkv, self.o, ws)
+        api.tp_attention_fwd(g, self.dq, self.seq, self.heads, self.qkv, self.o, ws, lse=self.lse)
         api.tp_linear_fwd(g, self.dp, self.o, self.W["o"], self.b["o"], self.y1, sv[1], ws)
         api.tp_add(self.x, self.y1, self.h1)
         api.tp_layernorm_fwd(g, self.dq, "X", self.eps, self.h1, self.ln["g2"], self.ln["be2"], self.c,
@@ -118,7 +121,8 @@ class TPBlock:
         api.tp_add(self.dout, self.dt, self.dh1)
         api.tp_linear_bwd(g, self.dp, self.dh1, self.o, self.W["o"], sv[1], self.do, self.dW["o"],
                           self.db["o"], ws)
-        api.tp_attention_bwd(g, self.dq, self.seq, self.heads, self.qkv, self.do, self.dqkv, ws)
+        api.tp_attention_bwd(g, self.dq, self.seq, self.heads, self.qkv, self.do, self.dqkv, ws,
+                             out=self.o, lse=self.lse)
         api.tp_linear_bwd(g, self.dq, self.dqkv, self.a, self.W["qkv"], sv[0], self.da,
                           self.dW["qkv"], self.db["qkv"], ws)
         api.tp_layernorm_bwd(g, self.dq, "X", self.da, self.x, self.ln["g1"], self.st1, self.dt,

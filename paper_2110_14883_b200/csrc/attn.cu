@@ -102,9 +102,10 @@ tp_status pack(const AttnPlan& P, const void* src, void* dst, int64_t ld, int64_
 }
 
 struct AttnWs {
-  void* buf[7] = {};  // q, k, v, o / do, dq, dk, dv: [problems, seq, d]
+  void* buf[8] = {};  // q, k, v, o / do, dq, dk, dv, o (fused backward): [problems, seq, d]
   void* rsa = nullptr;
   size_t rsa_bytes = 0;
+  void* fb = nullptr;  // fused backward: fp32 dQ accumulator + row deltas
 };
 
 tp_status attn_carve(const AttnPlan& P, Carver& c, AttnWs* w) {
@@ -112,6 +113,7 @@ tp_status attn_carve(const AttnPlan& P, Carver& c, AttnWs* w) {
   for (auto& b : w->buf) b = c.take(one);
   TP_TRY(rsa_ws_bytes(local_grid(), &P.rd, &w->rsa_bytes));
   w->rsa = c.take(w->rsa_bytes);
+  if (flash_supported(P.d, P.rd.dtype)) w->fb = c.take(flash_bwd_ws_bytes(P.problems, P.seq, P.d));
   return TP_OK;
 }
 
@@ -129,7 +131,8 @@ tp_status attention_ws_bytes(const tp_grid* g, const tp_linear_desc* qd, int64_t
 }
 
 tp_status attention_fwd(tp_grid* g, const tp_linear_desc* qd, int64_t seq, int64_t heads, float scale,
-                        const void* qkv, void* out, void* ws, size_t ws_bytes, cudaStream_t s) {
+                        const void* qkv, void* out, float* lse, void* ws, size_t ws_bytes,
+                        cudaStream_t s) {
   AttnPlan P;
   TP_TRY(attn_plan(g, qd, seq, heads, scale, &P));
   size_t need = 0;
@@ -152,7 +155,7 @@ tp_status attention_fwd(tp_grid* g, const tp_linear_desc* qd, int64_t seq, int64
   if (use_flash && flash_supported(d, qd->dtype) && P.problems <= 65535) {
     // fused forward: the scores stay on chip (flash.cu)
     const float sc = scale != 0.f ? scale : 1.f / std::sqrt(static_cast<float>(d));
-    TP_TRY(flash_attn_fwd(P.problems, P.seq, d, w.buf[0], w.buf[1], w.buf[2], w.buf[3], sc, s));
+    TP_TRY(flash_attn_fwd(P.problems, P.seq, d, w.buf[0], w.buf[1], w.buf[2], w.buf[3], sc, s, lse));
   } else {
     TP_TRY(rsa_fwd(local_grid(), &P.rd, w.buf[0], w.buf[1], w.buf[2], w.buf[3], w.rsa, w.rsa_bytes, s));
   }
@@ -160,8 +163,8 @@ tp_status attention_fwd(tp_grid* g, const tp_linear_desc* qd, int64_t seq, int64
 }
 
 tp_status attention_bwd(tp_grid* g, const tp_linear_desc* qd, int64_t seq, int64_t heads, float scale,
-                        const void* qkv, const void* dout, void* dqkv, void* ws, size_t ws_bytes,
-                        cudaStream_t s) {
+                        const void* qkv, const void* out, const float* lse, const void* dout,
+                        void* dqkv, void* ws, size_t ws_bytes, cudaStream_t s) {
   AttnPlan P;
   TP_TRY(attn_plan(g, qd, seq, heads, scale, &P));
   size_t need = 0;
@@ -176,8 +179,20 @@ tp_status attention_bwd(tp_grid* g, const tp_linear_desc* qd, int64_t seq, int64
   const int64_t ld = P.e.cols, d = P.d;
   for (int comp = 0; comp < 3; ++comp) TP_TRY(pack(P, qkv, w.buf[comp], ld, comp * d, 3 * d, 0, s));
   TP_TRY(pack(P, dout, w.buf[3], P.heads_local * d, 0, d, 0, s));
-  TP_TRY(rsa_bwd(local_grid(), &P.rd, w.buf[0], w.buf[1], w.buf[2], w.buf[3], w.buf[4], w.buf[5],
-                 w.buf[6], w.rsa, w.rsa_bytes, s));
+  static const int use_flash = [] {
+    const char* e = std::getenv("TP_FLASH");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (use_flash && out && lse && w.fb && P.problems <= 65535) {
+    // fused backward: P recomputed on chip from the forward's lse (scores never in HBM)
+    TP_TRY(pack(P, out, w.buf[7], P.heads_local * d, 0, d, 0, s));
+    const float sc = scale != 0.f ? scale : 1.f / std::sqrt(static_cast<float>(d));
+    TP_TRY(flash_attn_bwd(P.problems, P.seq, d, w.buf[0], w.buf[1], w.buf[2], w.buf[7], w.buf[3], lse,
+                          w.buf[4], w.buf[5], w.buf[6], sc, w.fb, s));
+  } else {
+    TP_TRY(rsa_bwd(local_grid(), &P.rd, w.buf[0], w.buf[1], w.buf[2], w.buf[3], w.buf[4], w.buf[5],
+                   w.buf[6], w.rsa, w.rsa_bytes, s));
+  }
   for (int comp = 0; comp < 3; ++comp) TP_TRY(pack(P, w.buf[4 + comp], dqkv, ld, comp * d, 3 * d, 1, s));
   return TP_OK;
 }

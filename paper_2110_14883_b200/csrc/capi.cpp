@@ -1173,25 +1173,26 @@ extern "C" tp_status tp_attention_ws_size(const tp_grid* g, const tp_linear_desc
 
 extern "C" tp_status tp_attention_fwd(tp_grid* g, const tp_linear_desc* d, int64_t seq,
                                       int64_t heads, float scale, const void* qkv, void* out,
-                                      void* ws, size_t ws_bytes, void* stream) {
+                                      float* lse, void* ws, size_t ws_bytes, void* stream) {
   tp::NvtxRange nvtx_("tp_attention_fwd");
   if (!g) return tp::fail(TP_ERR_ARG, "tp_attention_fwd: null grid");
   TP_TRY(tp::contract_check(g, tp::kCallAttnFwd, d,
                             {uint64_t(seq), uint64_t(heads), tp::f32_word(scale)}));
   TP_CUDA(cudaSetDevice(g->device));
-  return tp::attention_fwd(g, d, seq, heads, scale, qkv, out, ws, ws_bytes,
+  return tp::attention_fwd(g, d, seq, heads, scale, qkv, out, lse, ws, ws_bytes,
                            static_cast<cudaStream_t>(stream));
 }
 
 extern "C" tp_status tp_attention_bwd(tp_grid* g, const tp_linear_desc* d, int64_t seq,
-                                      int64_t heads, float scale, const void* qkv, const void* dout,
-                                      void* dqkv, void* ws, size_t ws_bytes, void* stream) {
+                                      int64_t heads, float scale, const void* qkv, const void* out,
+                                      const float* lse, const void* dout, void* dqkv, void* ws,
+                                      size_t ws_bytes, void* stream) {
   tp::NvtxRange nvtx_("tp_attention_bwd");
   if (!g) return tp::fail(TP_ERR_ARG, "tp_attention_bwd: null grid");
   TP_TRY(tp::contract_check(g, tp::kCallAttnBwd, d,
                             {uint64_t(seq), uint64_t(heads), tp::f32_word(scale)}));
   TP_CUDA(cudaSetDevice(g->device));
-  return tp::attention_bwd(g, d, seq, heads, scale, qkv, dout, dqkv, ws, ws_bytes,
+  return tp::attention_bwd(g, d, seq, heads, scale, qkv, out, lse, dout, dqkv, ws, ws_bytes,
                            static_cast<cudaStream_t>(stream));
 }
 

@@ -100,6 +100,9 @@ struct FParams {
   float* acc;
   float* ml;
   int carry_in, last;
+  // optional: per-row log-sum-exp in scaled log2 units, lse = m + log2(l), so that the
+  // probabilities are exp2(s scale log2e - lse) (the fused backward recomputes them)
+  float* lse;
 };
 
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -422,6 +425,7 @@ __global__ void __launch_bounds__(f_threads<D>(), two_cta<D>() ? 2 : 1) flash_fw
     }
     const int64_t q = q0 + r;
     const float inv = l > 0.f ? 1.f / l : 0.f;
+    if (F.last && F.lse && half == 0 && q < F.s) F.lse[row_base + q] = m + __log2f(l);
     if (!F.last) {  // carry out: unnormalised O (fp32) and (m, l) for the next ring block
 #pragma unroll 1
       for (int c = 0; c < OC / 32; ++c) {
@@ -510,7 +514,7 @@ bool flash_supported(int64_t d, tp_dtype dt) { return dt == TP_BF16 && (d == 64 
 
 // q, k, v, out: [problems, s, d] bf16 contiguous.
 tp_status flash_attn_fwd(int64_t problems, int64_t s, int64_t d, const void* q, const void* k,
-                         const void* v, void* out, float scale, cudaStream_t st) {
+                         const void* v, void* out, float scale, cudaStream_t st, float* lse) {
   if (!problems || !s) return TP_OK;
   if (d != 64 && d != 128) return fail(TP_ERR_UNSUPPORTED, "flash: d must be 64 or 128");
   if (problems > 65535) return fail(TP_ERR_UNSUPPORTED, "flash: too many problems for one grid");
@@ -525,6 +529,7 @@ tp_status flash_attn_fwd(int64_t problems, int64_t s, int64_t d, const void* q, 
   F.scale_log2 = scale * 1.4426950408889634f;
   F.dbg = g_flash_dbg;
   F.last = 1;
+  F.lse = lse;
   return d == 64 ? launch<64>(F, st) : launch<128>(F, st);
 }
 

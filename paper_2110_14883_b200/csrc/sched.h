@@ -53,8 +53,17 @@ tp_status rsa_bwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k
 
 // Fused attention forward (flash.cu): [problems, s, d] bf16, d in {64, 128}.
 bool flash_supported(int64_t d, tp_dtype dt);
+// lse (optional, [problems*s] fp32): per-row log-sum-exp in scaled log2 units (for flash_attn_bwd)
 tp_status flash_attn_fwd(int64_t problems, int64_t s, int64_t d, const void* q, const void* k,
-                         const void* v, void* out, float scale, cudaStream_t st);
+                         const void* v, void* out, float scale, cudaStream_t st,
+                         float* lse = nullptr);
+// Fused attention backward (flash_bwd.cu): q, k, v, o, dout [problems, s, d] bf16, lse
+// [problems*s] fp32 from flash_attn_fwd; writes dq, dk, dv [problems, s, d] bf16. ws: fp32
+// scratch of flash_bwd_ws_bytes (dQ accumulator, row deltas).
+size_t flash_bwd_ws_bytes(int64_t problems, int64_t s, int64_t d);
+tp_status flash_attn_bwd(int64_t problems, int64_t s, int64_t d, const void* q, const void* k,
+                         const void* v, const void* o, const void* dout, const float* lse,
+                         void* dq, void* dk, void* dv, float scale, void* ws, cudaStream_t st);
 tp_status flash_attn_fwd_carry(int64_t problems, int64_t s, int64_t d, const void* q, const void* k,
                                const void* v, void* out, float* acc, float* ml, bool carry_in,
                                bool last, float scale, cudaStream_t st);
@@ -63,10 +72,11 @@ tp_status flash_attn_fwd_carry(int64_t problems, int64_t s, int64_t d, const voi
 tp_status attention_ws_bytes(const tp_grid* g, const tp_linear_desc* qd, int64_t seq, int64_t heads,
                              size_t* bytes);
 tp_status attention_fwd(tp_grid* g, const tp_linear_desc* qd, int64_t seq, int64_t heads, float scale,
-                        const void* qkv, void* out, void* ws, size_t ws_bytes, cudaStream_t s);
-tp_status attention_bwd(tp_grid* g, const tp_linear_desc* qd, int64_t seq, int64_t heads, float scale,
-                        const void* qkv, const void* dout, void* dqkv, void* ws, size_t ws_bytes,
+                        const void* qkv, void* out, float* lse, void* ws, size_t ws_bytes,
                         cudaStream_t s);
+tp_status attention_bwd(tp_grid* g, const tp_linear_desc* qd, int64_t seq, int64_t heads, float scale,
+                        const void* qkv, const void* out, const float* lse, const void* dout,
+                        void* dqkv, void* ws, size_t ws_bytes, cudaStream_t s);
 
 tp_status sched_fwd(Run& R, const void* x, const void* w, const void* bias, void* y);
 tp_status sched_bwd(Run& R, const void* dy, const void* x, const void* w, void* dx, void* dw,

@@ -27,7 +27,7 @@ def api():
     return api
 
 
-def run_attn(api, mode, p, d, M, h, seq, heads, dtype, qkv, dout, sq, sp):
+def run_attn(api, mode, p, d, M, h, seq, heads, dtype, qkv, dout, sq, sp, fused_bwd=False):
     transport = api.TP_TRANSPORT_LOCAL if p > 1 else api.TP_TRANSPORT_NONE
     uid = api.tp_get_unique_id(transport)
     gq, gd = to_dev(qkv, dtype), to_dev(dout, dtype)
@@ -49,9 +49,12 @@ def run_attn(api, mode, p, d, M, h, seq, heads, dtype, qkv, dout, sq, sp):
                 api.tp_pack(g, dp, "X", gd, do)
                 ws = torch.empty(api.tp_attention_ws_size(g, dq, seq, heads), device="cuda",
                                  dtype=torch.uint8)
-                api.tp_attention_fwd(g, dq, seq, heads, x, out, ws)
+                hl = eq[3] // (3 * (h // heads))  # heads held by this rank
+                lse = torch.empty(hl * eq[1], device="cuda", dtype=torch.float32) if fused_bwd else None
+                api.tp_attention_fwd(g, dq, seq, heads, x, out, ws, lse=lse)
                 dx = torch.empty_like(x)
-                api.tp_attention_bwd(g, dq, seq, heads, x, do, dx, ws)
+                api.tp_attention_bwd(g, dq, seq, heads, x, do, dx, ws, out=out if fused_bwd else None,
+                                     lse=lse)
             st.synchronize()
             return {"out": to_np(out), "dqkv": to_np(dx)}
         finally:
@@ -78,6 +81,35 @@ def test_attention_core_vs_oracle(api, lay, dtype):
     tol = 1e-2 if dtype == "bf16" else 1e-5
     assert rel_fro(out, mha.mha_fwd(qkv, seq, heads)) <= tol
     assert rel_fro(dqkv, mha.mha_bwd(qkv, dout, seq, heads)) <= tol
+
+
+@pytest.mark.parametrize("lay", LAYOUTS, ids=lambda l: "-".join(map(str, l)))
+@pytest.mark.parametrize("seq,heads,dh", [(128, 4, 64), (256, 2, 128), (197, 6, 64), (300, 2, 128)])
+def test_attention_fused_backward_vs_oracle(api, lay, seq, heads, dh):
+    """bf16, d in {64, 128}: the forward writes the row log-sum-exp and the backward runs the
+    fused kernel (flash_bwd.cu: P recomputed on chip, dQ accumulated across key tiles) - aligned
+    and ragged sequences (197 = ViT-S/16, 300: a partial last tile of keys and of queries)."""
+    mode, p, d, sq, sp = lay
+    h = heads * dh
+    nseq = 8
+    M = seq * nseq
+    qkv = synth.tensor(37, 0, M, 3 * h, dtype="bf16").astype(np.float64)
+    dout = synth.tensor(37, 1, M, h, dtype="bf16").astype(np.float64)
+    try:
+        per = run_attn(api, mode, p, d, M, h, seq, heads, "bf16", qkv, dout, sq, sp, fused_bwd=True)
+    except api.TPError as e:  # a layout whose blocks split a head (heads % column split)
+        assert "head" in str(e)
+        pytest.skip(str(e))
+    grid = build_grid(mode, p, d)
+    out = gather_full(grid, spec_of(M, h, h, sp, sp), {r: per[r]["out"] for r in range(p)}, "X")
+    dqkv = gather_full(grid, spec_of(M, h, 3 * h, sq, sq), {r: per[r]["dqkv"] for r in range(p)}, "Y")
+    assert rel_fro(out, mha.mha_fwd(qkv, seq, heads)) <= 1e-2
+    ref = mha.mha_bwd(qkv, dout, seq, heads)
+    assert rel_fro(dqkv, ref) <= 1e-2
+    # each of dQ, dK, dV on its own (columns [q | k | v] per head)
+    for c in range(3):
+        cols = np.concatenate([np.arange(3 * dh * g + c * dh, 3 * dh * g + (c + 1) * dh) for g in range(heads)])
+        assert rel_fro(dqkv[:, cols], ref[:, cols]) <= 1e-2, "qkv"[c]
 
 
 def test_attention_rejects_split_heads_and_sequences(api):
