@@ -1445,6 +1445,11 @@ tp_status launch_wide(const GemmArgs* gs, int n, cudaStream_t s) {
   G.total_units = units;
   int cap = clusters;
   if (gs[0].reserve_sms > 0) cap = std::max(1, std::min(cap, (sm_count() - gs[0].reserve_sms) / 2));
+  static const int env_np = [] {  // measurement knob: one tile per cluster, hardware-scheduled
+    const char* e = std::getenv("TP_GEMM_WIDE_NP");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (env_np && gs[0].reserve_sms <= 0) cap = units;
   const int grid = 2 * (units < cap ? units : cap);
   const int tok = prof_begin(0, s, flops);
   TP_CUDA(launch_pdl(kern, dim3(grid), dim3(threads_of<4>()), kWSmem, s, G));
