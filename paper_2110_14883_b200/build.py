@@ -45,9 +45,10 @@ def nvcc():
 
 def common_flags():
     inc, _ = nccl_paths()
+    extra = os.environ.get("TP_NVCC_FLAGS", "").split()  # diagnostics builds, e.g. -DTP_LOOP_CLOCKS=1
     return ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
                    "-I", os.path.join(ROOT, "include"), "-I", inc,
-                   "--expt-relaxed-constexpr", "-Xptxas", "-v" if os.environ.get("TP_PTXAS_V") else "-O3"]
+                   "--expt-relaxed-constexpr", "-Xptxas", "-v" if os.environ.get("TP_PTXAS_V") else "-O3"] + extra
 
 
 def sources():
