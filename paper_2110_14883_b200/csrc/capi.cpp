@@ -1042,6 +1042,7 @@ extern "C" tp_status tp_cost_model(tp_mode mode, int world, int q, int d, const 
   const double e = desc->dtype == TP_BF16 ? 2.0 : 4.0;
   const int j = g.q, dd = g.d;
   const bool row = desc->split_1d != 0;
+  double cannon_acc = 0;  // Cannon backward accumulator elements (fp32 on the wire)
   tp_cost c{};
   switch (mode) {
     case TP_1D:  // col: AR of dX in bwd; row: AR of Y in fwd (one ring AR per layer, A3)
@@ -1054,8 +1055,12 @@ extern "C" tp_status tp_cost_model(tp_mode mode, int world, int q, int d, const 
     case TP_2D:  // SUMMA: fwd bcast X,W; bwd bcast W + reduce dX, bcast X + reduce dW (A4)
       c.paper_elems = 3.0 * (j - 1) * (Sx + Sw);
       c.counted_elems = c.paper_elems;
-      // Cannon forward: skew (q-1)/q + (q-1) unit shifts of X and W (oracle/cannon.py)
-      if (desc->flags & TP_FLAG_CANNON) c.counted_elems += (j - 1) * (Sx + Sw) / j;
+      // Cannon (oracle/cannon.py): forward skew (q-1)/q + (q-1) unit shifts of X and W; backward
+      // (reading N7) the same for W / X plus q accumulator shifts and the delivery (q-1)/q
+      if (desc->flags & TP_FLAG_CANNON) {
+        cannon_acc = (j + (j - 1.0) / j) * (Sx + Sw);
+        c.counted_elems = 2.0 * ((j - 1.0) / j + (j - 1)) * (Sx + Sw) + cannon_acc;
+      }
       c.mem_x = Sx / p;
       c.mem_w = Sw / p;
       c.mem_y = Sy / p;
@@ -1074,7 +1079,11 @@ extern "C" tp_status tp_cost_model(tp_mode mode, int world, int q, int d, const 
       }
       c.paper_elems = 3.0 * (j - 1) * (Sx / dd + Sw);
       c.counted_elems = dd * 3.0 * (j - 1) * (Sx / dd + Sw) + 2.0 * (dd - 1) * Sw;
-      if (desc->flags & TP_FLAG_CANNON) c.counted_elems += dd * (j - 1) * (Sx / dd + Sw) / j;
+      if (desc->flags & TP_FLAG_CANNON) {  // per plane as in 2D (reading N7), + the depth term
+        cannon_acc = dd * (j + (j - 1.0) / j) * (Sx / dd + Sw);
+        c.counted_elems = dd * 2.0 * ((j - 1.0) / j + (j - 1)) * (Sx / dd + Sw) + cannon_acc +
+                          2.0 * (dd - 1) * Sw;
+      }
       c.mem_x = Sx / p;
       c.mem_w = (desc->flags & TP_FLAG_W25_DEPTH_SHARDED) ? Sw / p : Sw / (double(j) * j);
       c.mem_y = Sy / p;
@@ -1089,7 +1098,8 @@ extern "C" tp_status tp_cost_model(tp_mode mode, int world, int q, int d, const 
     default:
       return tp::fail(TP_ERR_ARG, "tp_cost_model: unknown mode");
   }
-  c.link_bytes = c.counted_elems / p * e;
+  // Cannon's backward carries fp32 accumulators: those elements cost 4 bytes
+  c.link_bytes = (c.counted_elems - cannon_acc) / p * e + cannon_acc / p * 4.0;
   c.flops = 6.0 * M * K * N / p;
   if (peak_tflops > 0) c.t_tensor_us = c.flops / (peak_tflops * 1e12) * 1e6;
   if (link_gbs > 0) c.t_link_us = c.link_bytes / (link_gbs * 1e9) * 1e6;

@@ -536,6 +536,78 @@ tp_status cannon_ab(Ctx& C, const Plane& P, const void* x, const void* W, const 
   return TP_OK;
 }
 
+// Cannon's backward (TP_FLAG_CANNON; reading N7, oracle/cannon.cannon_bwd): one product, the
+// operand `B` circulating along `bline` (skew by `bskew`, then +1 per step) and the fp32
+// accumulator along `aline` (+1 after every step, then a delivery shift by `deliver`).
+//   ABT (dX = dY W^T): part_t = dY . W_t^T   [mb, kq]  W along the column, acc along the row
+//   ATB (dW = X^T dY): part_t = X_t^T . dY   [kq, nq]  X along the row, acc along the column
+// Step t: the GEMM writes part_t (fp32) while the accumulator of step t-1 and the operand of
+// step t+1 travel on the comm stream; acc_t = part_t + acc_{t-1} (fp32 add), then shifted.
+tp_status cannon_bwd_product(Ctx& C, const Plane& P, bool abt, const void* stat, const void* B,
+                             void* out) {
+  const int q = P.q;
+  Comm* bline = abt ? P.col : P.row;
+  Comm* aline = abt ? P.row : P.col;
+  const int bskew = abt ? P.j : P.i;
+  const int deliver = abt ? -P.i : -P.j;
+  const int64_t bsz = abt ? P.kq * P.nq : P.mb * P.kq;   // circulating operand (dtype)
+  const int64_t am = abt ? P.mb : P.kq, an = abt ? P.kq : P.nq;  // accumulator [am, an]
+  const int64_t asz = am * an;
+  void* bb[2] = {C.ws(bsz), C.ws(bsz)};
+  float* part[2] = {static_cast<float*>(C.ws(asz, 4)), static_cast<float*>(C.ws(asz, 4))};
+  float* recv[2] = {static_cast<float*>(C.ws(asz, 4)), static_cast<float*>(C.ws(asz, 4))};
+  if (C.R.plan) return TP_OK;
+  TP_TRY(C.order(C.R.s, C.R.cs));
+  const void* cb = B;
+  int ib = 0;
+  if (bskew) {
+    TP_TRY(bline->shift(B, bb[0], bsz, C.dt, bskew, C.R.cs));
+    cb = bb[0];
+    ib = 1;
+  }
+  TP_TRY(C.order(C.R.cs, C.R.s));
+  cudaEvent_t acc_in = nullptr;
+  for (int t = 0; t < q; ++t) {
+    const bool last = t == q - 1;
+    cudaEvent_t moved = nullptr;
+    void* nb = bb[ib];
+    if (!last) {  // the next operand block moves while this step's GEMM runs
+      TP_TRY(C.order(C.R.s, C.R.cs));
+      TP_TRY(bline->shift(cb, nb, bsz, C.dt, 1, C.R.cs));
+      moved = C.record(C.R.cs);
+    }
+    float* pt = part[t & 1];
+    C.ovb = double(last ? 0 : bsz) * C.esz + double(t > 0 ? asz : 0) * 4;
+    if (abt)
+      TP_TRY(C.mm(P.mb, P.kq, P.nq, stat, false, cb, true, pt, TP_FP32, 1.f, nullptr, nullptr));
+    else
+      TP_TRY(C.mm(P.kq, P.nq, P.mb, cb, true, stat, false, pt, TP_FP32, 1.f, nullptr, nullptr));
+    C.ovb = 0;
+    if (t > 0) {  // + the accumulator that arrived from the neighbour
+      TP_CUDA(cudaStreamWaitEvent(C.R.s, acc_in, 0));
+      TP_TRY(launch_add(pt, recv[(t - 1) & 1], pt, size_t(asz), TP_FP32, C.R.s));
+    }
+    TP_TRY(C.order(C.R.s, C.R.cs));
+    TP_TRY(aline->shift(pt, recv[t & 1], asz, TP_FP32, 1, C.R.cs));
+    acc_in = C.record(C.R.cs);
+    if (!last) {
+      TP_CUDA(cudaStreamWaitEvent(C.R.s, moved, 0));
+      cb = nb;
+      ib ^= 1;
+    }
+  }
+  // deliver: the accumulator of this rank's block sits `deliver` positions away
+  float* fin = recv[(q - 1) & 1];
+  if (deliver % q) {
+    float* dst = part[0];  // free: every step's reads of it completed before the last shift
+    TP_TRY(aline->shift(fin, dst, asz, TP_FP32, deliver, C.R.cs));
+    fin = dst;
+  }
+  TP_TRY(C.order(C.R.cs, C.R.s));
+  // out = alpha * acc in the layer dtype (the GEMM epilogue with K = 0)
+  return C.mm(am, an, 0, nullptr, false, nullptr, false, out, C.dt, C.d->alpha, fin, nullptr);
+}
+
 // SUMMA "ABT" (a-6): dX[i,k] = reduce_row( dY[i,j] . W[k,j]^T ), W panels down the columns.
 tp_status summa_abt(Ctx& C, const Plane& P, const void* dy, const void* W, void* dx) {
   const float alpha = C.d->alpha;
@@ -886,6 +958,9 @@ tp_status bwd_2d(Ctx& C, const void* dy, const void* x, const void* w, const voi
     if (!C.R.plan)
       TP_TRY(C.mm2(C.args(P.mb, P.kq, P.nq, dy, false, W, true, dx, C.dt, C.d->alpha, nullptr, nullptr),
                    C.args(P.kq, P.nq, P.mb, x, true, dy, false, dwt, C.dt, C.d->alpha, nullptr, nullptr)));
+  } else if (C.d->flags & TP_FLAG_CANNON) {  // NEXT-4: Cannon's backward (reading N7)
+    if (dx) TP_TRY(cannon_bwd_product(C, P, true, dy, W, dx));
+    TP_TRY(cannon_bwd_product(C, P, false, dy, x, dwt));
   } else {
     if (dx) TP_TRY(summa_abt(C, P, dy, W, dx));
     TP_TRY(summa_atb(C, P, x, dy, dwt));

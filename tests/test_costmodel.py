@@ -85,8 +85,8 @@ def test_errors():
 
 @pytest.mark.parametrize("q", [2, 3, 4])
 def test_cannon_volume_matches_oracle_ledger(q):
-    """Cannon's forward moves the SUMMA forward volume plus the skew: checked against the
-    message count of the oracle's Cannon program (oracle/cannon.py)."""
+    """Cannon's volume (forward: SUMMA's plus the skew; backward: moving accumulators, reading N7)
+    equals the message count of the oracle's Cannon programs (oracle/cannon.py)."""
     import numpy as np
     from oracle import cannon
     from oracle.fabric import Fabric
@@ -98,11 +98,13 @@ def test_cannon_volume_matches_oracle_ledger(q):
     fab = Fabric()
     X, W = np.ones((M, K)), np.ones((K, N))
     cannon.cannon_fwd(grid, shard(grid, spec, X, "X"), shard(grid, spec, W, "W"), fab=fab)
-    fwd = fab.ledger.total()
+    cannon.cannon_bwd(grid, shard(grid, spec, np.ones((M, N)), "Y"), shard(grid, spec, X, "X"),
+                      shard(grid, spec, W, "W"), fab=fab)
     c0 = api.tp_cost_model("2d", q * q, api.desc(M, K, N), q=q)
     c1 = api.tp_cost_model("2d", q * q, api.desc(M, K, N, flags=0x10), q=q)
-    summa_fwd = cf.counted_volume("2d", M, K, N, q=q, part="fwd")
-    assert c1["counted_elems"] - c0["counted_elems"] == pytest.approx(fwd - summa_fwd)
+    summa = cf.counted_volume("2d", M, K, N, q=q, part="fwd+bwd")
+    assert c0["counted_elems"] == pytest.approx(summa)
+    assert c1["counted_elems"] == pytest.approx(fab.ledger.total())
 
 
 def test_solomonik_volume_equals_oracle():

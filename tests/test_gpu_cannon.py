@@ -41,6 +41,11 @@ def test_cannon_vs_oracle(api, mode, p, d, flags):
         Yc = cannon.cannon_fwd(grid, shard(grid, spec, X, "X"), shard(grid, spec, W, "W"),
                                shard(grid, spec, b, "B"), 0.5, Fabric())
         assert rel_fro(gather(mode, p, d, spec, per, "Y", "Y"), gather_full(grid, spec, Yc, "Y")) <= 1e-2
+        # the backward ran Cannon's schedule too (reading N7): equal to the oracle's program
+        dXc, dWc = cannon.cannon_bwd(grid, shard(grid, spec, dY, "Y"), shard(grid, spec, X, "X"),
+                                     shard(grid, spec, W, "W"), 0.5, Fabric())
+        assert rel_fro(gather(mode, p, d, spec, per, "dX", "X"), gather_full(grid, spec, dXc, "X")) <= 1e-2
+        assert rel_fro(gather(mode, p, d, spec, per, "dW", "W"), gather_full(grid, spec, dWc, "W")) <= 1e-2
 
 
 def test_cannon_exact_integer_bit_equal(api):
@@ -48,5 +53,8 @@ def test_cannon_exact_integer_bit_equal(api):
     X, W, dY, _ = synth.layer_inputs(5, M, K, N, kind="ternary")
     per = tp_layer(api, "2d", 9, 1, M, K, N, X, W, dY, None, "bf16", 0, 0, CANNON)
     spec = spec_of(M, K, N)
-    Yr, _, _, _ = oracle_layer("2d", 9, 1, spec, X, W, dY)
+    Yr, dXr, dWr, _ = oracle_layer("2d", 9, 1, spec, X, W, dY)
     assert np.array_equal(gather("2d", 9, 1, spec, per, "Y", "Y"), Yr)
+    # Cannon's backward: fp32 accumulators on the wire, exact for these integer sums
+    assert np.array_equal(gather("2d", 9, 1, spec, per, "dX", "X"), dXr)
+    assert np.array_equal(gather("2d", 9, 1, spec, per, "dW", "W"), dWr)
