@@ -518,6 +518,8 @@ def run_ours(a):
         "gpu_launches": launches,
         "roofline": roof,
         "memory_per_rank": mem,
+        # library tuning knobs not at their measured defaults (tp_knobs): empty in a normal run
+        "tuning_overrides": {k["name"]: k["value"] for k in api.tp_knobs() if k["source"] != "default"},
         "clocks": clk.summary(),
         "e2e": e2e,
         "cpu_baseline": cpu,

@@ -147,6 +147,17 @@ tp_status tp_grid_destroy(tp_grid* grid);
  * Collective when the grid is shared: every rank must set the same value. */
 tp_status tp_grid_set_contract_check(tp_grid* grid, int enable);
 
+/* Tuning knobs: every kernel-variant / dispatch choice the library does not derive from the
+ * problem itself (GEMM kernel and tile forcing, split-K, raster, wide tiles, PDL, fused
+ * attention, comm SM reservation). Defaults are the measured choices; a TP_* environment
+ * variable of the same name, read once, overrides the default; tp_knob_set overrides both for
+ * later calls (process-wide). tp_knobs writes a JSON array of {name, value, default, source
+ * ("default" | "env" | "api"), what} into buf (NUL-terminated, truncated to cap; *needed =
+ * required size). Errors: TP_ERR_ARG for an unknown name. */
+tp_status tp_knob_set(const char* name, int value);
+tp_status tp_knob_get(const char* name, int* value);
+tp_status tp_knobs(char* buf, size_t cap, size_t* needed);
+
 /* Failure detection. tp_grid_check: TP_OK, or TP_ERR_NCCL with the detail when a
  * communicator of the grid reports an asynchronous error (ncclCommGetAsyncError: a peer died,
  * a network / NVLink fault); non-blocking, callable from a watchdog thread while collectives

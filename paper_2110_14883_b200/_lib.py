@@ -36,7 +36,7 @@ TP_FLAG_PEER_STAGED = 0x40
 EXPORTED = [
     "tp_status_string", "tp_last_error", "tp_version", "tp_get_unique_id", "tp_grid_init",
     "tp_grid_coords", "tp_grid_dims", "tp_grid_group", "tp_grid_destroy", "tp_shard_extent",
-    "tp_grid_set_contract_check", "tp_grid_check", "tp_grid_abort", "tp_axis_collective", "tp_peer_staged_bytes", "tp_prof_spans",
+    "tp_knob_set", "tp_knob_get", "tp_knobs", "tp_grid_set_contract_check", "tp_grid_check", "tp_grid_abort", "tp_axis_collective", "tp_peer_staged_bytes", "tp_prof_spans",
     "tp_workspace_size", "tp_linear_fwd", "tp_linear_bwd", "tp_pack", "tp_unpack", "tp_gemm",
     "tp_gemm_ws_bytes",
     "tp_colsum", "tp_fill", "tp_l2_flush", "tp_prof_enable", "tp_prof_reset", "tp_prof_read",
@@ -85,6 +85,9 @@ _sigs = {
     "tp_grid_destroy": (_i, [_vp]),
     "tp_grid_set_contract_check": (_i, [_vp, _i]),
     "tp_grid_check": (_i, [_vp]),
+    "tp_knob_set": (_i, [C.c_char_p, _i]),
+    "tp_knob_get": (_i, [C.c_char_p, C.POINTER(_i)]),
+    "tp_knobs": (_i, [C.c_char_p, _sz, C.POINTER(_sz)]),
     "tp_grid_abort": (_i, [_vp]),
     "tp_axis_collective": (_i, [_vp, _i, _i, _vp, _vp, _sz, _i, _i, _vp]),
     "tp_peer_staged_bytes": (_i, [_vp, C.POINTER(C.c_uint64)]),

@@ -149,6 +149,26 @@ def tp_peer_staged_bytes(g) -> int:
     return int(v.value)
 
 
+def tp_knob_set(name, value):
+    _check(lib.tp_knob_set(name.encode(), int(value)), "tp_knob_set")
+
+
+def tp_knob_get(name) -> int:
+    v = C.c_int()
+    _check(lib.tp_knob_get(name.encode(), C.byref(v)), "tp_knob_get")
+    return v.value
+
+
+def tp_knobs():
+    """The library's tuning knobs: list of {name, value, default, source, what}."""
+    import json
+    need = C.c_size_t()
+    _check(lib.tp_knobs(None, 0, C.byref(need)), "tp_knobs")
+    buf = C.create_string_buffer(need.value)
+    _check(lib.tp_knobs(buf, need.value, C.byref(need)), "tp_knobs")
+    return json.loads(buf.value.decode())
+
+
 def tp_grid_check(g):
     """Raise TPError if a communicator of the grid reports an asynchronous error."""
     _check(lib.tp_grid_check(g), "tp_grid_check")

@@ -148,10 +148,7 @@ tp_status attention_fwd(tp_grid* g, const tp_linear_desc* qd, int64_t seq, int64
   TP_TRY(attn_carve(P, c, &w));
   const int64_t ld = P.e.cols, d = P.d;
   for (int comp = 0; comp < 3; ++comp) TP_TRY(pack(P, qkv, w.buf[comp], ld, comp * d, 3 * d, 0, s));
-  static const int use_flash = [] {
-    const char* e = std::getenv("TP_FLASH");
-    return e ? std::atoi(e) : 1;
-  }();
+  const int use_flash = knob("TP_FLASH");
   if (use_flash && flash_supported(d, qd->dtype) && P.problems <= 65535) {
     // fused forward: the scores stay on chip (flash.cu)
     const float sc = scale != 0.f ? scale : 1.f / std::sqrt(static_cast<float>(d));
@@ -179,10 +176,7 @@ tp_status attention_bwd(tp_grid* g, const tp_linear_desc* qd, int64_t seq, int64
   const int64_t ld = P.e.cols, d = P.d;
   for (int comp = 0; comp < 3; ++comp) TP_TRY(pack(P, qkv, w.buf[comp], ld, comp * d, 3 * d, 0, s));
   TP_TRY(pack(P, dout, w.buf[3], P.heads_local * d, 0, d, 0, s));
-  static const int use_flash = [] {
-    const char* e = std::getenv("TP_FLASH");
-    return e ? std::atoi(e) : 1;
-  }();
+  const int use_flash = knob("TP_FLASH");
   if (use_flash && out && lse && w.fb && P.problems <= 65535) {
     // fused backward: P recomputed on chip from the forward's lse (scores never in HBM)
     TP_TRY(pack(P, out, w.buf[7], P.heads_local * d, 0, d, 0, s));

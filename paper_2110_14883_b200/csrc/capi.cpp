@@ -27,6 +27,66 @@ tp_status fail(tp_status s, const std::string& msg) {
 
 std::atomic<int64_t> g_launches{0};
 
+// ---- tuning knobs: every dispatch / kernel-variant choice the library makes from outside its
+// own measurements, in one table (defaults = the measured choices, see DESIGN / profiles).
+namespace {
+struct KnobDef {
+  const char* name;
+  int def;
+  const char* what;
+};
+constexpr KnobDef kKnobs[] = {
+    {"TP_PDL", 1, "programmatic dependent launch for the GEMM kernels (0 off)"},
+    {"TP_GEMM_KERNEL", 0, "force the GEMM kernel: 1 = 1-CTA tiles, 2 = CTA-pair tiles (0 auto)"},
+    {"TP_GEMM_BN", 0, "force the pair tile width 128 / 256 (0 auto)"},
+    {"TP_GEMM_MC", 0, "force a pair-kernel cluster: 2/3 = A/B multicast over 2 pairs, 4 = 2x2, 5 = K-split pair cluster (0/1 none)"},
+    {"TP_GEMM_EPI_WARPS", 0, "force 4 or 8 epilogue warps in the pair kernel (0 auto)"},
+    {"TP_GEMM_SPLITK", 1, "split-K in the pair kernel when tiles are few (0 off)"},
+    {"TP_GEMM_SPLIT_OWNER", 1, "split-K owner-wait / exchange when all splits are co-resident (0 last-arriver)"},
+    {"TP_GEMM_GROUP", 1, "independent products (dX, dW) as one grouped launch (0 separate)"},
+    {"TP_GEMM_GROUP_BN", 256, "pair tile width of grouped launches"},
+    {"TP_GEMM_GROUP_SPLIT", 1, "split-K inside grouped launches for long-K members (0 off)"},
+    {"TP_GEMM_RASTER", 8, "pair-tile rows per raster band"},
+    {"TP_GEMM_WIDE", -1, "512x256 wide pair tiles: -1 auto (K >= 12288, >= #SMs tiles), 0 off, 1 wherever legal"},
+    {"TP_GEMM_WIDE_RASTER", 8, "wide-tile rows per raster band"},
+    {"TP_GEMM_WIDE_NP", 0, "wide tiles non-persistent (one tile per cluster; measured equal)"},
+    {"TP_GEMM_V1_BN", 0, "force the 1-CTA tile width 128 / 256 (0 auto)"},
+    {"TP_GEMM_V1_TMA_STORE", 1, "1-CTA kernel TMA-store epilogue (0 per-element stores)"},
+    {"TP_COMM_SMS", -1, "SMs a GEMM leaves to a collective running under it (-1 sized to the transfer)"},
+    {"TP_FLASH", 1, "fused attention kernels (0 = two-pass through HBM)"},
+    {"TP_RSA_FUSED", 1, "online-softmax ring for Ring Self-Attention in bf16 (0 two-pass)"},
+};
+constexpr int kNumKnobs = sizeof(kKnobs) / sizeof(kKnobs[0]);
+struct KnobState {
+  bool init = false, overridden = false, from_env = false;
+  int value = 0;
+};
+std::mutex g_knob_mu;
+KnobState g_knob[kNumKnobs];
+int knob_index(const char* name) {
+  for (int i = 0; i < kNumKnobs; ++i)
+    if (std::strcmp(kKnobs[i].name, name) == 0) return i;
+  return -1;
+}
+KnobState& knob_state(int i) {  // caller holds g_knob_mu
+  KnobState& k = g_knob[i];
+  if (!k.init) {
+    const char* e = std::getenv(kKnobs[i].name);
+    k.from_env = e != nullptr;
+    k.value = e ? std::atoi(e) : kKnobs[i].def;
+    k.init = true;
+  }
+  return k;
+}
+}  // namespace
+
+int knob(const char* name) {
+  const int i = knob_index(name);
+  if (i < 0) return 0;
+  std::lock_guard<std::mutex> lk(g_knob_mu);
+  return knob_state(i).value;
+}
+
 // NVTX range over an entry point (host-side; nsys / ncu --nvtx show the library's calls)
 struct NvtxRange {
   explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
@@ -108,10 +168,7 @@ bool prof_on() { return g_prof_on.load(std::memory_order_relaxed); }
 thread_local int t_rank = -1;
 
 bool pdl_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("TP_PDL");
-    return !e || std::atoi(e) != 0;
-  }();
+  const bool on = knob("TP_PDL") != 0;
   return on;
 }
 
@@ -517,6 +574,46 @@ tp_status tp_grid_abort(tp_grid* g) {
   for (auto& a : g->unit_axis)
     if (a) a->abort();
   if (g->nccl) nccl_world_abort(g->nccl);
+  return TP_OK;
+}
+
+tp_status tp_knob_set(const char* name, int value) {
+  const int i = name ? knob_index(name) : -1;
+  if (i < 0) return fail(TP_ERR_ARG, std::string("tp_knob_set: unknown knob ") + (name ? name : "(null)"));
+  std::lock_guard<std::mutex> lk(g_knob_mu);
+  KnobState& k = knob_state(i);
+  k.value = value;
+  k.overridden = true;
+  return TP_OK;
+}
+
+tp_status tp_knob_get(const char* name, int* value) {
+  const int i = name ? knob_index(name) : -1;
+  if (i < 0 || !value) return fail(TP_ERR_ARG, "tp_knob_get: unknown knob or null output");
+  std::lock_guard<std::mutex> lk(g_knob_mu);
+  *value = knob_state(i).value;
+  return TP_OK;
+}
+
+tp_status tp_knobs(char* buf, size_t cap, size_t* needed) {
+  std::string j = "[";
+  {
+    std::lock_guard<std::mutex> lk(g_knob_mu);
+    for (int i = 0; i < kNumKnobs; ++i) {
+      const KnobState& k = knob_state(i);
+      j += std::string(i ? "," : "") + "{\"name\":\"" + kKnobs[i].name + "\",\"value\":" +
+           std::to_string(k.value) + ",\"default\":" + std::to_string(kKnobs[i].def) +
+           ",\"source\":\"" + (k.overridden ? "api" : k.from_env ? "env" : "default") +
+           "\",\"what\":\"" + kKnobs[i].what + "\"}";
+    }
+  }
+  j += "]";
+  if (needed) *needed = j.size() + 1;
+  if (buf && cap) {
+    const size_t n = std::min(cap - 1, j.size());
+    std::memcpy(buf, j.data(), n);
+    buf[n] = 0;
+  }
   return TP_OK;
 }
 

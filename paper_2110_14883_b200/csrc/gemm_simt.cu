@@ -170,10 +170,7 @@ tp_status gemm(const GemmArgs& g, cudaStream_t s) {
                 "of 8 elements (lda=" + std::to_string(g.lda) + ", ldb=" + std::to_string(g.ldb) + ")");
   // Kernel choice: the CTA-pair kernel unless the problem is a single 128-row strip or the
   // output cannot take TMA stores; TP_GEMM_KERNEL=1|2 forces one (A/B measurements).
-  static const int force = [] {
-    const char* e = std::getenv("TP_GEMM_KERNEL");
-    return e ? std::atoi(e) : 0;
-  }();
+  const int force = knob("TP_GEMM_KERNEL");
   // The pair kernel needs enough 256x256 pair tiles to occupy the SM pairs; below that, the
   // streaming-bound small-M shapes run faster as 1-CTA tiles (measured, see
   // profiles/r01_gemm_v2_summary.md).
@@ -222,14 +219,8 @@ bool group_eligible(const GemmArgs& g) {
 }  // namespace
 
 tp_status gemm_group(const GemmArgs* gs, int n, cudaStream_t s) {
-  static const int force = [] {
-    const char* e = std::getenv("TP_GEMM_KERNEL");
-    return e ? std::atoi(e) : 0;
-  }();
-  static const int group_env = [] {
-    const char* e = std::getenv("TP_GEMM_GROUP");
-    return e ? std::atoi(e) : 1;
-  }();
+  const int force = knob("TP_GEMM_KERNEL");
+  const int group_env = knob("TP_GEMM_GROUP");
   bool all = n >= 1 && n <= 4 && force != 1 && group_env;
   for (int i = 0; all && i < n; ++i) all = group_eligible(gs[i]);
   if (all && n > 1) return gemm_tc2_group(gs, n, s);

@@ -603,10 +603,7 @@ tp_status launch(const GemmArgs& g, cudaStream_t s) {
   // D through TMA stores when its rows are 16-byte aligned (bf16 box 64 x 32, fp32 32 x 32)
   CUtensorMap td;
   std::memset(&td, 0, sizeof(td));
-  static const int env_tma = [] {
-    const char* e = std::getenv("TP_GEMM_V1_TMA_STORE");
-    return e ? std::atoi(e) : 1;
-  }();
+  const int env_tma = knob("TP_GEMM_V1_TMA_STORE");
   // A TMA store writes whole 16-byte granules of the inner dimension: when a row of D does not
   // end on a granule (N * osz % 16 != 0) it would also write zeros to the columns between N and
   // the next granule - elements outside D (measured: tools/gemm_probe_ragged.py). Those
@@ -634,10 +631,7 @@ tp_status gemm_tc_bf16(const GemmArgs& g, cudaStream_t s) {
   int dev = 0;
   TP_CUDA(cudaGetDevice(&dev));
   const int64_t tiles256 = ((g.M + BM - 1) / BM) * ((g.N + 255) / 256);
-  static const int force_bn = [] {
-    const char* e = std::getenv("TP_GEMM_V1_BN");
-    return e ? std::atoi(e) : 0;
-  }();
+  const int force_bn = knob("TP_GEMM_V1_BN");
   // measured (profiles/r01_gemm_v2_summary.md): 128x256 tiles win once ~120+ of them exist
   const bool wide = force_bn ? force_bn == 256 : tiles256 >= (num_sms(dev) * 13) / 16;
   if (wide) {

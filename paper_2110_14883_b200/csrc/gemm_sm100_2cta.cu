@@ -1243,10 +1243,7 @@ tp_status setup_prob(const GemmArgs& g, Prob& pr, int clusters, int split_mode, 
   const int ptiles = supers * pairs_of(MC);
   const int num_k = pr.num_kb;
   int S = 1;
-  static const int env_split = [] {
-    const char* e = std::getenv("TP_GEMM_SPLITK");
-    return e ? std::atoi(e) : 1;
-  }();
+  const int env_split = knob("TP_GEMM_SPLITK");
   // split_mode > 0: a single problem -- split K only when the grid would leave more than half
   // of the clusters idle (up to 16 ways, every split >= 4 k-blocks). split_mode < 0: a problem
   // of a group whose tiles are far longer than the group's per-cluster share of work
@@ -1308,10 +1305,7 @@ tp_status launch2(const GemmArgs* gs, int n, cudaStream_t s) {
     }
     clusters = c;
   }
-  static const int env_raster = [] {
-    const char* e = std::getenv("TP_GEMM_RASTER");
-    return e ? std::max(1, std::atoi(e)) : 8;
-  }();
+  const int env_raster = std::max(1, knob("TP_GEMM_RASTER"));
   Group G;
   G.nprob = n;
   G.raster = env_raster;
@@ -1323,10 +1317,7 @@ tp_status launch2(const GemmArgs* gs, int n, cudaStream_t s) {
   for (int i = 0; i < n; ++i) {
     // no split-K inside a group: measured slower (the partial round trip outweighs the balance
     // gain on the C2 backward, 0.135 vs 0.126 ms/step)
-    static const int group_split = [] {
-      const char* e = std::getenv("TP_GEMM_GROUP_SPLIT");
-      return e ? std::atoi(e) : 1;
-    }();
+    const int group_split = knob("TP_GEMM_GROUP_SPLIT");
     int mode = n == 1 ? 1 : 0;
     if (n > 1 && group_split) {
       // per-cluster share of the group's work (tiles x k-blocks); a problem whose tiles are
@@ -1354,10 +1345,7 @@ tp_status launch2(const GemmArgs* gs, int n, cudaStream_t s) {
     cap = std::max(1, std::min(cap, (sm_count() - gs[0].reserve_sms) / (2 * pairs_of(MC))));
   const int grid = 2 * pairs_of(MC) * (units < cap ? units : cap);
   // split 0 may wait for its sibling splits only when every unit has its own resident cluster
-  static const int env_owner = [] {
-    const char* e = std::getenv("TP_GEMM_SPLIT_OWNER");
-    return e ? std::atoi(e) : 1;
-  }();
+  const int env_owner = knob("TP_GEMM_SPLIT_OWNER");
   for (int i = 0; i < n; ++i)
     G.p[i].owner_wait = (env_owner && g_shared_device_grids.load() == 0 && G.p[i].splits > 1 &&
                          units <= grid / (2 * pairs_of(MC))) ? 1 : 0;
@@ -1393,10 +1381,7 @@ tp_status launch_wide(const GemmArgs* gs, int n, cudaStream_t s) {
     }
     clusters = c;
   }
-  static const int env_raster = [] {
-    const char* e = std::getenv("TP_GEMM_WIDE_RASTER");
-    return e ? std::max(1, std::atoi(e)) : 8;
-  }();
+  const int env_raster = std::max(1, knob("TP_GEMM_WIDE_RASTER"));
   Group G;
   G.nprob = n;
   G.raster = env_raster;
@@ -1445,10 +1430,7 @@ tp_status launch_wide(const GemmArgs* gs, int n, cudaStream_t s) {
   G.total_units = units;
   int cap = clusters;
   if (gs[0].reserve_sms > 0) cap = std::max(1, std::min(cap, (sm_count() - gs[0].reserve_sms) / 2));
-  static const int env_np = [] {  // measurement knob: one tile per cluster, hardware-scheduled
-    const char* e = std::getenv("TP_GEMM_WIDE_NP");
-    return e ? std::atoi(e) : 0;
-  }();
+  const int env_np = knob("TP_GEMM_WIDE_NP");
   if (env_np && gs[0].reserve_sms <= 0) cap = units;
   const int grid = 2 * (units < cap ? units : cap);
   const int tok = prof_begin(0, s, flops);
@@ -1483,10 +1465,7 @@ size_t gemm_tc2_ws_bytes() {
 // (>= 12288: the un-overlapped epilogue of the single TMEM accumulator is then ~1%, and the
 // operand panels overflow L2). TP_GEMM_WIDE=0 turns it off (A/B measurements), =1 forces it.
 static int wide_mode() {
-  static const int m = [] {
-    const char* e = std::getenv("TP_GEMM_WIDE");
-    return e ? std::atoi(e) : -1;
-  }();
+  const int m = knob("TP_GEMM_WIDE");
   return m;
 }
 
@@ -1509,14 +1488,8 @@ tp_status gemm_tc2_bf16(const GemmArgs& g, cudaStream_t s) {
   if (want_wide(&g, 1)) return launch_wide(&g, 1, s);
   // Pair tile 256x256 when those tiles fill the SM pairs, else 256x128 (twice the tiles).
   // TP_GEMM_BN / TP_GEMM_MC force a width / cluster shape (tests, A/B measurements).
-  static const int force_bn = [] {
-    const char* e = std::getenv("TP_GEMM_BN");
-    return e ? std::atoi(e) : 0;
-  }();
-  static const int force_mc = [] {
-    const char* e = std::getenv("TP_GEMM_MC");
-    return e ? std::atoi(e) : 0;
-  }();
+  const int force_bn = knob("TP_GEMM_BN");
+  const int force_mc = knob("TP_GEMM_MC");
   const int64_t tiles256 = ((g.M + 255) / 256) * ((g.N + 255) / 256);
   const int pairs = sm_count() / 2;
   const bool wide = force_bn ? force_bn == 256 : tiles256 >= pairs;
@@ -1530,10 +1503,7 @@ tp_status gemm_tc2_bf16(const GemmArgs& g, cudaStream_t s) {
     if (mc == 2 && ncols >= 2) return launch2<256, 2>(&g, 1, s);
     if (mc == 3 && nrows >= 2) return launch2<256, 3>(&g, 1, s);
     // epilogue-bound (1-2 k-blocks per tile, e.g. a dW over 64 tokens): 8 epilogue warps
-    static const int env_ew = [] {
-      const char* e = std::getenv("TP_GEMM_EPI_WARPS");
-      return e ? std::atoi(e) : 0;
-    }();
+    const int env_ew = knob("TP_GEMM_EPI_WARPS");
     const bool ew8 = env_ew ? env_ew == 8 : kblocks <= 2;
     if (ew8) return launch2<256, 1, 8>(&g, 1, s);
     return launch2<256, 1>(&g, 1, s);
@@ -1553,10 +1523,7 @@ tp_status gemm_tc2_group(const GemmArgs* in, int n, cudaStream_t s) {
   for (int i = 0; i < n; ++i) gs[i] = in[i];
   auto kblocks = [](const GemmArgs& g) { return g.K * (g.npanels > 1 ? g.npanels : 1); };
   std::stable_sort(gs, gs + n, [&](const GemmArgs& x, const GemmArgs& y) { return kblocks(x) > kblocks(y); });
-  static const int group_bn = [] {
-    const char* e = std::getenv("TP_GEMM_GROUP_BN");
-    return e ? std::atoi(e) : 256;
-  }();
+  const int group_bn = knob("TP_GEMM_GROUP_BN");
   if (group_bn == 128) return launch2<128, 1>(gs, n, s);
   return launch2<256, 1>(gs, n, s);
 }

@@ -356,10 +356,7 @@ tp_status rsa_fwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k
   const float scale = d->scale != 0.f ? d->scale : 1.f / std::sqrt(static_cast<float>(P.d));
   const int64_t bd = P.b * P.d;
   std::vector<GemmArgs> gs;
-  static const int env_fused = [] {
-    const char* e = std::getenv("TP_RSA_FUSED");
-    return e ? std::atoi(e) : 1;
-  }();
+  const int env_fused = knob("TP_RSA_FUSED");
   const bool fused = env_fused && P.fchunk > 0;
   const int64_t step_heads = fused ? P.fchunk : P.chunk;
   for (int64_t h0 = 0; h0 < P.heads; h0 += step_heads) {

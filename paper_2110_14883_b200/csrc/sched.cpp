@@ -83,10 +83,7 @@ struct Ctx {
   // created with maxCTAs = 16). TP_COMM_SMS=n forces n.
   int comm_sms(double gemm_flops) const {
     if (g->world == 1 || R.cs == R.s || ovb <= 0) return 0;
-    static const int forced = [] {
-      const char* e = std::getenv("TP_COMM_SMS");
-      return e ? std::atoi(e) : -1;
-    }();
+    const int forced = knob("TP_COMM_SMS");
     if (forced >= 0) return forced;
     if (g->transport != TP_TRANSPORT_NCCL) return 0;
     const double t = std::max(gemm_flops / 1.4e15, 1e-6);

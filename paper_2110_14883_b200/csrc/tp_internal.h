@@ -33,6 +33,12 @@ tp_status fail(tp_status s, const std::string& msg);
 
 inline size_t dtype_size(tp_dtype t) { return t == TP_BF16 ? 2 : 4; }
 
+// ---- tuning knobs (capi.cpp registry; tp_knob_set / tp_knob_get / tp_knobs) ---------------
+// The effective value of a registered knob: tp_knob_set override, else the TP_* environment
+// variable (read once), else the measured default. Unknown names abort in debug builds and
+// return 0.
+int knob(const char* name);
+
 // ---- per-device one-time setup ---------------------------------------------------------
 // Kernel attributes (cudaFuncSetAttribute) belong to a device context: set_smem_attr runs
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, current device); callers

@@ -185,3 +185,31 @@ def test_rsa_and_layernorm_planning_errors():
         api.tp_rsa_ws_size(g3, api.rsa_desc(100, 16, 1))
     assert api.tp_rsa_ws_size(g3, api.rsa_desc(96, 16, 2)) > 2 * 32 * 96 * 4
     api.tp_grid_destroy(g3)
+
+
+def test_tuning_knobs_registry(api):
+    """Every dispatch / variant knob is in one registry: listed with its default and source,
+    settable through the API, overridable by its TP_* environment variable (read once)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    ks = {k["name"]: k for k in api.tp_knobs()}
+    for name in ("TP_PDL", "TP_GEMM_KERNEL", "TP_GEMM_WIDE", "TP_GEMM_RASTER", "TP_COMM_SMS",
+                 "TP_FLASH", "TP_RSA_FUSED", "TP_GEMM_SPLITK"):
+        assert name in ks and ks[name]["what"]
+    assert ks["TP_GEMM_WIDE"]["default"] == -1 and ks["TP_PDL"]["default"] == 1
+    old = api.tp_knob_get("TP_GEMM_RASTER")
+    api.tp_knob_set("TP_GEMM_RASTER", 4)
+    assert api.tp_knob_get("TP_GEMM_RASTER") == 4
+    assert {k["name"]: k for k in api.tp_knobs()}["TP_GEMM_RASTER"]["source"] == "api"
+    api.tp_knob_set("TP_GEMM_RASTER", old)
+    with pytest.raises(api.TPError):
+        api.tp_knob_set("TP_NO_SUCH_KNOB", 1)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import json; from paper_2110_14883_b200 import api; "
+            "print(json.dumps({k['name']: k for k in api.tp_knobs()}['TP_GEMM_WIDE']))")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                       env=dict(os.environ, TP_GEMM_WIDE="0"), timeout=120)
+    k = json.loads(r.stdout.strip().splitlines()[-1])
+    assert k["value"] == 0 and k["source"] == "env"
