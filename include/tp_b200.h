@@ -355,16 +355,22 @@ typedef struct {
   float scale;
 } tp_rsa_desc;
 tp_status tp_rsa_ws_size(const tp_grid* grid, const tp_rsa_desc* desc, size_t* ws_bytes);
+/* lse (nullable): fp32 [heads, seq/p] - the online-softmax ring's row log-sum-exp (base 2,
+ * scaled scores), written by the bf16 d_k in {64, 128} ring; with `out` it selects the fused
+ * ring backward. */
 tp_status tp_rsa_fwd(tp_grid* grid, const tp_rsa_desc* desc, const void* q, const void* k,
-                     const void* v, void* out, void* ws, size_t ws_bytes, void* stream);
+                     const void* v, void* out, float* lse, void* ws, size_t ws_bytes, void* stream);
 /* Backward (the chain rule of the same definition; the paper describes the forward only):
  * given dout = dL/dout [heads, seq/p, d_k] of this rank's rows, writes dq, dk, dv (same layout).
- * Scores are recomputed with the K ring; dP uses the V ring, dq the K ring; every rank's
- * contributions to each key block's dk / dv are reduce-scattered over the ring (fp32).
- * Same workspace as the forward (tp_rsa_ws_size covers both). */
+ * With the forward's out and lse (bf16, d_k 64 / 128): the fused ring backward - K and V travel
+ * the ring, each step one fused attention-backward launch (scores recomputed on chip from lse)
+ * adds this rank's queries' dq (fp32) and writes the visiting block's dk / dv contributions;
+ * the contributions are reduce-scattered to the blocks' owners (fp32). Otherwise the two-pass
+ * form: scores recomputed with the K ring; dP uses the V ring, dq the K ring, dk / dv
+ * contributions reduce-scattered. Same workspace as the forward (tp_rsa_ws_size). */
 tp_status tp_rsa_bwd(tp_grid* grid, const tp_rsa_desc* desc, const void* q, const void* k,
-                     const void* v, const void* dout, void* dq, void* dk, void* dv, void* ws,
-                     size_t ws_bytes, void* stream);
+                     const void* v, const void* out, const float* lse, const void* dout, void* dq,
+                     void* dk, void* dv, void* ws, size_t ws_bytes, void* stream);
 
 /* ---- multi-head attention core in the TP layouts ---------------------- */
 /* Between a QKV linear (qkv_desc: M tokens = batch x seq, K = h, N = 3h) and the output

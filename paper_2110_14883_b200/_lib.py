@@ -118,8 +118,8 @@ _sigs = {
     "tp_layernorm_bwd": (_i, [_vp, C.POINTER(tp_linear_desc), _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                               _vp, _sz, _vp]),
     "tp_rsa_ws_size": (_i, [_vp, C.POINTER(tp_rsa_desc), C.POINTER(_sz)]),
-    "tp_rsa_fwd": (_i, [_vp, C.POINTER(tp_rsa_desc), _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
-    "tp_rsa_bwd": (_i, [_vp, C.POINTER(tp_rsa_desc), _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz,
+    "tp_rsa_fwd": (_i, [_vp, C.POINTER(tp_rsa_desc), _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "tp_rsa_bwd": (_i, [_vp, C.POINTER(tp_rsa_desc), _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz,
                         _vp]),
     "tp_attention_ws_size": (_i, [_vp, C.POINTER(tp_linear_desc), _i64, _i64, C.POINTER(_sz)]),
     "tp_attention_fwd": (_i, [_vp, C.POINTER(tp_linear_desc), _i64, _i64, _f, _vp, _vp, _vp, _vp,

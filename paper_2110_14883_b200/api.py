@@ -333,16 +333,18 @@ def tp_rsa_ws_size(g, d: tp_rsa_desc) -> int:
     return n.value
 
 
-def tp_rsa_fwd(g, d: tp_rsa_desc, q, k, v, out, ws, stream=None, ws_bytes=None):
+def tp_rsa_fwd(g, d: tp_rsa_desc, q, k, v, out, ws, stream=None, ws_bytes=None, lse=None):
     wb = _nbytes(ws) if ws_bytes is None else ws_bytes
-    _check(lib.tp_rsa_fwd(g, C.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(ws), wb,
-                          _stream(stream)), "tp_rsa_fwd")
+    _check(lib.tp_rsa_fwd(g, C.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), _ptr(ws),
+                          wb, _stream(stream)), "tp_rsa_fwd")
 
 
-def tp_rsa_bwd(g, d: tp_rsa_desc, q, k, v, dout, dq, dk, dv, ws, stream=None, ws_bytes=None):
+def tp_rsa_bwd(g, d: tp_rsa_desc, q, k, v, dout, dq, dk, dv, ws, stream=None, ws_bytes=None,
+               out=None, lse=None):
+    """out / lse (the forward's, bf16 d_k 64 / 128): the fused ring backward."""
     wb = _nbytes(ws) if ws_bytes is None else ws_bytes
-    _check(lib.tp_rsa_bwd(g, C.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(dout), _ptr(dq), _ptr(dk),
-                          _ptr(dv), _ptr(ws), wb, _stream(stream)), "tp_rsa_bwd")
+    _check(lib.tp_rsa_bwd(g, C.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), _ptr(dout),
+                          _ptr(dq), _ptr(dk), _ptr(dv), _ptr(ws), wb, _stream(stream)), "tp_rsa_bwd")
 
 
 def tp_attention_ws_size(g, d, seq, heads) -> int:

@@ -1249,26 +1249,29 @@ extern "C" tp_status tp_rsa_ws_size(const tp_grid* g, const tp_rsa_desc* d, size
 }
 
 extern "C" tp_status tp_rsa_fwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k,
-                                const void* v, void* out, void* ws, size_t ws_bytes, void* stream) {
+                                const void* v, void* out, float* lse, void* ws, size_t ws_bytes,
+                                void* stream) {
   tp::NvtxRange nvtx_("tp_rsa_fwd");
   if (!g || !d) return tp::fail(TP_ERR_ARG, "tp_rsa_fwd: null grid or desc");
   TP_TRY(tp::contract_check(g, tp::kCallRsaFwd, nullptr,
                             {uint64_t(d->seq), uint64_t(d->d_k), uint64_t(d->heads),
                              uint64_t(d->dtype), tp::f32_word(d->scale)}));
   TP_CUDA(cudaSetDevice(g->device));
-  return tp::rsa_fwd(g, d, q, k, v, out, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+  return tp::rsa_fwd(g, d, q, k, v, out, ws, ws_bytes, static_cast<cudaStream_t>(stream), lse);
 }
 
 extern "C" tp_status tp_rsa_bwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k,
-                                const void* v, const void* dout, void* dq, void* dk, void* dv,
-                                void* ws, size_t ws_bytes, void* stream) {
+                                const void* v, const void* out, const float* lse, const void* dout,
+                                void* dq, void* dk, void* dv, void* ws, size_t ws_bytes,
+                                void* stream) {
   tp::NvtxRange nvtx_("tp_rsa_bwd");
   if (!g || !d) return tp::fail(TP_ERR_ARG, "tp_rsa_bwd: null grid or desc");
   TP_TRY(tp::contract_check(g, tp::kCallRsaBwd, nullptr,
                             {uint64_t(d->seq), uint64_t(d->d_k), uint64_t(d->heads),
                              uint64_t(d->dtype), tp::f32_word(d->scale)}));
   TP_CUDA(cudaSetDevice(g->device));
-  return tp::rsa_bwd(g, d, q, k, v, dout, dq, dk, dv, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+  return tp::rsa_bwd(g, d, q, k, v, dout, dq, dk, dv, ws, ws_bytes, static_cast<cudaStream_t>(stream),
+                      out, lse);
 }
 
 // ---------------------------------------------------------------- multi-head attention core

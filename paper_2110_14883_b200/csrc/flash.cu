@@ -537,7 +537,7 @@ tp_status flash_attn_fwd(int64_t problems, int64_t s, int64_t d, const void* q, 
 // acc [problems*s, d] fp32 and ml [problems*s, 2] fp32 carry the online softmax between calls.
 tp_status flash_attn_fwd_carry(int64_t problems, int64_t s, int64_t d, const void* q, const void* k,
                                const void* v, void* out, float* acc, float* ml, bool carry_in,
-                               bool last, float scale, cudaStream_t st) {
+                               bool last, float scale, cudaStream_t st, float* lse) {
   if (!problems || !s) return TP_OK;
   if (d != 64 && d != 128) return fail(TP_ERR_UNSUPPORTED, "flash: d must be 64 or 128");
   if (problems > 65535) return fail(TP_ERR_UNSUPPORTED, "flash: too many problems for one grid");
@@ -556,6 +556,7 @@ tp_status flash_attn_fwd_carry(int64_t problems, int64_t s, int64_t d, const voi
   F.ml = ml;
   F.carry_in = carry_in ? 1 : 0;
   F.last = last ? 1 : 0;
+  F.lse = last ? lse : nullptr;
   return d == 64 ? launch<64>(F, st) : launch<128>(F, st);
 }
 

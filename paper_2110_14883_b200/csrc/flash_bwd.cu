@@ -56,6 +56,7 @@ struct BParams {
   const float* delta;  // [problems*s]
   float* dq_acc;       // [problems*s, D] fp32 (zeroed)
   __nv_bfloat16 *dk, *dv;
+  float *dk32, *dv32;  // non-null: dK / dV written in fp32 here instead (ring partials)
   int64_t s;
   float scale, scale_log2;
 };
@@ -323,13 +324,20 @@ __global__ void __launch_bounds__(320, 1) flash_bwd_kernel(const __grid_constant
 #pragma unroll 1
     for (int which = 0; which < 2; ++which) {
       __nv_bfloat16* dst = (which == 0 ? F.dv : F.dk) + (row_base + key0 + r) * D;
+      float* dst32 = F.dk32 ? (which == 0 ? F.dv32 : F.dk32) + (row_base + key0 + r) * D : nullptr;
       const uint32_t col0 = which == 0 ? C::TDV : C::TDK;
 #pragma unroll 1
       for (int c = 0; c < D / 32; ++c) {
         uint32_t v[32];
         tmem_ld32(tmem + col0 + lane_off + c * 32, v);
         tmem_wait_ld();
-        if (key_ok) {
+        if (key_ok && dst32) {
+#pragma unroll
+          for (int k = 0; k < 32; k += 4)
+            *reinterpret_cast<float4*>(dst32 + c * 32 + k) =
+                make_float4(__uint_as_float(v[k]), __uint_as_float(v[k + 1]), __uint_as_float(v[k + 2]),
+                            __uint_as_float(v[k + 3]));
+        } else if (key_ok) {
 #pragma unroll
           for (int k = 0; k < 32; k += 8) {
             uint4 u;
@@ -455,6 +463,52 @@ tp_status launch_bwd(const BParams& F, int64_t problems, cudaStream_t s) {
 }
 
 }  // namespace
+
+tp_status flash_bwd_delta_launch(int64_t rows, int64_t d, const void* o, const void* dout,
+                                 float* delta, cudaStream_t st) {
+  if (!rows) return TP_OK;
+  const unsigned G = static_cast<unsigned>((rows * 32 + 255) / 256);
+  flash_bwd_delta<<<G, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(o),
+                                      static_cast<const __nv_bfloat16*>(dout), rows, static_cast<int>(d), delta);
+  count_launch();
+  TP_CUDA(cudaGetLastError());
+  return TP_OK;
+}
+
+tp_status flash_bwd_cast_launch(const float* src, int64_t n, void* dst, cudaStream_t st) {
+  if (!n) return TP_OK;
+  const unsigned G = static_cast<unsigned>((n / 4 + 255) / 256 + 1);
+  flash_bwd_cast<<<G, 256, 0, st>>>(src, n, static_cast<__nv_bfloat16*>(dst));
+  count_launch();
+  TP_CUDA(cudaGetLastError());
+  return TP_OK;
+}
+
+// One ring step of the fused backward: local queries q / dout / lse / delta against the visiting
+// key block k / v; dQ added into dq_acc (fp32, not zeroed here), dK / dV of the visiting block
+// written in fp32 to dk32 / dv32.
+tp_status flash_bwd_step(int64_t problems, int64_t s, int64_t d, const void* q, const void* k,
+                         const void* v, const void* dout, const float* lse, const float* delta,
+                         float* dq_acc, float* dk32, float* dv32, float scale, cudaStream_t st) {
+  if (!problems || !s) return TP_OK;
+  if (d != 64 && d != 128) return fail(TP_ERR_UNSUPPORTED, "flash bwd: d must be 64 or 128");
+  if (problems > 65535) return fail(TP_ERR_UNSUPPORTED, "flash bwd: too many problems for one grid");
+  const int64_t rows = problems * s;
+  BParams F{};
+  TP_TRY(map_b(&F.tmQ, q, uint64_t(rows), static_cast<int>(d)));
+  TP_TRY(map_b(&F.tmK, k, uint64_t(rows), static_cast<int>(d)));
+  TP_TRY(map_b(&F.tmV, v, uint64_t(rows), static_cast<int>(d)));
+  TP_TRY(map_b(&F.tmdO, dout, uint64_t(rows), static_cast<int>(d)));
+  F.lse = lse;
+  F.delta = delta;
+  F.dq_acc = dq_acc;
+  F.dk32 = dk32;
+  F.dv32 = dv32;
+  F.s = s;
+  F.scale = scale;
+  F.scale_log2 = scale * 1.4426950408889634f;
+  return d == 64 ? launch_bwd<64>(F, problems, st) : launch_bwd<128>(F, problems, st);
+}
 
 size_t flash_bwd_ws_bytes(int64_t problems, int64_t s, int64_t d) {
   const size_t rows = size_t(problems) * size_t(s);

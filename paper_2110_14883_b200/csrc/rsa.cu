@@ -339,7 +339,7 @@ tp_status rsa_ws_bytes(const tp_grid* g, const tp_rsa_desc* d, size_t* bytes) {
 }
 
 tp_status rsa_fwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k, const void* v,
-                  void* out, void* ws, size_t ws_bytes, cudaStream_t s) {
+                  void* out, void* ws, size_t ws_bytes, cudaStream_t s, float* lse) {
   RsaPlan P;
   TP_TRY(rsa_plan(g, d, &P));
   size_t need = 0;
@@ -385,7 +385,8 @@ tp_status rsa_fwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k
           TP_TRY(ring->shift(ck, w.fk[t & 1], size_t(nh) * bd, dt, -1, cs));
           TP_TRY(ring->shift(cv, w.vv[t & 1], size_t(nh) * bd, dt, -1, cs));
         }
-        TP_TRY(flash_attn_fwd_carry(nh, P.b, P.d, qc, ck, cv, oc, w.facc, w.ml, t > 0, last, scale, s));
+        TP_TRY(flash_attn_fwd_carry(nh, P.b, P.d, qc, ck, cv, oc, w.facc, w.ml, t > 0, last, scale, s,
+                                    lse ? lse + h0 * P.b : nullptr));
         if (!last) {
           if (cs != s) {
             ev_flash = g->ev();
@@ -452,9 +453,77 @@ tp_status rsa_fwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k
 //   V ring -> dP = dO V_j^T;  dS = scale P (dP - rowsum(P dP)) (over P);
 //   K ring -> dQ = sum_j dS[:, j] K_j;  dK parts dS[:, j]^T Q_r;
 //   reduce-scatter of the dK / dV parts over the ring -> this rank's blocks.
+// Fused ring backward (reading N4 with the online-softmax forward's lse): K and V travel the
+// ring together (double-buffered on the comm stream, block t+1 moving under launch t); each step
+// one flash_bwd_step adds this rank's queries' dQ (fp32 accumulator) and writes the visiting
+// block's dK / dV contribution (fp32) into its slot of the reduce-scatter buffers; at the end
+// the contributions are reduce-scattered to the blocks' owners and everything cast to dtype.
+tp_status rsa_bwd_fused(tp_grid* g, const RsaPlan& P, const RsaWs& w, const void* q, const void* k,
+                        const void* v, const void* out, const float* lse, const void* dout, void* dq,
+                        void* dk, void* dv, float scale, cudaStream_t s) {
+  Comm* ring = g->axis[0].get();
+  const tp_dtype dt = TP_BF16;
+  const int64_t bd = P.b * P.d;
+  cudaStream_t cs = g->comm_stream ? g->comm_stream : s;
+  for (int64_t h0 = 0; h0 < P.heads; h0 += P.chunk) {
+    const int64_t nh = std::min<int64_t>(P.chunk, P.heads - h0);
+    const int64_t n = nh * bd;
+    const char* qc = static_cast<const char*>(q) + h0 * bd * P.esz;
+    const char* oc = static_cast<const char*>(out) + h0 * bd * P.esz;
+    const char* doc = static_cast<const char*>(dout) + h0 * bd * P.esz;
+    const float* lc = lse + h0 * P.b;
+    float* delta = w.ml;        // [nh b] (the forward's carry buffer, free here)
+    float* dq_acc = w.acc;      // [nh b d] fp32
+    TP_TRY(flash_bwd_delta_launch(nh * P.b, P.d, oc, doc, delta, s));
+    TP_CUDA(cudaMemsetAsync(dq_acc, 0, size_t(n) * 4, s));
+    const void* ck = static_cast<const char*>(k) + h0 * bd * P.esz;
+    const void* cv = static_cast<const char*>(v) + h0 * bd * P.esz;
+    cudaEvent_t ev_used = nullptr;
+    if (P.p > 1 && cs != s) {
+      cudaEvent_t e = g->ev();
+      TP_CUDA(cudaEventRecord(e, s));
+      TP_CUDA(cudaStreamWaitEvent(cs, e, 0));
+    }
+    for (int t = 0; t < P.p; ++t) {
+      const bool last = t + 1 == P.p;
+      const int j = ((P.r - t) % P.p + P.p) % P.p;  // the visiting block's owner
+      if (!last) {  // block t+1 moves while block t is processed
+        if (ev_used && cs != s) TP_CUDA(cudaStreamWaitEvent(cs, ev_used, 0));
+        TP_TRY(ring->shift(ck, w.fk[t & 1], size_t(n), dt, -1, cs));
+        TP_TRY(ring->shift(cv, w.vv[t & 1], size_t(n), dt, -1, cs));
+      }
+      TP_TRY(flash_bwd_step(nh, P.b, P.d, qc, ck, cv, doc, lc, delta, dq_acc,
+                            w.parts_k + int64_t(j) * n, w.parts_v + int64_t(j) * n, scale, s));
+      if (!last) {
+        if (cs != s) {
+          ev_used = g->ev();
+          TP_CUDA(cudaEventRecord(ev_used, s));
+          cudaEvent_t arrived = g->ev();
+          TP_CUDA(cudaEventRecord(arrived, cs));
+          TP_CUDA(cudaStreamWaitEvent(s, arrived, 0));
+        }
+        ck = w.fk[t & 1];
+        cv = w.vv[t & 1];
+      }
+    }
+    const float* rk = w.parts_k;
+    const float* rv = w.parts_v;
+    if (ring) {
+      TP_TRY(ring->reducescatter(w.parts_k, w.red_k, n, TP_FP32, s));
+      TP_TRY(ring->reducescatter(w.parts_v, w.red_v, n, TP_FP32, s));
+      rk = w.red_k;
+      rv = w.red_v;
+    }
+    TP_TRY(flash_bwd_cast_launch(dq_acc, n, static_cast<char*>(dq) + h0 * bd * P.esz, s));
+    TP_TRY(flash_bwd_cast_launch(rk, n, static_cast<char*>(dk) + h0 * bd * P.esz, s));
+    TP_TRY(flash_bwd_cast_launch(rv, n, static_cast<char*>(dv) + h0 * bd * P.esz, s));
+  }
+  return TP_OK;
+}
+
 tp_status rsa_bwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k, const void* v,
                   const void* dout, void* dq, void* dk, void* dv, void* ws, size_t ws_bytes,
-                  cudaStream_t s) {
+                  cudaStream_t s, const void* out, const float* lse) {
   RsaPlan P;
   TP_TRY(rsa_plan(g, d, &P));
   size_t need = 0;
@@ -470,6 +539,8 @@ tp_status rsa_bwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k
   const tp_dtype dt = d->dtype;
   const float scale = d->scale != 0.f ? d->scale : 1.f / std::sqrt(static_cast<float>(P.d));
   const int64_t bd = P.b * P.d;
+  if (out && lse && P.fchunk > 0 && knob("TP_RSA_FUSED"))
+    return rsa_bwd_fused(g, P, w, q, k, v, out, lse, dout, dq, dk, dv, scale, s);
   std::vector<GemmArgs> gs;
   for (int64_t h0 = 0; h0 < P.heads; h0 += P.chunk) {
     const int64_t nh = std::min<int64_t>(P.chunk, P.heads - h0);

@@ -46,10 +46,10 @@ tp_status layernorm_bwd(tp_grid* g, const tp_linear_desc* d, int tensor, const v
 // Ring Self-Attention forward (rsa.cu).
 tp_status rsa_ws_bytes(const tp_grid* g, const tp_rsa_desc* d, size_t* bytes);
 tp_status rsa_fwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k, const void* v,
-                  void* out, void* ws, size_t ws_bytes, cudaStream_t s);
+                  void* out, void* ws, size_t ws_bytes, cudaStream_t s, float* lse = nullptr);
 tp_status rsa_bwd(tp_grid* g, const tp_rsa_desc* d, const void* q, const void* k, const void* v,
                   const void* dout, void* dq, void* dk, void* dv, void* ws, size_t ws_bytes,
-                  cudaStream_t s);
+                  cudaStream_t s, const void* out = nullptr, const float* lse = nullptr);
 
 // Fused attention forward (flash.cu): [problems, s, d] bf16, d in {64, 128}.
 bool flash_supported(int64_t d, tp_dtype dt);
@@ -61,12 +61,20 @@ tp_status flash_attn_fwd(int64_t problems, int64_t s, int64_t d, const void* q, 
 // [problems*s] fp32 from flash_attn_fwd; writes dq, dk, dv [problems, s, d] bf16. ws: fp32
 // scratch of flash_bwd_ws_bytes (dQ accumulator, row deltas).
 size_t flash_bwd_ws_bytes(int64_t problems, int64_t s, int64_t d);
+// building blocks of the ring (sequence-parallel) backward: row deltas, one ring step, cast
+tp_status flash_bwd_delta_launch(int64_t rows, int64_t d, const void* o, const void* dout,
+                                 float* delta, cudaStream_t st);
+tp_status flash_bwd_step(int64_t problems, int64_t s, int64_t d, const void* q, const void* k,
+                         const void* v, const void* dout, const float* lse, const float* delta,
+                         float* dq_acc, float* dk32, float* dv32, float scale, cudaStream_t st);
+tp_status flash_bwd_cast_launch(const float* src, int64_t n, void* dst, cudaStream_t st);
 tp_status flash_attn_bwd(int64_t problems, int64_t s, int64_t d, const void* q, const void* k,
                          const void* v, const void* o, const void* dout, const float* lse,
                          void* dq, void* dk, void* dv, float scale, void* ws, cudaStream_t st);
+// lse (optional): written at the last ring block (F.last), as flash_attn_fwd's
 tp_status flash_attn_fwd_carry(int64_t problems, int64_t s, int64_t d, const void* q, const void* k,
                                const void* v, void* out, float* acc, float* ml, bool carry_in,
-                               bool last, float scale, cudaStream_t st);
+                               bool last, float scale, cudaStream_t st, float* lse = nullptr);
 
 // Multi-head attention core in the TP layouts (attn.cu).
 tp_status attention_ws_bytes(const tp_grid* g, const tp_linear_desc* qd, int64_t seq, int64_t heads,

@@ -154,3 +154,49 @@ def test_rsa_online_softmax_ring_ragged(api, p, s, d):
     Q, K, V = inputs(31 + p, heads, s, d, "bf16")
     got = run_rsa(api, p, heads, s, d, "bf16", Q, K, V)
     assert rel_fro(got, oracle_out(Q, K, V)) <= 1e-2
+
+
+def run_rsa_fused_bwd(api, p, heads, s, d, Q, K, V, dO):
+    """bf16: the online-softmax ring forward writing lse, then the fused ring backward."""
+    transport = api.TP_TRANSPORT_LOCAL if p > 1 else api.TP_TRANSPORT_NONE
+    uid = api.tp_get_unique_id(transport)
+    b = s // p
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32)).cuda().to(torch.bfloat16)
+
+    def rank_fn(r):
+        g = api.tp_grid_init("1d", p, r, 0, 1, 0, transport, uid)
+        st = torch.cuda.Stream()
+        try:
+            with torch.cuda.stream(st):
+                ds = api.rsa_desc(s, d, heads, "bf16", 0.0)
+                q, k, v, do = (dev(X[:, r * b:(r + 1) * b, :]) for X in (Q, K, V, dO))
+                out = torch.empty_like(q)
+                lse = torch.empty(heads * b, device="cuda", dtype=torch.float32)
+                ws = torch.empty(api.tp_rsa_ws_size(g, ds), device="cuda", dtype=torch.uint8)
+                api.tp_rsa_fwd(g, ds, q, k, v, out, ws, lse=lse)
+                dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+                api.tp_rsa_bwd(g, ds, q, k, v, do, dq, dk, dv, ws, out=out, lse=lse)
+            st.synchronize()
+            return to_np(dq), to_np(dk), to_np(dv)
+        finally:
+            st.synchronize()
+            api.tp_grid_destroy(g)
+
+    per = run_ranks(p, rank_fn)
+    return tuple(np.concatenate([x[i] for x in per], axis=1) for i in range(3))
+
+
+@pytest.mark.parametrize("p,s,d", [(1, 512, 64), (2, 512, 128), (4, 1024, 64), (8, 1024, 128),
+                                   (2, 2 * 130, 64), (3, 3 * 200, 128)], ids=lambda v: str(v))
+def test_rsa_fused_ring_backward_vs_oracle(api, p, s, d):
+    """The fused ring backward (K / V travel the ring, one flash_bwd_step per block, dK / dV
+    contributions reduce-scattered): each of dQ, dK, dV within 1e-2 of the fp64 chain rule,
+    aligned and ragged blocks (b = 130, 200), rings up to p = 8."""
+    heads = 3
+    Q, K, V = inputs(41 + p, heads, s, d, "bf16")
+    dO = np.stack([synth.tensor(41, 8 * h + 3, s, d, dtype="bf16") for h in range(heads)]).astype(np.float64)
+    dq, dk, dv = run_rsa_fused_bwd(api, p, heads, s, d, Q, K, V, dO)
+    ref = [rsa.attention_bwd(Q[h], K[h], V[h], dO[h]) for h in range(heads)]
+    for i, got in enumerate((dq, dk, dv)):
+        want = np.stack([ref[h][i] for h in range(heads)])
+        assert rel_fro(got, want) <= 1e-2, ("dq", "dk", "dv")[i]

@@ -41,10 +41,31 @@ def main():
     score_bytes = 12.0 * s * s * heads
     ref = torch.nn.functional.scaled_dot_product_attention(q[None].float(), k[None].float(), v[None].float())[0]
     err = float((out.float() - ref).norm() / ref.norm())
+    # backward: the fused ring backward (lse from the forward) vs the two-pass form
+    lse = torch.empty(heads * s, device="cuda", dtype=torch.float32)
+    api.tp_rsa_fwd(g, ds, q, k, v, out, ws, lse=lse)
+    do = torch.randn_like(q)
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+
+    def t_of(fn, reps=5):
+        fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            fn()
+        b.record()
+        b.synchronize()
+        return a.elapsed_time(b) / reps
+
+    fused = t_of(lambda: api.tp_rsa_bwd(g, ds, q, k, v, do, dq, dk, dv, ws, out=out, lse=lse))
+    two = t_of(lambda: api.tp_rsa_bwd(g, ds, q, k, v, do, dq, dk, dv, ws))
     print(json.dumps({"op": "rsa_fwd", "s": s, "d_k": d, "heads": heads, "ms": round(ms, 4),
                       "tflops": round(flops / ms / 1e9, 1),
                       "score_roundtrip_gbs": round(score_bytes / ms / 1e6, 1),
-                      "rel_err_vs_torch_sdpa_fp32": round(err, 5)}))
+                      "rel_err_vs_torch_sdpa_fp32": round(err, 5),
+                      "bwd_fused_ms": round(fused, 4), "bwd_fused_tflops": round(2.5 * flops / fused / 1e9, 1),
+                      "bwd_two_pass_ms": round(two, 4), "bwd_two_pass_tflops": round(2.5 * flops / two / 1e9, 1)}))
 
 
 if __name__ == "__main__":
