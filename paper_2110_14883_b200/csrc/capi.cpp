@@ -55,6 +55,7 @@ constexpr KnobDef kKnobs[] = {
     {"TP_COMM_SMS", -1, "SMs a GEMM leaves to a collective running under it (-1 sized to the transfer)"},
     {"TP_FLASH", 1, "fused attention kernels (0 = two-pass through HBM)"},
     {"TP_RSA_FUSED", 1, "online-softmax ring for Ring Self-Attention in bf16 (0 two-pass)"},
+    {"TP_FB_NODQ", 0, "diagnostics: the fused attention backward skips its dQ accumulation (wrong dQ)"},
 };
 constexpr int kNumKnobs = sizeof(kKnobs) / sizeof(kKnobs[0]);
 struct KnobState {

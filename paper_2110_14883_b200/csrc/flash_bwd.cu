@@ -40,13 +40,17 @@ constexpr int kTileB = kT * 128;  // one [128 rows][128 B] chunk
 
 template <int D>
 struct BC {
-  static constexpr int NS = D == 64 ? 2 : 1;           // Q / dO ring stages
+  static constexpr int NS = 2;                         // Q / dO ring stages
   static constexpr int Chunk = D / 64;                 // 64-wide column chunks of a [128 x D] tile
   static constexpr int TileBytes = kT * D * 2;         // K, V, Q, dO tiles
   static constexpr int PBytes = kT * kT * 2;           // P^T, dS^T tiles (two 64-query chunks)
-  static constexpr int Smem = 2 * TileBytes + NS * 2 * TileBytes + 2 * PBytes + 2 * 2 * kT * 4 + 1024 + 256;
+  // d = 128: P^T and dS^T share one smem tile (dS^T overwrites P^T once the dV MMA read it)
+  static constexpr bool SharePdS = D != 64;
+  static constexpr int Smem = 2 * TileBytes + NS * 2 * TileBytes + (SharePdS ? 1 : 2) * PBytes +
+                              2 * kT * 4 + 1024 + 256;  // d = 128: 231,680 B of the 232,448
   static constexpr uint32_t TDV = 0, TDK = D, TS = 2 * D, TDP = 2 * D + 128;
-  static constexpr uint32_t TDQ = D == 64 ? 2 * D + 256 : 2 * D;  // d = 128: aliases S^T
+  // d = 128: TMEM is full, dQ_i reuses dP^T's columns (free once the key rows formed dS_i)
+  static constexpr uint32_t TDQ = D == 64 ? 2 * D + 256 : TDP;
   static constexpr bool Alias = D != 64;
 };
 
@@ -57,6 +61,7 @@ struct BParams {
   float* dq_acc;       // [problems*s, D] fp32 (zeroed)
   __nv_bfloat16 *dk, *dv;
   float *dk32, *dv32;  // non-null: dK / dV written in fp32 here instead (ring partials)
+  int no_dq;           // diagnostics (knob TP_FB_NODQ): skip the dQ accumulation
   int64_t s;
   float scale, scale_log2;
 };
@@ -95,9 +100,9 @@ __global__ void __launch_bounds__(320, 1) flash_bwd_kernel(const __grid_constant
   uint8_t* sQ = sV + C::TileBytes;              // [NS]
   uint8_t* sdO = sQ + NS * C::TileBytes;        // [NS]
   uint8_t* sP = sdO + NS * C::TileBytes;
-  uint8_t* sdS = sP + C::PBytes;
-  float* sLD = reinterpret_cast<float*>(sdS + C::PBytes);  // [2 buffers][lse 128 | delta 128]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sLD + 2 * 2 * kT);
+  uint8_t* sdS = C::SharePdS ? sP : sP + C::PBytes;
+  float* sLD = reinterpret_cast<float*>(sdS + C::PBytes);  // [lse 128 | delta 128] of the tile
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sLD + 2 * kT);
   uint64_t* kv_full = bars;
   uint64_t* q_full = kv_full + 1;     // [NS]
   uint64_t* q_empty = q_full + NS;    // [NS]
@@ -190,11 +195,8 @@ __global__ void __launch_bounds__(320, 1) flash_bwd_kernel(const __grid_constant
         const uint64_t qd_mn = sdesc_sw128(smem_u32(sQ + st * C::TileBytes), kTileB, 1024);
         const uint64_t od = sdesc_sw128(smem_u32(sdO + st * C::TileBytes), 16, 1024);
         const uint64_t od_mn = sdesc_sw128(smem_u32(sdO + st * C::TileBytes), kTileB, 1024);
-        // S^T = K_j Q_i^T   (the key rows took tile i-1's scores; d = 128: dQ_{i-1} drained)
-        if (i > 0) {
-          mbar_wait(s_free, php);
-          if (C::Alias) mbar_wait(dq_free, php);
-        }
+        // S^T = K_j Q_i^T   (the key rows took tile i-1's scores)
+        if (i > 0) mbar_wait(s_free, php);
         tc_fence_after();
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
@@ -202,8 +204,11 @@ __global__ void __launch_bounds__(320, 1) flash_bwd_kernel(const __grid_constant
           umma_bf16_cg1(tmem + C::TS, kd + off, qd + off, idSS, k > 0 ? 1u : 0u);
         }
         umma_commit_cg1(s_full);
-        // dP^T = V_j dO_i^T
-        if (i > 0) mbar_wait(dp_free, php);
+        // dP^T = V_j dO_i^T   (d = 128: dQ_{i-1}, in the same columns, drained)
+        if (i > 0) {
+          mbar_wait(dp_free, php);
+          if (C::Alias) mbar_wait(dq_free, php);
+        }
         tc_fence_after();
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
@@ -220,20 +225,19 @@ __global__ void __launch_bounds__(320, 1) flash_bwd_kernel(const __grid_constant
           umma_bf16_cg1(tmem + C::TDV, pd + offa, od_mn + k * (2048 / 16), idKV, (i > 0 || k > 0) ? 1u : 0u);
         }
         umma_commit_cg1(p_free);
-        // dK += dS^T Q_i ; dQ_i = dS K_j   (K = queries / keys)
+        // dQ_i = dS K_j first (its drain then overlaps the dK MMA), then dK += dS^T Q_i
         mbar_wait(ds_full, ph);
-        tc_fence_after();
-#pragma unroll
-        for (int k = 0; k < kT / 16; ++k) {
-          const uint32_t offa = (k / 4) * (kTileB / 16) + (k % 4) * 2;
-          umma_bf16_cg1(tmem + C::TDK, dsd + offa, qd_mn + k * (2048 / 16), idKV, (i > 0 || k > 0) ? 1u : 0u);
-        }
         if (!C::Alias && i > 0) mbar_wait(dq_free, php);
         tc_fence_after();
 #pragma unroll
         for (int k = 0; k < kT / 16; ++k)
           umma_bf16_cg1(tmem + C::TDQ, dsd_mn + k * (2048 / 16), kd_mn + k * (2048 / 16), idQ, k > 0 ? 1u : 0u);
         umma_commit_cg1(dq_full);
+#pragma unroll
+        for (int k = 0; k < kT / 16; ++k) {
+          const uint32_t offa = (k / 4) * (kTileB / 16) + (k % 4) * 2;
+          umma_bf16_cg1(tmem + C::TDK, dsd + offa, qd_mn + k * (2048 / 16), idKV, (i > 0 || k > 0) ? 1u : 0u);
+        }
         umma_commit_cg1(ds_free);
         umma_commit_cg1(&q_empty[st]);
       }
@@ -247,15 +251,21 @@ __global__ void __launch_bounds__(320, 1) flash_bwd_kernel(const __grid_constant
     const int t = (warp - 2) * 32 + lane;  // 0..127: this thread's query slot for lse / delta
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
     const bool key_ok = key0 + r < F.s;
+    // this thread's lse / delta slot of the next query tile, loaded one tile ahead
+    float nl = t < F.s ? F.lse[row_base + t] : INFINITY;
+    float nd = t < F.s ? F.delta[row_base + t] : 0.f;
     for (int i = 0; i < nq; ++i) {
       const uint32_t ph = i & 1, php = (i - 1) & 1;
-      float* L = sLD + (i & 1) * 2 * kT;
-      {
-        const int64_t q = int64_t(i) * kT + t;
-        L[t] = q < F.s ? F.lse[row_base + q] : INFINITY;
-        L[kT + t] = q < F.s ? F.delta[row_base + q] : 0.f;
-      }
+      float* L = sLD;
+      if (i > 0) named_barrier_sync(1, 128);  // every key row is done with tile i-1's values
+      L[t] = nl;
+      L[kT + t] = nd;
       named_barrier_sync(1, 128);
+      {
+        const int64_t q = int64_t(i + 1) * kT + t;
+        nl = q < F.s ? F.lse[row_base + q] : INFINITY;
+        nd = q < F.s ? F.delta[row_base + q] : 0.f;
+      }
       // P^T row = exp2(S^T row c - lse[q])
       mbar_wait(s_full, ph);
       tc_fence_after();
@@ -278,7 +288,9 @@ __global__ void __launch_bounds__(320, 1) flash_bwd_kernel(const __grid_constant
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(s_free);
-      if (i > 0) mbar_wait(p_free, php);  // the dV MMA of tile i-1 read the P^T tile
+      // the P^T tile is free: the dV MMA of tile i-1 read it (and, shared with dS^T, the dQ / dK
+      // MMAs of tile i-1 read dS^T)
+      if (i > 0) mbar_wait(C::SharePdS ? ds_free : p_free, php);
 #pragma unroll
       for (int c = 0; c < kT / 32; ++c) {
         uint32_t w[16];
@@ -292,7 +304,10 @@ __global__ void __launch_bounds__(320, 1) flash_bwd_kernel(const __grid_constant
       // dS^T row = P (dP^T row - delta[q]) scale
       mbar_wait(dp_full, ph);
       tc_fence_after();
-      if (i > 0) mbar_wait(ds_free, php);  // the dK / dQ MMAs of tile i-1 read the dS^T tile
+      // the dS^T tile is free: shared with P^T, once the dV MMA of THIS tile read P^T; else once
+      // the dQ / dK MMAs of tile i-1 read dS^T
+      if (C::SharePdS) mbar_wait(p_free, ph);
+      else if (i > 0) mbar_wait(ds_free, php);
 #pragma unroll
       for (int c = 0; c < kT / 32; ++c) {
         uint32_t dv[32];
@@ -366,7 +381,7 @@ __global__ void __launch_bounds__(320, 1) flash_bwd_kernel(const __grid_constant
         uint32_t v[32];
         tmem_ld32(tmem + C::TDQ + lane_off + c * 32, v);
         tmem_wait_ld();
-        if (q < F.s) {
+        if (q < F.s && !F.no_dq) {
 #pragma unroll
           for (int k = 0; k < 32; k += 4)
             red_add_v4(dst + c * 32 + k, __uint_as_float(v[k]), __uint_as_float(v[k + 1]),
@@ -545,6 +560,7 @@ tp_status flash_attn_bwd(int64_t problems, int64_t s, int64_t d, const void* q, 
   F.s = s;
   F.scale = scale;
   F.scale_log2 = scale * 1.4426950408889634f;
+  F.no_dq = knob("TP_FB_NODQ");
   TP_TRY(d == 64 ? launch_bwd<64>(F, problems, st) : launch_bwd<128>(F, problems, st));
   const int64_t n = rows * d;
   const unsigned G = static_cast<unsigned>((n / 4 + 255) / 256 + 1);
