@@ -60,9 +60,15 @@ def expected():
 
 
 def sampled_outputs(api, mode, p, d, flags, idx):
-    """Run the two-layer step on p in-process ranks; every rank reads the sampled entries that
-    fall inside its shards. Returns {name: [rows, cols] float64}, replicas checked bit-equal."""
+    return sampled_outputs_cfg(api, mode, p, d, flags, idx, M, LAYERS)
+
+
+def sampled_outputs_cfg(api, mode, p, d, flags, idx, M, LAYERS):
+    """Run the two-layer step (M rows, LAYERS widths) on p in-process ranks; every rank reads the
+    sampled entries that fall inside its shards. Returns {name: [rows, cols] float64}, replicas
+    checked bit-equal."""
     from paper_2110_14883_b200.mlp import TPMLP
+    OUTPUTS = {"Y": (1, "Y"), "dX": (0, "X"), "dW1": (0, "W"), "dW2": (1, "W")}
     transport = api.TP_TRANSPORT_LOCAL if p > 1 else api.TP_TRANSPORT_NONE
     uid = api.tp_get_unique_id(transport)
     grid = build_grid(mode, p, d)
@@ -79,7 +85,7 @@ def sampled_outputs(api, mode, p, d, flags, idx):
                 m.step()
                 bufs = {"Y": m.Y[-1], "dX": m.dX[0], "dW1": m.dW[0], "dW2": m.dW[1]}
                 got = {}
-                for name, (layer, t, _, _) in OUTPUTS.items():
+                for name, (layer, t) in OUTPUTS.items():
                     e = extent(grid, specs[layer], r, t)
                     ri, ci = idx[name]
                     rs = np.nonzero((ri >= e.row0) & (ri < e.row0 + e.rows))[0]
