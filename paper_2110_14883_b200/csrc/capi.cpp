@@ -50,6 +50,7 @@ constexpr KnobDef kKnobs[] = {
     {"TP_GEMM_WIDE", -1, "512x256 wide pair tiles: -1 auto (K >= 12288, >= #SMs tiles), 0 off, 1 wherever legal"},
     {"TP_GEMM_WIDE_RASTER", 8, "wide-tile rows per raster band"},
     {"TP_GEMM_WIDE_NP", 0, "wide tiles non-persistent (one tile per cluster; measured equal)"},
+    {"TP_GEMM_NARROW", 1, "ragged last n-tile of <= 128 columns as a half-width pair tile (0 off)"},
     {"TP_GEMM_V1_BN", 0, "force the 1-CTA tile width 128 / 256 (0 auto)"},
     {"TP_GEMM_V1_TMA_STORE", 1, "1-CTA kernel TMA-store epilogue (0 per-element stores)"},
     {"TP_COMM_SMS", -1, "SMs a GEMM leaves to a collective running under it (-1 sized to the transfer)"},

@@ -98,6 +98,7 @@ struct Prob {
   int ptiles;      // pair tiles of this problem (split-K flag layout)
   int npanels, kb_panel, num_kb;  // K = npanels panels of kb_panel 64-wide k-blocks
   int unit0;  // first unit of this problem in the launch's unit space
+  int narrow_nb;  // n-tile index computed as a half-width (N = 128) pair tile, -1 none
 };
 
 struct Group {
@@ -424,7 +425,10 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
         const int kb0 = t.split * pr.kb_per_split;  // MC 5: split = this pair's K half
         const int kb1 = min(pr.num_kb, kb0 + pr.kb_per_split);
         const int m0 = t.mb * 256 + static_cast<int>(rank) * kBM;
-        const int n0 = t.nb * BNP + static_cast<int>(rank) * P::BNC;
+        // ragged last n-tile of <= BNP/2 columns: an N = BNP/2 pair tile (half the B bytes and
+        // MMA time instead of a full tile whose second half is zero fill)
+        const bool nar = MC == 1 && BNP == 256 && t.nb == pr.narrow_nb;
+        const int n0 = t.nb * BNP + static_cast<int>(rank) * (nar ? P::BNC / 2 : P::BNC);
         // k-block kb lives in K-panel kb / kb_panel (its own tensor maps, e.g. a peer's shard);
         // the panel and in-panel column advance incrementally (no division in the loop: the
         // single producer thread's instruction latency is on the pipeline's critical path)
@@ -448,7 +452,7 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
           mbar_wait(&empty[stage], phase ^ 1);
 #endif
           if (elect_one()) {
-          if (leader) mbar_expect_tx(&full[stage], 2 * P::StageBytes);
+          if (leader) mbar_expect_tx(&full[stage], 2 * (nar ? kABytes + P::BBytes / 2 : P::StageBytes));
           uint8_t* a_dst = sA + stage * kABytes;
           uint8_t* b_dst = sB + stage * P::BBytes;
           // ---- A: this CTA's 128 rows (K-major: one box; MN-major: two 64-wide chunks)
@@ -470,9 +474,9 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
           // ---- B: this CTA's BNP/2 columns
           if (!mc_b(MC)) {
             if (!b_mn) {
-              tma_load_2d_pair(mB, &full[stage], b_dst, kc, n0);
+              tma_load_2d_pair(nar ? &tmB[1] : mB, &full[stage], b_dst, kc, n0);  // [1]: 64-row box
             } else {
-              for (int c = 0; c < P::BNC / 64; ++c)
+              for (int c = 0; c < (nar ? P::BNC / 128 : P::BNC / 64); ++c)
                 tma_load_2d_pair(mB, &full[stage], b_dst + c * (kBK * 128), n0 + c * 64, kc);
             }
           } else {  // pairs stacked in M share B: this pair fetches half b_idx, multicasts it
@@ -522,7 +526,8 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
         const int num_k = pr.num_kb;
         const int kb0 = t.split * pr.kb_per_split;
         const int kb1 = min(num_k, kb0 + pr.kb_per_split);
-        const uint32_t idesc = idesc_bf16_f32(256, BNP, pr.a_mn != 0, pr.b_mn != 0);
+        const bool nar = MC == 1 && BNP == 256 && t.nb == pr.narrow_nb;
+        const uint32_t idesc = idesc_bf16_f32(256, nar ? BNP / 2 : BNP, pr.a_mn != 0, pr.b_mn != 0);
         // K-major: +32 B per 16-element K step inside the 128 B swizzle atom (SBO = 8 rows).
         // MN-major: +16 rows x 128 B per K step; LBO = one 64-wide MN chunk (BK rows).
         // Descriptors are built once per unit; per k-block / K step only the 16-byte-granular
@@ -696,16 +701,18 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
         __syncwarp();
         if (lane == 0) mbar_arrive_remote(&tempty[acc], lead);
       } else if (pr.splits == 1) {
+        // a narrow tile holds BNP/2 accumulator columns (the rest of the buffer is stale)
+        const bool nar = MC == 1 && BNP == 256 && t.nb == pr.narrow_nb;
         if (pr.out_bf16) {
 #pragma unroll 1
-          for (int sub = s64_0; sub < s64_1; ++sub) {
+          for (int sub = s64_0; sub < (nar ? min(s64_1, kSub64 / 2) : s64_1); ++sub) {
             float v[64];
             tmem_cols<64>(t_row, sub, v);
             store_box<64>(pr, stg, nbox, lane, v, row, n0 + sub * 64, row0);
           }
         } else {
 #pragma unroll 1
-          for (int sub = s32_0; sub < s32_1; ++sub) {
+          for (int sub = s32_0; sub < (nar ? min(s32_1, kSub32 / 2) : s32_1); ++sub) {
             float v[32];
             tmem_cols<32>(t_row, sub, v);
             store_box<32>(pr, stg, nbox, lane, v, row, n0 + sub * 32, row0);
@@ -1196,6 +1203,7 @@ tp_status setup_prob(const GemmArgs& g, Prob& pr, int clusters, int split_mode, 
   const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   pr.a_mn = g.trans_a ? 1 : 0;
   pr.b_mn = g.trans_b ? 0 : 1;
+  pr.narrow_nb = -1;
   // multicast halves: MC 2 loads half of the A rows per pair, MC 3 half of the B tile
   pr.npanels = g.npanels > 1 ? g.npanels : 1;
   if (pr.npanels > kMaxPanels) return fail(TP_ERR_UNSUPPORTED, "gemm: more than 4 K-panels");
@@ -1275,6 +1283,15 @@ tp_status setup_prob(const GemmArgs& g, Prob& pr, int clusters, int split_mode, 
   if (S < 1) S = 1;
   pr.splits = S;
   pr.kb_per_split = S > 1 ? kbps : num_k;
+  // half-width last n-tile (single pass only: the split-K paths move whole tiles); K-major B
+  // loads it through a 64-row box map in the free second panel slot
+  pr.narrow_nb = -1;
+  const int64_t n_tail = g.N % BNP;
+  if (MC == 1 && BNP == 256 && S == 1 && pr.npanels == 1 && n_tail > 0 && n_tail <= BNP / 2 &&
+      knob("TP_GEMM_NARROW")) {
+    pr.narrow_nb = pr.num_n - 1;
+    if (!pr.b_mn) TP_TRY(make_map2(&pr.tmB[1], BF, 2, g.B, g.K, g.N, g.ldb, kBK, P::BNC / 2));
+  }
   if (S > 1) {
     pr.counters = reinterpret_cast<int*>(ws);
     pr.ptiles = ptiles;
@@ -1423,6 +1440,7 @@ tp_status launch_wide(const GemmArgs* gs, int n, cudaStream_t s) {
     pr.num_kb = pr.kb_panel;
     pr.kb_per_split = pr.num_kb;
     pr.ptiles = pr.num_m * pr.num_n;
+    pr.narrow_nb = -1;
     pr.unit0 = units;
     units += pr.num_m * pr.num_n;
     flops += 2.0 * double(g.M) * double(g.N) * double(g.K);

@@ -164,6 +164,7 @@ def test_gemm_split_k_is_deterministic(api):
     {"TP_GEMM_KERNEL": "2", "TP_GEMM_BN": "256", "TP_GEMM_SPLITK": "0"},
     {"TP_GEMM_KERNEL": "2", "TP_GEMM_BN": "256", "TP_GEMM_EPI_WARPS": "8"},  # 8 epilogue warps
     {"TP_GEMM_KERNEL": "2", "TP_GEMM_WIDE": "1"},              # 512x256 pair tiles wherever legal
+    {"TP_GEMM_NARROW": "0"},                                   # ragged last n-tile at full width
 ], ids=lambda e: "-".join(f"{k[8:]}{v}" for k, v in e.items()))
 def test_gemm_kernel_variants_forced(api, env):
     """Every kernel variant the dispatcher can pick, forced for every shape of the GEMM parity
@@ -175,7 +176,7 @@ def test_gemm_kernel_variants_forced(api, env):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "tests/test_gpu_kernels.py",
                         "-k", "bf16_vs_oracle or exact_integer or wide_tile or epilogue or pair_kernel or short_k"
-                              " or deterministic or wide_pair"],
+                              " or deterministic or wide_pair or narrow"],
                        cwd=root, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
@@ -293,3 +294,16 @@ def test_gemm_wide_pair_tiles(api, ta, tb):
         got, ref = _gemm_case(api, ta, tb, M, N, K, "bf16", "bf16", seed=29, alpha=0.5, with_c=True,
                               with_bias=True)
         assert rel_fro(got, ref) <= 1e-2
+
+
+@pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("M,N,K", [(10240, 384, 256), (9000, 264, 200), (10000, 640, 136)])
+def test_gemm_narrow_last_tile(api, ta, tb, M, N, K):
+    """256 x 256 pair tiles whose last n-tile holds <= 128 columns (C4's N = 384 products): that
+    tile runs as an N = 128 pair MMA on half the B box (TP_GEMM_NARROW). Ragged M and a ragged
+    narrow tail included; fp32 out exact to accumulation order, bf16 with alpha, C and bias."""
+    got, ref = _gemm_case(api, ta, tb, M, N, K, "bf16", "fp32", seed=31)
+    assert rel_fro(got, ref) <= 2e-5
+    got, ref = _gemm_case(api, ta, tb, M, N, K, "bf16", "bf16", seed=31, alpha=0.5, with_c=True,
+                          with_bias=True)
+    assert rel_fro(got, ref) <= 1e-2 and np.isfinite(got).all()
