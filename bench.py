@@ -85,6 +85,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--eager", action="store_true", help="time eager launches instead of a CUDA graph")
+    ap.add_argument("--graph", action="store_true",
+                    help="N > 1: capture the step (and its NCCL collectives) as a CUDA graph; the "
+                         "default at N > 1 is eager launches (graph capture of the collectives has "
+                         "not run on a multi-GPU box)")
     ap.add_argument("--fused", action="store_true",
                     help="N > 1: fused peer-panel schedule (TP_FLAG_PEER_FUSED; 2D / 2.5D / 3D l=2)")
     return ap.parse_args()
@@ -180,12 +184,29 @@ def run_ours(a):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # TP_BENCH_DEVICE: every rank on that device (one-GPU multi-process test runs, tests/ncclshim)
+    local = int(os.environ.get("TP_BENCH_DEVICE", os.environ.get("LOCAL_RANK", "0")))
     if world != a.gpus:
         raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # torch.distributed is rendezvous + timing plumbing only (barriers, the max over ranks);
+        # TP_BENCH_DIST_BACKEND=gloo is for one-GPU multi-process test runs (tests/ncclshim)
+        backend = os.environ.get("TP_BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+        if not a.graph:
+            a.eager = True
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+        t = torch.tensor([v], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
     wl = WORKLOADS[a.workload]
     mode = DEFAULT_MODE.get(world, "1d") if a.mode == "auto" else a.mode
     depth = a.depth if mode == "2.5d" else 1
@@ -286,11 +307,7 @@ def run_ours(a):
         barrier()
         t_wall = time.perf_counter() - t_wall
     launches = launches_per_step * a.steps
-    ms = sum(s.elapsed_time(e) for s, e in ev) / a.steps
-    if world > 1:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(sum(s.elapsed_time(e) for s, e in ev) / a.steps)
     flops = sum(6.0 * M * K * N for K, N in layers)
     value = flops / (ms * 1e-3) / 1e12
 
@@ -323,12 +340,7 @@ def run_ours(a):
                 e1.record(stream)
                 e1.synchronize()
                 tot += e0.elapsed_time(e1)
-            t_ms = tot / n_e2e
-            if world > 1:
-                t = torch.tensor([t_ms], device="cuda", dtype=torch.float64)
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                t_ms = float(t.item())
-            return t_ms
+            return max_over_ranks(tot / n_e2e)
 
         def resident():
             cs.wait_stream(stream)
@@ -393,11 +405,7 @@ def run_ours(a):
         pipelined_run(n_e2e)
         p1.record(stream)
         p1.synchronize()
-        pms = p0.elapsed_time(p1) / n_e2e
-        if world > 1:
-            t = torch.tensor([pms], device="cuda", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            pms = float(t.item())
+        pms = max_over_ranks(p0.elapsed_time(p1) / n_e2e)
         ems = timed(resident)
         sms = timed(streamed)
         e2e = {"value": round(flops / (pms * 1e-3) / 1e12, 3), "unit": "TFLOP/s",

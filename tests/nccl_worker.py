@@ -90,6 +90,9 @@ def main():
             for i in reversed(range(len(Ws))):
                 d, dWs[i], _ = dense.linear_bwd(d, acts[i], Ws[i])
             og = build_grid(a.mode, world, a.depth)
+            if a.flags & api.TP_FLAG_SOLOMONIK:  # Solomonik 2.5D keeps its own shard layout
+                from oracle import solomonik as so
+                gather_full = lambda g_, sp, sh, t: so.gather_full(g_, sp, sh, t)  # noqa: E731
             sharded = bool(a.flags & api.TP_FLAG_W25_DEPTH_SHARDED)
             specs = [LayerSpec(a.M, K, N, split_1d="row" if i % 2 else "col", parity=i % 2,
                                w_depth_sharded=sharded) for i, (K, N) in enumerate(layers)]
