@@ -175,8 +175,8 @@ def test_gemm_kernel_variants_forced(api, env):
     env = dict(os.environ, **env)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "tests/test_gpu_kernels.py",
-                        "-k", "bf16_vs_oracle or exact_integer or wide_tile or epilogue or pair_kernel or short_k"
-                              " or deterministic or wide_pair or narrow"],
+                        "-k", "(bf16_vs_oracle or exact_integer or wide_tile or epilogue or pair_kernel or short_k"
+                              " or deterministic or wide_pair or narrow) and not variants_forced"],
                        cwd=root, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
@@ -307,3 +307,24 @@ def test_gemm_narrow_last_tile(api, ta, tb, M, N, K):
     got, ref = _gemm_case(api, ta, tb, M, N, K, "bf16", "bf16", seed=31, alpha=0.5, with_c=True,
                           with_bias=True)
     assert rel_fro(got, ref) <= 1e-2 and np.isfinite(got).all()
+
+
+@pytest.mark.parametrize("sched", [1, 0])
+@pytest.mark.parametrize("M,K,N", [(256, 3072, 3072), (200, 2056, 3000)])
+def test_grouped_backward_unit_schedule(api, sched, M, K, N):
+    """A layer backward whose grouped launch mixes long-K dX tiles (K = N) with many short dW
+    tiles (K = M): more units than pair clusters and unequal unit lengths, so the longest-first
+    unit schedule (TP_GEMM_SCHED=1) assigns them; round robin (0) for comparison. Both must
+    match the oracle (dX, dW: every tile, ragged tails included)."""
+    from tp_harness import gather, oracle_layer, spec_of, tp_layer
+    old = api.tp_knob_get("TP_GEMM_SCHED")
+    api.tp_knob_set("TP_GEMM_SCHED", sched)
+    try:
+        X, W, dY, _ = synth.layer_inputs(23, M, K, N)
+        per = tp_layer(api, "1d", 1, 1, M, K, N, X, W, dY)
+    finally:
+        api.tp_knob_set("TP_GEMM_SCHED", old)
+    spec = spec_of(M, K, N)
+    ref = oracle_layer("1d", 1, 1, spec, X, W, dY)
+    for (key, t), r in zip((("Y", "Y"), ("dX", "X"), ("dW", "W")), ref):
+        assert rel_fro(gather("1d", 1, 1, spec, per, key, t), r) <= 1e-2, key
