@@ -28,6 +28,7 @@
 #include <climits>
 #include <cstdlib>
 #include <mutex>
+#include <vector>
 
 #include "sm100_ptx.cuh"
 #include "tp_internal.h"
@@ -35,6 +36,22 @@
 // per-k-block clock64 instrumentation of the main loops (tools/gemm_trace.py); off by default
 #ifndef TP_LOOP_CLOCKS
 #define TP_LOOP_CLOCKS 0
+#endif
+// per-unit timeline of the pair kernel (tools/gemm_timeline.py); off by default. Slots per CTA
+// (kTlStride, after the 300 x 16 wait-counter block of the trace buffer): 0 entry, 1 after the
+// prologue, 2 exit, 3 / 4 producer's first / last TMA issue; per unit i < 16: 8+i first MMA issued,
+// 24+i accumulator commit issued, 40+i epilogue saw the accumulator, 56+i epilogue released it
+// (warp 2); 72..75 epilogue phase sums of warp 2: TMEM load, staging-buffer wait, stage + fence,
+// store issue.
+#ifndef TP_TIMELINE
+#define TP_TIMELINE 0
+#endif
+#if TP_TIMELINE
+#define TL_SET(slot, v) do { if (G.trace) G.trace[300 * 16 + blockIdx.x * 128 + (slot)] = (v); } while (0)
+#define TL_ADD(slot, v) do { if (G.trace) G.trace[300 * 16 + blockIdx.x * 128 + (slot)] += (v); } while (0)
+#else
+#define TL_SET(slot, v) do { } while (0)
+#define TL_ADD(slot, v) do { } while (0)
 #endif
 
 namespace tp {
@@ -101,13 +118,31 @@ struct Prob {
   int narrow_nb;  // n-tile index computed as a half-width (N = 128) pair tile, -1 none
 };
 
+// Unit schedule: cluster c runs units sched_order[sched_start[c] .. sched_start[c + 1]) when
+// `sched` is set (a host-side longest-processing-time assignment for launches whose units differ
+// in length, e.g. the backward's long-K dX tiles next to many short dW tiles), else the static
+// round robin u = c, c + #clusters, ...
+constexpr int kMaxSchedClusters = 80;   // >= 148 / 2 pair clusters
+constexpr int kMaxSchedUnits = 1024;
 struct Group {
   Prob p[kMaxProbs];
   int nprob;
   int total_units;
   int raster;  // pair-tile rows per raster band (8; TP_GEMM_RASTER for measurements)
   unsigned long long* trace;  // optional per-CTA wait-cycle counters (tp_gemm_trace)
+  int sched;
+  int epi_diag;  // TP_TIMELINE builds only: 1 = epilogue skips the TMA stores, 2 = also the staging
+  uint16_t sched_start[kMaxSchedClusters + 1];
+  uint16_t sched_order[kMaxSchedUnits];
 };
+
+__device__ __forceinline__ int units_of_cluster(const Group& G, int cid, int ncl) {
+  if (G.sched) return G.sched_start[cid + 1] - G.sched_start[cid];
+  return cid < G.total_units ? (G.total_units - cid + ncl - 1) / ncl : 0;
+}
+__device__ __forceinline__ int unit_at(const Group& G, int cid, int ncl, int i) {
+  return G.sched ? static_cast<int>(G.sched_order[G.sched_start[cid] + i]) : cid + i * ncl;
+}
 
 __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb, int& nb, int G) {
   // G = pair-tile rows per raster band (Group::raster)
@@ -234,14 +269,43 @@ __device__ __forceinline__ void stage_row(uint8_t* stg, int lane, const float (&
 // bulk store (the other buffer's) is still reading shared memory.
 template <int CW>
 __device__ __forceinline__ void store_box(const Prob& ep, uint8_t* stg, int& nbox, int lane,
-                                          float (&v)[CW], int64_t row, int64_t col0, int64_t row0) {
+                                          float (&v)[CW], int64_t row, int64_t col0, int64_t row0,
+                                          unsigned long long* tl = nullptr, int diag = 0) {
+#if TP_TIMELINE
+  const unsigned long long cf = clock64();
+#endif
   finish_vals<CW>(ep, v, row, col0);
   uint8_t* buf = stg + (nbox & 1) * kOutBytes;
+#if TP_TIMELINE
+  unsigned long long c0 = clock64();
+  if (tl && lane == 0) tl[77] += c0 - cf;
+  if (diag == 2) {  // keep the values live, skip staging and store
+    if (v[0] == 12345.f && v[CW - 1] == -1.f) stg[lane] = 1;
+    ++nbox;
+    return;
+  }
+#endif
   if (lane == 0) bulk_wait_read1();
   __syncwarp();
+#if TP_TIMELINE
+  unsigned long long c1 = clock64();
+#endif
   stage_row<CW>(buf, lane, v);
   fence_proxy_async_smem();
   __syncwarp();
+#if TP_TIMELINE
+  unsigned long long c2 = clock64();
+  if (tl && lane == 0) {
+    tl[73] += c1 - c0;
+    tl[74] += c2 - c1;
+  }
+#endif
+#if TP_TIMELINE
+  if (diag == 1) {
+    ++nbox;
+    return;
+  }
+#endif
   if (lane == 0) {
     const int pi = ep.d_rows ? static_cast<int>(row0 / ep.d_rows) : 0;
     if (pi < kMaxDPanels) {
@@ -250,6 +314,9 @@ __device__ __forceinline__ void store_box(const Prob& ep, uint8_t* stg, int& nbo
       bulk_commit();
     }
   }
+#if TP_TIMELINE
+  if (tl && lane == 0) tl[75] += clock64() - c2;
+#endif
   ++nbox;
 }
 
@@ -358,6 +425,7 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
   if (G.trace && threadIdx.x == 0) {  // entry timestamps (tools only)
     G.trace[blockIdx.x * 16 + 7] = globaltimer();
     G.trace[blockIdx.x * 16 + 10] = clock64();
+    TL_SET(0, clock64());
   }
   const uint32_t crank = cluster_rank();
   const uint32_t rank = crank & 1;   // position in the CTA pair
@@ -409,6 +477,13 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
   pdl_launch_dependents();
   pdl_wait();
   if (G.trace && threadIdx.x == 0) G.trace[blockIdx.x * 16 + 8] = globaltimer();
+#if TP_TIMELINE
+  unsigned long long* tl = G.trace ? G.trace + 300 * 16 + blockIdx.x * 128 : nullptr;
+  if (threadIdx.x == 0) TL_SET(1, clock64());
+#else
+  unsigned long long* tl = nullptr;
+#endif
+  (void)tl;
 
   if (warp == 0) {
     {
@@ -419,7 +494,8 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
       int stage = 0;
       uint32_t phase = 0;
       unsigned long long t_wait = 0, t_begin = clock64();
-      for (int u = cid; u < G.total_units; u += ncl) {
+      for (int ui = 0, nu = units_of_cluster(G, cid, ncl); ui < nu; ++ui) {
+        const int u = unit_at(G, cid, ncl, ui);
         const Unit t = unit_of<MC>(G, u, pair);
         const Prob& pr = G.p[t.prob];
         const int kb0 = t.split * pr.kb_per_split;  // MC 5: split = this pair's K half
@@ -452,6 +528,10 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
           mbar_wait(&empty[stage], phase ^ 1);
 #endif
           if (elect_one()) {
+#if TP_TIMELINE
+          if (ui == 0 && kb == kb0) TL_SET(3, clock64());
+          TL_SET(4, clock64());
+#endif
           if (leader) mbar_expect_tx(&full[stage], 2 * (nar ? kABytes + P::BBytes / 2 : P::StageBytes));
           uint8_t* a_dst = sA + stage * kABytes;
           uint8_t* b_dst = sB + stage * P::BBytes;
@@ -520,7 +600,8 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
       uint32_t acc_phase = 0;
       unsigned long long t_full = 0, t_temp = 0, t_first = 0, t_unit0 = 0, t_steady = 0, n_steady = 0,
                          t_begin = clock64();
-      for (int u = cid; u < G.total_units; u += ncl) {
+      for (int ui = 0, nu = units_of_cluster(G, cid, ncl); ui < nu; ++ui) {
+        const int u = unit_at(G, cid, ncl, ui);
         const Unit t = unit_of<MC>(G, u, pair);
         const Prob& pr = G.p[t.prob];
         const int num_k = pr.num_kb;
@@ -568,6 +649,11 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
           const uint64_t ad = a_desc0 + static_cast<uint32_t>(stage * (kABytes / 16));
           const uint64_t bd = b_desc0 + static_cast<uint32_t>(stage * (P::BBytes / 16));
           if (elect_one()) {
+#if TP_TIMELINE
+            if (kb == kb0) {
+              if (ui < 16) TL_SET(8 + ui, clock64());
+            }
+#endif
 #pragma unroll
             for (int k = 0; k < kBK / 16; ++k)
               umma_bf16_cg2(d_tmem, ad + k * a_step4, bd + k * b_step4, idesc,
@@ -582,6 +668,9 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
           }
         }
         if (elect_one()) umma_commit_cg2_mc(&tfull[acc], pair_mask);  // accumulator ready
+#if TP_TIMELINE
+        if (lane == 0 && ui < 16) TL_SET(24 + ui, clock64());
+#endif
         __syncwarp();
         if (++acc == 2) {
           acc = 0;
@@ -613,7 +702,8 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
     uint32_t rx_round = 0;  // MC 5: DSMEM chunk rounds so far (both pairs count alike)
     unsigned long long t_tf = 0, t_begin = clock64();
     unsigned long long t_pub = 0, t_xwait = 0;  // split exchange: publish / sibling-wait cycles
-    for (int u = cid; u < G.total_units; u += ncl) {
+    for (int ui = 0, nu = units_of_cluster(G, cid, ncl); ui < nu; ++ui) {
+        const int u = unit_at(G, cid, ncl, ui);
       const Unit t = unit_of<MC>(G, u, pair);
       const Prob& pr = G.p[t.prob];
       const int64_t rloc = static_cast<int64_t>(rank) * kBM + quad * 32;  // row within pair tile
@@ -627,6 +717,9 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
         if (lane == 0) mbar_wait_sleep(&tfull[acc], acc_phase, 200);
         __syncwarp();
         t_tf += clock64() - t0;
+#if TP_TIMELINE
+        if (warp == 2 && lane == 0 && ui < 16) TL_SET(40 + ui, clock64());
+#endif
       }
       tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) +
@@ -703,13 +796,26 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
       } else if (pr.splits == 1) {
         // a narrow tile holds BNP/2 accumulator columns (the rest of the buffer is stale)
         const bool nar = MC == 1 && BNP == 256 && t.nb == pr.narrow_nb;
+#if TP_TIMELINE
+        if (warp == 2 && lane == 0 && tl) tl[76] += clock64() - tl[40 + min(ui, 15)];
+#endif
         if (pr.out_bf16) {
 #pragma unroll 1
           for (int sub = s64_0; sub < (nar ? min(s64_1, kSub64 / 2) : s64_1); ++sub) {
             float v[64];
+#if TP_TIMELINE
+            const unsigned long long c0 = clock64();
+#endif
             tmem_cols<64>(t_row, sub, v);
-            store_box<64>(pr, stg, nbox, lane, v, row, n0 + sub * 64, row0);
+#if TP_TIMELINE
+            if (warp == 2 && lane == 0 && tl) tl[72] += clock64() - c0;
+#endif
+            store_box<64>(pr, stg, nbox, lane, v, row, n0 + sub * 64, row0, warp == 2 ? tl : nullptr,
+                          G.epi_diag);
           }
+#if TP_TIMELINE
+          if (warp == 2 && lane == 0 && tl) tl[79] = clock64();
+#endif
         } else {
 #pragma unroll 1
           for (int sub = s32_0; sub < (nar ? min(s32_1, kSub32 / 2) : s32_1); ++sub) {
@@ -721,6 +827,10 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_remote(&tempty[acc], lead);
+#if TP_TIMELINE
+        if (warp == 2 && lane == 0 && ui < 16) TL_SET(56 + ui, clock64());
+        if (warp == 2 && lane == 0 && tl) tl[78] += clock64() - tl[79];
+#endif
       } else if (EW == 4 && pr.owner_wait && pr.splits == 2) {
         // ---- split-K of two, co-resident, reduce-scatter style: split s keeps the columns
         // [s BNP/2, (s+1) BNP/2) of the tile. Each split publishes its fp32 partial of the OTHER
@@ -923,6 +1033,7 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
   if (G.trace && threadIdx.x == 0) {
     G.trace[blockIdx.x * 16 + 9] = globaltimer();
     G.trace[blockIdx.x * 16 + 11] = clock64();
+    TL_SET(2, clock64());
   }
 }
 
@@ -1304,6 +1415,54 @@ tp_status setup_prob(const GemmArgs& g, Prob& pr, int clusters, int split_mode, 
   return TP_OK;
 }
 
+// Longest-processing-time assignment of units to clusters when their lengths differ (a group
+// whose members have different K, e.g. the C2 backward: 32 dX tiles of 64 k-blocks next to 256
+// dW tiles of 8; round robin gave the first 32 clusters 88 k-blocks against a mean of 55).
+// Unit cost = k-blocks x the MMA clocks of one pair k-block + a per-unit epilogue estimate
+// (TP_GEMM_SCHED_EPI clocks). Units longest first, each to the least-loaded cluster; a cluster
+// runs its units in the order they were assigned (long first).
+template <int BNP>
+void schedule_units(Group& G, int ncl) {
+  const int units = G.total_units;
+  if (!knob("TP_GEMM_SCHED") || ncl <= 0 || ncl > kMaxSchedClusters || units <= ncl ||
+      units > kMaxSchedUnits)
+    return;
+  std::vector<int64_t> cost(units);
+  int64_t cmin = INT64_MAX, cmax = 0;
+  const int64_t epi = knob("TP_GEMM_SCHED_EPI");
+  for (int i = 0; i < G.nprob; ++i) {
+    const Prob& pr = G.p[i];
+    if (pr.splits != 1) return;  // split-K units keep their co-residency rules
+    const int nu = pr.num_m * pr.num_n;
+    for (int t = 0; t < nu; ++t) {
+      const int64_t c = int64_t(pr.num_kb) * 512 * BNP / 256 + epi;
+      cost[pr.unit0 + t] = c;
+      cmin = std::min(cmin, c);
+      cmax = std::max(cmax, c);
+    }
+  }
+  if (cmin == cmax) return;  // uniform units: round robin is already balanced
+  std::vector<int> ord(units);
+  for (int u = 0; u < units; ++u) ord[u] = u;
+  std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+  std::vector<int64_t> load(ncl, 0);
+  std::vector<std::vector<int>> lists(ncl);
+  for (int u : ord) {
+    int best = 0;
+    for (int c = 1; c < ncl; ++c)
+      if (load[c] < load[best]) best = c;
+    load[best] += cost[u];
+    lists[best].push_back(u);
+  }
+  int k = 0;
+  for (int c = 0; c < ncl; ++c) {
+    G.sched_start[c] = static_cast<uint16_t>(k);
+    for (int u : lists[c]) G.sched_order[k++] = static_cast<uint16_t>(u);
+  }
+  G.sched_start[ncl] = static_cast<uint16_t>(k);
+  G.sched = 1;
+}
+
 template <int BNP, int MC, int EW = 4>
 tp_status launch2(const GemmArgs* gs, int n, cudaStream_t s) {
   using P = PC<BNP, MC, EW>;
@@ -1361,6 +1520,9 @@ tp_status launch2(const GemmArgs* gs, int n, cudaStream_t s) {
   if (gs[0].reserve_sms > 0)
     cap = std::max(1, std::min(cap, (sm_count() - gs[0].reserve_sms) / (2 * pairs_of(MC))));
   const int grid = 2 * pairs_of(MC) * (units < cap ? units : cap);
+  G.sched = 0;
+  if (MC == 1) schedule_units<BNP>(G, grid / 2);
+  G.epi_diag = TP_TIMELINE ? knob("TP_GEMM_EPI_DIAG") : 0;
   // split 0 may wait for its sibling splits only when every unit has its own resident cluster
   const int env_owner = knob("TP_GEMM_SPLIT_OWNER");
   for (int i = 0; i < n; ++i)
@@ -1403,6 +1565,8 @@ tp_status launch_wide(const GemmArgs* gs, int n, cudaStream_t s) {
   G.nprob = n;
   G.raster = env_raster;
   G.trace = nullptr;
+  G.sched = 0;
+  G.epi_diag = 0;
   const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   int units = 0;
   double flops = 0;
