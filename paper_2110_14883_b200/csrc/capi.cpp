@@ -49,7 +49,7 @@ constexpr KnobDef kKnobs[] = {
     {"TP_GEMM_RASTER", 8, "pair-tile rows per raster band"},
     {"TP_GEMM_SCHED", 1, "longest-first unit-to-cluster schedule for pair launches with unequal units (0 round robin)"},
     {"TP_GEMM_EPI_DIAG", 0, "diagnostics (TP_TIMELINE builds only): pair-kernel epilogue skips its stores (1) or staging and stores (2)"},
-    {"TP_GEMM_SCHED_EPI", 2048, "per-unit epilogue cost (SM clocks) in the unit schedule's cost model"},
+    {"TP_GEMM_SCHED_EPI", 800, "per-unit epilogue cost (SM clocks) in the unit schedule's cost model"},
     {"TP_GEMM_WIDE", -1, "512x256 wide pair tiles: -1 auto (K >= 12288, >= #SMs tiles), 0 off, 1 wherever legal"},
     {"TP_GEMM_WIDE_RASTER", 8, "wide-tile rows per raster band"},
     {"TP_GEMM_WIDE_NP", 0, "wide tiles non-persistent (one tile per cluster; measured equal)"},

@@ -82,6 +82,8 @@ constexpr int kMaxDPanels = 8;  // D row-panels per problem (fused 1D reduce-sca
 // Pair-tile width BNP (256 or 128): B columns per CTA, ring depth, TMEM, smem. MC 5 (K-split
 // pair cluster) gives one ring stage to the 32 KB DSMEM receive buffer of the split reduction.
 constexpr int kRxBytes = 2 * 32 * kBM * 4;  // MC 5: two [32 cols][128 rows] fp32 chunks
+// shared-memory copy of the problems' scalars (512 B) and of this cluster's unit list (256 B)
+constexpr int kScalBytes = 1024;
 template <int BNP, int MC = 1, int EW = 4>
 struct PC {
   static constexpr int BNC = BNP / 2;
@@ -91,13 +93,14 @@ struct PC {
   static constexpr int StageBytes = kABytes + BBytes;
   static constexpr int TmemCols = 2 * BNP;
   static constexpr int Rx = MC == 5 ? kRxBytes : 0;
-  static constexpr int Smem = Stages * StageBytes + 2 * EW * kOutBytes + Rx + 1024 + 256;
+  static constexpr int Smem = Stages * StageBytes + 2 * EW * kOutBytes + Rx + kScalBytes + 1024 + 256;
   static constexpr int TileElems = 256 * BNP;
 };
 
-struct Prob {
-  CUtensorMap tmA[kMaxPanels], tmB[kMaxPanels];  // one A/B map per K-panel
-  CUtensorMap tmD[kMaxDPanels];                   // one D map per row-panel (usually 1)
+// Per-problem scalars. The pair kernel copies them into shared memory once per CTA: the loops
+// read them per unit (unit decode, descriptors, epilogue parameters), and indexed loads from the
+// ~11 KB parameter block missed the constant cache (~1K clocks between units, tools/gemm_timeline).
+struct ProbS {
   int d_rows;                                      // rows per D panel (0: a single D)
   const float* C;
   const void* bias;
@@ -117,6 +120,12 @@ struct Prob {
   int unit0;  // first unit of this problem in the launch's unit space
   int narrow_nb;  // n-tile index computed as a half-width (N = 128) pair tile, -1 none
 };
+struct Prob : ProbS {
+  CUtensorMap tmA[kMaxPanels], tmB[kMaxPanels];  // one A/B map per K-panel
+  CUtensorMap tmD[kMaxDPanels];                   // one D map per row-panel (usually 1)
+};
+constexpr int kMaxClusterUnits = 128;  // scheduled units per cluster held in shared memory
+static_assert(sizeof(ProbS) * kMaxProbs <= 512, "problem scalars exceed their smem slot");
 
 // Unit schedule: cluster c runs units sched_order[sched_start[c] .. sched_start[c + 1]) when
 // `sched` is set (a host-side longest-processing-time assignment for launches whose units differ
@@ -142,6 +151,10 @@ __device__ __forceinline__ int units_of_cluster(const Group& G, int cid, int ncl
 }
 __device__ __forceinline__ int unit_at(const Group& G, int cid, int ncl, int i) {
   return G.sched ? static_cast<int>(G.sched_order[G.sched_start[cid] + i]) : cid + i * ncl;
+}
+// the same from the shared-memory copy of the cluster's list (pair kernel)
+__device__ __forceinline__ int unit_at_s(int sched, const uint16_t* ulist, int cid, int ncl, int i) {
+  return sched ? static_cast<int>(ulist[i]) : cid + i * ncl;
 }
 
 __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb, int& nb, int G) {
@@ -176,34 +189,34 @@ struct Unit {
 };
 
 template <int MC>
-__device__ __forceinline__ Unit unit_of(const Group& G, int u, int pair) {
+__device__ __forceinline__ Unit unit_of(const ProbS* sp, int nprob, int raster, int u, int pair) {
   Unit x;
   x.prob = 0;
 #pragma unroll
   for (int i = 1; i < kMaxProbs; ++i)
-    if (i < G.nprob && u >= G.p[i].unit0) x.prob = i;
-  const Prob& P = G.p[x.prob];
+    if (i < nprob && u >= sp[i].unit0) x.prob = i;
+  const ProbS& P = sp[x.prob];
   const int lu = u - P.unit0;
   const int st = lu / P.splits;
   x.split = lu % P.splits;
   if (MC == 5) {  // both pairs on the same tile; `split` = which half of K
-    tile_coords(st, P.num_m, P.num_n, x.mb, x.nb, G.raster);
+    tile_coords(st, P.num_m, P.num_n, x.mb, x.nb, raster);
     x.split = pair;
     x.ptile = st;
     return x;
   } else if (MC == 4) {
     int mbs, nbs;
-    tile_coords(st, (P.num_m + 1) / 2, (P.num_n + 1) / 2, mbs, nbs, G.raster);
+    tile_coords(st, (P.num_m + 1) / 2, (P.num_n + 1) / 2, mbs, nbs, raster);
     x.mb = mbs * 2 + (pair >> 1);
     x.nb = nbs * 2 + (pair & 1);
   } else if (MC == 3) {
     int mbs;
-    tile_coords(st, (P.num_m + 1) / 2, P.num_n, mbs, x.nb, G.raster);
+    tile_coords(st, (P.num_m + 1) / 2, P.num_n, mbs, x.nb, raster);
     x.mb = mbs * 2 + pair;
   } else {
     const int num_ns = (P.num_n + MC - 1) / MC;
     int nbs;
-    tile_coords(st, P.num_m, num_ns, x.mb, nbs, G.raster);
+    tile_coords(st, P.num_m, num_ns, x.mb, nbs, raster);
     x.nb = nbs * MC + pair;
   }
   x.ptile = st * pairs_of(MC) + pair;  // dense pair-tile id (split-K partials / counters)
@@ -212,7 +225,7 @@ __device__ __forceinline__ Unit unit_of(const Group& G, int u, int pair) {
 
 // alpha*(acc + C) + bias for CW consecutive columns starting at col0 of one row.
 template <int CW>
-__device__ __forceinline__ void finish_vals(const Prob& ep, float (&v)[CW], int64_t row, int64_t col0) {
+__device__ __forceinline__ void finish_vals(const ProbS& ep, float (&v)[CW], int64_t row, int64_t col0) {
   const bool in_row = row < ep.M;
   const bool full = col0 + CW <= ep.N;
   if (ep.C && in_row) {
@@ -268,7 +281,7 @@ __device__ __forceinline__ void stage_row(uint8_t* stg, int lane, const float (&
 // Two staging buffers per warp used alternately: before refilling one, wait until at most one
 // bulk store (the other buffer's) is still reading shared memory.
 template <int CW>
-__device__ __forceinline__ void store_box(const Prob& ep, uint8_t* stg, int& nbox, int lane,
+__device__ __forceinline__ void store_box(const ProbS& ep, const CUtensorMap* tmD, uint8_t* stg, int& nbox, int lane,
                                           float (&v)[CW], int64_t row, int64_t col0, int64_t row0,
                                           unsigned long long* tl = nullptr, int diag = 0) {
 #if TP_TIMELINE
@@ -278,7 +291,7 @@ __device__ __forceinline__ void store_box(const Prob& ep, uint8_t* stg, int& nbo
   uint8_t* buf = stg + (nbox & 1) * kOutBytes;
 #if TP_TIMELINE
   unsigned long long c0 = clock64();
-  if (tl && lane == 0) tl[77] += c0 - cf;
+  if (tl && lane == 0) tl[5] += c0 - cf;
   if (diag == 2) {  // keep the values live, skip staging and store
     if (v[0] == 12345.f && v[CW - 1] == -1.f) stg[lane] = 1;
     ++nbox;
@@ -296,8 +309,8 @@ __device__ __forceinline__ void store_box(const Prob& ep, uint8_t* stg, int& nbo
 #if TP_TIMELINE
   unsigned long long c2 = clock64();
   if (tl && lane == 0) {
-    tl[73] += c1 - c0;
-    tl[74] += c2 - c1;
+    tl[1] += c1 - c0;
+    tl[2] += c2 - c1;
   }
 #endif
 #if TP_TIMELINE
@@ -309,13 +322,13 @@ __device__ __forceinline__ void store_box(const Prob& ep, uint8_t* stg, int& nbo
   if (lane == 0) {
     const int pi = ep.d_rows ? static_cast<int>(row0 / ep.d_rows) : 0;
     if (pi < kMaxDPanels) {
-      tma_store_2d(&ep.tmD[pi], buf, static_cast<int>(col0),
+      tma_store_2d(&tmD[pi], buf, static_cast<int>(col0),
                    static_cast<int>(row0 - int64_t(pi) * ep.d_rows));
       bulk_commit();
     }
   }
 #if TP_TIMELINE
-  if (tl && lane == 0) tl[75] += clock64() - c2;
+  if (tl && lane == 0) tl[3] += clock64() - c2;
 #endif
   ++nbox;
 }
@@ -412,7 +425,8 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
   uint8_t* sB = sA + P::Stages * kABytes;
   uint8_t* sOut = sB + P::Stages * P::BBytes;
   float* rx = reinterpret_cast<float*>(sOut + 2 * EW * kOutBytes);  // MC 5: [2][32][128]
-  uint64_t* full = reinterpret_cast<uint64_t*>(sOut + 2 * EW * kOutBytes + P::Rx);
+  ProbS* sp = reinterpret_cast<ProbS*>(sOut + 2 * EW * kOutBytes + P::Rx);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sOut + 2 * EW * kOutBytes + P::Rx + kScalBytes);
   uint64_t* empty = full + P::Stages;
   uint64_t* tfull = empty + P::Stages;
   uint64_t* tempty = tfull + 2;
@@ -468,6 +482,17 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc_cg2(tslot, P::TmemCols);
+  // launch parameters the loops read per unit go to shared memory / registers here, under the
+  // barrier init and TMEM allocation (first reads of the parameter block miss the constant cache)
+  uint16_t* ulist = reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(sp) + 512);
+  const int sched = G.sched;
+  const int nu = units_of_cluster(G, cid, ncl);
+  if (warp == 2 && lane < G.nprob) sp[lane] = static_cast<const ProbS&>(G.p[lane]);
+  if (warp == 3 && sched) {
+    const int base = G.sched_start[cid];
+    for (int i = lane; i < nu; i += 32) ulist[i] = G.sched_order[base + i];
+  }
+  const int nprob = G.nprob, raster = G.raster;
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
@@ -494,10 +519,11 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
       int stage = 0;
       uint32_t phase = 0;
       unsigned long long t_wait = 0, t_begin = clock64();
-      for (int ui = 0, nu = units_of_cluster(G, cid, ncl); ui < nu; ++ui) {
-        const int u = unit_at(G, cid, ncl, ui);
-        const Unit t = unit_of<MC>(G, u, pair);
-        const Prob& pr = G.p[t.prob];
+      for (int ui = 0; ui < nu; ++ui) {
+        const int u = unit_at_s(sched, ulist, cid, ncl, ui);
+        const Unit t = unit_of<MC>(sp, nprob, raster, u, pair);
+        const ProbS& pr = sp[t.prob];
+        const Prob& pm = G.p[t.prob];
         const int kb0 = t.split * pr.kb_per_split;  // MC 5: split = this pair's K half
         const int kb1 = min(pr.num_kb, kb0 + pr.kb_per_split);
         const int m0 = t.mb * 256 + static_cast<int>(rank) * kBM;
@@ -511,12 +537,12 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
         const int kc_end = pr.kb_panel * kBK;
         int panel = kb0 / pr.kb_panel;
         int kc = (kb0 - panel * pr.kb_panel) * kBK;
-        const CUtensorMap* mA = &pr.tmA[panel];
-        const CUtensorMap* mB = &pr.tmB[panel];
+        const CUtensorMap* mA = &pm.tmA[panel];
+        const CUtensorMap* mB = &pm.tmB[panel];
         // copies: the asm "memory" clobbers below would otherwise force param-space reloads
         const bool a_mn = pr.a_mn != 0, b_mn = pr.b_mn != 0;
-        const CUtensorMap* const tmA = pr.tmA;
-        const CUtensorMap* const tmB = pr.tmB;
+        const CUtensorMap* const tmA = pm.tmA;
+        const CUtensorMap* const tmB = pm.tmB;
         for (int kb = kb0; kb < kb1; ++kb) {
 #if TP_LOOP_CLOCKS
           {
@@ -600,10 +626,10 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
       uint32_t acc_phase = 0;
       unsigned long long t_full = 0, t_temp = 0, t_first = 0, t_unit0 = 0, t_steady = 0, n_steady = 0,
                          t_begin = clock64();
-      for (int ui = 0, nu = units_of_cluster(G, cid, ncl); ui < nu; ++ui) {
-        const int u = unit_at(G, cid, ncl, ui);
-        const Unit t = unit_of<MC>(G, u, pair);
-        const Prob& pr = G.p[t.prob];
+      for (int ui = 0; ui < nu; ++ui) {
+        const int u = unit_at_s(sched, ulist, cid, ncl, ui);
+        const Unit t = unit_of<MC>(sp, nprob, raster, u, pair);
+        const ProbS& pr = sp[t.prob];
         const int num_k = pr.num_kb;
         const int kb0 = t.split * pr.kb_per_split;
         const int kb1 = min(num_k, kb0 + pr.kb_per_split);
@@ -691,6 +717,10 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
     // quadrant take the two halves of the tile's columns (`half`) =====
     const int quad = warp & 3;
     const int half = (warp - 2) / 4;
+#if TP_TIMELINE
+    unsigned long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // epilogue phase sums (warp 2)
+    unsigned long long t_saw = 0, t_loop_end = 0;
+#endif
     constexpr int kHalves = EW / 4;
     constexpr int kSub64 = BNP / 64, kSub32 = BNP / 32;  // column sub-chunks per tile
     const int s64_0 = half * (kSub64 / kHalves), s64_1 = s64_0 + kSub64 / kHalves;
@@ -702,10 +732,11 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
     uint32_t rx_round = 0;  // MC 5: DSMEM chunk rounds so far (both pairs count alike)
     unsigned long long t_tf = 0, t_begin = clock64();
     unsigned long long t_pub = 0, t_xwait = 0;  // split exchange: publish / sibling-wait cycles
-    for (int ui = 0, nu = units_of_cluster(G, cid, ncl); ui < nu; ++ui) {
-        const int u = unit_at(G, cid, ncl, ui);
-      const Unit t = unit_of<MC>(G, u, pair);
-      const Prob& pr = G.p[t.prob];
+    for (int ui = 0; ui < nu; ++ui) {
+        const int u = unit_at_s(sched, ulist, cid, ncl, ui);
+      const Unit t = unit_of<MC>(sp, nprob, raster, u, pair);
+      const ProbS& pr = sp[t.prob];
+      const Prob& pm = G.p[t.prob];
       const int64_t rloc = static_cast<int64_t>(rank) * kBM + quad * 32;  // row within pair tile
       const int64_t row0 = static_cast<int64_t>(t.mb) * 256 + rloc;       // first row of warp
       const int64_t row = row0 + lane;
@@ -719,6 +750,7 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
         t_tf += clock64() - t0;
 #if TP_TIMELINE
         if (warp == 2 && lane == 0 && ui < 16) TL_SET(40 + ui, clock64());
+        t_saw = clock64();
 #endif
       }
       tc_fence_after();
@@ -777,7 +809,7 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
               mbar_arrive_cluster(&rxe[1], peer);
             }
             if (pr.out_bf16) {
-              store_box<64>(pr, stg, nbox, lane, v, row, n0 + k * 64, row0);
+              store_box<64>(pr, pm.tmD, stg, nbox, lane, v, row, n0 + k * 64, row0);
             } else {
               float lo[32], hi[32];
 #pragma unroll
@@ -785,8 +817,8 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
                 lo[j] = v[j];
                 hi[j] = v[32 + j];
               }
-              store_box<32>(pr, stg, nbox, lane, lo, row, n0 + k * 64, row0);
-              store_box<32>(pr, stg, nbox, lane, hi, row, n0 + k * 64 + 32, row0);
+              store_box<32>(pr, pm.tmD, stg, nbox, lane, lo, row, n0 + k * 64, row0);
+              store_box<32>(pr, pm.tmD, stg, nbox, lane, hi, row, n0 + k * 64 + 32, row0);
             }
           }
         }
@@ -797,7 +829,7 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
         // a narrow tile holds BNP/2 accumulator columns (the rest of the buffer is stale)
         const bool nar = MC == 1 && BNP == 256 && t.nb == pr.narrow_nb;
 #if TP_TIMELINE
-        if (warp == 2 && lane == 0 && tl) tl[76] += clock64() - tl[40 + min(ui, 15)];
+        tacc[4] += clock64() - t_saw;
 #endif
         if (pr.out_bf16) {
 #pragma unroll 1
@@ -808,20 +840,25 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
 #endif
             tmem_cols<64>(t_row, sub, v);
 #if TP_TIMELINE
-            if (warp == 2 && lane == 0 && tl) tl[72] += clock64() - c0;
+            tacc[0] += clock64() - c0;
 #endif
-            store_box<64>(pr, stg, nbox, lane, v, row, n0 + sub * 64, row0, warp == 2 ? tl : nullptr,
+            store_box<64>(pr, pm.tmD, stg, nbox, lane, v, row, n0 + sub * 64, row0,
+#if TP_TIMELINE
+                          warp == 2 ? tacc : nullptr,
+#else
+                          nullptr,
+#endif
                           G.epi_diag);
           }
 #if TP_TIMELINE
-          if (warp == 2 && lane == 0 && tl) tl[79] = clock64();
+          t_loop_end = clock64();
 #endif
         } else {
 #pragma unroll 1
           for (int sub = s32_0; sub < (nar ? min(s32_1, kSub32 / 2) : s32_1); ++sub) {
             float v[32];
             tmem_cols<32>(t_row, sub, v);
-            store_box<32>(pr, stg, nbox, lane, v, row, n0 + sub * 32, row0);
+            store_box<32>(pr, pm.tmD, stg, nbox, lane, v, row, n0 + sub * 32, row0);
           }
         }
         tc_fence_before();
@@ -829,7 +866,7 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
         if (lane == 0) mbar_arrive_remote(&tempty[acc], lead);
 #if TP_TIMELINE
         if (warp == 2 && lane == 0 && ui < 16) TL_SET(56 + ui, clock64());
-        if (warp == 2 && lane == 0 && tl) tl[78] += clock64() - tl[79];
+        tacc[6] += clock64() - t_loop_end;
 #endif
       } else if (EW == 4 && pr.owner_wait && pr.splits == 2) {
         // ---- split-K of two, co-resident, reduce-scatter style: split s keeps the columns
@@ -886,7 +923,7 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
               v[4 * i + 2] += x[i].z;
               v[4 * i + 3] += x[i].w;
             }
-            store_box<64>(pr, stg, nbox, lane, v, row, n0 + sub * 64, row0);
+            store_box<64>(pr, pm.tmD, stg, nbox, lane, v, row, n0 + sub * 64, row0);
           }
         } else {
 #pragma unroll 1
@@ -902,7 +939,7 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
               v[4 * i + 2] += x.z;
               v[4 * i + 3] += x.w;
             }
-            store_box<32>(pr, stg, nbox, lane, v, row, n0 + ch * 32, row0);
+            store_box<32>(pr, pm.tmD, stg, nbox, lane, v, row, n0 + ch * 32, row0);
           }
         }
         tc_fence_before();
@@ -931,7 +968,7 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
             float v[64];
             tmem_cols<64>(t_row, sub, v);
             add_partials<64>(base, pr.splits, kSplitStride4, sub, v);
-            store_box<64>(pr, stg, nbox, lane, v, row, n0 + sub * 64, row0);
+            store_box<64>(pr, pm.tmD, stg, nbox, lane, v, row, n0 + sub * 64, row0);
           }
         } else {
 #pragma unroll 1
@@ -939,7 +976,7 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
             float v[32];
             tmem_cols<32>(t_row, sub, v);
             add_partials<32>(base, pr.splits, kSplitStride4, sub, v);
-            store_box<32>(pr, stg, nbox, lane, v, row, n0 + sub * 32, row0);
+            store_box<32>(pr, pm.tmD, stg, nbox, lane, v, row, n0 + sub * 32, row0);
           }
         }
         tc_fence_before();
@@ -996,14 +1033,14 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
             for (int sub = s64_0; sub < s64_1; ++sub) {
               float v[64];
               sum_partials<64>(base, pr.splits, kSplitStride4, sub, v);
-              store_box<64>(pr, stg, nbox, lane, v, row, n0 + sub * 64, row0);
+              store_box<64>(pr, pm.tmD, stg, nbox, lane, v, row, n0 + sub * 64, row0);
             }
           } else {
 #pragma unroll 1
             for (int sub = s32_0; sub < s32_1; ++sub) {
               float v[32];
               sum_partials<32>(base, pr.splits, kSplitStride4, sub, v);
-              store_box<32>(pr, stg, nbox, lane, v, row, n0 + sub * 32, row0);
+              store_box<32>(pr, pm.tmD, stg, nbox, lane, v, row, n0 + sub * 32, row0);
             }
           }
         }
@@ -1016,6 +1053,10 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
     // staging buffers must outlive the bulk stores' smem reads; the global writes complete with
     // the grid (as CUTLASS's store tail: wait_group.read, not a full-completion wait)
     if (lane == 0) bulk_wait_read0();
+#if TP_TIMELINE
+    if (warp == 2 && lane == 0 && tl)
+      for (int i = 0; i < 7; ++i) tl[72 + i] = tacc[i];
+#endif
     if (G.trace && warp == 2 && lane == 0) {
       G.trace[blockIdx.x * 16 + 5] = t_tf;
       G.trace[blockIdx.x * 16 + 15] = (t_xwait << 32) | (t_pub & 0xffffffffull);
@@ -1213,14 +1254,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(threads_of<4>(), 1)
           for (int sub = 0; sub < 4; ++sub) {
             float v[64];
             tmem_cols<64>(t_row, sub, v);
-            store_box<64>(pr, stg, nbox, lane, v, row, n0 + sub * 64, row0);
+            store_box<64>(pr, pr.tmD, stg, nbox, lane, v, row, n0 + sub * 64, row0);
           }
         } else {
 #pragma unroll 1
           for (int sub = 0; sub < 8; ++sub) {
             float v[32];
             tmem_cols<32>(t_row, sub, v);
-            store_box<32>(pr, stg, nbox, lane, v, row, n0 + sub * 32, row0);
+            store_box<32>(pr, pr.tmD, stg, nbox, lane, v, row, n0 + sub * 32, row0);
           }
         }
       }
@@ -1418,9 +1459,11 @@ tp_status setup_prob(const GemmArgs& g, Prob& pr, int clusters, int split_mode, 
 // Longest-processing-time assignment of units to clusters when their lengths differ (a group
 // whose members have different K, e.g. the C2 backward: 32 dX tiles of 64 k-blocks next to 256
 // dW tiles of 8; round robin gave the first 32 clusters 88 k-blocks against a mean of 55).
-// Unit cost = k-blocks x the MMA clocks of one pair k-block + a per-unit epilogue estimate
-// (TP_GEMM_SCHED_EPI clocks). Units longest first, each to the least-loaded cluster; a cluster
-// runs its units in the order they were assigned (long first).
+// Unit cost = k-blocks x the measured clocks of one pair k-block (576 at 256 columns: the SM's
+// operand ingress, not the 512-clock MMA, paces it) + a per-unit turnaround (TP_GEMM_SCHED_EPI
+// clocks: the next unit's first k-block arriving, the exposed epilogue share; tools/
+// gemm_timeline.py measured ~6.2K clocks per 8-k-block dW unit in the C2 group). Units longest
+// first, each to the least-loaded cluster; a cluster runs its units in the order assigned.
 template <int BNP>
 void schedule_units(Group& G, int ncl) {
   const int units = G.total_units;
@@ -1435,7 +1478,7 @@ void schedule_units(Group& G, int ncl) {
     if (pr.splits != 1) return;  // split-K units keep their co-residency rules
     const int nu = pr.num_m * pr.num_n;
     for (int t = 0; t < nu; ++t) {
-      const int64_t c = int64_t(pr.num_kb) * 512 * BNP / 256 + epi;
+      const int64_t c = int64_t(pr.num_kb) * 576 * BNP / 256 + epi;
       cost[pr.unit0 + t] = c;
       cmin = std::min(cmin, c);
       cmax = std::max(cmax, c);
@@ -1454,6 +1497,8 @@ void schedule_units(Group& G, int ncl) {
     load[best] += cost[u];
     lists[best].push_back(u);
   }
+  for (int c = 0; c < ncl; ++c)
+    if (lists[c].size() > size_t(kMaxClusterUnits)) return;
   int k = 0;
   for (int c = 0; c < ncl; ++c) {
     G.sched_start[c] = static_cast<uint16_t>(k);
@@ -1693,6 +1738,7 @@ tp_status gemm_tc2_bf16(const GemmArgs& g, cudaStream_t s) {
   if (mc == 4 && ncols >= 2 && nrows >= 2) return launch2<128, 4>(&g, 1, s);
   if (mc == 2 && ncols >= 2) return launch2<128, 2>(&g, 1, s);
   if (mc == 3 && nrows >= 2) return launch2<128, 3>(&g, 1, s);
+  if (knob("TP_GEMM_EPI_WARPS") == 8) return launch2<128, 1, 8>(&g, 1, s);
   return launch2<128, 1>(&g, 1, s);
 }
 
