@@ -310,12 +310,15 @@ def test_gemm_narrow_last_tile(api, ta, tb, M, N, K):
 
 
 @pytest.mark.parametrize("sched", [1, 0])
-@pytest.mark.parametrize("M,K,N", [(256, 3072, 3072), (200, 2056, 3000)])
+@pytest.mark.parametrize("M,K,N", [(256, 3072, 3072), (200, 2056, 3000), (65536, 384, 256),
+                                   (50000, 392, 264)])
 def test_grouped_backward_unit_schedule(api, sched, M, K, N):
-    """A layer backward whose grouped launch mixes long-K dX tiles (K = N) with many short dW
-    tiles (K = M): more units than pair clusters and unequal unit lengths, so the longest-first
-    unit schedule (TP_GEMM_SCHED=1) assigns them; round robin (0) for comparison. Both must
-    match the oracle (dX, dW: every tile, ragged tails included)."""
+    """A layer backward whose grouped launch mixes units of unequal length: long-K dX tiles
+    (K = N) next to many short dW tiles (K = M) (C2-like), or a long-K dW split into split-K
+    units next to many short dX tiles (C4-like, M >> K, N). More units than pair clusters: the
+    longest-first unit schedule (TP_GEMM_SCHED=1) assigns the C2-like launches (split-K launches
+    keep round robin); round robin (0) for comparison. Both must match the oracle (dX, dW: every
+    tile, ragged tails included)."""
     from tp_harness import gather, oracle_layer, spec_of, tp_layer
     old = api.tp_knob_get("TP_GEMM_SCHED")
     api.tp_knob_set("TP_GEMM_SCHED", sched)
