@@ -1297,6 +1297,16 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
+// L2 sector promotion of the operand loads (TP_GEMM_L2PROMO: 0 none, 1 64 B, 2 128 B, 3 256 B)
+CUtensorMapL2promotion l2_promotion() {
+  switch (knob("TP_GEMM_L2PROMO")) {
+    case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    case 1: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+    case 2: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    default: return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  }
+}
+
 tp_status make_map2(CUtensorMap* m, CUtensorMapDataType dt, size_t esz, const void* base,
                     uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_inner,
                     uint32_t box_outer) {
@@ -1308,7 +1318,7 @@ tp_status make_map2(CUtensorMap* m, CUtensorMapDataType dt, size_t esz, const vo
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return fail(TP_ERR_SHAPE, "cuTensorMapEncodeTiled (pair kernel) failed: " + std::to_string(int(r)));
   return TP_OK;
@@ -1740,6 +1750,22 @@ tp_status gemm_tc2_bf16(const GemmArgs& g, cudaStream_t s) {
   if (mc == 3 && nrows >= 2) return launch2<128, 3>(&g, 1, s);
   if (knob("TP_GEMM_EPI_WARPS") == 8) return launch2<128, 1, 8>(&g, 1, s);
   return launch2<128, 1>(&g, 1, s);
+}
+
+bool gemm_tc2_group_splits_member(const GemmArgs* gs, int n) {
+  // the per-cluster share launch2<256, 1> computes for a group (tiles x k-blocks / clusters)
+  const double clusters = sm_count() / 2;
+  double work = 0;
+  for (int j = 0; j < n; ++j) {
+    const double tiles = double((gs[j].M + 255) / 256) * double((gs[j].N + 255) / 256);
+    work += tiles * double((gs[j].K + kBK - 1) / kBK) * (gs[j].npanels > 1 ? gs[j].npanels : 1);
+  }
+  const double share = work / clusters;
+  for (int i = 0; i < n; ++i) {
+    const double kb = double((gs[i].K + kBK - 1) / kBK) * (gs[i].npanels > 1 ? gs[i].npanels : 1);
+    if (kb > 2 * share && share >= 8) return true;
+  }
+  return false;
 }
 
 // Up to four independent problems in one launch, 256x256 pair tiles; problems with more K

@@ -144,6 +144,10 @@ tp_status gemm_group(const GemmArgs* gs, int n, cudaStream_t s);
 tp_status gemm_tc_bf16(const GemmArgs& a, cudaStream_t s);  // tcgen05, 1 CTA per tile
 tp_status gemm_tc2_bf16(const GemmArgs& a, cudaStream_t s); // tcgen05 cta_group::2 pair tiles
 bool gemm_tc2_supported(const GemmArgs& a);
+// true when a grouped pair launch of these problems would split a long-K member (its tiles
+// far longer than the group's per-cluster share, e.g. a token-long dW next to many short dX
+// tiles): the dispatcher then launches them separately (TP_GEMM_GROUP_LONGK)
+bool gemm_tc2_group_splits_member(const GemmArgs* gs, int n);
 size_t gemm_tc2_ws_bytes();                                 // split-K scratch upper bound
 tp_status gemm_simt_f32(const GemmArgs& a, cudaStream_t s); // FFMA
 tp_status gemm_k0(const GemmArgs& a, cudaStream_t s);       // K == 0 epilogue only
