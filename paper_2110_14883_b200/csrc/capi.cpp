@@ -48,6 +48,7 @@ constexpr KnobDef kKnobs[] = {
     {"TP_GEMM_GROUP_SPLIT", 1, "split-K inside grouped launches for long-K members (0 off)"},
     {"TP_GEMM_GROUP_LONGK", 1, "a group member the group would split-K (long K) makes the problems launch separately (0: keep the group)"},
     {"TP_GEMM_RASTER", 8, "pair-tile rows per raster band"},
+    {"TP_GEMM_ABOX64", 0, "pair kernel: K-major A as two 64-row TMA boxes per k-block (measurement knob)"},
     {"TP_GEMM_L2PROMO", 3, "pair-kernel tensor maps' L2 promotion: 0 none, 1 64 B, 2 128 B, 3 256 B"},
     {"TP_GEMM_SCHED", 1, "longest-first unit-to-cluster schedule for pair launches with unequal units (0 round robin)"},
     {"TP_GEMM_EPI_DIAG", 0, "diagnostics (TP_TIMELINE builds only): pair-kernel epilogue skips its stores (1) or staging and stores (2)"},

@@ -119,6 +119,7 @@ struct ProbS {
   int npanels, kb_panel, num_kb;  // K = npanels panels of kb_panel 64-wide k-blocks
   int unit0;  // first unit of this problem in the launch's unit space
   int narrow_nb;  // n-tile index computed as a half-width (N = 128) pair tile, -1 none
+  int a_box64;    // K-major A loaded as two 64-row boxes (TP_GEMM_ABOX64, measurement knob)
 };
 struct Prob : ProbS {
   CUtensorMap tmA[kMaxPanels], tmB[kMaxPanels];  // one A/B map per K-panel
@@ -563,7 +564,10 @@ __global__ void __cluster_dims__(2 * pairs_of(MC), 1, 1) __launch_bounds__(threa
           uint8_t* b_dst = sB + stage * P::BBytes;
           // ---- A: this CTA's 128 rows (K-major: one box; MN-major: two 64-wide chunks)
           if (!mc_a(MC)) {
-            if (!a_mn) {
+            if (!a_mn && pr.a_box64) {
+              tma_load_2d_pair(mA, &full[stage], a_dst, kc, m0);
+              tma_load_2d_pair(mA, &full[stage], a_dst + 64 * 128, kc, m0 + 64);
+            } else if (!a_mn) {
               tma_load_2d_pair(mA, &full[stage], a_dst, kc, m0);
             } else {
               for (int c = 0; c < kBM / 64; ++c)
@@ -1372,8 +1376,10 @@ tp_status setup_prob(const GemmArgs& g, Prob& pr, int clusters, int split_mode, 
   for (int k = 0; k < pr.npanels; ++k) {
     const void* A = pr.npanels > 1 ? g.Ap[k] : g.A;
     const void* B = pr.npanels > 1 ? g.Bp[k] : g.B;
+    pr.a_box64 = (!mc_a(MC) && !pr.a_mn && knob("TP_GEMM_ABOX64")) ? 1 : 0;
     if (!pr.a_mn)
-      TP_TRY(make_map2(&pr.tmA[k], BF, 2, A, g.K, g.M, g.lda, kBK, mc_a(MC) ? kBM / 2 : kBM));
+      TP_TRY(make_map2(&pr.tmA[k], BF, 2, A, g.K, g.M, g.lda, kBK,
+                       (mc_a(MC) || pr.a_box64) ? kBM / 2 : kBM));
     else
       TP_TRY(make_map2(&pr.tmA[k], BF, 2, A, g.M, g.K, g.lda, 64, kBK));
     if (!pr.b_mn)
@@ -1660,6 +1666,7 @@ tp_status launch_wide(const GemmArgs* gs, int n, cudaStream_t s) {
     pr.kb_per_split = pr.num_kb;
     pr.ptiles = pr.num_m * pr.num_n;
     pr.narrow_nb = -1;
+    pr.a_box64 = 0;
     pr.unit0 = units;
     units += pr.num_m * pr.num_n;
     flops += 2.0 * double(g.M) * double(g.N) * double(g.K);
