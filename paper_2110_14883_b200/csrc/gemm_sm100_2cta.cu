@@ -28,6 +28,7 @@
 #include <climits>
 #include <cstdlib>
 #include <mutex>
+#include <queue>
 #include <vector>
 
 #include "sm100_ptx.cuh"
@@ -1501,26 +1502,28 @@ void schedule_units(Group& G, int ncl) {
     }
   }
   if (cmin == cmax) return;  // uniform units: round robin is already balanced
+  // units in order of decreasing cost (stable), each to the least-loaded cluster (min-heap of
+  // (load, cluster): ties go to the lower cluster index); host cost O(units log clusters)
   std::vector<int> ord(units);
   for (int u = 0; u < units; ++u) ord[u] = u;
   std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return cost[a] > cost[b]; });
-  std::vector<int64_t> load(ncl, 0);
-  std::vector<std::vector<int>> lists(ncl);
+  using LC = std::pair<int64_t, int>;
+  std::priority_queue<LC, std::vector<LC>, std::greater<LC>> heap;
+  for (int c = 0; c < ncl; ++c) heap.push(LC(0, c));
+  std::vector<int> owner(units), count(ncl, 0);
   for (int u : ord) {
-    int best = 0;
-    for (int c = 1; c < ncl; ++c)
-      if (load[c] < load[best]) best = c;
-    load[best] += cost[u];
-    lists[best].push_back(u);
+    LC top = heap.top();
+    heap.pop();
+    owner[u] = top.second;
+    if (++count[top.second] > kMaxClusterUnits) return;
+    top.first += cost[u];
+    heap.push(top);
   }
-  for (int c = 0; c < ncl; ++c)
-    if (lists[c].size() > size_t(kMaxClusterUnits)) return;
-  int k = 0;
-  for (int c = 0; c < ncl; ++c) {
-    G.sched_start[c] = static_cast<uint16_t>(k);
-    for (int u : lists[c]) G.sched_order[k++] = static_cast<uint16_t>(u);
-  }
-  G.sched_start[ncl] = static_cast<uint16_t>(k);
+  // per-cluster lists in assignment order (counting sort over the cost order)
+  std::vector<int> pos(ncl + 1, 0);
+  for (int c = 0; c < ncl; ++c) pos[c + 1] = pos[c] + count[c];
+  for (int c = 0; c <= ncl; ++c) G.sched_start[c] = static_cast<uint16_t>(pos[c]);
+  for (int u : ord) G.sched_order[pos[owner[u]]++] = static_cast<uint16_t>(u);
   G.sched = 1;
 }
 
