@@ -225,7 +225,8 @@ tp_status gemm_group(const GemmArgs* gs, int n, cudaStream_t s) {
   for (int i = 0; all && i < n; ++i) all = group_eligible(gs[i]);
   // a member that the group would split (long K: e.g. C4's token-long dW, HBM-bound, next to
   // 18912 short dX tiles) runs better in its own launch, split to fill the machine there
-  // (C4: 953 -> 1073 TFLOP/s; profiles/r02_c2_gemm.md)
+  // (C4 backward layer, ncu serialized: 1.88 ms grouped vs 1.69 ms as two launches;
+  // profiles/r02_c2_gemm.md)
   if (all && n > 1 && knob("TP_GEMM_GROUP_LONGK") && gemm_tc2_group_splits_member(gs, n)) all = false;
   if (all && n > 1) return gemm_tc2_group(gs, n, s);
   for (int i = 0; i < n; ++i) TP_TRY(gemm(gs[i], s));

@@ -1763,6 +1763,7 @@ tp_status gemm_tc2_bf16(const GemmArgs& g, cudaStream_t s) {
 }
 
 bool gemm_tc2_group_splits_member(const GemmArgs* gs, int n) {
+  if (!knob("TP_GEMM_GROUP_SPLIT")) return false;  // the group would not split: keep it
   // the per-cluster share launch2<256, 1> computes for a group (tiles x k-blocks / clusters)
   const double clusters = sm_count() / 2;
   double work = 0;
