@@ -196,9 +196,13 @@ def test_tuning_knobs_registry(api):
     import sys
     ks = {k["name"]: k for k in api.tp_knobs()}
     for name in ("TP_PDL", "TP_GEMM_KERNEL", "TP_GEMM_WIDE", "TP_GEMM_RASTER", "TP_COMM_SMS",
-                 "TP_FLASH", "TP_RSA_FUSED", "TP_GEMM_SPLITK"):
+                 "TP_FLASH", "TP_RSA_FUSED", "TP_GEMM_SPLITK", "TP_GEMM_SCHED", "TP_GEMM_SCHED_EPI",
+                 "TP_GEMM_GROUP_LONGK", "TP_GEMM_L2PROMO"):
         assert name in ks and ks[name]["what"]
     assert ks["TP_GEMM_WIDE"]["default"] == -1 and ks["TP_PDL"]["default"] == 1
+    # the measured defaults of session 3 (profiles/r02_c2_gemm.md)
+    assert ks["TP_GEMM_SCHED"]["default"] == 1 and ks["TP_GEMM_SCHED_EPI"]["default"] == 800
+    assert ks["TP_GEMM_GROUP_LONGK"]["default"] == 1 and ks["TP_GEMM_L2PROMO"]["default"] == 3
     old = api.tp_knob_get("TP_GEMM_RASTER")
     api.tp_knob_set("TP_GEMM_RASTER", 4)
     assert api.tp_knob_get("TP_GEMM_RASTER") == 4
